@@ -1,0 +1,118 @@
+"""ctypes front end of the C oracle (gbs_oracle.c) -- TEST INFRASTRUCTURE ONLY.
+
+`gbs_accumulate` has the reference signature (kernels.py:352-355) and its
+in-place semantics; `threads` adds the reference's flat observer-block
+scheduler (parallel.py:108-140).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import pathlib
+import subprocess
+
+import numpy as np
+
+_DIR = pathlib.Path(__file__).resolve().parent
+_LIB = _DIR / "liboracle_gbs.so"
+_lib = None
+
+_d = ctypes.POINTER(ctypes.c_double)
+_i32 = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i64 = ctypes.c_int64
+
+
+def build() -> pathlib.Path:
+    """Compile the oracle with the committed Makefile (gcc, no FMA)."""
+    subprocess.run(["make", "-s", "-C", str(_DIR)], check=True)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not _LIB.exists():
+            build()
+        lib = ctypes.CDLL(str(_LIB))
+        lib.oracle_gbs_accumulate.argtypes = [
+            _d, _d, _d, _d, _d, _d, _d, _i32, _i64, _d, _d, _d, _i64,
+            ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+            _d, _i64p, _i64, _i64, _i64, _i64, ctypes.c_int]
+        lib.oracle_gbs_accumulate.restype = ctypes.c_int
+        lib.oracle_nearest_on_segments.argtypes = [
+            _d, _d, _d, _d, _d, _d, _d, _i64, _i64, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, _d]
+        lib.oracle_nearest_on_segments.restype = None
+        _lib = lib
+    return _lib
+
+
+def _p(a, t=_d):
+    return a.ctypes.data_as(t)
+
+
+def _f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a
+
+
+def gbs_accumulate(seg_origin, seg_dir, seg_e1, seg_e2, seg_len, seg_s0, seg_refl,
+                   n_segs, max_seg, weights, obs, omegas, c, width_b, phi_amp,
+                   use_cutoff, acc, evals, obs_lo, obs_hi, beam_lo, beam_hi, threads=1):
+    lib = _load()
+    arrs = [_f64(x) for x in (seg_origin, seg_dir, seg_e1, seg_e2, seg_len, seg_s0,
+                              seg_refl)]
+    n_segs = np.ascontiguousarray(n_segs, dtype=np.int32)
+    weights = _f64(weights)
+    obs = _f64(obs)
+    omegas = _f64(np.atleast_1d(omegas))
+    if acc.dtype != np.complex128 or not acc.flags.c_contiguous:
+        raise TypeError("acc must be C-contiguous complex128")
+    if evals.dtype != np.int64 or not evals.flags.c_contiguous:
+        raise TypeError("evals must be C-contiguous int64")
+    rc = lib.oracle_gbs_accumulate(
+        *[_p(a) for a in arrs], _p(n_segs, _i32), int(max_seg), _p(weights), _p(obs),
+        _p(omegas), omegas.shape[0], float(c), float(width_b), float(phi_amp),
+        int(bool(use_cutoff)), acc.ctypes.data_as(_d), _p(evals, _i64p), int(obs_lo),
+        int(obs_hi), int(beam_lo), int(beam_hi), int(threads))
+    if rc != 0:
+        raise MemoryError("oracle thread allocation failed")
+
+
+def nearest_on_segments(seg_origin, seg_dir, seg_e1, seg_e2, seg_len, seg_s0, seg_refl,
+                        base, n_seg, px, py, pz):
+    lib = _load()
+    out = np.zeros(6)
+    arrs = [_f64(x) for x in (seg_origin, seg_dir, seg_e1, seg_e2, seg_len, seg_s0,
+                              seg_refl)]
+    lib.oracle_nearest_on_segments(*[_p(a) for a in arrs], int(base), int(n_seg),
+                                   float(px), float(py), float(pz), _p(out))
+    return int(out[0]), out[1], out[2], out[3], out[4], bool(out[5])
+
+
+def load_bundle(path):
+    """Rebuild the padded reference PathBundle arrays from a golden npz.
+
+    Returns a dict with the padded (n_beams*max_seg, ...) arrays exactly as
+    allocate_bundle (beamtrace.py:274-288) lays them out, plus the case data.
+    """
+    z = np.load(path, allow_pickle=False)
+    d = {k: z[k] for k in z.files}
+    n_segs = d["n_segs"].astype(np.int32)
+    S = int(d["max_seg"])
+    nb = n_segs.shape[0]
+    rows = nb * S
+    idx = np.concatenate([np.arange(i * S, i * S + int(n)) for i, n in enumerate(n_segs)])
+    out = dict(d)
+    for name, width in (("origin", 3), ("dir", 3), ("e1", 3), ("e2", 3)):
+        a = np.zeros((rows, width))
+        a[idx] = d["v_" + name]
+        out["seg_" + name] = a
+    for name, fill in (("len", 0.0), ("s0", 0.0), ("refl", 1.0)):
+        a = np.full(rows, fill)
+        a[idx] = d["v_" + name]
+        out["seg_" + name] = a
+    out["n_segs"] = n_segs
+    out["max_seg"] = S
+    return out
