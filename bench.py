@@ -1,0 +1,423 @@
+#!/usr/bin/env python3
+"""GBS stage benchmark: beam-receiver evaluations/s on B200 vs the CPU reference path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+A step is one pass of the hot path -- kernels.gbs_accumulate over ALL beams x
+ALL receivers of the workload -- on synthetic inputs traced
+on the device from the named scene.  Default workload: config 3 (city block,
+50 buildings, 500k rays, 1000x1000 receivers, 125 Hz), the north-star city
+shape.  `value` = N_beams x N_receivers / device time per step (max over
+ranks), inputs resident in HBM; `e2e` = the same metric through the
+reference-facing host-buffer call (H2D + kernels + D2H inside the timed
+region).  Under torchrun each rank sums its receiver tiles (shard.py) and the
+field is gathered to rank 0 inside the timed region (strong scaling).
+
+`--impl reference` times the reference algorithm's CPU implementation (the C
+oracle restatement in oracle/, bit-exact with the reference) on all host
+threads on a bounded receiver sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "beam-receiver evals/sec and GBS wall time at 1/2/4/8 B200 vs CPU ref (cores stated)"
+
+CONFIGS = {
+    "cfg1": dict(desc="open plane, 2k rays, 128x128 receivers (config 1)", scene="plane",
+                 scene_args=(1000.0,), src=(0.0, 0.0, 5.0), freqs=(500.0,), im_b=-12.0,
+                 n_theta=32, n_phi=64, n_steps=2000, r_max=4,
+                 grid=((-32.0, -32.0, 1.5), 0.5, 128, 128)),
+    "cfg2": dict(desc="open plane, 100k rays, 1024x1024 receivers (config 2)", scene="plane",
+                 scene_args=(2000.0,), src=(0.0, 0.0, 10.0), freqs=(500.0,), im_b=-10.0,
+                 n_theta=250, n_phi=400, n_steps=8000, r_max=4,
+                 grid=((-256.0, -256.0, 1.5), 0.5, 1024, 1024)),
+    "cfg3": dict(desc="city block, 50 buildings, 500k rays, 1000x1000 receivers (config 3)",
+                 scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0), src=(20.0, 0.0, 2.0),
+                 freqs=(125.0,), im_b=-10.0, n_theta=500, n_phi=1000, n_steps=5000, r_max=8,
+                 grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
+}
+
+
+def grid_points(origin, spacing, n1, n2):
+    """config.ObserverGridSpec.points ordering (config.py:39-46): j*n1 + i."""
+    o = np.asarray(origin, float)
+    a1 = np.array([spacing, 0.0, 0.0])
+    a2 = np.array([0.0, spacing, 0.0])
+    pts = (o[None, None, :] + np.arange(n1)[None, :, None] * a1[None, None, :]
+           + np.arange(n2)[:, None, None] * a2[None, None, :])
+    return np.ascontiguousarray(pts.reshape(-1, 3))
+
+
+def make_inputs(cfg):
+    from paper_2501_13382_b200 import beamtrace, scene
+    sc = (scene.make_ground_plane(*cfg["scene_args"]) if cfg["scene"] == "plane"
+          else scene.make_city(*cfg["scene_args"]))
+    src = beamtrace.SourceSpec(position=np.array(cfg["src"]), frequencies=cfg["freqs"],
+                               beam_param_im=cfg["im_b"])
+    launch = beamtrace.launch_directions(beamtrace.LaunchGrid(
+        0.0, 180.0, 0.0, 360.0, cfg["n_theta"], cfg["n_phi"]))
+    tcfg = beamtrace.TraceConfig(cfg["n_steps"], 1e-4, cfg["r_max"])
+    c = beamtrace.Atmosphere(20.0).sound_speed
+    obs = grid_points(*cfg["grid"])
+    return sc, src, launch, tcfg, c, obs
+
+
+def cpu_threads():
+    return len(os.sched_getaffinity(0))
+
+
+def time_oracle_sample(bundle, obs, omegas, c, width_b, phi, budget_s, threads):
+    """Oracle (C port of kernels.gbs_accumulate) on a strided receiver subset sized
+    for ~budget_s seconds of all-thread CPU work.  Returns (pairs/s, sample, idx, acc)."""
+    import oracle
+    nb = bundle["n_segs"].shape[0]
+    args = [bundle[k] for k in ("seg_origin", "seg_dir", "seg_e1", "seg_e2", "seg_len",
+                                "seg_s0", "seg_refl")]
+
+    def run(idx):
+        o = np.ascontiguousarray(obs[idx])
+        acc = np.zeros((o.shape[0], omegas.shape[0]), np.complex128)
+        ev = np.zeros(o.shape[0], np.int64)
+        t0 = time.perf_counter()
+        oracle.gbs_accumulate(*args, bundle["n_segs"], bundle["max_seg"], bundle["weights"], o,
+                              omegas, c, width_b, phi, True, acc, ev, 0, o.shape[0], 0, nb,
+                              threads=threads)
+        return time.perf_counter() - t0, acc, ev
+
+    probe = np.linspace(0, obs.shape[0] - 1, max(threads, 16)).astype(np.int64)
+    dt, _, _ = run(probe)
+    rate = probe.size * nb / max(dt, 1e-6)
+    n_sub = int(np.clip(rate * budget_s / nb, threads, obs.shape[0]))
+    stride = max(1, obs.shape[0] // n_sub)
+    idx = np.arange(0, obs.shape[0], stride)
+    dt, acc, ev = run(idx)
+    sample = (f"all {nb} beams x {idx.size} receivers (every {stride}th of {obs.shape[0]}), "
+              f"{threads} threads, {dt:.1f} s")
+    return idx.size * nb / dt, sample, idx, acc, ev, dt
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.out = out
+        return False
+
+    def summary(self):
+        if self.proc is None or not getattr(self, "out", ""):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        rows = [r.split(",") for r in self.out.strip().splitlines() if r.count(",") >= 6]
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[3 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 256 MiB write > 126 MB L2
+
+
+def flop_model(total_pairs_segs, p_nb, evals, nf):
+    """Algorithmic FLOP / MUFU of SURVEY.md 8(d) for the pairs evaluated."""
+    flop = 19.0 * total_pairs_segs + (16.0 + 5.0 * nf) * p_nb + 22.0 * evals
+    mufu = p_nb + 3.0 * evals
+    return flop, mufu
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_13382_b200 import _lib, engine, kernels, shard
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS[args.config]
+    sc, src, launch, tcfg, c, obs_np = make_inputs(cfg)
+    omegas = src.omegas
+    nf = omegas.shape[0]
+    width_b = -src.beam_param_im
+
+    # ---- inputs: trace on the device (sm_100a tracer), resident in HBM
+    dscene = engine.DeviceScene.from_scene(sc, dev)
+    tr = engine.trace_device_rows(dscene, src, launch, tcfg, c, 0, len(launch), dev)
+    bundle = tr["bundle"]
+    torch.cuda.synchronize()
+    nb = bundle.n_paths
+    sum_segs = int(bundle.n_segs.sum().item())
+    obs_all = torch.from_numpy(obs_np).to(dev)
+    n_total = obs_all.shape[0]
+    order = shard.tile_order(obs_all)
+    mine = shard.rank_indices(order, rank, world)
+    obs = obs_all.index_select(0, mine).contiguous()
+    n_loc = obs.shape[0]
+    acc = torch.zeros((n_loc, nf), dtype=torch.complex128, device=dev)
+    evals = torch.zeros(n_loc, dtype=torch.int64, device=dev)
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    prec = args.precision
+
+    def step():
+        acc.zero_()
+        evals.zero_()
+        engine.accumulate(bundle, obs, omegas, width_b, True, acc, evals, precision=prec,
+                          stream=stream, presorted=True)
+        if world > 1:
+            shard.gather_field(acc, evals, order, rank, world, n_total)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    peaks = _lib.probe_peaks(local) if rank == 0 else None
+
+    # ---- timed region (device events per step; L2 flushed between steps)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    ms_steps, kern_ms, stats = [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            ms_steps.append(e0.elapsed_time(e1))
+            st = _lib.last_stats()
+            kern_ms.append(st["kernel_ms"])
+            stats.append(st)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = float(np.mean(ms_steps))
+    t = torch.tensor([ms, float(np.mean(kern_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, kern_max = float(t[0]), float(t[1])
+    pairs = float(nb) * float(n_total)
+    value = pairs / (ms_max / 1e3)
+
+    # ---- e2e: reference-facing host-buffer call (C ABI bf_gbs_accumulate)
+    host = {k: torch.empty(tuple(getattr(bundle, k).shape), dtype=getattr(bundle, k).dtype,
+                           pin_memory=True) for k in engine.SEG_FIELDS + ("n_segs", "weights")}
+    for k, v in host.items():
+        v.copy_(getattr(bundle, k))
+    hb = {k: v.numpy() for k, v in host.items()}
+    obs_h = torch.empty((n_loc, 3), dtype=torch.float64, pin_memory=True)
+    obs_h.copy_(obs)
+    obs_h = obs_h.numpy()
+    acc_h = torch.zeros((n_loc, nf), dtype=torch.complex128, pin_memory=True).numpy()
+    ev_h = torch.zeros(n_loc, dtype=torch.int64, pin_memory=True).numpy()
+
+    def e2e_step():
+        kernels.gbs_accumulate(hb["seg_origin"], hb["seg_dir"], hb["seg_e1"], hb["seg_e2"],
+                               hb["seg_len"], hb["seg_s0"], hb["seg_refl"], hb["n_segs"],
+                               bundle.max_seg, hb["weights"], obs_h, omegas, c, width_b,
+                               src.amplitude_phi, True, acc_h, ev_h, 0, n_loc, 0, nb,
+                               precision=prec, device=local)
+
+    e2e_step()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_t.append(time.perf_counter() - t0)
+    tt = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s = float(tt[0])
+    rows = nb * bundle.max_seg
+    per_row = 24 * 2 + 8 * 3 + (48 if prec == "fp64" else 0)
+    h2d = rows * per_row + nb * 12 + n_loc * (24 + 16 * nf + 8)
+    d2h = n_loc * (16 * nf + 8)
+
+    out = None
+    if rank == 0:
+        st = stats[-1]
+        ev_sum = int(evals.sum().item())
+        p_nb = st["nonbehind_pairs"]
+        flop, mufu = flop_model(float(n_loc) * sum_segs, p_nb, ev_sum, nf)
+        kernel_s = kern_max / 1e3
+        ach = flop / kernel_s / 1e12
+        clocks = clk.summary()
+        peak = peaks["fp32_tflops"]
+        out = {
+            "metric": METRIC, "value": value, "unit": "beam-receiver evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "beams": nb,
+                       "receivers": n_total, "segments": sum_segs, "max_seg": bundle.max_seg,
+                       "freqs_hz": list(cfg["freqs"]), "im_b": cfg["im_b"],
+                       "precision": prec, "parallelism": f"receiver-tiles x{world}",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "inputs": "traced on device by the sm_100a tracer (bit-exact vs reference)"},
+            "gbs_wall_s": ms_max / 1e3,
+            "e2e": {"value": pairs / e2e_s, "unit": "beam-receiver evals/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "seconds_per_step": e2e_s,
+                    "path": "kernels.gbs_accumulate(host numpy, pinned) -> bf_gbs_accumulate"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak, "traffic": None,
+                         "peak_source": "measured FFMA stream (bf_probe_peaks), this GPU",
+                         "kernel": "gbs_fp32_kernel", "kernel_ms": kern_max,
+                         "flop_per_launch": flop, "mufu_per_launch": mufu,
+                         "mufu_tops": mufu / kernel_s / 1e12,
+                         "mufu_peak_tops": peaks["mufu_tops"],
+                         "mufu_frac": mufu / kernel_s / 1e12 / peaks["mufu_tops"],
+                         "algorithmic_model": "SURVEY.md 8(d): 19*N_r*sum(n_segs) + "
+                                              "(16+5F)*P_nb + 22*E FLOP; P_nb + 3E MUFU",
+                         "nonbehind_pairs": p_nb, "evaluations": ev_sum,
+                         "tie_pairs": st["tie_pairs"]},
+            "clocks": clocks,
+        }
+    if world == 1 and not args.no_cpu_baseline:
+        acc_gpu = acc.cpu().numpy()
+        ev_gpu = evals.cpu().numpy()
+        order_np = order.cpu().numpy()
+        hb_full = dict(hb, max_seg=bundle.max_seg)
+        th = cpu_threads()
+        rate, sample, idx, acc_cpu, ev_cpu, dt = time_oracle_sample(
+            hb_full, obs_np, omegas, c, width_b, src.amplitude_phi, args.cpu_budget, th)
+        pos = np.empty(n_total, np.int64)
+        pos[order_np] = np.arange(n_total)
+        mine_acc = acc_gpu[pos[idx]]
+        ref = acc_cpu
+        m = np.abs(ref) > 0
+        strong = m & (20 * np.log10(np.maximum(np.abs(ref), 1e-300) / np.abs(ref).max()) > -60)
+        out["cpu_baseline"] = {"value": rate, "unit": "beam-receiver evals/s", "cores": th,
+                               "kind": "port", "sample": sample,
+                               "impl": "oracle/gbs_oracle.c (bit-exact C restatement of "
+                                       "kernels.gbs_accumulate), WorkerPool.flat blocks"}
+        out["parity_vs_cpu_sample"] = {
+            "receivers": int(idx.size),
+            "rel_l2": float(np.linalg.norm(mine_acc - ref) / np.linalg.norm(ref)),
+            "max_dtl_db_above_-60dB": float(np.max(np.abs(20 * np.log10(
+                np.abs(mine_acc[strong]) / np.abs(ref[strong]))))) if strong.any() else 0.0,
+            "max_dtl_db_all": float(np.max(np.abs(20 * np.log10(
+                np.abs(mine_acc[m]) / np.abs(ref[m]))))) if m.any() else 0.0,
+            "evals_diff": int(np.abs(ev_gpu[pos[idx]] - ev_cpu).sum()),
+        }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm: the C oracle (bit-exact restatement of the reference numba kernel)
+    on all host threads, bounded receiver sample per step; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cfg = CONFIGS[args.config]
+    sc, src, launch, tcfg, c, obs = make_inputs(cfg)
+    th = cpu_threads()
+    t0 = time.perf_counter()
+    b = oracle.trace(sc.v0, sc.v1, sc.v2, sc.refl, sc.bounds, sc.diameter, src.position,
+                     launch.directions, launch.e1, launch.e2, tcfg.length_cap(c), tcfg.r_max,
+                     threads=th)
+    b["weights"] = launch.weights
+    t_trace = time.perf_counter() - t0
+    nb = b["n_segs"].shape[0]
+    per_step = max(2.0, args.ref_budget / max(1, args.steps + args.warmup))
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, sample, idx, _, _, dt = time_oracle_sample(
+            b, obs, src.omegas, c, -src.beam_param_im, src.amplitude_phi, per_step, th)
+        if i >= args.warmup:
+            rates.append(rate)
+    value = float(np.mean(rates))
+    pairs = float(nb) * obs.shape[0]
+    out = {"impl": "reference", "metric": METRIC, "value": value,
+           "unit": "beam-receiver evals/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": pairs / value * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config}: {cfg['desc']}", "beams": nb,
+                      "receivers": int(obs.shape[0]), "extrapolated": "full-field time = "
+                      "pairs / measured rate (per-receiver cost is independent)",
+                      "trace_s": t_trace},
+           "cpu_baseline": {"value": value, "unit": "beam-receiver evals/s", "cores": th,
+                            "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": "beam-receiver evals/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--precision", default="fp32", choices=("fp32", "fp64"))
+    ap.add_argument("--cpu-budget", type=float, default=15.0,
+                    help="seconds of all-thread CPU work for the cpu_baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="total seconds of CPU work for the --impl reference arm")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

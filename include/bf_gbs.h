@@ -1,0 +1,176 @@
+/*
+ * bf_gbs.h -- C ABI of the B200-native Gaussian Beam Summation (GBS) engine.
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  Every entry point
+ * returns a bf_status; on failure bf_last_error() returns a thread-local
+ * message.  All functions are thread-safe; calls on one device serialise on
+ * that device's engine stream unless a caller stream is given.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/beamfield/):
+ *
+ *   bf_gbs_accumulate        kernels.gbs_accumulate           kernels.py:352-399
+ *                            (called by parallel.run_pipeline.gbs_range,
+ *                             parallel.py:576-583, and gbs.sum_at_observer,
+ *                             gbs.py:196-201)
+ *   bf_gbs_accumulate_dev    same operator, device-resident buffers (the
+ *                            engine path used by run_pipeline on the GPU)
+ *   bf_nearest_on_segments   kernels.nearest_on_segments      kernels.py:304-349
+ *   bf_trace_range_dev       kernels.trace_range/trace_one    kernels.py:143-301
+ *                            (+ bvh_nearest semantics kernels.py:54-116)
+ *   bf_field_finalize_dev    parallel.py:599-600 (pressure = calibration*acc)
+ *                            + gbs.spl                        gbs.py:39-46
+ *   bf_plan_chunks           parallel.plan_chunks             parallel.py:347-361
+ *   bf_tile_order_dev        parallel.block_partition/WorkerPool.flat observer split
+ *                            (parallel.py:364-396), re-cut as spatial receiver tiles
+ *
+ * Array layouts are exactly the reference PathBundle's (beamtrace.py:218-288):
+ * seg_origin/seg_dir/seg_e1/seg_e2 are (n_beams*max_seg, 3) C-contiguous fp64,
+ * seg_len/seg_s0/seg_refl are (n_beams*max_seg,) fp64, beam b owns rows
+ * [b*max_seg, b*max_seg + n_segs[b]); obs is (n_obs, 3) fp64; acc is
+ * (n_obs, nf) complex128 stored as interleaved (re, im) doubles; evals is
+ * (n_obs,) int64.  acc/evals rows [obs_lo, obs_hi) are CONTINUED in place
+ * (kernels.py:358-359); nothing outside that range is touched.
+ */
+#ifndef BF_GBS_H
+#define BF_GBS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BF_OK = 0,
+    BF_EINVAL = 1,  /* bad argument (maps to ValueError in the Python shim) */
+    BF_ENOMEM = 2,  /* device or pinned-host allocation failed (MemoryError) */
+    BF_ECUDA = 3,   /* CUDA runtime / launch failure (RuntimeError) */
+    BF_ENODEV = 4,  /* no usable sm_100 device (RuntimeError) */
+    BF_EBUDGET = 5  /* memory budget cannot hold one ray (BudgetError, parallel.py:98-100) */
+} bf_status;
+
+/* Arithmetic of the summation kernel. */
+enum {
+    BF_PRECISION_FP32 = 0, /* fast path: fp32 FMA/MUFU, fp64 tie re-decision,
+                              fp64-anchored axial phase, fp64 accumulators */
+    BF_PRECISION_FP64 = 1  /* oracle mode: reference operation order, no FMA */
+};
+
+/* Library identification and diagnostics. */
+const char *bf_version(void);
+const char *bf_last_error(void);
+int bf_device_count(void);
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t bf_launch_count(void);
+
+/*
+ * Drop-in for kernels.gbs_accumulate (kernels.py:352-355) on HOST buffers.
+ * Argument order follows the reference; array sizes (n_beams = rows/max_seg,
+ * n_obs, nf) are passed right after the array they size.  Host->device copies
+ * of the beam range / observer range, the kernels and the device->host copy
+ * of acc/evals[obs_lo:obs_hi] all happen inside the call.
+ */
+int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir,
+                      const double *seg_e1, const double *seg_e2,
+                      const double *seg_len, const double *seg_s0,
+                      const double *seg_refl, const int32_t *n_segs, int64_t n_beams,
+                      int64_t max_seg, const double *weights, const double *obs,
+                      int64_t n_obs, const double *omegas, int64_t nf, double c,
+                      double width_b, double phi_amp, int use_cutoff, double *acc,
+                      int64_t *evals, int64_t obs_lo, int64_t obs_hi, int64_t beam_lo,
+                      int64_t beam_hi, int precision, int device);
+
+/* Flags of bf_gbs_accumulate_dev. */
+enum {
+    /* Observers [obs_lo, obs_hi) are already in spatial tile order (e.g. from
+     * bf_tile_order_dev): consecutive blocks of bf_tile_size() receivers form
+     * the kernel's tiles.  Used by the multi-GPU receiver-tile partition so a
+     * receiver's result does not depend on the number of ranks. */
+    BF_FLAG_OBS_PRESORTED = 1
+};
+
+/*
+ * Same operator on DEVICE buffers (all pointers are device pointers on
+ * `device`).  Asynchronous on `stream` (cudaStream_t, NULL = the engine's own
+ * stream, which the call synchronises before returning).
+ */
+int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
+                          const double *seg_e1, const double *seg_e2,
+                          const double *seg_len, const double *seg_s0,
+                          const double *seg_refl, const int32_t *n_segs, int64_t n_beams,
+                          int64_t max_seg, const double *weights, const double *obs,
+                          int64_t n_obs, const double *omegas, int64_t nf, double c,
+                          double width_b, double phi_amp, int use_cutoff, double *acc,
+                          int64_t *evals, int64_t obs_lo, int64_t obs_hi, int64_t beam_lo,
+                          int64_t beam_hi, int precision, int flags, int device,
+                          void *stream);
+
+/* Receivers per tile of the fp32 summation kernel. */
+int bf_tile_size(void);
+
+/*
+ * Spatial (Morton, 21 bits/axis over the bounding box) order of n device
+ * observers: perm[i] = index of the i-th receiver in tile order.  Deterministic,
+ * so every rank of a multi-GPU run derives the same receiver-tile partition.
+ */
+int bf_tile_order_dev(const double *obs, int64_t n, int32_t *perm, int device, void *stream);
+
+/*
+ * kernels.nearest_on_segments (kernels.py:304-349) for n_query (observer,
+ * beam) pairs on the device (fp64, reference operation order).  Host
+ * buffers.  out is (n_query, 6): k, s, q1, q2, refl, behind.
+ */
+int bf_nearest_on_segments(const double *seg_origin, const double *seg_dir,
+                           const double *seg_e1, const double *seg_e2,
+                           const double *seg_len, const double *seg_s0,
+                           const double *seg_refl, const int32_t *n_segs, int64_t n_beams,
+                           int64_t max_seg, const double *obs, int64_t n_obs,
+                           const int64_t *q_obs, const int64_t *q_beam, int64_t n_query,
+                           double *out, int device);
+
+/*
+ * Ray marching (kernels.trace_range, kernels.py:282-301) of launch rays
+ * [lo, hi) into bundle rows [(lo-row_base)*max_seg, ...), on DEVICE buffers.
+ * Nearest-hit semantics of bvh_nearest (kernels.py:54-116): smallest t in
+ * (EPS_HIT, remaining], ties to the lower triangle index.  fp64, reference
+ * operation order, no FMA.  v0/v1/v2 are (n_tri, 3); refl_coef (n_tri,);
+ * bounds = (bmin xyz, bmax xyz); dirs/e1s/e2s are (n_rays, 3).
+ */
+int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
+                       const double *refl_coef, int64_t n_tri, const double *bounds,
+                       double diameter, const double *origin, const double *dirs,
+                       const double *e1s, const double *e2s, double length_cap,
+                       int64_t r_max, int64_t max_seg, double *seg_origin, double *seg_dir,
+                       double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
+                       double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo,
+                       int64_t hi, int64_t row_base, int device, void *stream);
+
+/*
+ * pressure = calibration * acc (parallel.py:599) and spl = 20 log10(|p|/2e-5),
+ * -inf for |p| == 0 (gbs.py:39-46), over n complex values on the device.
+ */
+int bf_field_finalize_dev(const double *acc, int64_t n, double calibration,
+                          double *pressure, double *spl, int device, void *stream);
+
+/* parallel.plan_chunks (parallel.py:347-361): greedy maximal chunks.
+ * Writes up to max_chunks sizes, returns the count in *n_chunks. */
+int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_bytes,
+                   int64_t *chunk_sizes, int64_t max_chunks, int64_t *n_chunks);
+
+/* Statistics of the last fp32 bf_gbs_accumulate* call on this thread:
+ * candidate (beam, receiver) pairs after work-list culling, total pairs, fp64
+ * tie re-decisions, receiver tiles, non-behind pairs (P_nb) and the CUDA-event
+ * duration of the summation kernel on its launch stream. Any pointer may be NULL. */
+int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
+                  int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms);
+
+/* Microbenchmarks of the pipes the summation is bound by, on `device`:
+ * dependent-free FFMA stream (TFLOP/s, 2 flop per FFMA) and MUFU ex2 stream
+ * (Tops/s).  Used for the roofline denominators in bench.py. */
+int bf_probe_peaks(int device, double *fp32_tflops, double *mufu_tops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BF_GBS_H */

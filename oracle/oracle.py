@@ -116,3 +116,34 @@ def load_bundle(path):
     out["n_segs"] = n_segs
     out["max_seg"] = S
     return out
+
+
+def trace(v0, v1, v2, refl, bounds, diameter, origin, dirs, e1s, e2s, length_cap, r_max,
+          threads=1):
+    """C restatement of trace_range over all rays (trace_oracle.c); padded bundle dict."""
+    lib = _load()
+    if not hasattr(lib, "_trace_declared"):
+        lib.oracle_trace.argtypes = ([_d, _d, _d, _d, _i64, _d, ctypes.c_double, _d, _d, _d, _d,
+                                      _i64, ctypes.c_double, _i64, _i64] + [_d] * 7 +
+                                     [_i32, _i32, ctypes.c_int])
+        lib.oracle_trace.restype = ctypes.c_int
+        lib._trace_declared = True
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
+    v0, v1, v2, refl, bounds = f(v0), f(v1), f(v2), f(refl), f(bounds).reshape(-1)
+    origin, dirs, e1s, e2s = f(origin), f(dirs), f(e1s), f(e2s)
+    n = dirs.shape[0]
+    S = int(r_max) + 1
+    rows = n * S
+    out = dict(seg_origin=np.zeros((rows, 3)), seg_dir=np.zeros((rows, 3)),
+               seg_e1=np.zeros((rows, 3)), seg_e2=np.zeros((rows, 3)), seg_len=np.zeros(rows),
+               seg_s0=np.zeros(rows), seg_refl=np.ones(rows), n_segs=np.zeros(n, np.int32),
+               n_refls=np.zeros(n, np.int32), max_seg=S)
+    rc = lib.oracle_trace(_p(v0), _p(v1), _p(v2), _p(refl), v0.shape[0], _p(bounds),
+                          float(diameter), _p(origin), _p(dirs), _p(e1s), _p(e2s), n,
+                          float(length_cap), int(r_max), S,
+                          *[_p(out[k]) for k in ("seg_origin", "seg_dir", "seg_e1", "seg_e2",
+                                                 "seg_len", "seg_s0", "seg_refl")],
+                          _p(out["n_segs"], _i32), _p(out["n_refls"], _i32), int(threads))
+    if rc != 0:
+        raise MemoryError("oracle thread allocation failed")
+    return out

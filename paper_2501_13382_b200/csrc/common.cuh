@@ -1,0 +1,87 @@
+// common.cuh -- shared definitions of the B200 GBS engine (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bf_gbs.h"
+
+#define BF_MAXF 8            // frequencies per call supported by the kernels
+#define BF_CUTOFF_EXPONENT (-36.0)  // kernels.py:18
+#define BF_EPS_HIT 1e-6              // kernels.py:14
+
+namespace bf {
+
+// Records a failure message for bf_last_error() and returns the status.
+int fail(int status, const char *fmt, ...);
+// Counts one kernel launch of this library (bf_launch_count()).
+void note_launch(int n = 1);
+// Converts a CUDA error (if any) into BF_ECUDA with a message.
+int check_cuda(cudaError_t e, const char *what);
+
+#define BF_TRY_CUDA(expr)                                   \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) return ::bf::check_cuda(_e, #expr); \
+    } while (0)
+
+#define BF_TRY(expr)                 \
+    do {                             \
+        int _s = (expr);             \
+        if (_s != BF_OK) return _s;  \
+    } while (0)
+
+// Arguments of one summation over LOCAL ranges: beam 0 here is the caller's
+// beam_lo, observer 0 is obs_lo.  Row r of beam b is b*max_seg + r (padded
+// reference layout, beamtrace.py:274-288).
+struct GbsArgs {
+    const double *seg_origin, *seg_dir, *seg_e1, *seg_e2, *seg_len, *seg_s0, *seg_refl;
+    const int32_t *n_segs;
+    const double *weights;
+    const double *obs;
+    int64_t max_seg;
+    int64_t n_beams;  // local beam count
+    int64_t n_obs;    // local observer count
+    int nf;
+    double omegas[BF_MAXF];
+    double c, width_b, phi_amp;
+    int use_cutoff;
+    double *acc;      // (n_obs, nf) complex, interleaved
+    int64_t *evals;   // (n_obs,)
+};
+
+// Work-list statistics of the fp32 path (device counters, copied back).
+struct GbsStats {
+    unsigned long long candidate_pairs;  // (beam, receiver) pairs inside candidate tiles
+    unsigned long long tie_pairs;        // pairs re-decided in fp64
+    unsigned long long nb_pairs;         // non-behind pairs (P_nb of SURVEY 8(d))
+    float kernel_ms;                     // CUDA-event duration of the summation kernel
+};
+
+// Receiver tiling built per call for the fp32 path (engine.cu).
+struct Tiling {
+    int64_t n;          // receivers
+    int64_t n_tiles;
+    int tile;           // receivers per tile
+    const int32_t *perm;      // sorted position -> local observer index
+    const float4 *rloc;       // sorted position -> (p - centre) fp32, w = unused
+    const double4 *centre;    // per tile: centre xyz, radius
+};
+
+// Launchers (return BF_OK or an error status).
+int launch_gbs_fp64(const GbsArgs &a, cudaStream_t st);
+int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
+                    GbsStats *d_stats, cudaStream_t st);
+int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam,
+                   int64_t n_query, double *out, cudaStream_t st);
+int launch_trace(const double *v0, const double *v1, const double *v2, const double *refl,
+                 int64_t n_tri, const double *bounds, double diameter, const double *origin,
+                 const double *dirs, const double *e1s, const double *e2s, double length_cap,
+                 int64_t r_max, int64_t max_seg, double *seg_origin, double *seg_dir,
+                 double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
+                 double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
+                 int64_t row_base, cudaStream_t st);
+int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
+                    double *spl, cudaStream_t st);
+
+}  // namespace bf

@@ -1,0 +1,645 @@
+// engine.cu -- device contexts, receiver tiling and the extern "C" ABI.
+//
+// The ABI (include/bf_gbs.h) is the drop-in boundary for the reference's
+// kernels.gbs_accumulate (kernels.py:352-399) and its neighbours; this file
+// owns everything between that boundary and the kernels: argument checks that
+// mirror the reference's contracts, per-device streams and grow-only
+// workspaces, host<->device staging of the caller's ranges, the Morton
+// receiver tiling used by the fp32 kernel, and the beam segment prefix sums.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bf {
+
+int gbs_fp32_tile();
+
+namespace {
+thread_local char g_err[512] = "";
+thread_local GbsStats g_last_stats = {0, 0, 0, 0.f};
+thread_local int64_t g_last_total_pairs = 0, g_last_tiles = 0;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+int fail(int status, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return status;
+}
+
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int check_cuda(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return BF_OK;
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(BF_ENOMEM, "%s: %s", what, cudaGetErrorString(e));
+    }
+    return fail(BF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+namespace {
+
+// Grow-only device buffer.
+struct Buf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int get(size_t bytes, void **out) {
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            size_t want = bytes + bytes / 4 + 256;
+            BF_TRY_CUDA(cudaMalloc(&p, want));
+            cap = want;
+        }
+        *out = p;
+        return BF_OK;
+    }
+};
+
+enum BufId {
+    B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
+    B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
+    B_QOBS, B_QBEAM, B_QOUT, B_NSW, B_COUNT
+};
+
+struct DeviceCtx {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::mutex mu;
+    Buf buf[B_COUNT];
+    template <typename T>
+    int get(BufId id, size_t n, T **out) {
+        void *p;
+        BF_TRY(buf[id].get(n * sizeof(T) + 16, &p));
+        *out = (T *)p;
+        return BF_OK;
+    }
+};
+
+std::mutex g_ctx_mu;
+std::vector<DeviceCtx *> g_ctx;
+
+int get_ctx(int device, DeviceCtx **out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(BF_ENODEV, "no CUDA device available (%s)",
+                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= n) return fail(BF_EINVAL, "device %d out of range [0,%d)", device, n);
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    if ((int)g_ctx.size() < n) g_ctx.resize(n, nullptr);
+    if (!g_ctx[device]) {
+        BF_TRY_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        BF_TRY_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            return fail(BF_ENODEV, "device %d is sm_%d%d; this library is built for sm_100a",
+                        device, prop.major, prop.minor);
+        DeviceCtx *c = new DeviceCtx();
+        c->dev = device;
+        BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        g_ctx[device] = c;
+    }
+    *out = g_ctx[device];
+    return BF_OK;
+}
+
+// ------------------------------------------------------------ tiling ----
+
+__global__ void bbox_kernel(const double *obs, int64_t n, double *bbox) {
+    __shared__ double smin[3][256], smax[3][256];
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        for (int d = 0; d < 3; ++d) {
+            const double v = obs[3 * i + d];
+            mn[d] = fmin(mn[d], v);
+            mx[d] = fmax(mx[d], v);
+        }
+    for (int d = 0; d < 3; ++d) {
+        smin[d][threadIdx.x] = mn[d];
+        smax[d][threadIdx.x] = mx[d];
+    }
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s)
+            for (int d = 0; d < 3; ++d) {
+                smin[d][threadIdx.x] = fmin(smin[d][threadIdx.x], smin[d][threadIdx.x + s]);
+                smax[d][threadIdx.x] = fmax(smax[d][threadIdx.x], smax[d][threadIdx.x + s]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int d = 0; d < 3; ++d) {
+            bbox[d] = smin[d][0];
+            bbox[3 + d] = smax[d][0];
+        }
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+__global__ void morton_kernel(const double *obs, int64_t n, const double *bbox, uint64_t *keys,
+                              int32_t *vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t q[3];
+    for (int d = 0; d < 3; ++d) {
+        const double ext = bbox[3 + d] - bbox[d];
+        double u = ext > 0 ? (obs[3 * i + d] - bbox[d]) / ext : 0.0;
+        u = fmin(fmax(u, 0.0), 1.0);
+        q[d] = (uint64_t)(u * 2097151.0);
+    }
+    keys[i] = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+    vals[i] = (int32_t)i;
+}
+
+template <int T>
+__global__ void tile_kernel(const double *obs, int64_t n, const int32_t *perm, float4 *rloc,
+                            double4 *centre) {
+    using BR = cub::BlockReduce<double, T>;
+    __shared__ typename BR::TempStorage tmp;
+    __shared__ double s_c[3];
+    __shared__ float s_r;
+    const int64_t si = (int64_t)blockIdx.x * T + threadIdx.x;
+    const bool valid = si < n;
+    double p[3] = {0, 0, 0};
+    if (valid) {
+        const int64_t oi = perm[si];
+        for (int d = 0; d < 3; ++d) p[d] = obs[3 * oi + d];
+    }
+    for (int d = 0; d < 3; ++d) {
+        const double mn = BR(tmp).Reduce(valid ? p[d] : INFINITY, cub::Min());
+        __syncthreads();
+        const double mx = BR(tmp).Reduce(valid ? p[d] : -INFINITY, cub::Max());
+        __syncthreads();
+        if (threadIdx.x == 0) s_c[d] = 0.5 * (mn + mx);
+    }
+    __syncthreads();
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+        r.x = (float)(p[0] - s_c[0]);
+        r.y = (float)(p[1] - s_c[1]);
+        r.z = (float)(p[2] - s_c[2]);
+        rloc[si] = r;
+    }
+    const double rad = valid ? sqrt((double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z) : 0.0;
+    const double rmax = BR(tmp).Reduce(rad, cub::Max());
+    if (threadIdx.x == 0) s_r = (float)rmax;
+    __syncthreads();
+    if (threadIdx.x == 0) centre[blockIdx.x] = make_double4(s_c[0], s_c[1], s_c[2], (double)s_r);
+}
+
+__global__ void iota_kernel(int32_t *v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = (int32_t)i;
+}
+
+// Morton order of n observers into *perm (a workspace buffer).
+int morton_order(DeviceCtx *c, const double *obs, int64_t n, cudaStream_t st,
+                 const int32_t **perm) {
+    double *bbox;
+    uint64_t *k1, *k2;
+    int32_t *v1, *v2;
+    BF_TRY(c->get(B_BBOX, 6, &bbox));
+    BF_TRY(c->get(B_KEYS, n, &k1));
+    BF_TRY(c->get(B_KEYS2, n, &k2));
+    BF_TRY(c->get(B_VALS, n, &v1));
+    BF_TRY(c->get(B_VALS2, n, &v2));
+    bbox_kernel<<<1, 256, 0, st>>>(obs, n, bbox);
+    morton_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(obs, n, bbox, k1, v1);
+    note_launch(2);
+    BF_TRY_CUDA(cudaGetLastError());
+    cub::DoubleBuffer<uint64_t> dk(k1, k2);
+    cub::DoubleBuffer<int32_t> dv(v1, v2);
+    size_t tmp_bytes = 0;
+    BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)n, 0, 63, st));
+    void *tmp;
+    BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
+    BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, dv, (int)n, 0, 63, st));
+    note_launch(4);
+    *perm = dv.Current();
+    return BF_OK;
+}
+
+int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cudaStream_t st,
+                 Tiling *out) {
+    const int T = gbs_fp32_tile();
+    out->n = n;
+    out->tile = T;
+    out->n_tiles = (n + T - 1) / T;
+    if (n <= 0) return BF_OK;
+    if (n > INT32_MAX) return fail(BF_EINVAL, "observer range too large (%lld)", (long long)n);
+    float4 *rloc;
+    double4 *cen;
+    BF_TRY(c->get(B_RLOC, n, &rloc));
+    BF_TRY(c->get(B_CENTRE, out->n_tiles, &cen));
+    const int32_t *perm;
+    if (presorted) {
+        int32_t *id;
+        BF_TRY(c->get(B_VALS, n, &id));
+        iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(id, n);
+        note_launch();
+        perm = id;
+    } else {
+        BF_TRY(morton_order(c, obs, n, st, &perm));
+    }
+    if (T == 256)
+        tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm, rloc, cen);
+    else
+        return fail(BF_EINVAL, "unsupported tile size %d", T);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    out->perm = perm;
+    out->rloc = rloc;
+    out->centre = cen;
+    return BF_OK;
+}
+
+__global__ void widen_kernel(const int32_t *n_segs, int64_t nb, int32_t *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nb) out[i] = n_segs[i];
+    if (i == nb) out[i] = 0;
+}
+
+// seg_start[b] = sum_{j<b} n_segs[j], b in [0, nb]
+int build_seg_start(DeviceCtx *c, const int32_t *n_segs, int64_t nb, cudaStream_t st,
+                    int32_t **out) {
+    int32_t *tmpin, *ss;
+    BF_TRY(c->get(B_NSW, nb + 1, &tmpin));
+    BF_TRY(c->get(B_SEGSTART, nb + 1, &ss));
+    widen_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, st>>>(n_segs, nb, tmpin);
+    note_launch();
+    size_t tmp_bytes = 0;
+    BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tmpin, ss, (int)(nb + 1), st));
+    void *tmp;
+    BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
+    BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tmpin, ss, (int)(nb + 1), st));
+    note_launch();
+    *out = ss;
+    return BF_OK;
+}
+
+int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_t obs_lo,
+             int64_t obs_hi, int64_t beam_lo, int64_t beam_hi, int precision) {
+    if (max_seg < 1) return fail(BF_EINVAL, "max_seg must be >= 1");
+    if (nf < 0 || nf > BF_MAXF) return fail(BF_EINVAL, "nf=%lld outside 0..%d", (long long)nf, BF_MAXF);
+    if (obs_lo < 0 || obs_hi < obs_lo || obs_hi > n_obs)
+        return fail(BF_EINVAL, "observer range [%lld,%lld) outside [0,%lld)", (long long)obs_lo,
+                    (long long)obs_hi, (long long)n_obs);
+    if (beam_lo < 0 || beam_hi < beam_lo || beam_hi > n_beams)
+        return fail(BF_EINVAL, "beam range [%lld,%lld) outside [0,%lld)", (long long)beam_lo,
+                    (long long)beam_hi, (long long)n_beams);
+    if (precision != BF_PRECISION_FP32 && precision != BF_PRECISION_FP64)
+        return fail(BF_EINVAL, "unknown precision %d", precision);
+    return BF_OK;
+}
+
+// Runs the operator on device-resident LOCAL ranges (a.obs etc. already offset).
+int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st) {
+    g_last_stats = {0, 0, 0, 0.f};
+    g_last_total_pairs = a.n_obs * a.n_beams;
+    g_last_tiles = 0;
+    if (a.n_obs <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
+    if (precision == BF_PRECISION_FP64) return launch_gbs_fp64(a, st);
+    Tiling t;
+    BF_TRY(build_tiling(c, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
+    int32_t *seg_start;
+    BF_TRY(build_seg_start(c, a.n_segs, a.n_beams, st, &seg_start));
+    GbsStats *d_stats;
+    BF_TRY(c->get(B_STATS, 1, &d_stats));
+    BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
+    if (!c->ev0) {
+        BF_TRY_CUDA(cudaEventCreate(&c->ev0));
+        BF_TRY_CUDA(cudaEventCreate(&c->ev1));
+    }
+    BF_TRY_CUDA(cudaEventRecord(c->ev0, st));
+    BF_TRY(launch_gbs_fp32(a, t, seg_start, d_stats, st));
+    BF_TRY_CUDA(cudaEventRecord(c->ev1, st));
+    GbsStats h;
+    BF_TRY_CUDA(cudaMemcpyAsync(&h, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost, st));
+    BF_TRY_CUDA(cudaStreamSynchronize(st));
+    BF_TRY_CUDA(cudaEventElapsedTime(&h.kernel_ms, c->ev0, c->ev1));
+    h.candidate_pairs = (unsigned long long)g_last_total_pairs;
+    g_last_stats = h;
+    g_last_tiles = t.n_tiles;
+    return BF_OK;
+}
+
+}  // namespace
+}  // namespace bf
+
+using namespace bf;
+
+extern "C" {
+
+const char *bf_version(void) { return "paper_2501_13382_b200 0.1.0 (sm_100a)"; }
+
+const char *bf_last_error(void) { return g_err; }
+
+int bf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint64_t bf_launch_count(void) { return g_launches.load(); }
+
+int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
+                  int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms) {
+    if (nonbehind_pairs) *nonbehind_pairs = (int64_t)g_last_stats.nb_pairs;
+    if (kernel_ms) *kernel_ms = (double)g_last_stats.kernel_ms;
+    if (candidate_pairs) *candidate_pairs = (int64_t)g_last_stats.candidate_pairs;
+    if (total_pairs) *total_pairs = g_last_total_pairs;
+    if (tie_pairs) *tie_pairs = (int64_t)g_last_stats.tie_pairs;
+    if (n_tiles) *n_tiles = g_last_tiles;
+    return BF_OK;
+}
+
+int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
+                          const double *seg_e1, const double *seg_e2,
+                          const double *seg_len, const double *seg_s0,
+                          const double *seg_refl, const int32_t *n_segs, int64_t n_beams,
+                          int64_t max_seg, const double *weights, const double *obs,
+                          int64_t n_obs, const double *omegas, int64_t nf, double c,
+                          double width_b, double phi_amp, int use_cutoff, double *acc,
+                          int64_t *evals, int64_t obs_lo, int64_t obs_hi, int64_t beam_lo,
+                          int64_t beam_hi, int precision, int flags, int device,
+                          void *stream) {
+    BF_TRY(validate(n_beams, max_seg, n_obs, nf, obs_lo, obs_hi, beam_lo, beam_hi, precision));
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    GbsArgs a;
+    const int64_t r0 = beam_lo * max_seg;
+    a.seg_origin = seg_origin + 3 * r0;
+    a.seg_dir = seg_dir + 3 * r0;
+    a.seg_e1 = seg_e1 ? seg_e1 + 3 * r0 : nullptr;
+    a.seg_e2 = seg_e2 ? seg_e2 + 3 * r0 : nullptr;
+    a.seg_len = seg_len + r0;
+    a.seg_s0 = seg_s0 + r0;
+    a.seg_refl = seg_refl + r0;
+    a.n_segs = n_segs + beam_lo;
+    a.weights = weights + beam_lo;
+    a.obs = obs + 3 * obs_lo;
+    a.max_seg = max_seg;
+    a.n_beams = beam_hi - beam_lo;
+    a.n_obs = obs_hi - obs_lo;
+    a.nf = (int)nf;
+    for (int f = 0; f < BF_MAXF; ++f) a.omegas[f] = f < nf ? omegas[f] : 0.0;
+    a.c = c;
+    a.width_b = width_b;
+    a.phi_amp = phi_amp;
+    a.use_cutoff = use_cutoff ? 1 : 0;
+    a.acc = acc + 2 * obs_lo * nf;
+    a.evals = evals + obs_lo;
+    if (precision == BF_PRECISION_FP64 && (!seg_e1 || !seg_e2))
+        return fail(BF_EINVAL, "fp64 mode needs seg_e1/seg_e2");
+    BF_TRY(run_gbs(ctx, a, precision, flags, st));
+    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
+
+int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const double *seg_e1,
+                      const double *seg_e2, const double *seg_len, const double *seg_s0,
+                      const double *seg_refl, const int32_t *n_segs, int64_t n_beams,
+                      int64_t max_seg, const double *weights, const double *obs, int64_t n_obs,
+                      const double *omegas, int64_t nf, double c, double width_b,
+                      double phi_amp, int use_cutoff, double *acc, int64_t *evals,
+                      int64_t obs_lo, int64_t obs_hi, int64_t beam_lo, int64_t beam_hi,
+                      int precision, int device) {
+    BF_TRY(validate(n_beams, max_seg, n_obs, nf, obs_lo, obs_hi, beam_lo, beam_hi, precision));
+    const int64_t nb = beam_hi - beam_lo, no = obs_hi - obs_lo;
+    if (nb == 0 || no == 0 || nf == 0) return BF_OK;
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = ctx->stream;
+    const bool need_frame = precision == BF_PRECISION_FP64;
+    const int64_t rows = nb * max_seg, r0 = beam_lo * max_seg;
+    double *d_or, *d_dir, *d_e1 = nullptr, *d_e2 = nullptr, *d_len, *d_s0, *d_refl, *d_w, *d_obs,
+                                *d_acc;
+    int32_t *d_ns;
+    int64_t *d_ev;
+    BF_TRY(ctx->get(B_ORIGIN, 3 * rows, &d_or));
+    BF_TRY(ctx->get(B_DIR, 3 * rows, &d_dir));
+    if (need_frame) {
+        BF_TRY(ctx->get(B_E1, 3 * rows, &d_e1));
+        BF_TRY(ctx->get(B_E2, 3 * rows, &d_e2));
+    }
+    BF_TRY(ctx->get(B_LEN, rows, &d_len));
+    BF_TRY(ctx->get(B_S0, rows, &d_s0));
+    BF_TRY(ctx->get(B_REFL, rows, &d_refl));
+    BF_TRY(ctx->get(B_NSEGS, nb, &d_ns));
+    BF_TRY(ctx->get(B_W, nb, &d_w));
+    BF_TRY(ctx->get(B_OBS, 3 * no, &d_obs));
+    BF_TRY(ctx->get(B_ACC, 2 * no * nf, &d_acc));
+    BF_TRY(ctx->get(B_EVALS, no, &d_ev));
+    const auto H2D = cudaMemcpyHostToDevice;
+    BF_TRY_CUDA(cudaMemcpyAsync(d_or, seg_origin + 3 * r0, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_dir, seg_dir + 3 * r0, 24 * rows, H2D, st));
+    if (need_frame) {
+        BF_TRY_CUDA(cudaMemcpyAsync(d_e1, seg_e1 + 3 * r0, 24 * rows, H2D, st));
+        BF_TRY_CUDA(cudaMemcpyAsync(d_e2, seg_e2 + 3 * r0, 24 * rows, H2D, st));
+    }
+    BF_TRY_CUDA(cudaMemcpyAsync(d_len, seg_len + r0, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_s0, seg_s0 + r0, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_refl, seg_refl + r0, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_ns, n_segs + beam_lo, 4 * nb, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_w, weights + beam_lo, 8 * nb, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_obs, obs + 3 * obs_lo, 24 * no, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_acc, acc + 2 * obs_lo * nf, 16 * no * nf, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_ev, evals + obs_lo, 8 * no, H2D, st));
+    GbsArgs a;
+    a.seg_origin = d_or;
+    a.seg_dir = d_dir;
+    a.seg_e1 = d_e1;
+    a.seg_e2 = d_e2;
+    a.seg_len = d_len;
+    a.seg_s0 = d_s0;
+    a.seg_refl = d_refl;
+    a.n_segs = d_ns;
+    a.weights = d_w;
+    a.obs = d_obs;
+    a.max_seg = max_seg;
+    a.n_beams = nb;
+    a.n_obs = no;
+    a.nf = (int)nf;
+    for (int f = 0; f < BF_MAXF; ++f) a.omegas[f] = f < nf ? omegas[f] : 0.0;
+    a.c = c;
+    a.width_b = width_b;
+    a.phi_amp = phi_amp;
+    a.use_cutoff = use_cutoff ? 1 : 0;
+    a.acc = d_acc;
+    a.evals = d_ev;
+    BF_TRY(run_gbs(ctx, a, precision, 0, st));
+    const auto D2H = cudaMemcpyDeviceToHost;
+    BF_TRY_CUDA(cudaMemcpyAsync(acc + 2 * obs_lo * nf, d_acc, 16 * no * nf, D2H, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(evals + obs_lo, d_ev, 8 * no, D2H, st));
+    BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
+
+int bf_nearest_on_segments(const double *seg_origin, const double *seg_dir,
+                           const double *seg_e1, const double *seg_e2, const double *seg_len,
+                           const double *seg_s0, const double *seg_refl, const int32_t *n_segs,
+                           int64_t n_beams, int64_t max_seg, const double *obs, int64_t n_obs,
+                           const int64_t *q_obs, const int64_t *q_beam, int64_t n_query,
+                           double *out, int device) {
+    if (max_seg < 1 || n_query < 0) return fail(BF_EINVAL, "bad sizes");
+    for (int64_t j = 0; j < n_query; ++j)
+        if (q_obs[j] < 0 || q_obs[j] >= n_obs || q_beam[j] < 0 || q_beam[j] >= n_beams)
+            return fail(BF_EINVAL, "query %lld out of range", (long long)j);
+    if (n_query == 0) return BF_OK;
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = ctx->stream;
+    const int64_t rows = n_beams * max_seg;
+    double *d_or, *d_dir, *d_e1, *d_e2, *d_len, *d_s0, *d_refl, *d_obs, *d_out;
+    int32_t *d_ns;
+    int64_t *d_qo, *d_qb;
+    BF_TRY(ctx->get(B_ORIGIN, 3 * rows, &d_or));
+    BF_TRY(ctx->get(B_DIR, 3 * rows, &d_dir));
+    BF_TRY(ctx->get(B_E1, 3 * rows, &d_e1));
+    BF_TRY(ctx->get(B_E2, 3 * rows, &d_e2));
+    BF_TRY(ctx->get(B_LEN, rows, &d_len));
+    BF_TRY(ctx->get(B_S0, rows, &d_s0));
+    BF_TRY(ctx->get(B_REFL, rows, &d_refl));
+    BF_TRY(ctx->get(B_NSEGS, n_beams, &d_ns));
+    BF_TRY(ctx->get(B_OBS, 3 * n_obs, &d_obs));
+    BF_TRY(ctx->get(B_QOBS, n_query, &d_qo));
+    BF_TRY(ctx->get(B_QBEAM, n_query, &d_qb));
+    BF_TRY(ctx->get(B_QOUT, 6 * n_query, &d_out));
+    const auto H2D = cudaMemcpyHostToDevice;
+    BF_TRY_CUDA(cudaMemcpyAsync(d_or, seg_origin, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_dir, seg_dir, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_e1, seg_e1, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_e2, seg_e2, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_len, seg_len, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_s0, seg_s0, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_refl, seg_refl, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_ns, n_segs, 4 * n_beams, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_obs, obs, 24 * n_obs, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_qo, q_obs, 8 * n_query, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_qb, q_beam, 8 * n_query, H2D, st));
+    GbsArgs a{};
+    a.seg_origin = d_or;
+    a.seg_dir = d_dir;
+    a.seg_e1 = d_e1;
+    a.seg_e2 = d_e2;
+    a.seg_len = d_len;
+    a.seg_s0 = d_s0;
+    a.seg_refl = d_refl;
+    a.n_segs = d_ns;
+    a.obs = d_obs;
+    a.max_seg = max_seg;
+    a.n_beams = n_beams;
+    a.n_obs = n_obs;
+    BF_TRY(launch_nearest(a, d_qo, d_qb, n_query, d_out, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(out, d_out, 48 * n_query, cudaMemcpyDeviceToHost, st));
+    BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
+
+int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
+                       const double *refl_coef, int64_t n_tri, const double *bounds,
+                       double diameter, const double *origin, const double *dirs,
+                       const double *e1s, const double *e2s, double length_cap, int64_t r_max,
+                       int64_t max_seg, double *seg_origin, double *seg_dir, double *seg_e1,
+                       double *seg_e2, double *seg_len, double *seg_s0, double *seg_refl,
+                       int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
+                       int64_t row_base, int device, void *stream) {
+    if (r_max < 0 || max_seg < r_max + 1) return fail(BF_EINVAL, "max_seg must be >= r_max+1");
+    if (hi < lo || lo < row_base) return fail(BF_EINVAL, "bad ray range");
+    if (n_tri < 0) return fail(BF_EINVAL, "negative triangle count");
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    BF_TRY(launch_trace(v0, v1, v2, refl_coef, n_tri, bounds, diameter, origin, dirs, e1s, e2s,
+                        length_cap, r_max, max_seg, seg_origin, seg_dir, seg_e1, seg_e2, seg_len,
+                        seg_s0, seg_refl, n_segs, n_refls, lo, hi, row_base, st));
+    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
+
+int bf_field_finalize_dev(const double *acc, int64_t n, double calibration, double *pressure,
+                          double *spl, int device, void *stream) {
+    if (n < 0) return fail(BF_EINVAL, "negative size");
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    BF_TRY(launch_finalize(acc, n, calibration, pressure, spl, st));
+    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
+
+int bf_tile_size(void) { return gbs_fp32_tile(); }
+
+int bf_tile_order_dev(const double *obs, int64_t n, int32_t *perm, int device, void *stream) {
+    if (n < 0 || n > INT32_MAX) return fail(BF_EINVAL, "bad observer count");
+    if (n == 0) return BF_OK;
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    const int32_t *p;
+    BF_TRY(morton_order(ctx, obs, n, st, &p));
+    BF_TRY_CUDA(cudaMemcpyAsync(perm, p, 4 * n, cudaMemcpyDeviceToDevice, st));
+    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
+
+int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_bytes,
+                   int64_t *chunk_sizes, int64_t max_chunks, int64_t *n_chunks) {
+    if (total_rays < 1) return fail(BF_EINVAL, "need at least one ray to plan chunks");
+    if (per_ray_bytes <= 0) return fail(BF_EINVAL, "per-ray size must be positive");
+    const int64_t cap = memory_budget / per_ray_bytes;  // floor division, budget >= 0
+    if (memory_budget < 0 || cap <= 0)
+        return fail(BF_EBUDGET, "memory budget %lld cannot hold one ray of %lld bytes",
+                    (long long)memory_budget, (long long)per_ray_bytes);
+    const int64_t full = total_rays / cap, rem = total_rays % cap;
+    const int64_t n = full + (rem ? 1 : 0);
+    *n_chunks = n;
+    if (n > max_chunks) return fail(BF_EINVAL, "need %lld chunk slots", (long long)n);
+    for (int64_t i = 0; i < full; ++i) chunk_sizes[i] = cap;
+    if (rem) chunk_sizes[full] = rem;
+    return BF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""GPU parity of the sm_100a GBS path against the reference golden fixtures and the
+C oracle (all calls go through the C ABI in libbf_gbs.so).
+
+Tolerances (BASELINE.json north_star):
+  fp64 mode: relL2(acc) <= 1e-12, evals bit-exact, nearest-segment k/behind bit-exact;
+  fp32 mode: relL2(acc) <= 1e-4, max dTL <= 0.01 dB over receivers within 60 dB of the
+  field maximum (the all-receiver max is asserted <= 0.05 dB).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import CASES, gbs_args, load_case, rel_l2, tl_db
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-12
+FP32_L2 = 1e-4
+FP32_TL_DB = 0.01
+FP32_TL_ALL_DB = 0.05
+
+
+def run(b, precision, obs=None, calls=None):
+    from paper_2501_13382_b200 import kernels
+    obs = b["obs"] if obs is None else obs
+    acc = np.zeros((obs.shape[0], b["omegas"].shape[0]), np.complex128)
+    ev = np.zeros(obs.shape[0], np.int64)
+    calls = b["calls"] if calls is None else calls
+    for olo, ohi, blo, bhi in calls:
+        kernels.gbs_accumulate(*gbs_args(b, obs), acc, ev, olo, ohi, blo, bhi,
+                               precision=precision)
+    return acc, ev
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp64_mode_vs_reference(name):
+    b = load_case(name)
+    acc, ev = run(b, "fp64")
+    assert rel_l2(acc, b["acc"]) <= FP64_TOL
+    assert np.max(np.abs(acc - b["acc"])) <= FP64_TOL * np.max(np.abs(b["acc"]))
+    assert np.array_equal(ev, b["evals"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp32_mode_vs_reference(name):
+    b = load_case(name)
+    acc, ev = run(b, "fp32")
+    ref = b["acc"]
+    assert rel_l2(acc, ref) <= FP32_L2
+    assert tl_db(acc, ref, floor_db=-60.0) <= FP32_TL_DB
+    assert tl_db(acc, ref) <= FP32_TL_ALL_DB
+    # cutoff decisions may flip only at the e^-36 threshold
+    assert abs(int(ev.sum()) - int(b["evals"].sum())) <= 1e-4 * int(b["evals"].sum()) + 10
+
+
+@pytest.mark.parametrize("name", ["cfg1_open_plane", "city_street", "city_corner_f5"])
+def test_nearest_segment_bitexact(name):
+    from paper_2501_13382_b200 import kernels
+    b = load_case(name)
+    out = kernels.nearest_batch(b["seg_origin"], b["seg_dir"], b["seg_e1"], b["seg_e2"],
+                                b["seg_len"], b["seg_s0"], b["seg_refl"], b["n_segs"],
+                                b["max_seg"], b["obs"], b["ns_obs"], b["ns_beam"])
+    assert np.array_equal(out[:, 0].astype(np.int64), b["ns_k"])
+    assert np.array_equal(out[:, 5].astype(np.int8), b["ns_behind"])
+    for col, key in ((1, "ns_s"), (2, "ns_q1"), (3, "ns_q2"), (4, "ns_refl")):
+        assert np.array_equal(out[:, col], b[key])
+
+
+@pytest.mark.parametrize("name", ["cfg1_open_plane", "city_street", "city_corner_f5",
+                                  "open_paper_imb"])
+def test_tracer_bitexact_vs_reference(name):
+    """sm_100a tracer == reference trace_into bundle (beamtrace.py:291-306), bit for bit."""
+    import torch
+
+    from paper_2501_13382_b200 import beamtrace, engine, scene
+    z = np.load(f"tests/golden/{name}.npz")
+    b = load_case(name)
+    args = z["scene_args"]
+    sc = (scene.make_ground_plane(float(args[0])) if str(z["scene_kind"]) == "plane" else
+          scene.make_city(int(args[0]), int(args[1]), float(args[2]), float(args[3]),
+                          float(args[4])))
+    src = beamtrace.SourceSpec(position=z["src"], frequencies=tuple(z["freqs"]),
+                               beam_param_im=float(z["im_b"]))
+    grid = beamtrace.LaunchGrid(0.0, 180.0, 0.0, 360.0, int(z["n_theta"]), int(z["n_phi"]))
+    cfg = beamtrace.TraceConfig(int(z["n_steps"]), float(z["dt"]), int(z["r_max"]))
+    launch = beamtrace.launch_directions(grid)
+    dev = torch.device("cuda", 0)
+    out = engine.trace_device_rows(engine.DeviceScene.from_scene(sc, dev), src, launch, cfg,
+                                   float(z["c"]), 0, len(launch), dev)
+    torch.cuda.synchronize()
+    assert np.array_equal(out["n_segs"].cpu().numpy(), b["n_segs"])
+    assert np.array_equal(out["n_refls"].cpu().numpy(), z["n_refls"])
+    for f in ("seg_origin", "seg_dir", "seg_e1", "seg_e2", "seg_len", "seg_s0", "seg_refl"):
+        got = out[f].cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), b[f].view(np.uint64)), f
+
+
+def test_device_path_equals_host_path():
+    import torch
+
+    from paper_2501_13382_b200 import kernels
+    b = load_case("city_street")
+    acc_h, ev_h = run(b, "fp32")
+    dev = torch.device("cuda", 0)
+    t = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa
+    obs = b["obs"]
+    acc = torch.zeros((obs.shape[0], 1), dtype=torch.complex128, device=dev)
+    ev = torch.zeros(obs.shape[0], dtype=torch.int64, device=dev)
+    kernels.gbs_accumulate(t(b["seg_origin"]), t(b["seg_dir"]), t(b["seg_e1"]), t(b["seg_e2"]),
+                           t(b["seg_len"]), t(b["seg_s0"]), t(b["seg_refl"]),
+                           t(b["n_segs"], torch.int32), b["max_seg"], t(b["weights"]), t(obs),
+                           b["omegas"], float(b["c"]), -float(b["beam_param_im"]), 1.0, True,
+                           acc, ev, 0, obs.shape[0], 0, b["n_segs"].shape[0])
+    torch.cuda.synchronize()
+    assert np.array_equal(acc.cpu().numpy(), acc_h)
+    assert np.array_equal(ev.cpu().numpy(), ev_h)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_chunked_and_ranged_calls(precision):
+    """Beam chunks continue acc in place; rows outside [obs_lo, obs_hi) untouched."""
+    b = load_case("city_corner_f5")
+    obs = b["obs"][:1500]
+    nb = b["n_segs"].shape[0]
+    one, ev1 = run(b, precision, obs, [(0, 1500, 0, nb)])
+    many, evm = run(b, precision, obs, [(0, 1500, 0, 700), (0, 1500, 700, 701),
+                                        (0, 1500, 701, nb)])
+    if precision == "fp64":
+        assert np.array_equal(one, many)
+    else:
+        assert rel_l2(many, one) <= 1e-6
+    assert np.array_equal(ev1, evm) or precision == "fp32"
+    part, evp = run(b, precision, obs, [(100, 900, 0, nb)])
+    assert not part[:100].any() and not part[900:].any()
+    assert not evp[:100].any() and not evp[900:].any()
+    assert rel_l2(part[100:900], one[100:900]) <= (0 if precision == "fp64" else 1e-5)
+
+
+def test_edge_cases():
+    from paper_2501_13382_b200 import kernels
+    b = load_case("city_street")
+    obs = b["obs"][:300]
+    nb = b["n_segs"].shape[0]
+    # empty ranges are no-ops
+    acc = np.full((300, 1), 1 + 2j)
+    ev = np.full(300, 5, np.int64)
+    kernels.gbs_accumulate(*gbs_args(b, obs), acc, ev, 10, 10, 0, nb)
+    kernels.gbs_accumulate(*gbs_args(b, obs), acc, ev, 0, 300, 7, 7)
+    assert (acc == 1 + 2j).all() and (ev == 5).all()
+    # beams with n_segs == 0 contribute nothing (kernels.py:369-371)
+    a2 = list(gbs_args(b, obs))
+    ns = b["n_segs"].copy()
+    ns[::3] = 0
+    a2[7] = ns
+    for prec in ("fp64", "fp32"):
+        acc = np.zeros((300, 1), np.complex128)
+        ev = np.zeros(300, np.int64)
+        kernels.gbs_accumulate(*a2, acc, ev, 0, 300, 0, nb, precision=prec)
+        ref = np.zeros_like(acc)
+        rev = np.zeros_like(ev)
+        oracle.gbs_accumulate(*a2, ref, rev, 0, 300, 0, nb)
+        assert rel_l2(acc, ref) <= (FP64_TOL if prec == "fp64" else FP32_L2)
+    # bad arguments raise like the reference's callers would
+    with pytest.raises(ValueError):
+        kernels.gbs_accumulate(*gbs_args(b, obs), np.zeros((300, 1), np.complex128),
+                               np.zeros(300, np.int64), 0, 301, 0, nb)
+    with pytest.raises(TypeError):
+        kernels.gbs_accumulate(*gbs_args(b, obs), np.zeros((300, 1), np.complex64),
+                               np.zeros(300, np.int64), 0, 300, 0, nb)
+
+
+def test_sharded_equals_unsharded_bitexact():
+    """Receiver-tile partition (shard.py) gives identical bits for 1, 2, 3 and 8 ranks."""
+    import torch
+
+    from paper_2501_13382_b200 import engine, shard
+    b = load_case("city_corner_f5")
+    dev = torch.device("cuda", 0)
+    bundle = engine.DeviceBundle.from_host(_pb(b), dev)
+    obs = torch.from_numpy(b["obs"]).to(dev)
+    order = shard.tile_order(obs)
+    n = obs.shape[0]
+    full = {}
+    for world in (1, 2, 3, 8):
+        acc_full = torch.zeros((n, 5), dtype=torch.complex128, device=dev)
+        for r in range(world):
+            idx = shard.rank_indices(order, r, world)
+            o = obs.index_select(0, idx).contiguous()
+            acc = torch.zeros((o.shape[0], 5), dtype=torch.complex128, device=dev)
+            ev = torch.zeros(o.shape[0], dtype=torch.int64, device=dev)
+            engine.accumulate(bundle, o, b["omegas"], -float(b["beam_param_im"]), True, acc, ev,
+                              presorted=True)
+            acc_full[idx] = acc
+        torch.cuda.synchronize()
+        full[world] = acc_full.cpu().numpy()
+    for w in (2, 3, 8):
+        assert np.array_equal(full[w], full[1])
+    assert rel_l2(full[1], b["acc"]) <= FP32_L2
+
+
+def _pb(b):
+    from paper_2501_13382_b200.beamtrace import PathBundle
+    return PathBundle(seg_origin=b["seg_origin"], seg_dir=b["seg_dir"], seg_e1=b["seg_e1"],
+                      seg_e2=b["seg_e2"], seg_len=b["seg_len"], seg_s0=b["seg_s0"],
+                      seg_refl=b["seg_refl"], n_segs=b["n_segs"], n_refls=b["n_refls"],
+                      max_seg=int(b["max_seg"]), weights=b["weights"], gamma1=b["gamma1"],
+                      gamma2=b["gamma2"], c=float(b["c"]),
+                      beam_param_im=float(b["beam_param_im"]),
+                      amplitude_phi=float(b["amplitude_phi"]))
+
+
+def test_chunk_streamer_equals_single_call():
+    """Host-streamed beam chunks (double-buffered pinned copies) == one device call."""
+    import torch
+
+    from paper_2501_13382_b200 import engine
+    b = load_case("city_street")
+    dev = torch.device("cuda", 0)
+    pb = _pb(b)
+    obs = torch.from_numpy(b["obs"]).to(dev)
+    n = obs.shape[0]
+    ref = torch.zeros((n, 1), dtype=torch.complex128, device=dev)
+    rev = torch.zeros(n, dtype=torch.int64, device=dev)
+    engine.accumulate(engine.DeviceBundle.from_host(pb, dev, with_frame=False), obs,
+                      b["omegas"], 10.0, True, ref, rev, precision="fp32")
+    acc = torch.zeros_like(ref)
+    ev = torch.zeros_like(rev)
+    streamer = engine.ChunkStreamer(pb, [700, 700, 648], dev)
+    st = torch.cuda.current_stream(dev)
+
+    def consume(db, nb, lo):
+        engine.accumulate(db, obs, b["omegas"], 10.0, True, acc, ev, beam_hi=nb, stream=st)
+
+    streamer.run(consume, st)
+    torch.cuda.synchronize()
+    assert rel_l2(acc.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
+    assert torch.equal(ev, rev)
+
+
+def test_run_pipeline_city_vs_oracle():
+    """run_pipeline (GPU trace + GPU sum, uncalibrated) vs the oracle on the same bundle."""
+    from paper_2501_13382_b200 import (Atmosphere, ExecPlan, LaunchGrid, ObserverSet,
+                                       SourceSpec, TraceConfig, make_city, parallel)
+    z = np.load("tests/golden/city_street.npz")
+    b = load_case("city_street")
+    sc = make_city(5, 10, 40.0, 20.0, 300.0)
+    src = SourceSpec(position=z["src"], frequencies=(125.0,), beam_param_im=-10.0)
+    res, t = parallel.run_pipeline(sc, src, LaunchGrid(n_theta=32, n_phi=64),
+                                   TraceConfig(5000, 1e-4, 8), ObserverSet(b["obs"]),
+                                   ExecPlan(memory_budget=700 * 1080, per_ray_bytes=1080),
+                                   Atmosphere(20.0), calibration=1.0)
+    assert rel_l2(res.pressure, b["acc"]) <= FP32_L2
+    assert tl_db(res.pressure, b["acc"], -60.0) <= FP32_TL_DB
+    assert t.gbs_seconds > 0 and t.rt_seconds > 0
+    assert abs(t.gbs_evaluations - int(b["evals"].sum())) <= 1e-4 * b["evals"].sum() + 10
+
+
+def test_calibrate_phi_vs_reference():
+    from paper_2501_13382_b200 import Atmosphere, SourceSpec, gbs
+    z = np.load("tests/golden/calibration_origin.npz")
+    b = oracle.load_bundle("tests/golden/calibration_origin.npz")
+    pb = _pb(dict(b, gamma1=np.zeros(len(b["n_segs"])), gamma2=np.zeros(len(b["n_segs"])),
+                  n_refls=b["n_refls"]))
+    src = SourceSpec(position=np.zeros(3), frequencies=(500.0,), beam_param_im=-12.0)
+    for prec, tol in (("fp64", 1e-12), ("fp32", 1e-5)):
+        scale = gbs.calibrate_phi(pb, Atmosphere(20.0), src, precision=prec)
+        assert abs(scale / float(z["scale"]) - 1) <= tol
+        p = gbs.sum_at_observer(z["probe"], pb, src.omegas[0], Atmosphere(20.0), src,
+                                precision=prec)
+        assert abs(p - complex(z["probe_p"])) <= tol * abs(complex(z["probe_p"]))
