@@ -46,6 +46,11 @@ CONFIGS = {
                  scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0), src=(20.0, 0.0, 2.0),
                  freqs=(125.0,), im_b=-10.0, n_theta=500, n_phi=1000, n_steps=5000, r_max=8,
                  grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
+    # profiling variant of config 3: same scene/receivers, 20k rays (ncu replays stay short)
+    "cfg3s": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers (cfg3 profile "
+                       "variant)", scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0),
+                  src=(20.0, 0.0, 2.0), freqs=(125.0,), im_b=-10.0, n_theta=100, n_phi=200,
+                  n_steps=5000, r_max=8, grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
 }
 
 

@@ -267,7 +267,9 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
     } else {
         BF_TRY(morton_order(c, obs, n, st, &perm));
     }
-    if (T == 256)
+    if (T == 512)
+        tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm, rloc, cen);
+    else if (T == 256)
         tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm, rloc, cen);
     else
         return fail(BF_EINVAL, "unsupported tile size %d", T);

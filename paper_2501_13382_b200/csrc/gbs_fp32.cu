@@ -2,30 +2,36 @@
 //
 // Operator: kernels.gbs_accumulate (kernels.py:352-399) with its helper
 // nearest_on_segments (kernels.py:304-349), re-designed for the B200 FP32/MUFU
-// pipes:
+// pipes.  DESIGN.md holds the error analysis behind every tolerance here.
 //
-//  * One CTA owns a tile of TILE receivers that are spatially compact (Morton
-//    order, engine.cu).  Receivers are held in TILE-LOCAL fp32 coordinates
-//    r = p - c_T, so fp32 rounding never sees the ~100 m absolute coordinates.
+//  * One CTA owns a tile of TILE = THREADS x R receivers, spatially compact
+//    (Morton order, engine.cu); thread t holds receivers R*t..R*t+R-1, so a
+//    warp covers 128 consecutive Morton receivers (a compact patch).
+//    Receivers are held in TILE-LOCAL fp32 coordinates r = p - c_T.
 //  * Beams stream through shared memory in chunks (<= CB beams, <= ROWCAP
 //    segment rows).  Staging converts each segment once per tile, in fp64, to
-//    tile-local fp32 geometry (wc = c_T - o, d, len, centre projection) plus
-//    fp64-exact phase anchors frac(omega/(2 pi c) * s) at the three places the
-//    nearest point can sit (segment start, tile-centre projection, segment
-//    end).  The per-pair axial phase is anchor + kappa * (r . d) with |r| of a
-//    few metres, i.e. fp64-quality where the reference's omega*s/c reaches
-//    ~1e3 rad.
-//  * Per pair: fp32 nearest-segment scan (strict <, first wins), carrying the
-//    best and second-best clamped distance.  If the two are closer than a
-//    rigorous fp32 error bound, or the behind test (k==0, proj<0) is within
-//    its error bound of 0, the pair is RE-DECIDED in fp64 with the reference
-//    operation order and no FMA (__dadd_rn/__dmul_rn) -- corner ties at every
-//    reflection point are exact mathematical ties that the reference breaks
-//    by fp64 rounding, so only its exact arithmetic reproduces its choice.
-//  * Gaussian contribution in fp32 with MUFU ex2 / sin / cos / rcp, partial
-//    sums in fp32 per chunk, flushed into per-receiver fp64 accumulators that
-//    start from the caller's acc (in-place continuation, kernels.py:358-359).
-//    Beams are visited in ascending index order for every receiver.
+//    tile-local fp32 geometry (wc = c_T - o, d, len, centre projection Pc),
+//    the cutoff radius of the segment, fp64-exact phase anchors
+//    frac(omega/(2 pi c) * s) at the segment start / tile-centre projection /
+//    end, and keeps the fp64 row for exact re-decisions.
+//  * Per (warp, beam) a lane-parallel prepass (one lane per segment) bounds
+//    the warp patch against every segment: if every segment is provably cut
+//    (q_perp - R_W > R_cut) or, for segment 0, entirely behind the source,
+//    the beam is skipped for the warp; segments whose distance to the patch
+//    exceeds the nearest one by more than the patch diameter can never be
+//    the nearest point and are pruned.  Usually ONE segment survives and the
+//    pair needs no nearest-segment scan at all.
+//  * Several survivors: fp32 scan (strict <, first wins) carrying best and
+//    second-best clamped distance.  If the two are within the fp32 error
+//    bound -- corner ties at every reflection point are exact mathematical
+//    ties that the reference breaks by fp64 rounding -- the contenders are
+//    re-decided in fp64 with the reference operation order and no FMA.  The
+//    behind test (k==0, proj<0) is re-decided in fp64 the same way when
+//    |proj| is within its error bound.
+//  * Gaussian contribution in fp32 with MUFU ex2 / sin / cos / rcp, fp32
+//    partial sums per chunk flushed into per-receiver fp64 accumulators (in
+//    shared memory) that start from the caller's acc (in-place continuation,
+//    kernels.py:358-359).  Beams are visited in ascending order per receiver.
 #include <math.h>
 
 #include "common.cuh"
@@ -33,17 +39,25 @@
 namespace bf {
 namespace {
 
-constexpr int TILE = 256;    // receivers per CTA, one per thread
-constexpr int CB = 64;       // max beams per staged chunk
-constexpr int ROWCAP = 256;  // max segment rows per staged chunk
+constexpr int THREADS = 128;
+constexpr int R = 4;                    // receivers per thread
+constexpr int TILE = THREADS * R;       // receivers per CTA
+constexpr int CB = 64;                  // max beams per staged chunk
+constexpr int ROWCAP = 256;             // max segment rows per staged chunk
+constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
+constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
+constexpr float PROJ_ERR = 3.814697265625e-06f;     // 2^-18 (x D): bound on |fp32 proj error|
 
 struct Fp32Consts {
     float kappa[BF_MAXF];    // omega/(2 pi c), turns per metre
     double kappa64[BF_MAXF];
     float hk[BF_MAXF];       // omega*0.5/c: g = hk*q^2/m2 (kernels.py:382)
     float omega[BF_MAXF];
+    float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36)
     float b, b2;             // width_b, width_b^2
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
+    double rcut_scale;       // 72 c / (omega_min b): R_cut^2 = rcut_scale * (s_end^2 + b^2)
+    double b2_64;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -56,273 +70,420 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float sin_approx(float x) {
+    float y;
+    asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float cos_approx(float x) {
+    float y;
+    asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ double frac_turns(double x) { return x - rint(x); }
 
-// Exact fp64 nearest-segment decision (kernels.py:320-348) for one pair,
-// reference operation order, no FMA.  Returns k (or -1), and t, proj, plus the
-// perpendicular q^2 of the winner.
-struct Exact {
-    int k;
-    double t, proj, q2;
+// fp64 row staged for exact re-decisions (reference operation order).
+struct Row64 {
+    double ox, oy, oz, dx, dy, dz, len;
 };
-__device__ __noinline__ Exact nearest_exact64(const double *__restrict__ seg_origin,
-                                              const double *__restrict__ seg_dir,
-                                              const double *__restrict__ seg_len, int64_t base,
-                                              int ns, double px, double py, double pz) {
-    double best = INFINITY;
-    Exact r{-1, 0.0, 0.0, 0.0};
-    double bwx = 0, bwy = 0, bwz = 0, bdx = 0, bdy = 0, bdz = 0;
-    for (int k = 0; k < ns; ++k) {
-        const int64_t row = base + k;
-        const double ox = seg_origin[3 * row], oy = seg_origin[3 * row + 1],
-                     oz = seg_origin[3 * row + 2];
-        const double dx = seg_dir[3 * row], dy = seg_dir[3 * row + 1], dz = seg_dir[3 * row + 2];
-        const double wx = __dsub_rn(px, ox), wy = __dsub_rn(py, oy), wz = __dsub_rn(pz, oz);
-        const double proj =
-            __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
-        double t = proj;
-        const double len = seg_len[row];
-        if (t < 0.0)
-            t = 0.0;
-        else if (t > len)
-            t = len;
-        const double vx = __dsub_rn(wx, __dmul_rn(t, dx));
-        const double vy = __dsub_rn(wy, __dmul_rn(t, dy));
-        const double vz = __dsub_rn(wz, __dmul_rn(t, dz));
-        const double d2 =
-            __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-        if (d2 < best) {
-            best = d2;
-            r.k = k;
-            r.t = t;
-            r.proj = proj;
-            bwx = wx; bwy = wy; bwz = wz;
-            bdx = dx; bdy = dy; bdz = dz;
-        }
-    }
-    const double ux = bwx - r.proj * bdx, uy = bwy - r.proj * bdy, uz = bwz - r.proj * bdz;
-    r.q2 = ux * ux + uy * uy + uz * uz;
-    return r;
+
+// Exact fp64 clamped distance of kernels.py:328-340, no FMA.
+__device__ __forceinline__ double exact_d2(const Row64 &g, double px, double py, double pz,
+                                           double *proj_out, double *t_out) {
+    const double wx = __dsub_rn(px, g.ox), wy = __dsub_rn(py, g.oy), wz = __dsub_rn(pz, g.oz);
+    const double proj =
+        __dadd_rn(__dadd_rn(__dmul_rn(wx, g.dx), __dmul_rn(wy, g.dy)), __dmul_rn(wz, g.dz));
+    double t = proj;
+    if (t < 0.0)
+        t = 0.0;
+    else if (t > g.len)
+        t = g.len;
+    const double vx = __dsub_rn(wx, __dmul_rn(t, g.dx));
+    const double vy = __dsub_rn(wy, __dmul_rn(t, g.dy));
+    const double vz = __dsub_rn(wz, __dmul_rn(t, g.dz));
+    *proj_out = proj;
+    *t_out = t;
+    return __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
 }
 
 template <int NF>
-__global__ void __launch_bounds__(TILE, 2)
+struct Smem {
+    float4 geo0[ROWCAP];     // wc.xyz (c_T - o), len
+    float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_T)
+    float4 aux[ROWCAP];      // s0, A (amplitude factor), R_cut, D (error scale)
+    float anc[3 * NF][ROWCAP];  // phase anchors: centre proj / start / end (turns)
+    Row64 r64[ROWCAP];
+    int2 bhdr[CB];           // (first row, n_segs) of chunk beam j
+    float btie[CB];          // absolute tie tolerance of the beam
+    int brow[CB + 1];
+    int nbc;
+    double acc[TILE][NF][2];
+};
+
+// Gaussian-beam contribution of one pair, all frequencies (kernels.py:377-399).
+template <int NF>
+__device__ __forceinline__ void contribute(const Fp32Consts &K, int use_cutoff, float s, float q2,
+                                           float A, const float *base, float (&pre)[NF],
+                                           float (&pim)[NF], int &ev) {
+    const float m2 = fmaf(s, s, K.b2);
+    const float inv = rcp_approx(m2);
+    const float gq = q2 * inv;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        if (use_cutoff && q2 * K.cutk[f] > m2) continue;  // ex_re < -36 (kernels.py:384)
+        const float g = K.hk[f] * gq;
+        float turns = fmaf(g * s, 0.15915494309189535f, base[f]);
+        turns -= rintf(turns);
+        const float ph = turns * 6.283185307179586f;
+        const float sn = sin_approx(ph), cs = cos_approx(ph);
+        const float er = ex2_approx(g * (-K.b * 1.4426950408889634f));
+        const float amp = A * K.omega[f] * er * inv;
+        pre[f] = fmaf(-amp, fmaf(s, sn, K.b * cs), pre[f]);
+        pim[f] = fmaf(amp, fmaf(s, cs, -K.b * sn), pim[f]);
+        ++ev;
+    }
+}
+
+template <int NF>
+__global__ void __launch_bounds__(THREADS, 4)
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const int32_t *__restrict__ seg_start,
                     const Fp32Consts K, GbsStats *stats) {
-    __shared__ float4 s_g0[ROWCAP];  // wc (= c_T - o), len
-    __shared__ float4 s_g1[ROWCAP];  // d, centre projection Pc
-    __shared__ float2 s_g2[ROWCAP];  // s0, amplitude factor A
-    __shared__ float s_anc[3 * NF][ROWCAP];  // frac(kappa*s) at centre proj / start / end
-    __shared__ int s_brow[CB + 1];
-    __shared__ float s_bE[CB];
-    __shared__ int s_nbc;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<NF> &S = *reinterpret_cast<Smem<NF> *>(smem_raw);
 
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
     const int64_t tile = blockIdx.x;
-    const int64_t si = tile * TILE + tid;
-    const bool valid = si < tl.n;
     const double4 cen = tl.centre[tile];
     const float RT = (float)cen.w;
 
-    int oi = 0;
-    float rx = 0.f, ry = 0.f, rz = 0.f;
-    if (valid) {
-        oi = tl.perm[si];
-        const float4 rl = tl.rloc[si];
-        rx = rl.x;
-        ry = rl.y;
-        rz = rl.z;
-    }
-    double acc_re[NF], acc_im[NF];
-    float par_re[NF], par_im[NF];
+    // ---- receivers of this thread (tile-local coordinates)
+    float rx[R], ry[R], rz[R];
+    int oi[R];
+    bool valid[R];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
-        acc_re[f] = valid ? a.acc[2 * ((int64_t)oi * NF + f)] : 0.0;
-        acc_im[f] = valid ? a.acc[2 * ((int64_t)oi * NF + f) + 1] : 0.0;
-        par_re[f] = 0.f;
-        par_im[f] = 0.f;
+    for (int j = 0; j < R; ++j) {
+        const int64_t si = tile * TILE + R * tid + j;
+        valid[j] = si < tl.n;
+        oi[j] = 0;
+        rx[j] = ry[j] = rz[j] = 0.f;
+        if (valid[j]) {
+            oi[j] = tl.perm[si];
+            const float4 rl = tl.rloc[si];
+            rx[j] = rl.x;
+            ry[j] = rl.y;
+            rz[j] = rl.z;
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            S.acc[R * tid + j][f][0] = valid[j] ? a.acc[2 * ((int64_t)oi[j] * NF + f)] : 0.0;
+            S.acc[R * tid + j][f][1] = valid[j] ? a.acc[2 * ((int64_t)oi[j] * NF + f) + 1] : 0.0;
+        }
     }
-    int ev = 0;
-    int ties = 0;
-    int nbp = 0;
-    const int32_t seg_base0 = seg_start[0];
+    // ---- warp patch: bounding sphere of the warp's receivers
+    float cwx, cwy, cwz, RW;
+    {
+        float mnx = INFINITY, mny = INFINITY, mnz = INFINITY;
+        float mxx = -INFINITY, mxy = -INFINITY, mxz = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+            if (valid[j]) {
+                mnx = fminf(mnx, rx[j]); mxx = fmaxf(mxx, rx[j]);
+                mny = fminf(mny, ry[j]); mxy = fmaxf(mxy, ry[j]);
+                mnz = fminf(mnz, rz[j]); mxz = fmaxf(mxz, rz[j]);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+            mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+            mnz = fminf(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
+            mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+            mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+            mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+        }
+        if (mnx > mxx) mnx = mxx = mny = mxy = mnz = mxz = 0.f;  // warp without receivers
+        cwx = 0.5f * (mnx + mxx);
+        cwy = 0.5f * (mny + mxy);
+        cwz = 0.5f * (mnz + mxz);
+        float rr = 0.f;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+            if (valid[j]) {
+                const float ex = rx[j] - cwx, ey = ry[j] - cwy, ez = rz[j] - cwz;
+                rr = fmaxf(rr, ex * ex + ey * ey + ez * ez);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rr = fmaxf(rr, __shfl_xor_sync(0xffffffffu, rr, o));
+        RW = sqrtf(rr) * 1.0001f + 1e-4f;
+    }
+
+    float pre[R][NF], pim[R][NF];
+    int evr[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        evr[j] = 0;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
+    }
+    int ties = 0, nbp = 0;
 
     for (int64_t b0 = 0; b0 < a.n_beams;) {
-        // ---- choose the chunk [b0, b0+nbc): <= CB beams and <= ROWCAP rows
+        // ---- chunk [b0, b0+nbc): <= CB beams and <= ROWCAP rows
         if (tid == 0) {
             int64_t hi = b0 + CB < a.n_beams ? b0 + CB : a.n_beams;
             const int32_t r0 = seg_start[b0];
-            while (seg_start[hi] - r0 > ROWCAP) --hi;  // at most CB steps, S <= ROWCAP
-            s_nbc = (int)(hi - b0);
+            while (seg_start[hi] - r0 > ROWCAP) --hi;
+            S.nbc = (int)(hi - b0);
         }
         __syncthreads();
-        const int nbc = s_nbc;
-        for (int j = tid; j <= nbc; j += TILE) s_brow[j] = seg_start[b0 + j] - seg_start[b0];
+        const int nbc = S.nbc;
+        for (int j = tid; j <= nbc; j += THREADS) S.brow[j] = seg_start[b0 + j] - seg_start[b0];
         __syncthreads();
-        const int rows = s_brow[nbc];
+        const int rows = S.brow[nbc];
         // ---- stage: one thread per segment row, fp64 -> tile-local fp32
-        for (int r = tid; r < rows; r += TILE) {
-            int lo = 0, hi = nbc;  // s_brow[lo] <= r < s_brow[hi]
+        for (int r = tid; r < rows; r += THREADS) {
+            int lo = 0, hi = nbc;
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
-                if (s_brow[mid] <= r) lo = mid; else hi = mid;
+                if (S.brow[mid] <= r) lo = mid; else hi = mid;
             }
             const int jb = lo;
-            const int k = r - s_brow[jb];
+            const int k = r - S.brow[jb];
             const int64_t row = (b0 + jb) * a.max_seg + k;
-            const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
-                         oz = a.seg_origin[3 * row + 2];
-            const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
-                         dz = a.seg_dir[3 * row + 2];
-            const double len = a.seg_len[row], s0 = a.seg_s0[row];
-            const double wcx = cen.x - ox, wcy = cen.y - oy, wcz = cen.z - oz;
-            const double pc = wcx * dx + wcy * dy + wcz * dz;
-            s_g0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)len);
-            s_g1[r] = make_float4((float)dx, (float)dy, (float)dz, (float)pc);
+            Row64 g;
+            g.ox = a.seg_origin[3 * row];
+            g.oy = a.seg_origin[3 * row + 1];
+            g.oz = a.seg_origin[3 * row + 2];
+            g.dx = a.seg_dir[3 * row];
+            g.dy = a.seg_dir[3 * row + 1];
+            g.dz = a.seg_dir[3 * row + 2];
+            g.len = a.seg_len[row];
+            S.r64[r] = g;
+            const double s0 = a.seg_s0[row];
+            const double wcx = cen.x - g.ox, wcy = cen.y - g.oy, wcz = cen.z - g.oz;
+            const double pc = wcx * g.dx + wcy * g.dy + wcz * g.dz;
+            S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)g.len);
+            S.geo1[r] = make_float4((float)g.dx, (float)g.dy, (float)g.dz, (float)pc);
+            const double se = s0 + g.len;
+            const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
             const double A = K.amp_scale * a.seg_refl[row] * a.weights[b0 + jb];
-            s_g2[r] = make_float2((float)s0, (float)A);
+            const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + g.len) + RT + 1.f;
+            S.aux[r] = make_float4((float)s0, (float)A, (float)rcut, D);
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                s_anc[3 * f + 0][r] = (float)frac_turns(K.kappa64[f] * (s0 + pc));
-                s_anc[3 * f + 1][r] = (float)frac_turns(K.kappa64[f] * s0);
-                s_anc[3 * f + 2][r] = (float)frac_turns(K.kappa64[f] * (s0 + len));
+                S.anc[3 * f + 0][r] = (float)frac_turns(K.kappa64[f] * (s0 + pc));
+                S.anc[3 * f + 1][r] = (float)frac_turns(K.kappa64[f] * s0);
+                S.anc[3 * f + 2][r] = (float)frac_turns(K.kappa64[f] * se);
             }
         }
         __syncthreads();
-        // Per-beam bound on the fp32 error of any |w - t d|:
-        // |dv| <= 2^-18 (R_T + |wc| + len), max over the beam's segments.
-        for (int j = tid; j < nbc; j += TILE) {
-            float e = 0.f;
-            for (int r = s_brow[j]; r < s_brow[j + 1]; ++r) {
-                const float4 g = s_g0[r];
-                const float m = fabsf(g.x) + fabsf(g.y) + fabsf(g.z) + g.w + RT + 1e-3f;
-                e = fmaxf(e, m);
-            }
-            s_bE[j] = e * 3.814697265625e-06f;  // 2^-18
+        for (int j = tid; j < nbc; j += THREADS) {
+            float D = 0.f;
+            for (int r = S.brow[j]; r < S.brow[j + 1]; ++r) D = fmaxf(D, S.aux[r].w);
+            S.bhdr[j] = make_int2(S.brow[j], S.brow[j + 1] - S.brow[j]);
+            S.btie[j] = TIE_ABS * D * D;
         }
         __syncthreads();
 
         // ---- summation over the chunk's beams, ascending
-        if (valid) {
-            for (int jb = 0; jb < nbc; ++jb) {
-                const int r0 = s_brow[jb];
-                const int ns = s_brow[jb + 1] - r0;
-                if (ns == 0) continue;
-                float best = INFINITY, second = INFINITY;
-                int kb = 0;
-                for (int k = 0; k < ns; ++k) {
-                    const float4 g0 = s_g0[r0 + k];
-                    const float4 g1 = s_g1[r0 + k];
-                    const float wx = rx + g0.x, wy = ry + g0.y, wz = rz + g0.z;
-                    const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+        for (int jb = 0; jb < nbc; ++jb) {
+            const int2 h = S.bhdr[jb];
+            const int r0 = h.x, ns = h.y;
+            if (ns == 0) continue;
+            // lane-parallel prepass: one lane per segment vs the warp patch
+            float dc = INFINITY;
+            bool dead = true;
+            if (lane < ns) {
+                const float4 g0 = S.geo0[r0 + lane];
+                const float4 g1 = S.geo1[r0 + lane];
+                const float rcut = S.aux[r0 + lane].z;
+                const float wx = cwx + g0.x, wy = cwy + g0.y, wz = cwz + g0.z;
+                const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+                const float t = fminf(fmaxf(proj, 0.f), g0.w);
+                const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
+                dc = sqrtf(vx * vx + vy * vy + vz * vz);
+                const float ux = wx - proj * g1.x, uy = wy - proj * g1.y, uz = wz - proj * g1.z;
+                const float qp = sqrtf(ux * ux + uy * uy + uz * uz);
+                dead = qp > (rcut + RW) * 1.00001f + 1e-3f;
+                if (lane == 0) dead = dead || (proj + RW * 1.00001f + 1e-3f < 0.f);
+            }
+            if (__all_sync(0xffffffffu, dead)) continue;  // every pair of the patch is cut/behind
+            float dmin = dc;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+            const unsigned surv = __ballot_sync(
+                0xffffffffu, lane < ns && dc <= (dmin + 2.f * RW) * 1.00001f + 2e-3f);
+            const float tie_abs = S.btie[jb];
+            if ((surv & (surv - 1)) == 0) {
+                // ---- single surviving segment: it is the nearest for every receiver
+                const int k = __ffs(surv) - 1;
+                const int row = r0 + k;
+                const float4 g0 = S.geo0[row];
+                const float4 g1 = S.geo1[row];
+                const float4 ax = S.aux[row];
+                float anc[3 * NF];
+#pragma unroll
+                for (int q = 0; q < 3 * NF; ++q) anc[q] = S.anc[q][row];
+                const float tolp = PROJ_ERR * ax.w;
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    if (!valid[j]) continue;
+                    const float dl = rx[j] * g1.x + ry[j] * g1.y + rz[j] * g1.z;
+                    const float proj = dl + g1.w;
+                    if (k == 0 && proj < tolp) {
+                        if (proj < -tolp) continue;  // behind the source (kernels.py:348,375)
+                        const Row64 g = S.r64[row];
+                        const int64_t gi = 3 * (int64_t)oi[j];
+                        double p64, t64;
+                        exact_d2(g, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
+                        ++ties;
+                        if (p64 < 0.0) continue;
+                    }
                     const float t = fminf(fmaxf(proj, 0.f), g0.w);
-                    const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
-                    const float d2 = vx * vx + vy * vy + vz * vz;
-                    second = fminf(second, fmaxf(best, d2));
-                    kb = (d2 < best) ? k : kb;
-                    best = fminf(best, d2);
-                }
-                const float E = s_bE[jb];
-                bool need64 = false;
-                if (ns > 1) {
-                    const float tol = 4.f * sqrtf(second) * E + 2.f * E * E + 1e-6f * second;
-                    need64 = (second - best) <= tol;
-                }
-                float4 g0 = s_g0[r0 + kb];
-                float4 g1 = s_g1[r0 + kb];
-                float wx = rx + g0.x, wy = ry + g0.y, wz = rz + g0.z;
-                float proj = wx * g1.x + wy * g1.y + wz * g1.z;
-                if (kb == 0 && fabsf(proj) <= 4.f * E) need64 = true;
-                float s, q2;
-                int mode;  // 0: interior, 1: clamped at start, 2: clamped at end, 3: fp64 s
-                double s64 = 0.0;
-                int kw = kb;
-                float delta = 0.f;
-                if (!need64) {
-                    if (kb == 0 && proj < 0.f) continue;  // behind the source
-                    const float len = g0.w;
-                    const float t = fminf(fmaxf(proj, 0.f), len);
-                    s = s_g2[r0 + kb].x + t;
+                    const float s = ax.x + t;
+                    const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
                     const float ux = wx - proj * g1.x, uy = wy - proj * g1.y,
                                 uz = wz - proj * g1.z;
-                    q2 = ux * ux + uy * uy + uz * uz;
-                    if (proj <= 0.f) {
-                        mode = 1;
-                    } else if (proj >= len) {
-                        mode = 2;
-                    } else {
-                        mode = 0;
-                        delta = rx * g1.x + ry * g1.y + rz * g1.z;
+                    const float q2 = ux * ux + uy * uy + uz * uz;
+                    float base[NF];
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        base[f] = proj <= 0.f ? anc[3 * f + 1]
+                                              : (proj >= g0.w ? anc[3 * f + 2]
+                                                              : fmaf(K.kappa[f], dl, anc[3 * f]));
+                    ++nbp;
+                    contribute<NF>(K, a.use_cutoff, s, q2, ax.y, base, pre[j], pim[j], evr[j]);
+                }
+            } else {
+                // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
+                float best[R], second[R];
+                int kb[R];
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    best[j] = INFINITY;
+                    second[j] = INFINITY;
+                    kb[j] = 0;
+                }
+                for (unsigned m = surv; m; m &= m - 1) {
+                    const int k = __ffs(m) - 1;
+                    const float4 g0 = S.geo0[r0 + k];
+                    const float4 g1 = S.geo1[r0 + k];
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
+                        const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+                        const float t = fminf(fmaxf(proj, 0.f), g0.w);
+                        const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
+                        const float d2 = vx * vx + vy * vy + vz * vz;
+                        second[j] = fminf(second[j], fmaxf(best[j], d2));
+                        kb[j] = d2 < best[j] ? k : kb[j];
+                        best[j] = fminf(best[j], d2);
                     }
-                } else {
-                    ++ties;
-                    const int64_t gi = 3 * (int64_t)oi;
-                    const Exact ex = nearest_exact64(a.seg_origin, a.seg_dir, a.seg_len,
-                                                     (b0 + jb) * a.max_seg, ns, a.obs[gi],
-                                                     a.obs[gi + 1], a.obs[gi + 2]);
-                    if (ex.k == 0 && ex.t == 0.0 && ex.proj < 0.0) continue;  // behind
-                    kw = ex.k;
-                    const int64_t row = (b0 + jb) * a.max_seg + kw;
-                    s64 = a.seg_s0[row] + ex.t;
-                    s = (float)s64;
-                    q2 = (float)ex.q2;
-                    mode = 3;
                 }
-                ++nbp;
-                const float A = s_g2[r0 + kw].y;
-                const float m2 = fmaf(s, s, K.b2);
-                const float inv = rcp_approx(m2);
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    const float g = K.hk[f] * q2 * inv;
-                    const float ex_re = -g * K.b;
-                    if (a.use_cutoff && ex_re < (float)BF_CUTOFF_EXPONENT) continue;
-                    float base;
-                    if (mode == 3)
-                        base = (float)frac_turns(K.kappa64[f] * s64);
-                    else if (mode == 0)
-                        base = fmaf(K.kappa[f], delta, s_anc[3 * f + 0][r0 + kw]);
-                    else
-                        base = s_anc[3 * f + mode][r0 + kw];
-                    float turns = fmaf(g * s, 0.15915494309189535f, base);
-                    turns -= rintf(turns);
-                    float sn, cs;
-                    __sincosf(turns * 6.283185307179586f, &sn, &cs);
-                    const float er = ex2_approx(ex_re * 1.4426950408889634f);
-                    const float amp = A * K.omega[f] * er * inv;
-                    par_re[f] = fmaf(-amp, fmaf(s, sn, K.b * cs), par_re[f]);
-                    par_im[f] = fmaf(amp, fmaf(s, cs, -K.b * sn), par_im[f]);
-                    ++ev;
+                for (int j = 0; j < R; ++j) {
+                    if (!valid[j]) continue;
+                    const int k = kb[j];
+                    bool exact = second[j] - best[j] <= fmaf(TIE_REL, second[j], tie_abs);
+                    const float4 g0 = S.geo0[r0 + k];
+                    const float4 g1 = S.geo1[r0 + k];
+                    const float4 ax = S.aux[r0 + k];
+                    const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
+                    const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+                    if (k == 0 && fabsf(proj) <= PROJ_ERR * ax.w) exact = true;
+                    float s, q2, A, base[NF];
+                    if (!exact) {
+                        if (k == 0 && proj < 0.f) continue;  // behind the source
+                        const float t = fminf(fmaxf(proj, 0.f), g0.w);
+                        s = ax.x + t;
+                        A = ax.y;
+                        const float ux = wx - proj * g1.x, uy = wy - proj * g1.y,
+                                    uz = wz - proj * g1.z;
+                        q2 = ux * ux + uy * uy + uz * uz;
+                        const float dl = rx[j] * g1.x + ry[j] * g1.y + rz[j] * g1.z;
+#pragma unroll
+                        for (int f = 0; f < NF; ++f)
+                            base[f] = proj <= 0.f ? S.anc[3 * f + 1][r0 + k]
+                                                  : (proj >= g0.w ? S.anc[3 * f + 2][r0 + k]
+                                                                  : fmaf(K.kappa[f], dl, S.anc[3 * f][r0 + k]));
+                    } else {
+                        // exact re-decision among the contenders, ascending k, strict <
+                        ++ties;
+                        const int64_t gi = 3 * (int64_t)oi[j];
+                        const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
+                        double bd = INFINITY, bt = 0.0, bp = 0.0;
+                        int bk = -1;
+                        for (unsigned m = surv; m; m &= m - 1) {
+                            const int kk = __ffs(m) - 1;
+                            // a segment can beat the fp32 winner only within the error bound
+                            const float4 h0 = S.geo0[r0 + kk];
+                            const float4 h1 = S.geo1[r0 + kk];
+                            const float vx0 = rx[j] + h0.x, vy0 = ry[j] + h0.y, vz0 = rz[j] + h0.z;
+                            const float pj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
+                            const float tt = fminf(fmaxf(pj, 0.f), h0.w);
+                            const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y,
+                                        ez = vz0 - tt * h1.z;
+                            const float d2k = ex * ex + ey * ey + ez * ez;
+                            if (kk != k && fmaf(-TIE_REL, d2k, d2k - best[j]) > tie_abs) continue;
+                            double p64, t64;
+                            const double d2 = exact_d2(S.r64[r0 + kk], px, py, pz, &p64, &t64);
+                            if (d2 < bd) {
+                                bd = d2;
+                                bk = kk;
+                                bt = t64;
+                                bp = p64;
+                            }
+                        }
+                        if (bk == 0 && bt == 0.0 && bp < 0.0) continue;  // behind
+                        const int64_t grow = (b0 + jb) * a.max_seg + bk;
+                        const double s_ref = a.seg_s0[grow] + bt;  // reference s (kernels.py:344)
+                        s = (float)s_ref;
+                        const float4 h0 = S.geo0[r0 + bk];
+                        const float4 h1 = S.geo1[r0 + bk];
+                        A = S.aux[r0 + bk].y;
+                        const float vx0 = rx[j] + h0.x, vy0 = ry[j] + h0.y, vz0 = rz[j] + h0.z;
+                        const float pj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
+                        const float ux = vx0 - pj * h1.x, uy = vy0 - pj * h1.y,
+                                    uz = vz0 - pj * h1.z;
+                        q2 = ux * ux + uy * uy + uz * uz;
+#pragma unroll
+                        for (int f = 0; f < NF; ++f) base[f] = (float)frac_turns(K.kappa64[f] * s_ref);
+                    }
+                    ++nbp;
+                    contribute<NF>(K, a.use_cutoff, s, q2, A, base, pre[j], pim[j], evr[j]);
                 }
-            }
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-                acc_re[f] += (double)par_re[f];
-                acc_im[f] += (double)par_im[f];
-                par_re[f] = 0.f;
-                par_im[f] = 0.f;
             }
         }
+        // flush fp32 partial sums into the fp64 accumulators
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                S.acc[R * tid + j][f][0] += (double)pre[j][f];
+                S.acc[R * tid + j][f][1] += (double)pim[j][f];
+                pre[j][f] = pim[j][f] = 0.f;
+            }
         __syncthreads();
         b0 += nbc;
     }
-    (void)seg_base0;
-    if (valid) {
+    // ---- write back (in-place continuation) and evaluation counts (kernels.py:399)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (!valid[j]) continue;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-            a.acc[2 * ((int64_t)oi * NF + f)] = acc_re[f];
-            a.acc[2 * ((int64_t)oi * NF + f) + 1] = acc_im[f];
+            a.acc[2 * ((int64_t)oi[j] * NF + f)] = S.acc[R * tid + j][f][0];
+            a.acc[2 * ((int64_t)oi[j] * NF + f) + 1] = S.acc[R * tid + j][f][1];
         }
-        a.evals[oi] += ev;
+        a.evals[oi[j]] += evr[j];
     }
-    // Work-list statistics: tie re-decisions, non-behind pairs (warp-aggregated atomics).
     unsigned long long t = (unsigned long long)ties, q = (unsigned long long)nbp;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         t += __shfl_xor_sync(0xffffffffu, t, o);
         q += __shfl_xor_sync(0xffffffffu, q, o);
     }
-    if ((tid & 31) == 0) {
+    if (lane == 0) {
         if (t) atomicAdd(&stats->tie_pairs, t);
         if (q) atomicAdd(&stats->nb_pairs, q);
     }
@@ -331,7 +492,10 @@ __global__ void __launch_bounds__(TILE, 2)
 template <int NF>
 int launch_nf(const GbsArgs &a, const Tiling &t, const int32_t *seg_start, const Fp32Consts &K,
               GbsStats *stats, cudaStream_t st) {
-    gbs_fp32_kernel<NF><<<(unsigned)t.n_tiles, TILE, 0, st>>>(a, t, seg_start, K, stats);
+    const size_t smem = sizeof(Smem<NF>);
+    BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    gbs_fp32_kernel<NF><<<(unsigned)t.n_tiles, THREADS, smem, st>>>(a, t, seg_start, K, stats);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
@@ -344,19 +508,26 @@ int gbs_fp32_tile() { return TILE; }
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
                     GbsStats *d_stats, cudaStream_t st) {
     if (t.n <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
-    if (a.max_seg > ROWCAP) return fail(BF_EINVAL, "max_seg %lld exceeds %d", (long long)a.max_seg, ROWCAP);
+    if (a.max_seg > 32)
+        return fail(BF_EINVAL, "max_seg %lld exceeds 32 (r_max <= 31)", (long long)a.max_seg);
     Fp32Consts K;
     const double two_pi = 2.0 * 3.141592653589793;
+    double wmin = INFINITY;
     for (int f = 0; f < BF_MAXF; ++f) {
         const double w = f < a.nf ? a.omegas[f] : 0.0;
+        if (f < a.nf && w < wmin) wmin = w;
         K.kappa64[f] = w / (two_pi * a.c);
         K.kappa[f] = (float)K.kappa64[f];
         K.hk[f] = (float)(w * 0.5 / a.c);
         K.omega[f] = (float)w;
+        K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
     }
     K.b = (float)a.width_b;
     K.b2 = (float)(a.width_b * a.width_b);
+    K.b2_64 = a.width_b * a.width_b;
     K.amp_scale = a.phi_amp * sqrt(a.c) / (two_pi * a.c);
+    // Cut radius for the warp-patch prepass; without the cutoff nothing is ever cut.
+    K.rcut_scale = (a.use_cutoff && wmin > 0) ? 72.0 * a.c / (wmin * a.width_b) : INFINITY;
     switch (a.nf) {
         case 1: return launch_nf<1>(a, t, seg_start, K, d_stats, st);
         case 2: return launch_nf<2>(a, t, seg_start, K, d_stats, st);
