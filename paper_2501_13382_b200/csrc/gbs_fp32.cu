@@ -106,19 +106,24 @@ __device__ __forceinline__ double exact_d2(const Row64 &g, double px, double py,
     return __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
 }
 
+constexpr int NWARPS = THREADS / 32;
+
 template <int NF>
 struct Smem {
     float4 geo0[ROWCAP];     // wc.xyz (c_T - o), len
     float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_T)
+    float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_T's offset from the line)
     float4 aux[ROWCAP];      // s0, A (amplitude factor), R_cut, D (error scale)
     float anc[3 * NF][ROWCAP];  // phase anchors: centre proj / start / end (turns)
     Row64 r64[ROWCAP];
-    int2 bhdr[CB];           // (first row, n_segs) of chunk beam j
+    unsigned surv[NWARPS][CB];  // per warp patch and beam: surviving segments (+ behind flag)
     float btie[CB];          // absolute tie tolerance of the beam
     int brow[CB + 1];
     int nbc;
     double acc[TILE][NF][2];
 };
+
+constexpr unsigned BEHIND_CHECK = 0x80000000u;
 
 // Gaussian-beam contribution of one pair, all frequencies (kernels.py:377-399).
 template <int NF>
@@ -144,6 +149,31 @@ __device__ __forceinline__ void contribute(const Fp32Consts &K, int use_cutoff, 
     }
 }
 
+// Distance of the patch centre cW to segment row `r` (fp32, tile-local), the
+// unit vector from the nearest point, and whether the whole patch (radius RW)
+// is cut for this segment.
+template <int NF>
+__device__ __forceinline__ float patch_dist(const Smem<NF> &S, int r, float cwx, float cwy,
+                                            float cwz, float RW, float *ux, float *uy, float *uz,
+                                            bool *cut, float *proj_out) {
+    const float4 g0 = S.geo0[r];
+    const float4 g1 = S.geo1[r];
+    const float wx = cwx + g0.x, wy = cwy + g0.y, wz = cwz + g0.z;
+    const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+    const float t = fminf(fmaxf(proj, 0.f), g0.w);
+    const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
+    const float dc = sqrtf(vx * vx + vy * vy + vz * vz);
+    const float inv = dc > 1e-6f ? 1.f / dc : 0.f;
+    *ux = vx * inv;
+    *uy = vy * inv;
+    *uz = vz * inv;
+    const float px = wx - proj * g1.x, py = wy - proj * g1.y, pz = wz - proj * g1.z;
+    const float rc = (S.aux[r].z + RW) * 1.00002f + 2e-3f;
+    *cut = px * px + py * py + pz * pz > rc * rc;
+    *proj_out = proj;
+    return dc;
+}
+
 template <int NF>
 __global__ void __launch_bounds__(THREADS, 4)
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const int32_t *__restrict__ seg_start,
@@ -153,45 +183,42 @@ __global__ void __launch_bounds__(THREADS, 4)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    const int warp = tid >> 5;
     const int64_t tile = blockIdx.x;
     const double4 cen = tl.centre[tile];
     const float RT = (float)cen.w;
 
-    // ---- receivers of this thread (tile-local coordinates)
-    float rx[R], ry[R], rz[R];
+    // ---- receivers of this thread (tile-local coordinates); padding receivers
+    //      sit at the tile centre and are computed but never written back
+    float rx[R], ry[R], rz[R], rr[R];
     int oi[R];
-    bool valid[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int64_t si = tile * TILE + R * tid + j;
-        valid[j] = si < tl.n;
-        oi[j] = 0;
-        rx[j] = ry[j] = rz[j] = 0.f;
-        if (valid[j]) {
-            oi[j] = tl.perm[si];
-            const float4 rl = tl.rloc[si];
-            rx[j] = rl.x;
-            ry[j] = rl.y;
-            rz[j] = rl.z;
-        }
+        const bool valid = si < tl.n;
+        oi[j] = valid ? tl.perm[si] : -1;
+        float4 rl = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) rl = tl.rloc[si];
+        rx[j] = rl.x;
+        ry[j] = rl.y;
+        rz[j] = rl.z;
+        rr[j] = rl.x * rl.x + rl.y * rl.y + rl.z * rl.z;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-            S.acc[R * tid + j][f][0] = valid[j] ? a.acc[2 * ((int64_t)oi[j] * NF + f)] : 0.0;
-            S.acc[R * tid + j][f][1] = valid[j] ? a.acc[2 * ((int64_t)oi[j] * NF + f) + 1] : 0.0;
+            S.acc[R * tid + j][f][0] = valid ? a.acc[2 * ((int64_t)oi[j] * NF + f)] : 0.0;
+            S.acc[R * tid + j][f][1] = valid ? a.acc[2 * ((int64_t)oi[j] * NF + f) + 1] : 0.0;
         }
     }
     // ---- warp patch: bounding sphere of the warp's receivers
     float cwx, cwy, cwz, RW;
     {
-        float mnx = INFINITY, mny = INFINITY, mnz = INFINITY;
-        float mxx = -INFINITY, mxy = -INFINITY, mxz = -INFINITY;
+        float mnx = rx[0], mny = ry[0], mnz = rz[0], mxx = rx[0], mxy = ry[0], mxz = rz[0];
 #pragma unroll
-        for (int j = 0; j < R; ++j)
-            if (valid[j]) {
-                mnx = fminf(mnx, rx[j]); mxx = fmaxf(mxx, rx[j]);
-                mny = fminf(mny, ry[j]); mxy = fmaxf(mxy, ry[j]);
-                mnz = fminf(mnz, rz[j]); mxz = fmaxf(mxz, rz[j]);
-            }
+        for (int j = 1; j < R; ++j) {
+            mnx = fminf(mnx, rx[j]); mxx = fmaxf(mxx, rx[j]);
+            mny = fminf(mny, ry[j]); mxy = fmaxf(mxy, ry[j]);
+            mnz = fminf(mnz, rz[j]); mxz = fmaxf(mxz, rz[j]);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
@@ -201,20 +228,18 @@ __global__ void __launch_bounds__(THREADS, 4)
             mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
             mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
         }
-        if (mnx > mxx) mnx = mxx = mny = mxy = mnz = mxz = 0.f;  // warp without receivers
         cwx = 0.5f * (mnx + mxx);
         cwy = 0.5f * (mny + mxy);
         cwz = 0.5f * (mnz + mxz);
-        float rr = 0.f;
+        float q = 0.f;
 #pragma unroll
-        for (int j = 0; j < R; ++j)
-            if (valid[j]) {
-                const float ex = rx[j] - cwx, ey = ry[j] - cwy, ez = rz[j] - cwz;
-                rr = fmaxf(rr, ex * ex + ey * ey + ez * ez);
-            }
+        for (int j = 0; j < R; ++j) {
+            const float ex = rx[j] - cwx, ey = ry[j] - cwy, ez = rz[j] - cwz;
+            q = fmaxf(q, ex * ex + ey * ey + ez * ez);
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) rr = fmaxf(rr, __shfl_xor_sync(0xffffffffu, rr, o));
-        RW = sqrtf(rr) * 1.0001f + 1e-4f;
+        for (int o = 16; o > 0; o >>= 1) q = fmaxf(q, __shfl_xor_sync(0xffffffffu, q, o));
+        RW = sqrtf(q) * 1.0001f + 1e-4f;
     }
 
     float pre[R][NF], pim[R][NF];
@@ -262,8 +287,11 @@ __global__ void __launch_bounds__(THREADS, 4)
             const double s0 = a.seg_s0[row];
             const double wcx = cen.x - g.ox, wcy = cen.y - g.oy, wcz = cen.z - g.oz;
             const double pc = wcx * g.dx + wcy * g.dy + wcz * g.dz;
+            const double ucx = wcx - pc * g.dx, ucy = wcy - pc * g.dy, ucz = wcz - pc * g.dz;
             S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)g.len);
             S.geo1[r] = make_float4((float)g.dx, (float)g.dy, (float)g.dz, (float)pc);
+            S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
+                                    (float)(ucx * ucx + ucy * ucy + ucz * ucz));
             const double se = s0 + g.len;
             const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
             const double A = K.amp_scale * a.seg_refl[row] * a.weights[b0 + jb];
@@ -277,74 +305,103 @@ __global__ void __launch_bounds__(THREADS, 4)
             }
         }
         __syncthreads();
-        for (int j = tid; j < nbc; j += THREADS) {
+
+        // ---- warp work generation: one lane per beam bounds the warp patch
+        //      against the beam's segments (cut / behind / dominated segments)
+        for (int jb = lane; jb < nbc; jb += 32) {
+            const int r0 = S.brow[jb], ns = S.brow[jb + 1] - r0;
+            unsigned word = 0;
             float D = 0.f;
-            for (int r = S.brow[j]; r < S.brow[j + 1]; ++r) D = fmaxf(D, S.aux[r].w);
-            S.bhdr[j] = make_int2(S.brow[j], S.brow[j + 1] - S.brow[j]);
-            S.btie[j] = TIE_ABS * D * D;
+            for (int k = 0; k < ns; ++k) D = fmaxf(D, S.aux[r0 + k].w);
+            if (ns > 0) {
+                float best = INFINITY, p0 = 0.f;
+                int kj = 0;
+                bool all_dead = true;
+                for (int k = 0; k < ns; ++k) {
+                    float ux, uy, uz, proj;
+                    bool cut;
+                    const float dc = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut,
+                                                &proj);
+                    bool dead = cut;
+                    if (k == 0) {
+                        p0 = proj;
+                        dead = dead || (proj + RW * 1.00002f + 2e-3f < 0.f);
+                    }
+                    all_dead = all_dead && dead;
+                    if (dc < best) {
+                        best = dc;
+                        kj = k;
+                    }
+                }
+                if (!all_dead) {
+                    float ujx, ujy, ujz, pj;
+                    bool cj;
+                    const float dj = patch_dist(S, r0 + kj, cwx, cwy, cwz, RW, &ujx, &ujy, &ujz,
+                                                &cj, &pj);
+                    unsigned mask = 1u << kj;
+                    for (int k = 0; k < ns; ++k) {
+                        if (k == kj) continue;
+                        float ux, uy, uz, proj;
+                        bool cut;
+                        const float dk = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz,
+                                                    &cut, &proj);
+                        // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * Lip, with
+                        // Lip <= |u_k - u_j| + 4RW/d_k + 4RW/d_j (and always <= 2)
+                        const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
+                        float lip = sqrtf(ex * ex + ey * ey + ez * ez) +
+                                    4.f * RW * (1.f / fmaxf(dk, 1e-6f) + 1.f / fmaxf(dj, 1e-6f));
+                        lip = fminf(lip, 2.f);
+                        const bool pruned = dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk;
+                        if (!pruned) mask |= 1u << k;
+                    }
+                    word = mask;
+                    // segment 0 survives and the patch reaches its launch plane
+                    if ((mask & 1u) && p0 - RW * 1.00002f - 2e-3f <= PROJ_ERR * D)
+                        word |= BEHIND_CHECK;
+                }
+            }
+            S.surv[warp][jb] = word;
+            S.btie[jb] = TIE_ABS * D * D;  // same value from every warp
         }
-        __syncthreads();
+        __syncwarp();
 
         // ---- summation over the chunk's beams, ascending
         for (int jb = 0; jb < nbc; ++jb) {
-            const int2 h = S.bhdr[jb];
-            const int r0 = h.x, ns = h.y;
-            if (ns == 0) continue;
-            // lane-parallel prepass: one lane per segment vs the warp patch
-            float dc = INFINITY;
-            bool dead = true;
-            if (lane < ns) {
-                const float4 g0 = S.geo0[r0 + lane];
-                const float4 g1 = S.geo1[r0 + lane];
-                const float rcut = S.aux[r0 + lane].z;
-                const float wx = cwx + g0.x, wy = cwy + g0.y, wz = cwz + g0.z;
-                const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
-                const float t = fminf(fmaxf(proj, 0.f), g0.w);
-                const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
-                dc = sqrtf(vx * vx + vy * vy + vz * vz);
-                const float ux = wx - proj * g1.x, uy = wy - proj * g1.y, uz = wz - proj * g1.z;
-                const float qp = sqrtf(ux * ux + uy * uy + uz * uz);
-                dead = qp > (rcut + RW) * 1.00001f + 1e-3f;
-                if (lane == 0) dead = dead || (proj + RW * 1.00001f + 1e-3f < 0.f);
-            }
-            if (__all_sync(0xffffffffu, dead)) continue;  // every pair of the patch is cut/behind
-            float dmin = dc;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
-            const unsigned surv = __ballot_sync(
-                0xffffffffu, lane < ns && dc <= (dmin + 2.f * RW) * 1.00001f + 2e-3f);
-            const float tie_abs = S.btie[jb];
+            const unsigned word = S.surv[warp][jb];
+            if (!word) continue;  // every pair of the patch is cut or behind
+            const unsigned surv = word & ~BEHIND_CHECK;
+            const int r0 = S.brow[jb];
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
                 const int k = __ffs(surv) - 1;
                 const int row = r0 + k;
                 const float4 g0 = S.geo0[row];
                 const float4 g1 = S.geo1[row];
+                const float4 g2 = S.geo2[row];
                 const float4 ax = S.aux[row];
                 float anc[3 * NF];
 #pragma unroll
                 for (int q = 0; q < 3 * NF; ++q) anc[q] = S.anc[q][row];
                 const float tolp = PROJ_ERR * ax.w;
+                const bool chk = (word & BEHIND_CHECK) != 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    if (!valid[j]) continue;
-                    const float dl = rx[j] * g1.x + ry[j] * g1.y + rz[j] * g1.z;
+                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
-                    if (k == 0 && proj < tolp) {
+                    if (chk && proj < tolp) {
                         if (proj < -tolp) continue;  // behind the source (kernels.py:348,375)
-                        const Row64 g = S.r64[row];
+                        if (oi[j] < 0) continue;
                         const int64_t gi = 3 * (int64_t)oi[j];
                         double p64, t64;
-                        exact_d2(g, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
+                        exact_d2(S.r64[row], a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
                         ++ties;
                         if (p64 < 0.0) continue;
                     }
                     const float t = fminf(fmaxf(proj, 0.f), g0.w);
                     const float s = ax.x + t;
-                    const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
-                    const float ux = wx - proj * g1.x, uy = wy - proj * g1.y,
-                                uz = wz - proj * g1.z;
-                    const float q2 = ux * ux + uy * uy + uz * uz;
+                    const float q2 = fmaxf(
+                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                        0.f);
                     float base[NF];
 #pragma unroll
                     for (int f = 0; f < NF; ++f)
@@ -356,6 +413,7 @@ __global__ void __launch_bounds__(THREADS, 4)
                 }
             } else {
                 // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
+                const float tie_abs = S.btie[jb];
                 float best[R], second[R];
                 int kb[R];
 #pragma unroll
@@ -382,25 +440,23 @@ __global__ void __launch_bounds__(THREADS, 4)
                 }
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    if (!valid[j]) continue;
                     const int k = kb[j];
                     bool exact = second[j] - best[j] <= fmaf(TIE_REL, second[j], tie_abs);
                     const float4 g0 = S.geo0[r0 + k];
                     const float4 g1 = S.geo1[r0 + k];
                     const float4 ax = S.aux[r0 + k];
-                    const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
-                    const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
+                    const float proj = dl + g1.w;
                     if (k == 0 && fabsf(proj) <= PROJ_ERR * ax.w) exact = true;
                     float s, q2, A, base[NF];
                     if (!exact) {
                         if (k == 0 && proj < 0.f) continue;  // behind the source
+                        const float4 g2 = S.geo2[r0 + k];
                         const float t = fminf(fmaxf(proj, 0.f), g0.w);
                         s = ax.x + t;
                         A = ax.y;
-                        const float ux = wx - proj * g1.x, uy = wy - proj * g1.y,
-                                    uz = wz - proj * g1.z;
-                        q2 = ux * ux + uy * uy + uz * uz;
-                        const float dl = rx[j] * g1.x + ry[j] * g1.y + rz[j] * g1.z;
+                        q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                                   0.f);
 #pragma unroll
                         for (int f = 0; f < NF; ++f)
                             base[f] = proj <= 0.f ? S.anc[3 * f + 1][r0 + k]
@@ -408,6 +464,7 @@ __global__ void __launch_bounds__(THREADS, 4)
                                                                   : fmaf(K.kappa[f], dl, S.anc[3 * f][r0 + k]));
                     } else {
                         // exact re-decision among the contenders, ascending k, strict <
+                        if (oi[j] < 0) continue;
                         ++ties;
                         const int64_t gi = 3 * (int64_t)oi[j];
                         const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
@@ -438,14 +495,12 @@ __global__ void __launch_bounds__(THREADS, 4)
                         const int64_t grow = (b0 + jb) * a.max_seg + bk;
                         const double s_ref = a.seg_s0[grow] + bt;  // reference s (kernels.py:344)
                         s = (float)s_ref;
-                        const float4 h0 = S.geo0[r0 + bk];
                         const float4 h1 = S.geo1[r0 + bk];
+                        const float4 h2 = S.geo2[r0 + bk];
                         A = S.aux[r0 + bk].y;
-                        const float vx0 = rx[j] + h0.x, vy0 = ry[j] + h0.y, vz0 = rz[j] + h0.z;
-                        const float pj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
-                        const float ux = vx0 - pj * h1.x, uy = vy0 - pj * h1.y,
-                                    uz = vz0 - pj * h1.z;
-                        q2 = ux * ux + uy * uy + uz * uz;
+                        const float dk = fmaf(rx[j], h1.x, fmaf(ry[j], h1.y, rz[j] * h1.z));
+                        q2 = fmaxf(fmaf(-dk, dk, fmaf(h2.x, rx[j], fmaf(h2.y, ry[j], fmaf(h2.z, rz[j], h2.w + rr[j])))),
+                                   0.f);
 #pragma unroll
                         for (int f = 0; f < NF; ++f) base[f] = (float)frac_turns(K.kappa64[f] * s_ref);
                     }
@@ -469,7 +524,7 @@ __global__ void __launch_bounds__(THREADS, 4)
     // ---- write back (in-place continuation) and evaluation counts (kernels.py:399)
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        if (!valid[j]) continue;
+        if (oi[j] < 0) continue;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             a.acc[2 * ((int64_t)oi[j] * NF + f)] = S.acc[R * tid + j][f][0];
