@@ -322,7 +322,7 @@ def run_ours(args):
                          "algorithmic_model": "SURVEY.md 8(d): 19*N_r*sum(n_segs) + "
                                               "(16+5F)*P_nb + 22*E FLOP; P_nb + 3E MUFU",
                          "nonbehind_pairs": p_nb, "evaluations": ev_sum,
-                         "tie_pairs": st["tie_pairs"]},
+                         "tie_pairs": st["tie_pairs"], "patch_beams": st["patch_beams"]},
             "clocks": clocks,
         }
     if world == 1 and not args.no_cpu_baseline:

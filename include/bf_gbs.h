@@ -165,6 +165,12 @@ int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_by
 int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
                   int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms);
 
+/* Work-generation outcome of the last fp32 call on this thread, counted per
+ * (warp patch of 128 receivers, beam) item: culled (every pair cut/behind),
+ * single surviving segment, corner wedge (two segments, exact fp64 pick),
+ * general multi-segment scan. */
+int bf_last_path_stats(int64_t *culled, int64_t *single, int64_t *wedge, int64_t *multi);
+
 /* Microbenchmarks of the pipes the summation is bound by, on `device`:
  * dependent-free FFMA stream (TFLOP/s, 2 flop per FFMA) and MUFU ex2 stream
  * (Tops/s).  Used for the roofline denominators in bench.py. */

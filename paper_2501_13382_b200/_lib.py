@@ -22,7 +22,7 @@ EXPORTS = (
     "bf_version", "bf_last_error", "bf_device_count", "bf_launch_count",
     "bf_gbs_accumulate", "bf_gbs_accumulate_dev", "bf_nearest_on_segments",
     "bf_trace_range_dev", "bf_field_finalize_dev", "bf_plan_chunks", "bf_last_stats",
-    "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks",
+    "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats",
 )
 FLAG_OBS_PRESORTED = 1
 
@@ -60,6 +60,7 @@ def _declare(lib):
     lib.bf_plan_chunks.argtypes = [I64, I64, I64, I64P, I64, I64P]
     lib.bf_last_stats.argtypes = [I64P, I64P, I64P, I64P, I64P, D]
     lib.bf_probe_peaks.argtypes = [INT, D, D]
+    lib.bf_last_path_stats.argtypes = [I64P] * 4
     for name in EXPORTS:
         if name not in ("bf_version", "bf_last_error", "bf_device_count", "bf_launch_count"):
             getattr(lib, name).restype = INT
@@ -104,8 +105,12 @@ def last_stats() -> dict:
     ms = ctypes.c_double(0.0)
     check(load().bf_last_stats(*[ctypes.byref(v) for v in vals], ctypes.byref(ms)))
     cand, total, ties, tiles, nbp = (v.value for v in vals)
+    paths = [ctypes.c_int64(0) for _ in range(4)]
+    check(load().bf_last_path_stats(*[ctypes.byref(v) for v in paths]))
     return {"candidate_pairs": cand, "total_pairs": total, "tie_pairs": ties, "n_tiles": tiles,
-            "nonbehind_pairs": nbp, "kernel_ms": ms.value}
+            "nonbehind_pairs": nbp, "kernel_ms": ms.value,
+            "patch_beams": dict(zip(("culled", "single", "wedge", "multi"),
+                                    (v.value for v in paths)))}
 
 
 def probe_peaks(device: int = 0) -> dict:

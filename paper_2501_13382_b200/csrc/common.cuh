@@ -55,6 +55,7 @@ struct GbsStats {
     unsigned long long candidate_pairs;  // (beam, receiver) pairs inside candidate tiles
     unsigned long long tie_pairs;        // pairs re-decided in fp64
     unsigned long long nb_pairs;         // non-behind pairs (P_nb of SURVEY 8(d))
+    unsigned long long paths[4];         // (warp patch, beam) items: culled, single, wedge, multi
     float kernel_ms;                     // CUDA-event duration of the summation kernel
 };
 

@@ -26,7 +26,7 @@ int gbs_fp32_tile();
 
 namespace {
 thread_local char g_err[512] = "";
-thread_local GbsStats g_last_stats = {0, 0, 0, 0.f};
+thread_local GbsStats g_last_stats = {};
 thread_local int64_t g_last_total_pairs = 0, g_last_tiles = 0;
 std::atomic<uint64_t> g_launches{0};
 }  // namespace
@@ -322,7 +322,7 @@ int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_
 
 // Runs the operator on device-resident LOCAL ranges (a.obs etc. already offset).
 int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st) {
-    g_last_stats = {0, 0, 0, 0.f};
+    g_last_stats = GbsStats{};
     g_last_total_pairs = a.n_obs * a.n_beams;
     g_last_tiles = 0;
     if (a.n_obs <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
@@ -381,6 +381,14 @@ int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_p
     if (total_pairs) *total_pairs = g_last_total_pairs;
     if (tie_pairs) *tie_pairs = (int64_t)g_last_stats.tie_pairs;
     if (n_tiles) *n_tiles = g_last_tiles;
+    return BF_OK;
+}
+
+int bf_last_path_stats(int64_t *culled, int64_t *single, int64_t *wedge, int64_t *multi) {
+    if (culled) *culled = (int64_t)g_last_stats.paths[0];
+    if (single) *single = (int64_t)g_last_stats.paths[1];
+    if (wedge) *wedge = (int64_t)g_last_stats.paths[2];
+    if (multi) *multi = (int64_t)g_last_stats.paths[3];
     return BF_OK;
 }
 

@@ -124,6 +124,7 @@ struct Smem {
 };
 
 constexpr unsigned BEHIND_CHECK = 0x80000000u;
+constexpr unsigned WEDGE = 0x40000000u;
 
 // Gaussian-beam contribution of one pair, all frequencies (kernels.py:377-399).
 template <int NF>
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(THREADS, 4)
         for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
     }
     int ties = 0, nbp = 0;
+    unsigned pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0;  // path counts (lane 0)
 
     for (int64_t b0 = 0; b0 < a.n_beams;) {
         // ---- chunk [b0, b0+nbc): <= CB beams and <= ROWCAP rows
@@ -358,6 +360,18 @@ __global__ void __launch_bounds__(THREADS, 4)
                     // segment 0 survives and the patch reaches its launch plane
                     if ((mask & 1u) && p0 - RW * 1.00002f - 2e-3f <= PROJ_ERR * D)
                         word |= BEHIND_CHECK;
+                    // corner wedge: exactly segments k, k+1 survive and every receiver
+                    // projects beyond the end of k and before the start of k+1, so both
+                    // clamped distances are distances to the shared reflection point
+                    const int kl = __ffs(mask) - 1;
+                    if (mask == (3u << kl)) {
+                        float ux, uy, uz, pa, pb;
+                        bool cut;
+                        patch_dist(S, r0 + kl, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pa);
+                        patch_dist(S, r0 + kl + 1, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pb);
+                        const float m1 = PROJ_ERR * D + RW * 1.00002f + 2e-3f;
+                        if (pa - S.geo0[r0 + kl].w >= m1 && pb <= -m1) word = mask | WEDGE;
+                    }
                 }
             }
             S.surv[warp][jb] = word;
@@ -368,11 +382,15 @@ __global__ void __launch_bounds__(THREADS, 4)
         // ---- summation over the chunk's beams, ascending
         for (int jb = 0; jb < nbc; ++jb) {
             const unsigned word = S.surv[warp][jb];
-            if (!word) continue;  // every pair of the patch is cut or behind
-            const unsigned surv = word & ~BEHIND_CHECK;
+            if (!word) {  // every pair of the patch is cut or behind
+                pc0 += lane == 0;
+                continue;
+            }
+            const unsigned surv = word & ~(BEHIND_CHECK | WEDGE);
             const int r0 = S.brow[jb];
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
+                pc1 += lane == 0;
                 const int k = __ffs(surv) - 1;
                 const int row = r0 + k;
                 const float4 g0 = S.geo0[row];
@@ -382,37 +400,95 @@ __global__ void __launch_bounds__(THREADS, 4)
                 float anc[3 * NF];
 #pragma unroll
                 for (int q = 0; q < 3 * NF; ++q) anc[q] = S.anc[q][row];
-                const float tolp = PROJ_ERR * ax.w;
-                const bool chk = (word & BEHIND_CHECK) != 0;
+                // geometry of all R receivers, branch-free (independent chains)
+                float sj[R], q2j[R], pj[R], base[R][NF];
+                bool lv[R];
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
-                    if (chk && proj < tolp) {
-                        if (proj < -tolp) continue;  // behind the source (kernels.py:348,375)
-                        if (oi[j] < 0) continue;
+                    pj[j] = proj;
+                    sj[j] = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
+                    q2j[j] = fmaxf(
+                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                        0.f);
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        base[j][f] = proj <= 0.f ? anc[3 * f + 1]
+                                                 : (proj >= g0.w ? anc[3 * f + 2]
+                                                                 : fmaf(K.kappa[f], dl, anc[3 * f]));
+                    lv[j] = true;
+                }
+                if (word & BEHIND_CHECK) {
+                    // k == 0 and the patch reaches the launch plane: behind = proj < 0
+                    // (kernels.py:348,375), re-decided in fp64 within the error bound
+                    const float tolp = PROJ_ERR * ax.w;
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        if (pj[j] >= tolp) continue;
+                        lv[j] = false;
+                        if (pj[j] < -tolp || oi[j] < 0) continue;
                         const int64_t gi = 3 * (int64_t)oi[j];
                         double p64, t64;
                         exact_d2(S.r64[row], a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
                         ++ties;
-                        if (p64 < 0.0) continue;
+                        lv[j] = !(p64 < 0.0);
                     }
-                    const float t = fminf(fmaxf(proj, 0.f), g0.w);
-                    const float s = ax.x + t;
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    if (!lv[j]) continue;
+                    ++nbp;
+                    contribute<NF>(K, a.use_cutoff, sj[j], q2j[j], ax.y, base[j], pre[j], pim[j],
+                                   evr[j]);
+                }
+            } else if (word & WEDGE) {
+                pc2 += lane == 0;
+                // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
+                //      the reference picks by fp64 rounding, reproduced exactly here
+                const int k = __ffs(surv) - 1;
+                const int ra = r0 + k, rb = ra + 1;
+                const Row64 ga = S.r64[ra], gb = S.r64[rb];
+                const double ldx = __dmul_rn(ga.len, ga.dx), ldy = __dmul_rn(ga.len, ga.dy),
+                             ldz = __dmul_rn(ga.len, ga.dz);
+                const int64_t grow = (b0 + jb) * a.max_seg + k;
+                const float sa = (float)(a.seg_s0[grow] + ga.len);  // s0_k + t, t = len
+                const float sb = (float)a.seg_s0[grow + 1];          // s0_{k+1} + 0
+                const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
+                const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
+                const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    if (oi[j] < 0) continue;
+                    const int64_t gi = 3 * (int64_t)oi[j];
+                    const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
+                    const double vx = __dsub_rn(__dsub_rn(px, ga.ox), ldx);
+                    const double vy = __dsub_rn(__dsub_rn(py, ga.oy), ldy);
+                    const double vz = __dsub_rn(__dsub_rn(pz, ga.oz), ldz);
+                    const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)),
+                                                __dmul_rn(vz, vz));
+                    const double wx = __dsub_rn(px, gb.ox), wy = __dsub_rn(py, gb.oy),
+                                 wz = __dsub_rn(pz, gb.oz);
+                    const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)),
+                                                __dmul_rn(wz, wz));
+                    const bool wb = db < da;  // strict: equal distances keep segment k
+                    const float4 g1 = wb ? g1b : g1a;
+                    const float4 g2 = wb ? g2b : g2a;
+                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float q2 = fmaxf(
                         fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                         0.f);
                     float base[NF];
 #pragma unroll
-                    for (int f = 0; f < NF; ++f)
-                        base[f] = proj <= 0.f ? anc[3 * f + 1]
-                                              : (proj >= g0.w ? anc[3 * f + 2]
-                                                              : fmaf(K.kappa[f], dl, anc[3 * f]));
+                    for (int f = 0; f < NF; ++f) base[f] = wb ? S.anc[3 * f + 1][rb] : S.anc[3 * f + 2][ra];
+                    ++ties;
                     ++nbp;
-                    contribute<NF>(K, a.use_cutoff, s, q2, ax.y, base, pre[j], pim[j], evr[j]);
+                    contribute<NF>(K, a.use_cutoff, wb ? sb : sa, q2, wb ? Ab : Aa, base, pre[j],
+                                   pim[j], evr[j]);
                 }
             } else {
                 // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
+                pc3 += lane == 0;
                 const float tie_abs = S.btie[jb];
                 float best[R], second[R];
                 int kb[R];
@@ -541,6 +617,10 @@ __global__ void __launch_bounds__(THREADS, 4)
     if (lane == 0) {
         if (t) atomicAdd(&stats->tie_pairs, t);
         if (q) atomicAdd(&stats->nb_pairs, q);
+        atomicAdd(&stats->paths[0], (unsigned long long)pc0);
+        atomicAdd(&stats->paths[1], (unsigned long long)pc1);
+        atomicAdd(&stats->paths[2], (unsigned long long)pc2);
+        atomicAdd(&stats->paths[3], (unsigned long long)pc3);
     }
 }
 
