@@ -82,49 +82,55 @@ __device__ __forceinline__ float cos_approx(float x) {
 }
 __device__ __forceinline__ double frac_turns(double x) { return x - rint(x); }
 
-// fp64 row staged for exact re-decisions (reference operation order).
-struct Row64 {
-    double ox, oy, oz, dx, dy, dz, len;
-};
-
-// Exact fp64 clamped distance of kernels.py:328-340, no FMA.
-__device__ __forceinline__ double exact_d2(const Row64 &g, double px, double py, double pz,
-                                           double *proj_out, double *t_out) {
-    const double wx = __dsub_rn(px, g.ox), wy = __dsub_rn(py, g.oy), wz = __dsub_rn(pz, g.oz);
+// Exact fp64 clamped distance of kernels.py:328-340 for padded row `row`,
+// reference operation order, no FMA.
+__device__ __forceinline__ double exact_d2(const GbsArgs &a, int64_t row, double px, double py,
+                                           double pz, double *proj_out, double *t_out) {
+    const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
+                 oz = a.seg_origin[3 * row + 2];
+    const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1], dz = a.seg_dir[3 * row + 2];
+    const double len = a.seg_len[row];
+    const double wx = __dsub_rn(px, ox), wy = __dsub_rn(py, oy), wz = __dsub_rn(pz, oz);
     const double proj =
-        __dadd_rn(__dadd_rn(__dmul_rn(wx, g.dx), __dmul_rn(wy, g.dy)), __dmul_rn(wz, g.dz));
+        __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
     double t = proj;
     if (t < 0.0)
         t = 0.0;
-    else if (t > g.len)
-        t = g.len;
-    const double vx = __dsub_rn(wx, __dmul_rn(t, g.dx));
-    const double vy = __dsub_rn(wy, __dmul_rn(t, g.dy));
-    const double vz = __dsub_rn(wz, __dmul_rn(t, g.dz));
+    else if (t > len)
+        t = len;
+    const double vx = __dsub_rn(wx, __dmul_rn(t, dx));
+    const double vy = __dsub_rn(wy, __dmul_rn(t, dy));
+    const double vz = __dsub_rn(wz, __dmul_rn(t, dz));
     *proj_out = proj;
     *t_out = t;
     return __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
 }
 
-constexpr int NWARPS = THREADS / 32;
+constexpr int NWARPS = THREADS / 32;   // consumer warps (receiver patches)
 
+constexpr unsigned BEHIND_CHECK = 0x80000000u;
+constexpr unsigned WEDGE = 0x40000000u;
+
+// One staged chunk of beams, as seen from this tile.
 template <int NF>
-struct Smem {
+struct Stage {
     float4 geo0[ROWCAP];     // wc.xyz (c_T - o), len
     float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_T)
     float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_T's offset from the line)
     float4 aux[ROWCAP];      // s0, A (amplitude factor), R_cut, D (error scale)
     float anc[3 * NF][ROWCAP];  // phase anchors: centre proj / start / end (turns)
-    Row64 r64[ROWCAP];
-    unsigned surv[NWARPS][CB];  // per warp patch and beam: surviving segments (+ behind flag)
-    float btie[CB];          // absolute tie tolerance of the beam
     int brow[CB + 1];
-    int nbc;
-    double acc[TILE][NF][2];
+    long long b0;
+    int nbc;                 // beams in the chunk; -1 terminates
 };
 
-constexpr unsigned BEHIND_CHECK = 0x80000000u;
-constexpr unsigned WEDGE = 0x40000000u;
+template <int NF>
+struct Smem {
+    Stage<NF> st[2];         // double-buffered: chunk c+1 is staged while c is summed
+    unsigned surv[NWARPS][CB];  // per warp patch and beam: surviving segments + flags
+    float btie[NWARPS][CB];  // absolute tie tolerance of the beam
+    double acc[TILE][NF][2];
+};
 
 // Gaussian-beam contribution of one pair, all frequencies (kernels.py:377-399).
 template <int NF>
@@ -150,11 +156,11 @@ __device__ __forceinline__ void contribute(const Fp32Consts &K, int use_cutoff, 
     }
 }
 
-// Distance of the patch centre cW to segment row `r` (fp32, tile-local), the
-// unit vector from the nearest point, and whether the whole patch (radius RW)
-// is cut for this segment.
+// Distance of a patch centre c to segment row `r` (fp32, tile-local), the unit
+// vector from the nearest point, whether the whole patch (radius RW) is cut for
+// this segment, and the centre's axial projection.
 template <int NF>
-__device__ __forceinline__ float patch_dist(const Smem<NF> &S, int r, float cwx, float cwy,
+__device__ __forceinline__ float patch_dist(const Stage<NF> &S, int r, float cwx, float cwy,
                                             float cwz, float RW, float *ux, float *uy, float *uz,
                                             bool *cut, float *proj_out) {
     const float4 g0 = S.geo0[r];
@@ -175,8 +181,130 @@ __device__ __forceinline__ float patch_dist(const Smem<NF> &S, int r, float cwx,
     return dc;
 }
 
+// Bound on the angle swept by the nearest-point direction of a segment over a
+// ball of radius RW around a point at distance d: I - proj is nonexpansive, so
+// the residual moves by <= RW and the angle is <= asin(RW/d) <= x/sqrt(1-x^2).
+__device__ __forceinline__ float sweep(float RW, float d) {
+    const float x = RW / fmaxf(d, 1e-6f);
+    return x < 0.7f ? x * rsqrtf(1.f - x * x) * 1.0001f : 2.f;
+}
+
+// Work generation for one (patch, beam): survivor mask + flags (0 = culled).
 template <int NF>
-__global__ void __launch_bounds__(THREADS, 4)
+__device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns, float cwx,
+                                             float cwy, float cwz, float RW, float D) {
+    if (ns <= 0) return 0u;
+    float best = INFINITY, p0 = 0.f;
+    int kj = 0;
+    bool all_dead = true;
+    for (int k = 0; k < ns; ++k) {
+        float ux, uy, uz, proj;
+        bool cut;
+        const float dc = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &proj);
+        bool dead = cut;
+        if (k == 0) {
+            p0 = proj;
+            dead = dead || (proj + RW * 1.00002f + 2e-3f < 0.f);
+        }
+        all_dead = all_dead && dead;
+        if (dc < best) {
+            best = dc;
+            kj = k;
+        }
+    }
+    if (all_dead) return 0u;
+    float ujx, ujy, ujz, pj;
+    bool cj;
+    const float dj = patch_dist(S, r0 + kj, cwx, cwy, cwz, RW, &ujx, &ujy, &ujz, &cj, &pj);
+    const float sj = sweep(RW, dj);
+    unsigned mask = 1u << kj;
+    for (int k = 0; k < ns; ++k) {
+        if (k == kj) continue;
+        float ux, uy, uz, proj;
+        bool cut;
+        const float dk = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &proj);
+        // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * sup|grad d_k - grad d_j|
+        const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
+        const float lip = fminf(sqrtf(ex * ex + ey * ey + ez * ez) + sweep(RW, dk) + sj, 2.f);
+        if (!(dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk)) mask |= 1u << k;
+    }
+    unsigned word = mask;
+    // segment 0 survives and the patch reaches its launch plane
+    if ((mask & 1u) && p0 - RW * 1.00002f - 2e-3f <= PROJ_ERR * D) word |= BEHIND_CHECK;
+    // corner wedge: exactly segments k, k+1 survive and every receiver projects
+    // beyond the end of k and before the start of k+1, so both clamped
+    // distances are distances to the shared reflection point
+    const int kl = __ffs(mask) - 1;
+    if (mask == (3u << kl)) {
+        float ux, uy, uz, pa, pb;
+        bool cut;
+        patch_dist(S, r0 + kl, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pa);
+        patch_dist(S, r0 + kl + 1, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pb);
+        const float m1 = PROJ_ERR * D + RW * 1.00002f + 2e-3f;
+        if (pa - S.geo0[r0 + kl].w >= m1 && pb <= -m1) word = mask | WEDGE;
+    }
+    return word;
+}
+
+template <int NF>
+__device__ __forceinline__ void stage_chunk(Stage<NF> &G, const GbsArgs &a,
+                                            const int32_t *__restrict__ seg_start, int64_t b0,
+                                            int nbc, const double4 &cen, float RT,
+                                            const Fp32Consts &K, int tid) {
+    const int32_t base_row = seg_start[b0];
+    for (int j = tid; j <= nbc; j += THREADS) G.brow[j] = seg_start[b0 + j] - base_row;
+    if (tid == 0) {
+        G.nbc = nbc;
+        G.b0 = b0;
+    }
+    const int rows = seg_start[b0 + nbc] - base_row;
+    for (int r = tid; r < rows; r += THREADS) {
+        int lo = 0, hi = nbc;  // seg_start[b0+lo]-base <= r < seg_start[b0+hi]-base
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (seg_start[b0 + mid] - base_row <= r) lo = mid; else hi = mid;
+        }
+        const int jb = lo;
+        const int k = r - (seg_start[b0 + jb] - base_row);
+        const int64_t row = (b0 + jb) * a.max_seg + k;
+        const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
+                     oz = a.seg_origin[3 * row + 2];
+        const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
+                     dz = a.seg_dir[3 * row + 2];
+        const double len = a.seg_len[row], s0 = a.seg_s0[row];
+        const double wcx = cen.x - ox, wcy = cen.y - oy, wcz = cen.z - oz;
+        const double pc = wcx * dx + wcy * dy + wcz * dz;
+        const double ucx = wcx - pc * dx, ucy = wcy - pc * dy, ucz = wcz - pc * dz;
+        G.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)len);
+        G.geo1[r] = make_float4((float)dx, (float)dy, (float)dz, (float)pc);
+        G.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
+                                (float)(ucx * ucx + ucy * ucy + ucz * ucz));
+        const double se = s0 + len;
+        const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
+        const double A = K.amp_scale * a.seg_refl[row] * a.weights[b0 + jb];
+        const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + len) + RT + 1.f;
+        G.aux[r] = make_float4((float)s0, (float)A, (float)rcut, D);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            G.anc[3 * f + 0][r] = (float)frac_turns(K.kappa64[f] * (s0 + pc));
+            G.anc[3 * f + 1][r] = (float)frac_turns(K.kappa64[f] * s0);
+            G.anc[3 * f + 2][r] = (float)frac_turns(K.kappa64[f] * se);
+        }
+    }
+}
+
+// Greedy chunk after beam b0: <= CB beams and <= ROWCAP segment rows.
+__device__ __forceinline__ int chunk_len(const int32_t *__restrict__ seg_start, int64_t b0,
+                                         int64_t n_beams) {
+    if (b0 >= n_beams) return 0;
+    int64_t hi = b0 + CB < n_beams ? b0 + CB : n_beams;
+    const int32_t r0 = seg_start[b0];
+    while (seg_start[hi] - r0 > ROWCAP) --hi;
+    return (int)(hi - b0);
+}
+
+template <int NF>
+__global__ void __launch_bounds__(THREADS, (NF <= 2 ? 4 : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const int32_t *__restrict__ seg_start,
                     const Fp32Consts K, GbsStats *stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -189,9 +317,9 @@ __global__ void __launch_bounds__(THREADS, 4)
     const double4 cen = tl.centre[tile];
     const float RT = (float)cen.w;
 
-    // ---- receivers of this thread (tile-local coordinates); padding receivers
-    //      sit at the tile centre and are computed but never written back
-    float rx[R], ry[R], rz[R], rr[R];
+    // ---- receivers (tile-local coordinates); padding receivers sit at the
+    //      tile centre and are computed but never written back
+    float rx[R], ry[R], rz[R];
     int oi[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -203,7 +331,6 @@ __global__ void __launch_bounds__(THREADS, 4)
         rx[j] = rl.x;
         ry[j] = rl.y;
         rz[j] = rl.z;
-        rr[j] = rl.x * rl.x + rl.y * rl.y + rl.z * rl.z;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             S.acc[R * tid + j][f][0] = valid ? a.acc[2 * ((int64_t)oi[j] * NF + f)] : 0.0;
@@ -252,154 +379,60 @@ __global__ void __launch_bounds__(THREADS, 4)
         for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
     }
     int ties = 0, nbp = 0;
-    unsigned pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0;  // path counts (lane 0)
+    unsigned pc[4] = {0, 0, 0, 0};
 
-    for (int64_t b0 = 0; b0 < a.n_beams;) {
-        // ---- chunk [b0, b0+nbc): <= CB beams and <= ROWCAP rows
-        if (tid == 0) {
-            int64_t hi = b0 + CB < a.n_beams ? b0 + CB : a.n_beams;
-            const int32_t r0 = seg_start[b0];
-            while (seg_start[hi] - r0 > ROWCAP) --hi;
-            S.nbc = (int)(hi - b0);
-        }
-        __syncthreads();
-        const int nbc = S.nbc;
-        for (int j = tid; j <= nbc; j += THREADS) S.brow[j] = seg_start[b0 + j] - seg_start[b0];
-        __syncthreads();
-        const int rows = S.brow[nbc];
-        // ---- stage: one thread per segment row, fp64 -> tile-local fp32
-        for (int r = tid; r < rows; r += THREADS) {
-            int lo = 0, hi = nbc;
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (S.brow[mid] <= r) lo = mid; else hi = mid;
-            }
-            const int jb = lo;
-            const int k = r - S.brow[jb];
-            const int64_t row = (b0 + jb) * a.max_seg + k;
-            Row64 g;
-            g.ox = a.seg_origin[3 * row];
-            g.oy = a.seg_origin[3 * row + 1];
-            g.oz = a.seg_origin[3 * row + 2];
-            g.dx = a.seg_dir[3 * row];
-            g.dy = a.seg_dir[3 * row + 1];
-            g.dz = a.seg_dir[3 * row + 2];
-            g.len = a.seg_len[row];
-            S.r64[r] = g;
-            const double s0 = a.seg_s0[row];
-            const double wcx = cen.x - g.ox, wcy = cen.y - g.oy, wcz = cen.z - g.oz;
-            const double pc = wcx * g.dx + wcy * g.dy + wcz * g.dz;
-            const double ucx = wcx - pc * g.dx, ucy = wcy - pc * g.dy, ucz = wcz - pc * g.dz;
-            S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)g.len);
-            S.geo1[r] = make_float4((float)g.dx, (float)g.dy, (float)g.dz, (float)pc);
-            S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
-                                    (float)(ucx * ucx + ucy * ucy + ucz * ucz));
-            const double se = s0 + g.len;
-            const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
-            const double A = K.amp_scale * a.seg_refl[row] * a.weights[b0 + jb];
-            const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + g.len) + RT + 1.f;
-            S.aux[r] = make_float4((float)s0, (float)A, (float)rcut, D);
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-                S.anc[3 * f + 0][r] = (float)frac_turns(K.kappa64[f] * (s0 + pc));
-                S.anc[3 * f + 1][r] = (float)frac_turns(K.kappa64[f] * s0);
-                S.anc[3 * f + 2][r] = (float)frac_turns(K.kappa64[f] * se);
-            }
-        }
-        __syncthreads();
+    // ---- prologue: stage chunk 0; chunk bounds run one chunk ahead of staging
+    int64_t nb0 = 0;
+    int nnbc = chunk_len(seg_start, 0, a.n_beams);
+    if (nnbc > 0) stage_chunk(S.st[0], a, seg_start, nb0, nnbc, cen, RT, K, tid);
+    nb0 += nnbc;
+    nnbc = chunk_len(seg_start, nb0, a.n_beams);
+    __syncthreads();
 
-        // ---- warp work generation: one lane per beam bounds the warp patch
-        //      against the beam's segments (cut / behind / dominated segments)
+    for (int c = 0;; ++c) {
+        const Stage<NF> &G = S.st[c & 1];
+        const int nbc = G.nbc;
+        if (nnbc == 0 && c > 0 && nbc <= 0) break;
+        if (nbc <= 0) break;
+        const int64_t b0 = G.b0;
+        // stage the next chunk into the other buffer (free since the last barrier)
+        if (nnbc > 0) {
+            stage_chunk(S.st[(c + 1) & 1], a, seg_start, nb0, nnbc, cen, RT, K, tid);
+        } else if (tid == 0) {
+            S.st[(c + 1) & 1].nbc = 0;
+        }
+        nb0 += nnbc;
+        nnbc = chunk_len(seg_start, nb0, a.n_beams);
+        // ---- warp work generation on this chunk: one lane per beam bounds the
+        //      warp patch against the beam's segments (cut / behind / dominated)
         for (int jb = lane; jb < nbc; jb += 32) {
-            const int r0 = S.brow[jb], ns = S.brow[jb + 1] - r0;
-            unsigned word = 0;
+            const int r0 = G.brow[jb], ns = G.brow[jb + 1] - r0;
             float D = 0.f;
-            for (int k = 0; k < ns; ++k) D = fmaxf(D, S.aux[r0 + k].w);
-            if (ns > 0) {
-                float best = INFINITY, p0 = 0.f;
-                int kj = 0;
-                bool all_dead = true;
-                for (int k = 0; k < ns; ++k) {
-                    float ux, uy, uz, proj;
-                    bool cut;
-                    const float dc = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut,
-                                                &proj);
-                    bool dead = cut;
-                    if (k == 0) {
-                        p0 = proj;
-                        dead = dead || (proj + RW * 1.00002f + 2e-3f < 0.f);
-                    }
-                    all_dead = all_dead && dead;
-                    if (dc < best) {
-                        best = dc;
-                        kj = k;
-                    }
-                }
-                if (!all_dead) {
-                    float ujx, ujy, ujz, pj;
-                    bool cj;
-                    const float dj = patch_dist(S, r0 + kj, cwx, cwy, cwz, RW, &ujx, &ujy, &ujz,
-                                                &cj, &pj);
-                    unsigned mask = 1u << kj;
-                    for (int k = 0; k < ns; ++k) {
-                        if (k == kj) continue;
-                        float ux, uy, uz, proj;
-                        bool cut;
-                        const float dk = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz,
-                                                    &cut, &proj);
-                        // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * Lip, with
-                        // Lip <= |u_k - u_j| + 4RW/d_k + 4RW/d_j (and always <= 2)
-                        const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
-                        float lip = sqrtf(ex * ex + ey * ey + ez * ez) +
-                                    4.f * RW * (1.f / fmaxf(dk, 1e-6f) + 1.f / fmaxf(dj, 1e-6f));
-                        lip = fminf(lip, 2.f);
-                        const bool pruned = dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk;
-                        if (!pruned) mask |= 1u << k;
-                    }
-                    word = mask;
-                    // segment 0 survives and the patch reaches its launch plane
-                    if ((mask & 1u) && p0 - RW * 1.00002f - 2e-3f <= PROJ_ERR * D)
-                        word |= BEHIND_CHECK;
-                    // corner wedge: exactly segments k, k+1 survive and every receiver
-                    // projects beyond the end of k and before the start of k+1, so both
-                    // clamped distances are distances to the shared reflection point
-                    const int kl = __ffs(mask) - 1;
-                    if (mask == (3u << kl)) {
-                        float ux, uy, uz, pa, pb;
-                        bool cut;
-                        patch_dist(S, r0 + kl, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pa);
-                        patch_dist(S, r0 + kl + 1, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pb);
-                        const float m1 = PROJ_ERR * D + RW * 1.00002f + 2e-3f;
-                        if (pa - S.geo0[r0 + kl].w >= m1 && pb <= -m1) word = mask | WEDGE;
-                    }
-                }
-            }
+            for (int k = 0; k < ns; ++k) D = fmaxf(D, G.aux[r0 + k].w);
+            const unsigned word = classify(G, r0, ns, cwx, cwy, cwz, RW, D);
             S.surv[warp][jb] = word;
-            S.btie[jb] = TIE_ABS * D * D;  // same value from every warp
+            S.btie[warp][jb] = TIE_ABS * D * D;
+            const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
+            pc[word == 0 ? 0 : (word & WEDGE) ? 2 : (m & (m - 1)) ? 3 : 1] += 1;
         }
         __syncwarp();
-
         // ---- summation over the chunk's beams, ascending
         for (int jb = 0; jb < nbc; ++jb) {
             const unsigned word = S.surv[warp][jb];
-            if (!word) {  // every pair of the patch is cut or behind
-                pc0 += lane == 0;
-                continue;
-            }
+            if (!word) continue;  // every pair of the patch is cut or behind
             const unsigned surv = word & ~(BEHIND_CHECK | WEDGE);
-            const int r0 = S.brow[jb];
+            const int r0 = G.brow[jb];
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
-                pc1 += lane == 0;
                 const int k = __ffs(surv) - 1;
                 const int row = r0 + k;
-                const float4 g0 = S.geo0[row];
-                const float4 g1 = S.geo1[row];
-                const float4 g2 = S.geo2[row];
-                const float4 ax = S.aux[row];
+                const float4 g0 = G.geo0[row];
+                const float4 g1 = G.geo1[row];
+                const float4 g2 = G.geo2[row];
+                const float4 ax = G.aux[row];
                 float anc[3 * NF];
 #pragma unroll
-                for (int q = 0; q < 3 * NF; ++q) anc[q] = S.anc[q][row];
+                for (int q = 0; q < 3 * NF; ++q) anc[q] = G.anc[q][row];
                 // geometry of all R receivers, branch-free (independent chains)
                 float sj[R], q2j[R], pj[R], base[R][NF];
                 bool lv[R];
@@ -407,10 +440,11 @@ __global__ void __launch_bounds__(THREADS, 4)
                 for (int j = 0; j < R; ++j) {
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
+                    const float rr = fmaf(rx[j], rx[j], fmaf(ry[j], ry[j], rz[j] * rz[j]));
                     pj[j] = proj;
                     sj[j] = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
                     q2j[j] = fmaxf(
-                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
                         0.f);
 #pragma unroll
                     for (int f = 0; f < NF; ++f)
@@ -423,6 +457,7 @@ __global__ void __launch_bounds__(THREADS, 4)
                     // k == 0 and the patch reaches the launch plane: behind = proj < 0
                     // (kernels.py:348,375), re-decided in fp64 within the error bound
                     const float tolp = PROJ_ERR * ax.w;
+                    const int64_t grow = (b0 + jb) * a.max_seg + k;
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         if (pj[j] >= tolp) continue;
@@ -430,7 +465,7 @@ __global__ void __launch_bounds__(THREADS, 4)
                         if (pj[j] < -tolp || oi[j] < 0) continue;
                         const int64_t gi = 3 * (int64_t)oi[j];
                         double p64, t64;
-                        exact_d2(S.r64[row], a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
+                        exact_d2(a, grow, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
                         ++ties;
                         lv[j] = !(p64 < 0.0);
                     }
@@ -443,44 +478,49 @@ __global__ void __launch_bounds__(THREADS, 4)
                                    evr[j]);
                 }
             } else if (word & WEDGE) {
-                pc2 += lane == 0;
                 // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
                 //      the reference picks by fp64 rounding, reproduced exactly here
                 const int k = __ffs(surv) - 1;
                 const int ra = r0 + k, rb = ra + 1;
-                const Row64 ga = S.r64[ra], gb = S.r64[rb];
-                const double ldx = __dmul_rn(ga.len, ga.dx), ldy = __dmul_rn(ga.len, ga.dy),
-                             ldz = __dmul_rn(ga.len, ga.dz);
                 const int64_t grow = (b0 + jb) * a.max_seg + k;
-                const float sa = (float)(a.seg_s0[grow] + ga.len);  // s0_k + t, t = len
-                const float sb = (float)a.seg_s0[grow + 1];          // s0_{k+1} + 0
-                const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
-                const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
-                const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
+                const double lena = a.seg_len[grow];
+                const double oax = a.seg_origin[3 * grow], oay = a.seg_origin[3 * grow + 1],
+                             oaz = a.seg_origin[3 * grow + 2];
+                const double obx = a.seg_origin[3 * grow + 3], oby = a.seg_origin[3 * grow + 4],
+                             obz = a.seg_origin[3 * grow + 5];
+                const double ldx = __dmul_rn(lena, a.seg_dir[3 * grow]);
+                const double ldy = __dmul_rn(lena, a.seg_dir[3 * grow + 1]);
+                const double ldz = __dmul_rn(lena, a.seg_dir[3 * grow + 2]);
+                const float sa = (float)(a.seg_s0[grow] + lena);  // s0_k + t, t = len
+                const float sb = (float)a.seg_s0[grow + 1];       // s0_{k+1} + 0
+                const float4 g1a = G.geo1[ra], g2a = G.geo2[ra];
+                const float4 g1b = G.geo1[rb], g2b = G.geo2[rb];
+                const float Aa = G.aux[ra].y, Ab = G.aux[rb].y;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     if (oi[j] < 0) continue;
                     const int64_t gi = 3 * (int64_t)oi[j];
                     const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
-                    const double vx = __dsub_rn(__dsub_rn(px, ga.ox), ldx);
-                    const double vy = __dsub_rn(__dsub_rn(py, ga.oy), ldy);
-                    const double vz = __dsub_rn(__dsub_rn(pz, ga.oz), ldz);
+                    const double vx = __dsub_rn(__dsub_rn(px, oax), ldx);
+                    const double vy = __dsub_rn(__dsub_rn(py, oay), ldy);
+                    const double vz = __dsub_rn(__dsub_rn(pz, oaz), ldz);
                     const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)),
                                                 __dmul_rn(vz, vz));
-                    const double wx = __dsub_rn(px, gb.ox), wy = __dsub_rn(py, gb.oy),
-                                 wz = __dsub_rn(pz, gb.oz);
+                    const double wx = __dsub_rn(px, obx), wy = __dsub_rn(py, oby),
+                                 wz = __dsub_rn(pz, obz);
                     const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)),
                                                 __dmul_rn(wz, wz));
                     const bool wb = db < da;  // strict: equal distances keep segment k
                     const float4 g1 = wb ? g1b : g1a;
                     const float4 g2 = wb ? g2b : g2a;
+                    const float rr = fmaf(rx[j], rx[j], fmaf(ry[j], ry[j], rz[j] * rz[j]));
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float q2 = fmaxf(
-                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
                         0.f);
                     float base[NF];
 #pragma unroll
-                    for (int f = 0; f < NF; ++f) base[f] = wb ? S.anc[3 * f + 1][rb] : S.anc[3 * f + 2][ra];
+                    for (int f = 0; f < NF; ++f) base[f] = wb ? G.anc[3 * f + 1][rb] : G.anc[3 * f + 2][ra];
                     ++ties;
                     ++nbp;
                     contribute<NF>(K, a.use_cutoff, wb ? sb : sa, q2, wb ? Ab : Aa, base, pre[j],
@@ -488,8 +528,7 @@ __global__ void __launch_bounds__(THREADS, 4)
                 }
             } else {
                 // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
-                pc3 += lane == 0;
-                const float tie_abs = S.btie[jb];
+                const float tie_abs = S.btie[warp][jb];
                 float best[R], second[R];
                 int kb[R];
 #pragma unroll
@@ -500,8 +539,8 @@ __global__ void __launch_bounds__(THREADS, 4)
                 }
                 for (unsigned m = surv; m; m &= m - 1) {
                     const int k = __ffs(m) - 1;
-                    const float4 g0 = S.geo0[r0 + k];
-                    const float4 g1 = S.geo1[r0 + k];
+                    const float4 g0 = G.geo0[r0 + k];
+                    const float4 g1 = G.geo1[r0 + k];
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
@@ -518,26 +557,26 @@ __global__ void __launch_bounds__(THREADS, 4)
                 for (int j = 0; j < R; ++j) {
                     const int k = kb[j];
                     bool exact = second[j] - best[j] <= fmaf(TIE_REL, second[j], tie_abs);
-                    const float4 g0 = S.geo0[r0 + k];
-                    const float4 g1 = S.geo1[r0 + k];
-                    const float4 ax = S.aux[r0 + k];
+                    const float4 g0 = G.geo0[r0 + k];
+                    const float4 g1 = G.geo1[r0 + k];
+                    const float4 ax = G.aux[r0 + k];
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
+                    const float rr = fmaf(rx[j], rx[j], fmaf(ry[j], ry[j], rz[j] * rz[j]));
                     if (k == 0 && fabsf(proj) <= PROJ_ERR * ax.w) exact = true;
                     float s, q2, A, base[NF];
                     if (!exact) {
                         if (k == 0 && proj < 0.f) continue;  // behind the source
-                        const float4 g2 = S.geo2[r0 + k];
-                        const float t = fminf(fmaxf(proj, 0.f), g0.w);
-                        s = ax.x + t;
+                        const float4 g2 = G.geo2[r0 + k];
+                        s = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
                         A = ax.y;
-                        q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                        q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
                                    0.f);
 #pragma unroll
                         for (int f = 0; f < NF; ++f)
-                            base[f] = proj <= 0.f ? S.anc[3 * f + 1][r0 + k]
-                                                  : (proj >= g0.w ? S.anc[3 * f + 2][r0 + k]
-                                                                  : fmaf(K.kappa[f], dl, S.anc[3 * f][r0 + k]));
+                            base[f] = proj <= 0.f ? G.anc[3 * f + 1][r0 + k]
+                                                  : (proj >= g0.w ? G.anc[3 * f + 2][r0 + k]
+                                                                  : fmaf(K.kappa[f], dl, G.anc[3 * f][r0 + k]));
                     } else {
                         // exact re-decision among the contenders, ascending k, strict <
                         if (oi[j] < 0) continue;
@@ -549,17 +588,18 @@ __global__ void __launch_bounds__(THREADS, 4)
                         for (unsigned m = surv; m; m &= m - 1) {
                             const int kk = __ffs(m) - 1;
                             // a segment can beat the fp32 winner only within the error bound
-                            const float4 h0 = S.geo0[r0 + kk];
-                            const float4 h1 = S.geo1[r0 + kk];
+                            const float4 h0 = G.geo0[r0 + kk];
+                            const float4 h1 = G.geo1[r0 + kk];
                             const float vx0 = rx[j] + h0.x, vy0 = ry[j] + h0.y, vz0 = rz[j] + h0.z;
-                            const float pj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
-                            const float tt = fminf(fmaxf(pj, 0.f), h0.w);
+                            const float pjj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
+                            const float tt = fminf(fmaxf(pjj, 0.f), h0.w);
                             const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y,
                                         ez = vz0 - tt * h1.z;
                             const float d2k = ex * ex + ey * ey + ez * ez;
                             if (kk != k && fmaf(-TIE_REL, d2k, d2k - best[j]) > tie_abs) continue;
                             double p64, t64;
-                            const double d2 = exact_d2(S.r64[r0 + kk], px, py, pz, &p64, &t64);
+                            const double d2 = exact_d2(a, (b0 + jb) * a.max_seg + kk, px, py, pz,
+                                                       &p64, &t64);
                             if (d2 < bd) {
                                 bd = d2;
                                 bk = kk;
@@ -571,11 +611,11 @@ __global__ void __launch_bounds__(THREADS, 4)
                         const int64_t grow = (b0 + jb) * a.max_seg + bk;
                         const double s_ref = a.seg_s0[grow] + bt;  // reference s (kernels.py:344)
                         s = (float)s_ref;
-                        const float4 h1 = S.geo1[r0 + bk];
-                        const float4 h2 = S.geo2[r0 + bk];
-                        A = S.aux[r0 + bk].y;
+                        const float4 h1 = G.geo1[r0 + bk];
+                        const float4 h2 = G.geo2[r0 + bk];
+                        A = G.aux[r0 + bk].y;
                         const float dk = fmaf(rx[j], h1.x, fmaf(ry[j], h1.y, rz[j] * h1.z));
-                        q2 = fmaxf(fmaf(-dk, dk, fmaf(h2.x, rx[j], fmaf(h2.y, ry[j], fmaf(h2.z, rz[j], h2.w + rr[j])))),
+                        q2 = fmaxf(fmaf(-dk, dk, fmaf(h2.x, rx[j], fmaf(h2.y, ry[j], fmaf(h2.z, rz[j], h2.w + rr)))),
                                    0.f);
 #pragma unroll
                         for (int f = 0; f < NF; ++f) base[f] = (float)frac_turns(K.kappa64[f] * s_ref);
@@ -594,8 +634,7 @@ __global__ void __launch_bounds__(THREADS, 4)
                 S.acc[R * tid + j][f][1] += (double)pim[j][f];
                 pre[j][f] = pim[j][f] = 0.f;
             }
-        __syncthreads();
-        b0 += nbc;
+        __syncthreads();  // next chunk staged; this chunk's buffer may be reused
     }
     // ---- write back (in-place continuation) and evaluation counts (kernels.py:399)
 #pragma unroll
@@ -608,19 +647,19 @@ __global__ void __launch_bounds__(THREADS, 4)
         }
         a.evals[oi[j]] += evr[j];
     }
-    unsigned long long t = (unsigned long long)ties, q = (unsigned long long)nbp;
+    unsigned long long t[6] = {(unsigned long long)ties, (unsigned long long)nbp, pc[0], pc[1],
+                               pc[2], pc[3]};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        t += __shfl_xor_sync(0xffffffffu, t, o);
-        q += __shfl_xor_sync(0xffffffffu, q, o);
+    for (int i = 0; i < 6; ++i) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t[i] += __shfl_xor_sync(0xffffffffu, t[i], o);
     }
     if (lane == 0) {
-        if (t) atomicAdd(&stats->tie_pairs, t);
-        if (q) atomicAdd(&stats->nb_pairs, q);
-        atomicAdd(&stats->paths[0], (unsigned long long)pc0);
-        atomicAdd(&stats->paths[1], (unsigned long long)pc1);
-        atomicAdd(&stats->paths[2], (unsigned long long)pc2);
-        atomicAdd(&stats->paths[3], (unsigned long long)pc3);
+        if (t[0]) atomicAdd(&stats->tie_pairs, t[0]);
+        if (t[1]) atomicAdd(&stats->nb_pairs, t[1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (t[2 + i]) atomicAdd(&stats->paths[i], t[2 + i]);
     }
 }
 
