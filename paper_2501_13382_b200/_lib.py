@@ -7,12 +7,14 @@ present, calls raise immediately.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 import threading
 
 from .errors import BudgetError
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libbf_gbs.so"
+LIB_PATH = pathlib.Path(os.environ.get(
+    "BF_GBS_LIB", pathlib.Path(__file__).resolve().parent / "_lib" / "libbf_gbs.so"))
 
 BF_OK, BF_EINVAL, BF_ENOMEM, BF_ECUDA, BF_ENODEV, BF_EBUDGET = range(6)
 PRECISION = {"fp32": 0, "fp64": 1}

@@ -39,11 +39,20 @@
 namespace bf {
 namespace {
 
+#ifndef BF_CB
+#define BF_CB 32
+#endif
+#ifndef BF_ROWCAP
+#define BF_ROWCAP 128
+#endif
+#ifndef BF_MINB
+#define BF_MINB 5
+#endif
 constexpr int THREADS = 128;
 constexpr int R = 4;                    // receivers per thread
 constexpr int TILE = THREADS * R;       // receivers per CTA
-constexpr int CB = 64;                  // max beams per staged chunk
-constexpr int ROWCAP = 256;             // max segment rows per staged chunk
+constexpr int CB = BF_CB;               // max beams per staged chunk
+constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk
 constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
 constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
 constexpr float PROJ_ERR = 3.814697265625e-06f;     // 2^-18 (x D): bound on |fp32 proj error|
@@ -128,6 +137,7 @@ template <int NF>
 struct Smem {
     Stage<NF> st[2];         // double-buffered: chunk c+1 is staged while c is summed
     unsigned surv[NWARPS][CB];  // per warp patch and beam: surviving segments + flags
+    unsigned live[NWARPS][(CB + 31) / 32];  // per warp patch: beams with any work
     float btie[NWARPS][CB];  // absolute tie tolerance of the beam
     double acc[TILE][NF][2];
 };
@@ -138,11 +148,12 @@ __device__ __forceinline__ void contribute(const Fp32Consts &K, int use_cutoff, 
                                            float A, const float *base, float (&pre)[NF],
                                            float (&pim)[NF], int &ev) {
     const float m2 = fmaf(s, s, K.b2);
+    if (NF == 1 && use_cutoff && q2 * K.cutk[0] > m2) return;  // ex_re < -36 (kernels.py:384)
     const float inv = rcp_approx(m2);
     const float gq = q2 * inv;
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-        if (use_cutoff && q2 * K.cutk[f] > m2) continue;  // ex_re < -36 (kernels.py:384)
+        if (NF > 1 && use_cutoff && q2 * K.cutk[f] > m2) continue;  // ex_re < -36
         const float g = K.hk[f] * gq;
         float turns = fmaf(g * s, 0.15915494309189535f, base[f]);
         turns -= rintf(turns);
@@ -304,7 +315,7 @@ __device__ __forceinline__ int chunk_len(const int32_t *__restrict__ seg_start, 
 }
 
 template <int NF>
-__global__ void __launch_bounds__(THREADS, (NF <= 2 ? 4 : 2))
+__global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const int32_t *__restrict__ seg_start,
                     const Fp32Consts K, GbsStats *stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -405,21 +416,30 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? 4 : 2))
         nnbc = chunk_len(seg_start, nb0, a.n_beams);
         // ---- warp work generation on this chunk: one lane per beam bounds the
         //      warp patch against the beam's segments (cut / behind / dominated)
-        for (int jb = lane; jb < nbc; jb += 32) {
-            const int r0 = G.brow[jb], ns = G.brow[jb + 1] - r0;
-            float D = 0.f;
-            for (int k = 0; k < ns; ++k) D = fmaxf(D, G.aux[r0 + k].w);
-            const unsigned word = classify(G, r0, ns, cwx, cwy, cwz, RW, D);
-            S.surv[warp][jb] = word;
-            S.btie[warp][jb] = TIE_ABS * D * D;
-            const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
-            pc[word == 0 ? 0 : (word & WEDGE) ? 2 : (m & (m - 1)) ? 3 : 1] += 1;
+        for (int g = 0; 32 * g < nbc; ++g) {
+            const int jb = 32 * g + lane;
+            unsigned word = 0;
+            if (jb < nbc) {
+                const int r0 = G.brow[jb], ns = G.brow[jb + 1] - r0;
+                float D = 0.f;
+                for (int k = 0; k < ns; ++k) D = fmaxf(D, G.aux[r0 + k].w);
+                word = classify(G, r0, ns, cwx, cwy, cwz, RW, D);
+                S.surv[warp][jb] = word;
+                S.btie[warp][jb] = TIE_ABS * D * D;
+                const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
+                pc[word == 0 ? 0 : (word & WEDGE) ? 2 : (m & (m - 1)) ? 3 : 1] += 1;
+            }
+            const unsigned live = __ballot_sync(0xffffffffu, word != 0);
+            if (lane == 0) S.live[warp][g] = live;
         }
         __syncwarp();
-        // ---- summation over the chunk's beams, ascending
-        for (int jb = 0; jb < nbc; ++jb) {
+        // ---- summation over the chunk's live beams, ascending (culled beams,
+        //      where every pair of the patch is cut or behind, are never visited)
+        for (int g = 0; 32 * g < nbc; ++g)
+        for (unsigned lm = S.live[warp][g]; lm;) {
+            const int jb = 32 * g + __ffs(lm) - 1;
+            lm &= lm - 1;
             const unsigned word = S.surv[warp][jb];
-            if (!word) continue;  // every pair of the patch is cut or behind
             const unsigned surv = word & ~(BEHIND_CHECK | WEDGE);
             const int r0 = G.brow[jb];
             if ((surv & (surv - 1)) == 0) {
