@@ -289,7 +289,8 @@ def run_ours(args):
         st = stats[-1]
         ev_sum = int(evals.sum().item())
         p_nb = st["nonbehind_pairs"]
-        flop, mufu = flop_model(float(n_loc) * sum_segs, p_nb, ev_sum, nf)
+        # FLOP model over the work-list survivors: candidate pairs only
+        flop, mufu = flop_model(float(st["candidate_pair_segs"]), p_nb, ev_sum, nf)
         kernel_s = kern_max / 1e3
         ach = flop / kernel_s / 1e12
         clocks = clk.summary()
@@ -322,7 +323,9 @@ def run_ours(args):
                          "algorithmic_model": "SURVEY.md 8(d): 19*N_r*sum(n_segs) + "
                                               "(16+5F)*P_nb + 22*E FLOP; P_nb + 3E MUFU",
                          "nonbehind_pairs": p_nb, "evaluations": ev_sum,
-                         "tie_pairs": st["tie_pairs"], "patch_beams": st["patch_beams"]},
+                         "tie_pairs": st["tie_pairs"], "patch_beams": st["patch_beams"],
+                         "candidate_pairs": st["candidate_pairs"],
+                         "dense_pairs": int(nb) * int(n_loc)},
             "clocks": clocks,
         }
     if world == 1 and not args.no_cpu_baseline:

@@ -106,6 +106,20 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
                           int64_t beam_hi, int precision, int flags, int device,
                           void *stream);
 
+/*
+ * Work list of the fp32 path, exposed for verification: the
+ * Morton receiver order perm (n_obs), tile centres/radii centre (n_tiles x 4:
+ * x, y, z, R_T) and the candidate bitmask bits (n_tiles x ceil(n_beams/32)
+ * uint32, bit b%32 of word b/32 = beam b may contribute to some receiver of the
+ * tile).  Host buffers; exact fp64 test, reproduced bit for bit by
+ * oracle/worklist_oracle.c.
+ */
+int bf_worklist(const double *seg_origin, const double *seg_dir, const double *seg_len,
+                const double *seg_s0, const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
+                const double *obs, int64_t n_obs, const double *omegas, int64_t nf, double c,
+                double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
+                int64_t n_tiles_cap, int64_t *n_tiles_out, int device);
+
 /* Receivers per tile of the fp32 summation kernel. */
 int bf_tile_size(void);
 
@@ -159,11 +173,13 @@ int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_by
                    int64_t *chunk_sizes, int64_t max_chunks, int64_t *n_chunks);
 
 /* Statistics of the last fp32 bf_gbs_accumulate* call on this thread:
- * candidate (beam, receiver) pairs after work-list culling, total pairs, fp64
- * tie re-decisions, receiver tiles, non-behind pairs (P_nb) and the CUDA-event
- * duration of the summation kernel on its launch stream. Any pointer may be NULL. */
+ * candidate (beam, receiver) pairs of the tile work list, total pairs, fp64
+ * tie re-decisions, receiver tiles, non-behind pairs (P_nb), the CUDA-event
+ * duration of the summation kernel on its launch stream, and the sum of n_segs
+ * over candidate pairs (the scan term of the FLOP model). Any pointer may be NULL. */
 int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
-                  int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms);
+                  int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms,
+                  int64_t *candidate_pair_segs);
 
 /* Work-generation outcome of the last fp32 call on this thread, counted per
  * (warp patch of 128 receivers, beam) item: culled (every pair cut/behind),

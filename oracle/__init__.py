@@ -5,4 +5,5 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 (paper_2501_13382_b200) never imports it and fails loudly without its CUDA
 library.
 """
-from .oracle import build, gbs_accumulate, load_bundle, nearest_on_segments, trace  # noqa: F401
+from .oracle import (build, gbs_accumulate, load_bundle, nearest_on_segments,  # noqa: F401
+                     trace, worklist)

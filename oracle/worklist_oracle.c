@@ -1,0 +1,55 @@
+/*
+ * CPU ORACLE -- test infrastructure only.  Bit-exact restatement of the tile-level
+ * work list of the fp32 GBS path (repo:paper_2501_13382_b200/csrc/exact_fp64.cu,
+ * beam_dead_for_tile / worklist_kernel), i.e. of SURVEY.md 8(a) row a9:
+ * a beam is not a candidate for a receiver tile (centre c, radius R_T) when every
+ * segment k is either cut for the whole tile (its infinite line is farther than
+ * R_k + R_T, R_k^2 = 72 c (s_end^2 + b^2)/(omega_min b), kernels.py:377-385) or,
+ * for k == 0, the tile lies behind the launch plane (kernels.py:348,375).
+ * Same fp64 operation order, no FMA (-ffp-contract=off), IEEE sqrt.
+ */
+#include <math.h>
+#include <stdint.h>
+
+static int beam_dead(const double *so, const double *sd, const double *sl, const double *ss0,
+                     const int32_t *n_segs, int64_t max_seg, double width_b, int64_t b,
+                     double cx, double cy, double cz, double rt, double rscale) {
+    int ns = n_segs[b];
+    for (int k = 0; k < ns; ++k) {
+        int64_t row = b * max_seg + k;
+        double wx = cx - so[3 * row], wy = cy - so[3 * row + 1], wz = cz - so[3 * row + 2];
+        double dx = sd[3 * row], dy = sd[3 * row + 1], dz = sd[3 * row + 2];
+        double proj = wx * dx + wy * dy + wz * dz;
+        double ux = wx - proj * dx, uy = wy - proj * dy, uz = wz - proj * dz;
+        double qp = sqrt(ux * ux + uy * uy + uz * uz);
+        double se = ss0[row] + sl[row];
+        double rk = sqrt(rscale * (se * se + width_b * width_b));
+        int dead = qp - rt > rk * (1.0 + 1e-6) + 1e-6;
+        if (k == 0) dead = dead || (proj + rt < -1e-6);
+        if (!dead) return 0;
+    }
+    return 1;
+}
+
+/* centre: (n_tiles, 4) = x, y, z, R_T.  bits: (n_tiles, ceil(n_beams/32)). */
+void oracle_worklist(const double *so, const double *sd, const double *sl, const double *ss0,
+                     const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
+                     const double *centre, int64_t n_tiles, double c, double width_b,
+                     double omega_min, int use_cutoff, uint32_t *bits) {
+    const double rscale = use_cutoff ? 72.0 * c / (omega_min * width_b) : INFINITY;
+    const int64_t n_words = (n_beams + 31) / 32;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        const double *ct = centre + 4 * t;
+        for (int64_t w = 0; w < n_words; ++w) {
+            uint32_t m = 0;
+            for (int j = 0; j < 32; ++j) {
+                int64_t b = 32 * w + j;
+                if (b < n_beams &&
+                    !beam_dead(so, sd, sl, ss0, n_segs, max_seg, width_b, b, ct[0], ct[1], ct[2],
+                               ct[3], rscale))
+                    m |= 1u << j;
+            }
+            bits[t * n_words + w] = m;
+        }
+    }
+}

@@ -24,7 +24,7 @@ EXPORTS = (
     "bf_version", "bf_last_error", "bf_device_count", "bf_launch_count",
     "bf_gbs_accumulate", "bf_gbs_accumulate_dev", "bf_nearest_on_segments",
     "bf_trace_range_dev", "bf_field_finalize_dev", "bf_plan_chunks", "bf_last_stats",
-    "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats",
+    "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats", "bf_worklist",
 )
 FLAG_OBS_PRESORTED = 1
 
@@ -60,9 +60,11 @@ def _declare(lib):
                                         I64] + [VP] * 9 + [I64, I64, I64, INT, VP])
     lib.bf_field_finalize_dev.argtypes = [VP, I64, F64, VP, VP, INT, VP]
     lib.bf_plan_chunks.argtypes = [I64, I64, I64, I64P, I64, I64P]
-    lib.bf_last_stats.argtypes = [I64P, I64P, I64P, I64P, I64P, D]
+    lib.bf_last_stats.argtypes = [I64P, I64P, I64P, I64P, I64P, D, I64P]
     lib.bf_probe_peaks.argtypes = [INT, D, D]
     lib.bf_last_path_stats.argtypes = [I64P] * 4
+    lib.bf_worklist.argtypes = [VP, VP, VP, VP, VP, I64, I64, VP, I64, VP, I64, F64, F64, INT,
+                                VP, VP, VP, I64, I64P, INT]
     for name in EXPORTS:
         if name not in ("bf_version", "bf_last_error", "bf_device_count", "bf_launch_count"):
             getattr(lib, name).restype = INT
@@ -105,12 +107,14 @@ def last_stats() -> dict:
     """Statistics of the last fp32 summation on this thread (bf_last_stats)."""
     vals = [ctypes.c_int64(0) for _ in range(5)]
     ms = ctypes.c_double(0.0)
-    check(load().bf_last_stats(*[ctypes.byref(v) for v in vals], ctypes.byref(ms)))
+    cps = ctypes.c_int64(0)
+    check(load().bf_last_stats(*[ctypes.byref(v) for v in vals], ctypes.byref(ms),
+                               ctypes.byref(cps)))
     cand, total, ties, tiles, nbp = (v.value for v in vals)
     paths = [ctypes.c_int64(0) for _ in range(4)]
     check(load().bf_last_path_stats(*[ctypes.byref(v) for v in paths]))
     return {"candidate_pairs": cand, "total_pairs": total, "tie_pairs": ties, "n_tiles": tiles,
-            "nonbehind_pairs": nbp, "kernel_ms": ms.value,
+            "nonbehind_pairs": nbp, "kernel_ms": ms.value, "candidate_pair_segs": cps.value,
             "patch_beams": dict(zip(("culled", "single", "wedge", "multi"),
                                     (v.value for v in paths)))}
 

@@ -55,6 +55,7 @@ struct GbsStats {
     unsigned long long candidate_pairs;  // (beam, receiver) pairs inside candidate tiles
     unsigned long long tie_pairs;        // pairs re-decided in fp64
     unsigned long long nb_pairs;         // non-behind pairs (P_nb of SURVEY 8(d))
+    unsigned long long cand_pair_segs;   // sum over candidate pairs of the beam's n_segs
     unsigned long long paths[4];         // (warp patch, beam) items: culled, single, wedge, multi
     float kernel_ms;                     // CUDA-event duration of the summation kernel
 };
@@ -67,6 +68,8 @@ struct Tiling {
     const int32_t *perm;      // sorted position -> local observer index
     const float4 *rloc;       // sorted position -> (p - centre) fp32, w = unused
     const double4 *centre;    // per tile: centre xyz, radius
+    const uint32_t *wl_bits;  // work list: (tile, beam) candidate bits, wl_words per tile
+    int64_t wl_words;
 };
 
 // Launchers (return BF_OK or an error status).
@@ -82,6 +85,9 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                  double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
                  double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
                  int64_t row_base, cudaStream_t st);
+int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
+                    uint32_t *bits, unsigned long long *cand_beams,
+                    unsigned long long *cand_segs, cudaStream_t st);
 int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
                     double *spl, cudaStream_t st);
 

@@ -73,7 +73,7 @@ struct Buf {
 enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
-    B_QOBS, B_QBEAM, B_QOUT, B_NSW, B_COUNT
+    B_QOBS, B_QBEAM, B_QOUT, B_NSW, B_WLBITS, B_WLCNT, B_COUNT
 };
 
 struct DeviceCtx {
@@ -320,6 +320,24 @@ int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_
     return BF_OK;
 }
 
+// Tile-level work list (exact fp64 candidate test, exact_fp64.cu) for tiling t.
+int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st,
+                   unsigned long long **cand_out) {
+    const int64_t n_words = (a.n_beams + 31) / 32;
+    uint32_t *bits;
+    unsigned long long *cand;
+    BF_TRY(c->get(B_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
+    BF_TRY(c->get(B_WLCNT, (size_t)(2 * t.n_tiles), &cand));
+    BF_TRY_CUDA(cudaMemsetAsync(cand, 0, 2 * sizeof(unsigned long long) * t.n_tiles, st));
+    double wmin = INFINITY;
+    for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
+    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, cand, cand + t.n_tiles, st));
+    t.wl_bits = bits;
+    t.wl_words = n_words;
+    if (cand_out) *cand_out = cand;
+    return BF_OK;
+}
+
 // Runs the operator on device-resident LOCAL ranges (a.obs etc. already offset).
 int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st) {
     g_last_stats = GbsStats{};
@@ -331,6 +349,8 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     BF_TRY(build_tiling(c, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
     int32_t *seg_start;
     BF_TRY(build_seg_start(c, a.n_segs, a.n_beams, st, &seg_start));
+    unsigned long long *d_cand;
+    BF_TRY(build_worklist(c, a, t, st, &d_cand));
     GbsStats *d_stats;
     BF_TRY(c->get(B_STATS, 1, &d_stats));
     BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
@@ -345,7 +365,17 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     BF_TRY_CUDA(cudaMemcpyAsync(&h, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost, st));
     BF_TRY_CUDA(cudaStreamSynchronize(st));
     BF_TRY_CUDA(cudaEventElapsedTime(&h.kernel_ms, c->ev0, c->ev1));
-    h.candidate_pairs = (unsigned long long)g_last_total_pairs;
+    std::vector<unsigned long long> cand((size_t)(2 * t.n_tiles));
+    BF_TRY_CUDA(cudaMemcpy(cand.data(), d_cand, 2 * sizeof(unsigned long long) * t.n_tiles,
+                           cudaMemcpyDeviceToHost));
+    unsigned long long cp = 0, cs = 0;
+    for (int64_t i = 0; i < t.n_tiles; ++i) {
+        const int64_t in_tile = (i + 1 < t.n_tiles) ? t.tile : a.n_obs - i * t.tile;
+        cp += cand[(size_t)i] * (unsigned long long)in_tile;
+        cs += cand[(size_t)(t.n_tiles + i)] * (unsigned long long)in_tile;
+    }
+    h.candidate_pairs = cp;
+    h.cand_pair_segs = cs;
     g_last_stats = h;
     g_last_tiles = t.n_tiles;
     return BF_OK;
@@ -374,7 +404,9 @@ int bf_device_count(void) {
 uint64_t bf_launch_count(void) { return g_launches.load(); }
 
 int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
-                  int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms) {
+                  int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms,
+                  int64_t *candidate_pair_segs) {
+    if (candidate_pair_segs) *candidate_pair_segs = (int64_t)g_last_stats.cand_pair_segs;
     if (nonbehind_pairs) *nonbehind_pairs = (int64_t)g_last_stats.nb_pairs;
     if (kernel_ms) *kernel_ms = (double)g_last_stats.kernel_ms;
     if (candidate_pairs) *candidate_pairs = (int64_t)g_last_stats.candidate_pairs;
@@ -619,6 +651,64 @@ int bf_field_finalize_dev(const double *acc, int64_t n, double calibration, doub
 }
 
 int bf_tile_size(void) { return gbs_fp32_tile(); }
+
+int bf_worklist(const double *seg_origin, const double *seg_dir, const double *seg_len,
+                const double *seg_s0, const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
+                const double *obs, int64_t n_obs, const double *omegas, int64_t nf, double c,
+                double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
+                int64_t n_tiles_cap, int64_t *n_tiles_out, int device) {
+    if (max_seg < 1 || n_beams < 1 || n_obs < 1 || nf < 1 || nf > BF_MAXF)
+        return fail(BF_EINVAL, "bad sizes");
+    const int64_t T = gbs_fp32_tile(), n_tiles = (n_obs + T - 1) / T;
+    *n_tiles_out = n_tiles;
+    if (n_tiles > n_tiles_cap) return fail(BF_EINVAL, "need %lld tile slots", (long long)n_tiles);
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(device));
+    cudaStream_t st = ctx->stream;
+    const int64_t rows = n_beams * max_seg;
+    double *d_or, *d_dir, *d_len, *d_s0, *d_obs;
+    int32_t *d_ns;
+    BF_TRY(ctx->get(B_ORIGIN, 3 * rows, &d_or));
+    BF_TRY(ctx->get(B_DIR, 3 * rows, &d_dir));
+    BF_TRY(ctx->get(B_LEN, rows, &d_len));
+    BF_TRY(ctx->get(B_S0, rows, &d_s0));
+    BF_TRY(ctx->get(B_NSEGS, n_beams, &d_ns));
+    BF_TRY(ctx->get(B_OBS, 3 * n_obs, &d_obs));
+    const auto H2D = cudaMemcpyHostToDevice;
+    BF_TRY_CUDA(cudaMemcpyAsync(d_or, seg_origin, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_dir, seg_dir, 24 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_len, seg_len, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_s0, seg_s0, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_ns, n_segs, 4 * n_beams, H2D, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(d_obs, obs, 24 * n_obs, H2D, st));
+    GbsArgs a{};
+    a.seg_origin = d_or;
+    a.seg_dir = d_dir;
+    a.seg_len = d_len;
+    a.seg_s0 = d_s0;
+    a.n_segs = d_ns;
+    a.obs = d_obs;
+    a.max_seg = max_seg;
+    a.n_beams = n_beams;
+    a.n_obs = n_obs;
+    a.nf = (int)nf;
+    for (int f = 0; f < BF_MAXF; ++f) a.omegas[f] = f < nf ? omegas[f] : 0.0;
+    a.c = c;
+    a.width_b = width_b;
+    a.use_cutoff = use_cutoff ? 1 : 0;
+    Tiling t;
+    BF_TRY(build_tiling(ctx, d_obs, n_obs, false, st, &t));
+    BF_TRY(build_worklist(ctx, a, t, st, nullptr));
+    const int64_t n_words = (n_beams + 31) / 32;
+    const auto D2H = cudaMemcpyDeviceToHost;
+    BF_TRY_CUDA(cudaMemcpyAsync(perm, t.perm, 4 * n_obs, D2H, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(centre, t.centre, 32 * n_tiles, D2H, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(bits, t.wl_bits, 4 * n_tiles * n_words, D2H, st));
+    BF_TRY_CUDA(cudaStreamSynchronize(st));
+    return BF_OK;
+}
 
 int bf_tile_order_dev(const double *obs, int64_t n, int32_t *perm, int device, void *stream) {
     if (n < 0 || n > INT32_MAX) return fail(BF_EINVAL, "bad observer count");

@@ -364,6 +364,65 @@ __global__ void __launch_bounds__(128) trace_kernel(const TraceArgs a) {
     a.n_refls[i - a.row_base] = n_refl;
 }
 
+// ------------------------------------------------------------ work list ----
+// Candidate (receiver tile, beam) pairs, SURVEY.md 8(a) row a9.  A beam is NOT a
+// candidate for a tile (centre c, radius R_T) when for every segment k either
+//   * the whole tile lies outside the cutoff cylinder of k's infinite line:
+//     |w - (w.d) d| - R_T > R_k (1 + 1e-6) + 1e-6 with w = c - o_k and
+//     R_k^2 = 72 c (s_end^2 + b^2) / (omega_min b), s_end = s0 + len
+//     (q^2 of the winner is measured to its infinite line, kernels.py:345-346,377, and
+//     s <= s_end, so ex_re < -36 for every receiver if k wins, kernels.py:382-385), or
+//   * k == 0 and the tile lies behind the launch plane: w.d + R_T < -1e-6 (if k = 0
+//     wins it is `behind`, kernels.py:348,375).
+// Fixed fp64 operation order, no FMA (this file is -fmad=false), IEEE sqrt/div:
+// oracle/worklist_oracle.c reproduces the bitmask bit for bit.
+__device__ __forceinline__ bool beam_dead_for_tile(const GbsArgs &a, int64_t b, double cx,
+                                                   double cy, double cz, double rt,
+                                                   double rscale) {
+    const int ns = a.n_segs[b];
+    for (int k = 0; k < ns; ++k) {
+        const int64_t row = b * a.max_seg + k;
+        const double wx = cx - a.seg_origin[3 * row], wy = cy - a.seg_origin[3 * row + 1],
+                     wz = cz - a.seg_origin[3 * row + 2];
+        const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
+                     dz = a.seg_dir[3 * row + 2];
+        const double proj = wx * dx + wy * dy + wz * dz;
+        const double ux = wx - proj * dx, uy = wy - proj * dy, uz = wz - proj * dz;
+        const double qp = sqrt(ux * ux + uy * uy + uz * uz);
+        const double se = a.seg_s0[row] + a.seg_len[row];
+        const double rk = sqrt(rscale * (se * se + a.width_b * a.width_b));
+        bool dead = qp - rt > rk * (1.0 + 1e-6) + 1e-6;
+        if (k == 0) dead = dead || (proj + rt < -1e-6);
+        if (!dead) return false;
+    }
+    return true;
+}
+
+// One warp per (tile, 32-beam word): bit j = beam 32*word + j is a candidate.
+__global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t n_tiles,
+                                int64_t n_words, double rscale, uint32_t *bits,
+                                unsigned long long *cand_beams, unsigned long long *cand_segs) {
+    const int64_t tile = blockIdx.x;
+    const int64_t word = (int64_t)blockIdx.y * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (tile >= n_tiles || word >= n_words) return;
+    const double4 c = centre[tile];
+    const int64_t b = 32 * word + lane;
+    bool cand = false;
+    if (b < a.n_beams) cand = !beam_dead_for_tile(a, b, c.x, c.y, c.z, c.w, rscale);
+    const unsigned m = __ballot_sync(0xffffffffu, cand);
+    int segs = cand ? a.n_segs[b] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) segs += __shfl_xor_sync(0xffffffffu, segs, o);
+    if (lane == 0) {
+        bits[tile * n_words + word] = m;
+        if (m) {
+            atomicAdd(&cand_beams[tile], (unsigned long long)__popc(m));
+            atomicAdd(&cand_segs[tile], (unsigned long long)segs);
+        }
+    }
+}
+
 __global__ void finalize_kernel(const double *acc, int64_t n, double calibration,
                                 double *pressure, double *spl) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -421,6 +480,21 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                 seg_s0, seg_refl, n_segs, n_refls, lo, hi, row_base};
     const unsigned blocks = (unsigned)((hi - lo + 127) / 128);
     trace_kernel<<<blocks, 128, 0, st>>>(a);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
+                    uint32_t *bits, unsigned long long *cand_beams,
+                    unsigned long long *cand_segs, cudaStream_t st) {
+    if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
+    const int64_t n_words = (a.n_beams + 31) / 32;
+    // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
+    const double rscale = a.use_cutoff ? 72.0 * a.c / (omega_min * a.width_b) : INFINITY;
+    dim3 grid((unsigned)n_tiles, (unsigned)((n_words + 3) / 4));
+    worklist_kernel<<<grid, 128, 0, st>>>(a, centre, n_tiles, n_words, rscale, bits, cand_beams,
+                                          cand_segs);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

@@ -423,7 +423,9 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                 const int r0 = G.brow[jb], ns = G.brow[jb + 1] - r0;
                 float D = 0.f;
                 for (int k = 0; k < ns; ++k) D = fmaxf(D, G.aux[r0 + k].w);
-                word = classify(G, r0, ns, cwx, cwy, cwz, RW, D);
+                const int64_t gb = b0 + jb;  // tile-level work list (exact fp64 test)
+                if ((tl.wl_bits[tile * tl.wl_words + (gb >> 5)] >> (gb & 31)) & 1u)
+                    word = classify(G, r0, ns, cwx, cwy, cwz, RW, D);
                 S.surv[warp][jb] = word;
                 S.btie[warp][jb] = TIE_ABS * D * D;
                 const unsigned m = word & ~(BEHIND_CHECK | WEDGE);

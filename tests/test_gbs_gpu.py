@@ -268,3 +268,36 @@ def test_calibrate_phi_vs_reference():
         p = gbs.sum_at_observer(z["probe"], pb, src.omegas[0], Atmosphere(20.0), src,
                                 precision=prec)
         assert abs(p - complex(z["probe_p"])) <= tol * abs(complex(z["probe_p"]))
+
+
+@pytest.mark.parametrize("name", ["city_street", "city_corner_f5", "cfg1_open_plane",
+                                  "city_street_nocut"])
+def test_worklist_bitexact_vs_oracle(name):
+    """Device work list (tile, beam) candidates == the C restatement, bit for bit."""
+    import ctypes
+
+    from paper_2501_13382_b200 import _lib
+    b = load_case(name)
+    obs = b["obs"]
+    n = obs.shape[0]
+    nb = b["n_segs"].shape[0]
+    T = int(_lib.load().bf_tile_size())
+    nt = -(-n // T)
+    perm = np.zeros(n, np.int32)
+    centre = np.zeros((nt, 4))
+    bits = np.zeros((nt, -(-nb // 32)), np.uint32)
+    got = ctypes.c_int64(0)
+    p = lambda a: ctypes.c_void_p(np.ascontiguousarray(a).ctypes.data)  # noqa: E731
+    use_cut = bool(b["use_cutoff"])
+    _lib.check(_lib.load().bf_worklist(
+        p(b["seg_origin"]), p(b["seg_dir"]), p(b["seg_len"]), p(b["seg_s0"]),
+        p(b["n_segs"].astype(np.int32)), nb, int(b["max_seg"]), p(obs), n, p(b["omegas"]),
+        b["omegas"].shape[0], float(b["c"]), -float(b["beam_param_im"]), int(use_cut),
+        ctypes.c_void_p(perm.ctypes.data), ctypes.c_void_p(centre.ctypes.data),
+        ctypes.c_void_p(bits.ctypes.data), nt, ctypes.byref(got), 0))
+    assert got.value == nt
+    assert np.array_equal(np.sort(perm), np.arange(n))
+    ref = oracle.worklist(b["seg_origin"], b["seg_dir"], b["seg_len"], b["seg_s0"],
+                          b["n_segs"], b["max_seg"], centre, float(b["c"]),
+                          -float(b["beam_param_im"]), b["omegas"].min(), use_cut)
+    assert np.array_equal(bits, ref)

@@ -87,3 +87,35 @@ def test_oracle_tracer_bitexact_vs_reference(name):
     assert np.array_equal(out["n_refls"], z["n_refls"])
     for f in ("seg_origin", "seg_dir", "seg_e1", "seg_e2", "seg_len", "seg_s0", "seg_refl"):
         assert np.array_equal(out[f].view(np.uint64), b[f].view(np.uint64)), f
+
+
+@pytest.mark.parametrize("name", ["city_street", "city_corner_f5", "cfg1_open_plane"])
+def test_worklist_is_sound(name):
+    """Culled (tile, beam) pairs are pairs the reference skips: no receiver of a culled
+    tile gets an evaluation from that beam (kernels.py:375,384-385)."""
+    b = load_case(name)
+    n1 = int(b["grid_n"][0])
+    obs = b["obs"][: n1 * 32]
+    # spatially compact 4x4 receiver blocks of the row-major grid
+    tiles = [np.array([(j0 + dj) * n1 + i0 + di for dj in range(4) for di in range(4)])
+             for j0 in range(0, 32, 4) for i0 in range(0, n1, 4)]
+    centre = []
+    for t in tiles:
+        p = obs[t]
+        c = 0.5 * (p.min(0) + p.max(0))
+        centre.append([*c, np.linalg.norm(p - c, axis=1).max()])
+    centre = np.array(centre)
+    om = b["omegas"]
+    bits = oracle.worklist(b["seg_origin"], b["seg_dir"], b["seg_len"], b["seg_s0"],
+                           b["n_segs"], b["max_seg"], centre, float(b["c"]),
+                           -float(b["beam_param_im"]), om.min(), True)
+    nb = b["n_segs"].shape[0]
+    cand = np.unpackbits(bits.view(np.uint8), bitorder="little").reshape(len(tiles), -1)[:, :nb]
+    assert 0 < cand.mean() < 1
+    for bi in range(0, nb, 3):
+        ev = np.zeros(obs.shape[0], np.int64)
+        acc = np.zeros((obs.shape[0], om.shape[0]), np.complex128)
+        oracle.gbs_accumulate(*gbs_args(b, obs), acc, ev, 0, obs.shape[0], bi, bi + 1)
+        for ti, t in enumerate(tiles):
+            if not cand[ti, bi]:
+                assert not ev[t].any() and not acc[t].any()
