@@ -270,15 +270,20 @@ def test_calibrate_phi_vs_reference():
         assert abs(p - complex(z["probe_p"])) <= tol * abs(complex(z["probe_p"]))
 
 
-@pytest.mark.parametrize("name", ["city_street", "city_corner_f5", "cfg1_open_plane",
-                                  "city_street_nocut"])
-def test_worklist_bitexact_vs_oracle(name):
+@pytest.mark.parametrize("name,dense", [("city_street", False), ("city_street", True),
+                                        ("city_corner_f5", True), ("cfg1_open_plane", True),
+                                        ("city_street_nocut", True)])
+def test_worklist_bitexact_vs_oracle(name, dense):
     """Device work list (tile, beam) candidates == the C restatement, bit for bit."""
     import ctypes
 
     from paper_2501_13382_b200 import _lib
     b = load_case(name)
     obs = b["obs"]
+    if dense:  # config-3 receiver spacing (0.25 m): small tiles, non-trivial candidate sets
+        x = np.arange(160) * 0.25 - 20.0
+        X, Y = np.meshgrid(x, x, indexing="xy")
+        obs = np.stack([X.ravel(), Y.ravel(), np.full(X.size, 1.8)], axis=1)
     n = obs.shape[0]
     nb = b["n_segs"].shape[0]
     T = int(_lib.load().bf_tile_size())
@@ -287,7 +292,13 @@ def test_worklist_bitexact_vs_oracle(name):
     centre = np.zeros((nt, 4))
     bits = np.zeros((nt, -(-nb // 32)), np.uint32)
     got = ctypes.c_int64(0)
-    p = lambda a: ctypes.c_void_p(np.ascontiguousarray(a).ctypes.data)  # noqa: E731
+    keep = []  # the arrays must outlive the call
+
+    def p(a):
+        a = np.ascontiguousarray(a)
+        keep.append(a)
+        return ctypes.c_void_p(a.ctypes.data)
+
     use_cut = bool(b["use_cutoff"])
     _lib.check(_lib.load().bf_worklist(
         p(b["seg_origin"]), p(b["seg_dir"]), p(b["seg_len"]), p(b["seg_s0"]),
@@ -301,3 +312,5 @@ def test_worklist_bitexact_vs_oracle(name):
                           b["n_segs"], b["max_seg"], centre, float(b["c"]),
                           -float(b["beam_param_im"]), b["omegas"].min(), use_cut)
     assert np.array_equal(bits, ref)
+    if dense:
+        assert 0 < np.unpackbits(bits.view(np.uint8)).mean() < 1
