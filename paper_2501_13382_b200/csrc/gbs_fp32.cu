@@ -63,6 +63,8 @@ struct Fp32Consts {
     float hk[BF_MAXF];       // omega*0.5/c: g = hk*q^2/m2 (kernels.py:382)
     float omega[BF_MAXF];
     float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36)
+    float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
+    float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
     float b, b2;             // width_b, width_b^2
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
     double rcut_scale;       // 72 c / (omega_min b): R_cut^2 = rcut_scale * (s_end^2 + b^2)
@@ -142,28 +144,51 @@ struct Smem {
     double acc[TILE][NF][2];
 };
 
-// Gaussian-beam contribution of one pair, all frequencies (kernels.py:377-399).
+// Gaussian-beam contribution of one pair whose cutoff test (NF == 1) already passed,
+// all frequencies (kernels.py:377-399): field = phi refl sqrt(c) (s + i b)/m2
+// exp(-g b) exp(i(omega s/c + g s)), contribution = i omega/(2 pi c) w_b field.
+template <int NF>
+__device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
+                                          float m2, float A, const float *base,
+                                          float (&pre)[NF], float (&pim)[NF], int &ev) {
+    const float inv = rcp_approx(m2);
+    const float gq = q2 * inv;
+    const float ainv = A * inv;
+    const float gqs = gq * s;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        if (NF > 1 && use_cutoff && q2 * K.cutk[f] > m2) continue;  // ex_re < -36
+        float turns = fmaf(gqs, K.hk2pi[f], base[f]);
+        turns -= rintf(turns);
+        const float ph = turns * 6.283185307179586f;
+        const float sn = sin_approx(ph), cs = cos_approx(ph);
+        const float amp = ainv * K.omega[f] * ex2_approx(gq * K.nhkbl2e[f]);
+        pre[f] = fmaf(-amp, fmaf(s, sn, K.b * cs), pre[f]);
+        pim[f] = fmaf(amp, fmaf(s, cs, -K.b * sn), pim[f]);
+        ++ev;
+    }
+}
+
 template <int NF>
 __device__ __forceinline__ void contribute(const Fp32Consts &K, int use_cutoff, float s, float q2,
                                            float A, const float *base, float (&pre)[NF],
                                            float (&pim)[NF], int &ev) {
     const float m2 = fmaf(s, s, K.b2);
     if (NF == 1 && use_cutoff && q2 * K.cutk[0] > m2) return;  // ex_re < -36 (kernels.py:384)
-    const float inv = rcp_approx(m2);
-    const float gq = q2 * inv;
+    eval_pair<NF>(K, use_cutoff, s, q2, m2, A, base, pre, pim, ev);
+}
+
+// Phase anchor of the nearest point: interior -> centre anchor + kappa (r.d);
+// clamped -> exact start / end anchor (turns).
+template <int NF>
+__device__ __forceinline__ void phase_base(const Fp32Consts &K, float proj, float dl, float len,
+                                           const float *anc, float *base) {
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-        if (NF > 1 && use_cutoff && q2 * K.cutk[f] > m2) continue;  // ex_re < -36
-        const float g = K.hk[f] * gq;
-        float turns = fmaf(g * s, 0.15915494309189535f, base[f]);
-        turns -= rintf(turns);
-        const float ph = turns * 6.283185307179586f;
-        const float sn = sin_approx(ph), cs = cos_approx(ph);
-        const float er = ex2_approx(g * (-K.b * 1.4426950408889634f));
-        const float amp = A * K.omega[f] * er * inv;
-        pre[f] = fmaf(-amp, fmaf(s, sn, K.b * cs), pre[f]);
-        pim[f] = fmaf(amp, fmaf(s, cs, -K.b * sn), pim[f]);
-        ++ev;
+        float bf = fmaf(K.kappa[f], dl, anc[3 * f]);
+        bf = proj >= len ? anc[3 * f + 2] : bf;
+        bf = proj <= 0.f ? anc[3 * f + 1] : bf;
+        base[f] = bf;
     }
 }
 
@@ -205,30 +230,29 @@ template <int NF>
 __device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns, float cwx,
                                              float cwy, float cwz, float RW, float D) {
     if (ns <= 0) return 0u;
+    // pass 1: nearest segment at the patch centre
     float best = INFINITY, p0 = 0.f;
     int kj = 0;
-    bool all_dead = true;
     for (int k = 0; k < ns; ++k) {
         float ux, uy, uz, proj;
         bool cut;
         const float dc = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &proj);
-        bool dead = cut;
-        if (k == 0) {
-            p0 = proj;
-            dead = dead || (proj + RW * 1.00002f + 2e-3f < 0.f);
-        }
-        all_dead = all_dead && dead;
+        if (k == 0) p0 = proj;
         if (dc < best) {
             best = dc;
             kj = k;
         }
     }
-    if (all_dead) return 0u;
+    // pass 2: survivors (segments that can be the nearest for some receiver of the
+    // patch) and whether every survivor is dead for the whole patch -- pruned
+    // segments never win, so then no pair of the patch contributes
     float ujx, ujy, ujz, pj;
     bool cj;
     const float dj = patch_dist(S, r0 + kj, cwx, cwy, cwz, RW, &ujx, &ujy, &ujz, &cj, &pj);
     const float sj = sweep(RW, dj);
+    const bool behind0 = p0 + RW * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
     unsigned mask = 1u << kj;
+    bool all_dead = cj || (kj == 0 && behind0);
     for (int k = 0; k < ns; ++k) {
         if (k == kj) continue;
         float ux, uy, uz, proj;
@@ -237,8 +261,12 @@ __device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns,
         // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * sup|grad d_k - grad d_j|
         const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
         const float lip = fminf(sqrtf(ex * ex + ey * ey + ez * ez) + sweep(RW, dk) + sj, 2.f);
-        if (!(dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk)) mask |= 1u << k;
+        if (!(dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk)) {
+            mask |= 1u << k;
+            all_dead = all_dead && (cut || (k == 0 && behind0));
+        }
     }
+    if (all_dead) return 0u;
     unsigned word = mask;
     // segment 0 survives and the patch reaches its launch plane
     if ((mask & 1u) && p0 - RW * 1.00002f - 2e-3f <= PROJ_ERR * D) word |= BEHIND_CHECK;
@@ -255,6 +283,30 @@ __device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns,
         if (pa - S.geo0[r0 + kl].w >= m1 && pb <= -m1) word = mask | WEDGE;
     }
     return word;
+}
+
+// Live mask of the R receivers of a single-segment-0 beam whose patch reaches the
+// launch plane: behind = proj < 0 (kernels.py:348,375); |proj| within the fp32
+// error bound is re-decided with the reference's exact fp64 projection.
+__device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Consts &K,
+                                             const float (&pj)[R], const int (&oi)[R], float D,
+                                             int64_t beam, int k, int &ties) {
+    const float tolp = PROJ_ERR * D;
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (pj[j] >= tolp) {
+            m |= 1u << j;
+            continue;
+        }
+        if (pj[j] < -tolp || oi[j] < 0) continue;
+        const int64_t gi = 3 * (int64_t)oi[j];
+        double p64, t64;
+        exact_d2(a, beam * a.max_seg + k, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
+        ++ties;
+        if (!(p64 < 0.0)) m |= 1u << j;
+    }
+    return m;
 }
 
 template <int NF>
@@ -456,8 +508,7 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
 #pragma unroll
                 for (int q = 0; q < 3 * NF; ++q) anc[q] = G.anc[q][row];
                 // geometry of all R receivers, branch-free (independent chains)
-                float sj[R], q2j[R], pj[R], base[R][NF];
-                bool lv[R];
+                float sj[R], q2j[R], pj[R], m2j[R], base[R][NF];
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
@@ -468,37 +519,22 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                     q2j[j] = fmaxf(
                         fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
                         0.f);
-#pragma unroll
-                    for (int f = 0; f < NF; ++f)
-                        base[j][f] = proj <= 0.f ? anc[3 * f + 1]
-                                                 : (proj >= g0.w ? anc[3 * f + 2]
-                                                                 : fmaf(K.kappa[f], dl, anc[3 * f]));
-                    lv[j] = true;
+                    m2j[j] = fmaf(sj[j], sj[j], K.b2);
+                    phase_base<NF>(K, proj, dl, g0.w, anc, base[j]);
                 }
-                if (word & BEHIND_CHECK) {
-                    // k == 0 and the patch reaches the launch plane: behind = proj < 0
-                    // (kernels.py:348,375), re-decided in fp64 within the error bound
-                    const float tolp = PROJ_ERR * ax.w;
-                    const int64_t grow = (b0 + jb) * a.max_seg + k;
+                unsigned lvm = (1u << R) - 1;
+                if (word & BEHIND_CHECK) lvm = behind_mask(a, K, pj, oi, ax.w, b0 + jb, k, ties);
+                nbp += __popc(lvm);
+                if (NF == 1 && a.use_cutoff) {
 #pragma unroll
-                    for (int j = 0; j < R; ++j) {
-                        if (pj[j] >= tolp) continue;
-                        lv[j] = false;
-                        if (pj[j] < -tolp || oi[j] < 0) continue;
-                        const int64_t gi = 3 * (int64_t)oi[j];
-                        double p64, t64;
-                        exact_d2(a, grow, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
-                        ++ties;
-                        lv[j] = !(p64 < 0.0);
-                    }
+                    for (int j = 0; j < R; ++j)
+                        if (q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);  // ex_re < -36
                 }
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    if (!lv[j]) continue;
-                    ++nbp;
-                    contribute<NF>(K, a.use_cutoff, sj[j], q2j[j], ax.y, base[j], pre[j], pim[j],
-                                   evr[j]);
-                }
+                for (int j = 0; j < R; ++j)
+                    if (lvm & (1u << j))
+                        eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], ax.y, base[j],
+                                      pre[j], pim[j], evr[j]);
             } else if (word & WEDGE) {
                 // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
                 //      the reference picks by fp64 rounding, reproduced exactly here
@@ -594,11 +630,10 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                         A = ax.y;
                         q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
                                    0.f);
+                        float anc[3 * NF];
 #pragma unroll
-                        for (int f = 0; f < NF; ++f)
-                            base[f] = proj <= 0.f ? G.anc[3 * f + 1][r0 + k]
-                                                  : (proj >= g0.w ? G.anc[3 * f + 2][r0 + k]
-                                                                  : fmaf(K.kappa[f], dl, G.anc[3 * f][r0 + k]));
+                        for (int q = 0; q < 3 * NF; ++q) anc[q] = G.anc[q][r0 + k];
+                        phase_base<NF>(K, proj, dl, g0.w, anc, base);
                     } else {
                         // exact re-decision among the contenders, ascending k, strict <
                         if (oi[j] < 0) continue;
@@ -717,6 +752,8 @@ int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
         K.hk[f] = (float)(w * 0.5 / a.c);
         K.omega[f] = (float)w;
         K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
+        K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
+        K.nhkbl2e[f] = (float)(-(w * 0.5 / a.c) * a.width_b * 1.4426950408889634);
     }
     K.b = (float)a.width_b;
     K.b2 = (float)(a.width_b * a.width_b);
