@@ -72,10 +72,28 @@ struct Tiling {
     int64_t wl_words;
 };
 
+// Workspace of the fp32 path (engine.cu allocates, gbs_fp32.cu fills and uses).
+// Row arrays use the padded row index b*max_seg + k of the reference bundle.
+struct Fp32Work {
+    double4 *p0;              // per row: origin xyz, len
+    double4 *p1;              // per row: direction xyz, s0
+    float2 *p2;               // per row: amplitude factor A, cutoff radius R_cut
+    float *pa;                // per row and frequency: phase anchors at s0, s0+len (turns)
+    float4 *prl;              // sorted receiver -> patch-local fp32 coordinates, |r|^2
+    double4 *pcen;            // per patch: centre xyz, radius
+    int *done;                // per patch: beam ranges already folded into acc
+    unsigned *unit_ctr;       // persistent-kernel work queue head
+    int64_t n_patches, n_ranges, range_beams;
+};
+
 // Launchers (return BF_OK or an error status).
 int launch_gbs_fp64(const GbsArgs &a, cudaStream_t st);
-int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
-                    GbsStats *d_stats, cudaStream_t st);
+int gbs_fp32_tile();
+int gbs_fp32_patch();
+int64_t gbs_fp32_range_beams(int64_t n_beams);
+int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st);
+int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
+                    cudaStream_t st);
 int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam,
                    int64_t n_query, double *out, cudaStream_t st);
 int launch_trace(const double *v0, const double *v1, const double *v2, const double *refl,

@@ -22,8 +22,6 @@
 
 namespace bf {
 
-int gbs_fp32_tile();
-
 namespace {
 thread_local char g_err[512] = "";
 thread_local GbsStats g_last_stats = {};
@@ -73,7 +71,8 @@ struct Buf {
 enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
-    B_QOBS, B_QBEAM, B_QOUT, B_NSW, B_WLBITS, B_WLCNT, B_COUNT
+    B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
+    B_DONE, B_UCTR, B_COUNT
 };
 
 struct DeviceCtx {
@@ -281,30 +280,6 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
     return BF_OK;
 }
 
-__global__ void widen_kernel(const int32_t *n_segs, int64_t nb, int32_t *out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nb) out[i] = n_segs[i];
-    if (i == nb) out[i] = 0;
-}
-
-// seg_start[b] = sum_{j<b} n_segs[j], b in [0, nb]
-int build_seg_start(DeviceCtx *c, const int32_t *n_segs, int64_t nb, cudaStream_t st,
-                    int32_t **out) {
-    int32_t *tmpin, *ss;
-    BF_TRY(c->get(B_NSW, nb + 1, &tmpin));
-    BF_TRY(c->get(B_SEGSTART, nb + 1, &ss));
-    widen_kernel<<<(unsigned)((nb + 1 + 255) / 256), 256, 0, st>>>(n_segs, nb, tmpin);
-    note_launch();
-    size_t tmp_bytes = 0;
-    BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tmpin, ss, (int)(nb + 1), st));
-    void *tmp;
-    BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
-    BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tmpin, ss, (int)(nb + 1), st));
-    note_launch();
-    *out = ss;
-    return BF_OK;
-}
-
 int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_t obs_lo,
              int64_t obs_hi, int64_t beam_lo, int64_t beam_hi, int precision) {
     if (max_seg < 1) return fail(BF_EINVAL, "max_seg must be >= 1");
@@ -347,10 +322,27 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     if (precision == BF_PRECISION_FP64) return launch_gbs_fp64(a, st);
     Tiling t;
     BF_TRY(build_tiling(c, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
-    int32_t *seg_start;
-    BF_TRY(build_seg_start(c, a.n_segs, a.n_beams, st, &seg_start));
     unsigned long long *d_cand;
     BF_TRY(build_worklist(c, a, t, st, &d_cand));
+    Fp32Work w{};
+    const int64_t rows = a.n_beams * a.max_seg;
+    const int P = gbs_fp32_patch();
+    w.n_patches = (a.n_obs + P - 1) / P;
+    w.range_beams = gbs_fp32_range_beams(a.n_beams);
+    w.n_ranges = (a.n_beams + w.range_beams - 1) / w.range_beams;
+    if (w.n_patches * w.n_ranges >= (int64_t)1 << 31)
+        return fail(BF_EINVAL, "too many (patch, beam range) units; split the call");
+    BF_TRY(c->get(B_P0, rows, &w.p0));
+    BF_TRY(c->get(B_P1, rows, &w.p1));
+    BF_TRY(c->get(B_P2, rows, &w.p2));
+    BF_TRY(c->get(B_PA, 2 * rows * a.nf, &w.pa));
+    BF_TRY(c->get(B_PRL, a.n_obs, &w.prl));
+    BF_TRY(c->get(B_PCEN, w.n_patches, &w.pcen));
+    BF_TRY(c->get(B_DONE, w.n_patches, &w.done));
+    BF_TRY(c->get(B_UCTR, 1, &w.unit_ctr));
+    BF_TRY_CUDA(cudaMemsetAsync(w.done, 0, sizeof(int) * w.n_patches, st));
+    BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, sizeof(unsigned), st));
+    BF_TRY(launch_fp32_prepare(a, t, w, st));
     GbsStats *d_stats;
     BF_TRY(c->get(B_STATS, 1, &d_stats));
     BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
@@ -359,7 +351,7 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         BF_TRY_CUDA(cudaEventCreate(&c->ev1));
     }
     BF_TRY_CUDA(cudaEventRecord(c->ev0, st));
-    BF_TRY(launch_gbs_fp32(a, t, seg_start, d_stats, st));
+    BF_TRY(launch_gbs_fp32(a, t, w, d_stats, st));
     BF_TRY_CUDA(cudaEventRecord(c->ev1, st));
     GbsStats h;
     BF_TRY_CUDA(cudaMemcpyAsync(&h, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost, st));

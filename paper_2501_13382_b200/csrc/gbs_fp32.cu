@@ -4,34 +4,28 @@
 // nearest_on_segments (kernels.py:304-349), re-designed for the B200 FP32/MUFU
 // pipes.  DESIGN.md holds the error analysis behind every tolerance here.
 //
-//  * One CTA owns a tile of TILE = THREADS x R receivers, spatially compact
-//    (Morton order, engine.cu); thread t holds receivers R*t..R*t+R-1, so a
-//    warp covers 128 consecutive Morton receivers (a compact patch).
-//    Receivers are held in TILE-LOCAL fp32 coordinates r = p - c_T.
-//  * Beams stream through shared memory in chunks (<= CB beams, <= ROWCAP
-//    segment rows).  Staging converts each segment once per tile, in fp64, to
-//    tile-local fp32 geometry (wc = c_T - o, d, len, centre projection Pc),
-//    the cutoff radius of the segment, fp64-exact phase anchors
-//    frac(omega/(2 pi c) * s) at the segment start / tile-centre projection /
-//    end, and keeps the fp64 row for exact re-decisions.
-//  * Per (warp, beam) a lane-parallel prepass (one lane per segment) bounds
-//    the warp patch against every segment: if every segment is provably cut
-//    (q_perp - R_W > R_cut) or, for segment 0, entirely behind the source,
-//    the beam is skipped for the warp; segments whose distance to the patch
-//    exceeds the nearest one by more than the patch diameter can never be
-//    the nearest point and are pruned.  Usually ONE segment survives and the
-//    pair needs no nearest-segment scan at all.
-//  * Several survivors: fp32 scan (strict <, first wins) carrying best and
-//    second-best clamped distance.  If the two are within the fp32 error
-//    bound -- corner ties at every reflection point are exact mathematical
-//    ties that the reference breaks by fp64 rounding -- the contenders are
-//    re-decided in fp64 with the reference operation order and no FMA.  The
-//    behind test (k==0, proj<0) is re-decided in fp64 the same way when
-//    |proj| is within its error bound.
-//  * Gaussian contribution in fp32 with MUFU ex2 / sin / cos / rcp, fp32
-//    partial sums per chunk flushed into per-receiver fp64 accumulators (in
-//    shared memory) that start from the caller's acc (in-place continuation,
-//    kernels.py:358-359).  Beams are visited in ascending order per receiver.
+//  * Receivers are Morton-sorted (engine.cu); 128 consecutive receivers form a
+//    warp PATCH (lane l holds receivers 4l..4l+3), four patches a work-list
+//    TILE.  patch_kernel stores every receiver in PATCH-LOCAL fp32
+//    coordinates r = p - c_P (fp64 subtraction) with |r|^2, so fp32 never
+//    represents ~100 m absolute coordinates.
+//  * pack_kernel converts the reference's padded fp64 bundle once per call into
+//    a row SoA: origin/len and direction/s0 in fp64, the amplitude factor and
+//    cutoff radius in fp32, and fp64-exact phase anchors (turns) at both ends.
+//  * The kernel is PERSISTENT: every warp is an independent worker that pulls
+//    (patch, beam range) units from an atomic queue (range-major, so all warps
+//    share one L2-resident slice of the bundle).  No CTA barriers at all.
+//  * Per unit the warp walks the candidate beams of its tile (the exact fp64
+//    work-list bitmask, exact_fp64.cu), <= 32 beams / ROWCAP rows per chunk:
+//    stage the rows into warp-private shared memory in patch-local fp32
+//    (fp64 conversion), classify each (patch, beam) with one lane per beam
+//    (cut / behind / dominated segments), then sum the live
+//    beams in ascending order through the single / corner-wedge / multi paths.
+//  * fp32 partial sums are flushed per chunk into fp64 accumulators; a unit
+//    folds its fp64 partial into the caller's acc (in-place continuation,
+//    kernels.py:358-359) only after the unit of the previous beam range of the
+//    same patch did (acquire/release flag per patch) -- the result is
+//    deterministic and independent of scheduling and of the number of ranks.
 #include <math.h>
 
 #include "common.cuh"
@@ -39,19 +33,21 @@
 namespace bf {
 namespace {
 
-#ifndef BF_CB
-#define BF_CB 32
-#endif
 #ifndef BF_ROWCAP
-#define BF_ROWCAP 128
+#define BF_ROWCAP 96
 #endif
 #ifndef BF_MINB
-#define BF_MINB 5
+#define BF_MINB 4
 #endif
-constexpr int THREADS = 128;
-constexpr int R = 4;                    // receivers per thread
-constexpr int TILE = THREADS * R;       // receivers per CTA
-constexpr int CB = BF_CB;               // max beams per staged chunk
+#ifndef BF_RANGES
+#define BF_RANGES 32
+#endif
+constexpr int R = 4;                    // receivers per lane
+constexpr int PATCH = 32 * R;           // receivers per warp patch
+constexpr int TILE = 4 * PATCH;         // receivers per work-list tile
+constexpr int WARPS = 4;                // independent warps per CTA
+constexpr int THREADS = 32 * WARPS;
+constexpr int CB = 32;                  // max beams per staged chunk
 constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk
 constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
 constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
@@ -60,7 +56,6 @@ constexpr float PROJ_ERR = 3.814697265625e-06f;     // 2^-18 (x D): bound on |fp
 struct Fp32Consts {
     float kappa[BF_MAXF];    // omega/(2 pi c), turns per metre
     double kappa64[BF_MAXF];
-    float hk[BF_MAXF];       // omega*0.5/c: g = hk*q^2/m2 (kernels.py:382)
     float omega[BF_MAXF];
     float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36)
     float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
@@ -91,7 +86,21 @@ __device__ __forceinline__ float cos_approx(float x) {
     asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ double frac_turns(double x) { return x - rint(x); }
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Exact fp64 clamped distance of kernels.py:328-340 for padded row `row`,
 // reference operation order, no FMA.
@@ -117,40 +126,36 @@ __device__ __forceinline__ double exact_d2(const GbsArgs &a, int64_t row, double
     return __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
 }
 
-constexpr int NWARPS = THREADS / 32;   // consumer warps (receiver patches)
-
 constexpr unsigned BEHIND_CHECK = 0x80000000u;
 constexpr unsigned WEDGE = 0x40000000u;
 
-// One staged chunk of beams, as seen from this tile.
+// Warp-private shared memory: one staged chunk of beams as seen from the patch,
+// plus the patch's fp64 accumulators.
 template <int NF>
-struct Stage {
-    float4 geo0[ROWCAP];     // wc.xyz (c_T - o), len
-    float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_T)
-    float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_T's offset from the line)
+struct WarpSmem {
+    float4 geo0[ROWCAP];     // wc.xyz (c_P - o), len
+    float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_P)
+    float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
     float4 aux[ROWCAP];      // s0, A (amplitude factor), R_cut, D (error scale)
-    float anc[3 * NF][ROWCAP];  // phase anchors: centre proj / start / end (turns)
-    int brow[CB + 1];
-    long long b0;
-    int nbc;                 // beams in the chunk; -1 terminates
+    float4 anc[NF][ROWCAP];  // phase anchors (turns): centre proj, start, end, -
+    int rowbeam[ROWCAP];     // chunk row -> chunk beam
+    int brow[CB + 1];        // chunk beam -> first chunk row
+    int gbeam[CB];           // chunk beam -> local beam index
+    unsigned surv[CB];       // surviving segments + flags (0 = culled)
+    float btie[CB];          // absolute tie tolerance of the beam
+    double acc[PATCH][NF][2];
+    int evc[PATCH];          // evaluation counts of the unit
 };
 
-template <int NF>
-struct Smem {
-    Stage<NF> st[2];         // double-buffered: chunk c+1 is staged while c is summed
-    unsigned surv[NWARPS][CB];  // per warp patch and beam: surviving segments + flags
-    unsigned live[NWARPS][(CB + 31) / 32];  // per warp patch: beams with any work
-    float btie[NWARPS][CB];  // absolute tie tolerance of the beam
-    double acc[TILE][NF][2];
-};
-
-// Gaussian-beam contribution of one pair whose cutoff test (NF == 1) already passed,
-// all frequencies (kernels.py:377-399): field = phi refl sqrt(c) (s + i b)/m2
-// exp(-g b) exp(i(omega s/c + g s)), contribution = i omega/(2 pi c) w_b field.
+// Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
+// sqrt(c) (s + i b)/m2 exp(-g b) exp(i(omega s/c + g s)), contribution
+// i omega/(2 pi c) w_b field.  `base[f]` is the fp64-anchored axial phase
+// omega s/(2 pi c) reduced to turns.
 template <int NF>
 __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
                                           float m2, float A, const float *base,
-                                          float (&pre)[NF], float (&pim)[NF], int &ev) {
+                                          float (&pre)[NF], float (&pim)[NF], unsigned &ev,
+                                          int shift) {
     const float inv = rcp_approx(m2);
     const float gq = q2 * inv;
     const float ainv = A * inv;
@@ -165,54 +170,45 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
         const float amp = ainv * K.omega[f] * ex2_approx(gq * K.nhkbl2e[f]);
         pre[f] = fmaf(-amp, fmaf(s, sn, K.b * cs), pre[f]);
         pim[f] = fmaf(amp, fmaf(s, cs, -K.b * sn), pim[f]);
-        ++ev;
+        ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
     }
-}
-
-template <int NF>
-__device__ __forceinline__ void contribute(const Fp32Consts &K, int use_cutoff, float s, float q2,
-                                           float A, const float *base, float (&pre)[NF],
-                                           float (&pim)[NF], int &ev) {
-    const float m2 = fmaf(s, s, K.b2);
-    if (NF == 1 && use_cutoff && q2 * K.cutk[0] > m2) return;  // ex_re < -36 (kernels.py:384)
-    eval_pair<NF>(K, use_cutoff, s, q2, m2, A, base, pre, pim, ev);
 }
 
 // Phase anchor of the nearest point: interior -> centre anchor + kappa (r.d);
 // clamped -> exact start / end anchor (turns).
 template <int NF>
 __device__ __forceinline__ void phase_base(const Fp32Consts &K, float proj, float dl, float len,
-                                           const float *anc, float *base) {
+                                           const WarpSmem<NF> &G, int row, float *base) {
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-        float bf = fmaf(K.kappa[f], dl, anc[3 * f]);
-        bf = proj >= len ? anc[3 * f + 2] : bf;
-        bf = proj <= 0.f ? anc[3 * f + 1] : bf;
+        const float4 an = G.anc[f][row];
+        float bf = fmaf(K.kappa[f], dl, an.x);
+        bf = proj >= len ? an.z : bf;
+        bf = proj <= 0.f ? an.y : bf;
         base[f] = bf;
     }
 }
 
-// Distance of a patch centre c to segment row `r` (fp32, tile-local), the unit
-// vector from the nearest point, whether the whole patch (radius RW) is cut for
-// this segment, and the centre's axial projection.
+// Distance of the patch centre (the origin of patch-local coordinates) to
+// segment row `r` (fp32), the unit vector from the nearest point, whether the
+// whole patch (radius RW) is cut for this segment, and the centre's projection.
 template <int NF>
-__device__ __forceinline__ float patch_dist(const Stage<NF> &S, int r, float cwx, float cwy,
-                                            float cwz, float RW, float *ux, float *uy, float *uz,
-                                            bool *cut, float *proj_out) {
+__device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, int r, float RW, float *ux,
+                                            float *uy, float *uz, bool *cut, float *proj_out) {
     const float4 g0 = S.geo0[r];
     const float4 g1 = S.geo1[r];
-    const float wx = cwx + g0.x, wy = cwy + g0.y, wz = cwz + g0.z;
-    const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
+    const float wx = g0.x, wy = g0.y, wz = g0.z;
+    const float proj = g1.w;
     const float t = fminf(fmaxf(proj, 0.f), g0.w);
     const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
-    const float dc = sqrtf(vx * vx + vy * vy + vz * vz);
-    const float inv = dc > 1e-6f ? 1.f / dc : 0.f;
+    const float dc = sqrt_approx(vx * vx + vy * vy + vz * vz);
+    const float inv = dc > 1e-6f ? rcp_approx(dc) : 0.f;
     *ux = vx * inv;
     *uy = vy * inv;
     *uz = vz * inv;
-    const float px = wx - proj * g1.x, py = wy - proj * g1.y, pz = wz - proj * g1.z;
+    // |u_c|^2 is the centre's squared distance to the infinite line
     const float rc = (S.aux[r].z + RW) * 1.00002f + 2e-3f;
-    *cut = px * px + py * py + pz * pz > rc * rc;
+    *cut = S.geo2[r].w > rc * rc;
     *proj_out = proj;
     return dc;
 }
@@ -221,46 +217,50 @@ __device__ __forceinline__ float patch_dist(const Stage<NF> &S, int r, float cwx
 // ball of radius RW around a point at distance d: I - proj is nonexpansive, so
 // the residual moves by <= RW and the angle is <= asin(RW/d) <= x/sqrt(1-x^2).
 __device__ __forceinline__ float sweep(float RW, float d) {
-    const float x = RW / fmaxf(d, 1e-6f);
+    const float x = RW * rcp_approx(fmaxf(d, 1e-6f));
     return x < 0.7f ? x * rsqrtf(1.f - x * x) * 1.0001f : 2.f;
 }
 
 // Work generation for one (patch, beam): survivor mask + flags (0 = culled).
 template <int NF>
-__device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns, float cwx,
-                                             float cwy, float cwz, float RW, float D) {
+__device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, int r0, int ns, float RW,
+                                             float D) {
     if (ns <= 0) return 0u;
     // pass 1: nearest segment at the patch centre
-    float best = INFINITY, p0 = 0.f;
+    float best = INFINITY;
     int kj = 0;
+#pragma unroll 1
     for (int k = 0; k < ns; ++k) {
-        float ux, uy, uz, proj;
-        bool cut;
-        const float dc = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &proj);
-        if (k == 0) p0 = proj;
-        if (dc < best) {
-            best = dc;
+        const float4 g0 = S.geo0[r0 + k];
+        const float4 g1 = S.geo1[r0 + k];
+        const float t = fminf(fmaxf(g1.w, 0.f), g0.w);
+        const float vx = g0.x - t * g1.x, vy = g0.y - t * g1.y, vz = g0.z - t * g1.z;
+        const float d2 = vx * vx + vy * vy + vz * vz;
+        if (d2 < best) {
+            best = d2;
             kj = k;
         }
     }
+    const float p0 = S.geo1[r0].w;
     // pass 2: survivors (segments that can be the nearest for some receiver of the
     // patch) and whether every survivor is dead for the whole patch -- pruned
     // segments never win, so then no pair of the patch contributes
     float ujx, ujy, ujz, pj;
     bool cj;
-    const float dj = patch_dist(S, r0 + kj, cwx, cwy, cwz, RW, &ujx, &ujy, &ujz, &cj, &pj);
+    const float dj = patch_dist(S, r0 + kj, RW, &ujx, &ujy, &ujz, &cj, &pj);
     const float sj = sweep(RW, dj);
     const bool behind0 = p0 + RW * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
     unsigned mask = 1u << kj;
     bool all_dead = cj || (kj == 0 && behind0);
+#pragma unroll 1
     for (int k = 0; k < ns; ++k) {
         if (k == kj) continue;
         float ux, uy, uz, proj;
         bool cut;
-        const float dk = patch_dist(S, r0 + k, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &proj);
+        const float dk = patch_dist(S, r0 + k, RW, &ux, &uy, &uz, &cut, &proj);
         // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * sup|grad d_k - grad d_j|
         const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
-        const float lip = fminf(sqrtf(ex * ex + ey * ey + ez * ez) + sweep(RW, dk) + sj, 2.f);
+        const float lip = fminf(sqrt_approx(ex * ex + ey * ey + ez * ez) + sweep(RW, dk) + sj, 2.f);
         if (!(dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk)) {
             mask |= 1u << k;
             all_dead = all_dead && (cut || (k == 0 && behind0));
@@ -275,10 +275,7 @@ __device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns,
     // distances are distances to the shared reflection point
     const int kl = __ffs(mask) - 1;
     if (mask == (3u << kl)) {
-        float ux, uy, uz, pa, pb;
-        bool cut;
-        patch_dist(S, r0 + kl, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pa);
-        patch_dist(S, r0 + kl + 1, cwx, cwy, cwz, RW, &ux, &uy, &uz, &cut, &pb);
+        const float pa = S.geo1[r0 + kl].w, pb = S.geo1[r0 + kl + 1].w;
         const float m1 = PROJ_ERR * D + RW * 1.00002f + 2e-3f;
         if (pa - S.geo0[r0 + kl].w >= m1 && pb <= -m1) word = mask | WEDGE;
     }
@@ -288,9 +285,9 @@ __device__ __forceinline__ unsigned classify(const Stage<NF> &S, int r0, int ns,
 // Live mask of the R receivers of a single-segment-0 beam whose patch reaches the
 // launch plane: behind = proj < 0 (kernels.py:348,375); |proj| within the fp32
 // error bound is re-decided with the reference's exact fp64 projection.
-__device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Consts &K,
-                                             const float (&pj)[R], const int (&oi)[R], float D,
-                                             int64_t beam, int k, int &ties) {
+__device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&pj)[R],
+                                             const int32_t *perm, int nvalid, float D,
+                                             int64_t beam, int k, unsigned &ties) {
     const float tolp = PROJ_ERR * D;
     unsigned m = 0;
 #pragma unroll
@@ -299,8 +296,8 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Cons
             m |= 1u << j;
             continue;
         }
-        if (pj[j] < -tolp || oi[j] < 0) continue;
-        const int64_t gi = 3 * (int64_t)oi[j];
+        if (pj[j] < -tolp || j >= nvalid) continue;
+        const int64_t gi = 3 * (int64_t)perm[j];
         double p64, t64;
         exact_d2(a, beam * a.max_seg + k, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
         ++ties;
@@ -309,238 +306,246 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Cons
     return m;
 }
 
-template <int NF>
-__device__ __forceinline__ void stage_chunk(Stage<NF> &G, const GbsArgs &a,
-                                            const int32_t *__restrict__ seg_start, int64_t b0,
-                                            int nbc, const double4 &cen, float RT,
-                                            const Fp32Consts &K, int tid) {
-    const int32_t base_row = seg_start[b0];
-    for (int j = tid; j <= nbc; j += THREADS) G.brow[j] = seg_start[b0 + j] - base_row;
-    if (tid == 0) {
-        G.nbc = nbc;
-        G.b0 = b0;
-    }
-    const int rows = seg_start[b0 + nbc] - base_row;
-    for (int r = tid; r < rows; r += THREADS) {
-        int lo = 0, hi = nbc;  // seg_start[b0+lo]-base <= r < seg_start[b0+hi]-base
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (seg_start[b0 + mid] - base_row <= r) lo = mid; else hi = mid;
+struct ExactPick {
+    double bt, bp, len;  // clamped t, projection and length of the winning segment
+    int bk;              // winning segment (ascending k, strict <)
+};
+
+// Exact re-decision of a near tie among the surviving segments `surv` of one
+// beam (kernels.py:320-348 with the reference's fp64 operations): only segments
+// whose fp32 distance is within the tie bound of the fp32 best can win.  Out of
+// line: one copy of the code serves every call site of the multi path.
+__device__ __noinline__ ExactPick exact_pick(const double *__restrict__ seg_origin,
+                                             const double *__restrict__ seg_dir,
+                                             const double *__restrict__ seg_len, int64_t row0,
+                                             const float4 *geo0, const float4 *geo1,
+                                             unsigned surv, int kf, float rx, float ry, float rz,
+                                             float best, float tie_abs, const double *p) {
+    const double px = p[0], py = p[1], pz = p[2];
+    ExactPick e{0.0, 0.0, 0.0, -1};
+    double bd = INFINITY;
+#pragma unroll 1
+    for (unsigned m = surv; m; m &= m - 1) {
+        const int kk = __ffs(m) - 1;
+        const float4 h0 = geo0[kk];
+        const float4 h1 = geo1[kk];
+        const float vx0 = rx + h0.x, vy0 = ry + h0.y, vz0 = rz + h0.z;
+        const float pjj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
+        const float tt = fminf(fmaxf(pjj, 0.f), h0.w);
+        const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y, ez = vz0 - tt * h1.z;
+        const float d2k = ex * ex + ey * ey + ez * ez;
+        if (kk != kf && fmaf(-TIE_REL, d2k, d2k - best) > tie_abs) continue;
+        const int64_t row = row0 + kk;
+        const double ox = seg_origin[3 * row], oy = seg_origin[3 * row + 1],
+                     oz = seg_origin[3 * row + 2];
+        const double dx = seg_dir[3 * row], dy = seg_dir[3 * row + 1], dz = seg_dir[3 * row + 2];
+        const double len = seg_len[row];
+        const double wx = __dsub_rn(px, ox), wy = __dsub_rn(py, oy), wz = __dsub_rn(pz, oz);
+        const double proj =
+            __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
+        const double t = proj < 0.0 ? 0.0 : (proj > len ? len : proj);
+        const double vx = __dsub_rn(wx, __dmul_rn(t, dx));
+        const double vy = __dsub_rn(wy, __dmul_rn(t, dy));
+        const double vz = __dsub_rn(wz, __dmul_rn(t, dz));
+        const double d2 =
+            __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+        if (d2 < bd) {
+            bd = d2;
+            e.bk = kk;
+            e.bt = t;
+            e.bp = proj;
+            e.len = len;
         }
-        const int jb = lo;
-        const int k = r - (seg_start[b0 + jb] - base_row);
-        const int64_t row = (b0 + jb) * a.max_seg + k;
-        const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
-                     oz = a.seg_origin[3 * row + 2];
-        const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
-                     dz = a.seg_dir[3 * row + 2];
-        const double len = a.seg_len[row], s0 = a.seg_s0[row];
-        const double wcx = cen.x - ox, wcy = cen.y - oy, wcz = cen.z - oz;
-        const double pc = wcx * dx + wcy * dy + wcz * dz;
-        const double ucx = wcx - pc * dx, ucy = wcy - pc * dy, ucz = wcz - pc * dz;
-        G.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)len);
-        G.geo1[r] = make_float4((float)dx, (float)dy, (float)dz, (float)pc);
-        G.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
+    }
+    return e;
+}
+
+// Stage chunk rows [0, nrows) into warp-private shared memory, patch-local.
+template <int NF>
+__device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, int64_t max_seg,
+                                           int nrows, double cx, double cy, double cz, float RW,
+                                           const Fp32Consts &K, int lane) {
+#pragma unroll 1
+    for (int r = lane; r < nrows; r += 32) {
+        const int jb = S.rowbeam[r];
+        const int64_t grow = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
+        const double4 P0 = w.p0[grow];  // o.xyz, len
+        const double4 P1 = w.p1[grow];  // d.xyz, s0
+        const float2 P2 = w.p2[grow];   // A, R_cut
+        const double wcx = cx - P0.x, wcy = cy - P0.y, wcz = cz - P0.z;
+        const double pc = wcx * P1.x + wcy * P1.y + wcz * P1.z;
+        const double ucx = wcx - pc * P1.x, ucy = wcy - pc * P1.y, ucz = wcz - pc * P1.z;
+        S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)P0.w);
+        S.geo1[r] = make_float4((float)P1.x, (float)P1.y, (float)P1.z, (float)pc);
+        S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
                                 (float)(ucx * ucx + ucy * ucy + ucz * ucz));
-        const double se = s0 + len;
-        const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
-        const double A = K.amp_scale * a.seg_refl[row] * a.weights[b0 + jb];
-        const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + len) + RT + 1.f;
-        G.aux[r] = make_float4((float)s0, (float)A, (float)rcut, D);
+        const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + P0.w) + RW + 1.f;
+        S.aux[r] = make_float4((float)P1.w, P2.x, P2.y, D);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-            G.anc[3 * f + 0][r] = (float)frac_turns(K.kappa64[f] * (s0 + pc));
-            G.anc[3 * f + 1][r] = (float)frac_turns(K.kappa64[f] * s0);
-            G.anc[3 * f + 2][r] = (float)frac_turns(K.kappa64[f] * se);
+            const float2 ae = reinterpret_cast<const float2 *>(w.pa)[grow * NF + f];
+            S.anc[f][r] = make_float4((float)frac_turns(K.kappa64[f] * (P1.w + pc)), ae.x, ae.y, 0.f);
         }
     }
 }
 
-// Greedy chunk after beam b0: <= CB beams and <= ROWCAP segment rows.
-__device__ __forceinline__ int chunk_len(const int32_t *__restrict__ seg_start, int64_t b0,
-                                         int64_t n_beams) {
-    if (b0 >= n_beams) return 0;
-    int64_t hi = b0 + CB < n_beams ? b0 + CB : n_beams;
-    const int32_t r0 = seg_start[b0];
-    while (seg_start[hi] - r0 > ROWCAP) --hi;
-    return (int)(hi - b0);
-}
+struct WarpCounters {
+    unsigned long long ties = 0, nbp = 0;  // per lane: fp64 re-decided / non-behind pairs
+    unsigned long long pc0 = 0, pc2 = 0, pc3 = 0, items = 0;  // (patch, beam) items (uniform)
+};
 
+// One (patch, beam range) unit.
 template <int NF>
-__global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
-    gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const int32_t *__restrict__ seg_start,
-                    const Fp32Consts K, GbsStats *stats) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem<NF> &S = *reinterpret_cast<Smem<NF> *>(smem_raw);
-
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const int64_t tile = blockIdx.x;
-    const double4 cen = tl.centre[tile];
-    const float RT = (float)cen.w;
-
-    // ---- receivers (tile-local coordinates); padding receivers sit at the
-    //      tile centre and are computed but never written back
-    float rx[R], ry[R], rz[R];
-    int oi[R];
+__device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, const Fp32Work &w,
+                                         const Fp32Consts &K, WarpSmem<NF> &S, int64_t p,
+                                         int64_t q, int lane, WarpCounters &wc) {
+    const double4 pcen = w.pcen[p];
+    const float RW = (float)pcen.w;
+    // ---- receivers (patch-local); padding receivers sit at the centre and are
+    //      computed but never written back
+    float rx[R], ry[R], rz[R], rr[R];
+    const int64_t sb = p * PATCH + R * lane;  // sorted position of receiver j = sb + j
+    const int32_t *perm = tl.perm + sb;       // observer index of receiver j = perm[j]
+    const int nvalid = tl.n - sb < R ? (int)(tl.n - sb) : R;  // receivers j < nvalid are real
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        const int64_t si = tile * TILE + R * tid + j;
-        const bool valid = si < tl.n;
-        oi[j] = valid ? tl.perm[si] : -1;
         float4 rl = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) rl = tl.rloc[si];
+        if (j < nvalid) rl = w.prl[sb + j];
         rx[j] = rl.x;
         ry[j] = rl.y;
         rz[j] = rl.z;
+        rr[j] = rl.w;
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            S.acc[R * tid + j][f][0] = valid ? a.acc[2 * ((int64_t)oi[j] * NF + f)] : 0.0;
-            S.acc[R * tid + j][f][1] = valid ? a.acc[2 * ((int64_t)oi[j] * NF + f) + 1] : 0.0;
-        }
+        for (int f = 0; f < NF; ++f) S.acc[R * lane + j][f][0] = S.acc[R * lane + j][f][1] = 0.0;
+        S.evc[R * lane + j] = 0;
     }
-    // ---- warp patch: bounding sphere of the warp's receivers
-    float cwx, cwy, cwz, RW;
-    {
-        float mnx = rx[0], mny = ry[0], mnz = rz[0], mxx = rx[0], mxy = ry[0], mxz = rz[0];
-#pragma unroll
-        for (int j = 1; j < R; ++j) {
-            mnx = fminf(mnx, rx[j]); mxx = fmaxf(mxx, rx[j]);
-            mny = fminf(mny, ry[j]); mxy = fmaxf(mxy, ry[j]);
-            mnz = fminf(mnz, rz[j]); mxz = fmaxf(mxz, rz[j]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
-            mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
-            mnz = fminf(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
-            mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
-            mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
-            mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
-        }
-        cwx = 0.5f * (mnx + mxx);
-        cwy = 0.5f * (mny + mxy);
-        cwz = 0.5f * (mnz + mxz);
-        float q = 0.f;
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const float ex = rx[j] - cwx, ey = ry[j] - cwy, ez = rz[j] - cwz;
-            q = fmaxf(q, ex * ex + ey * ey + ez * ez);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) q = fmaxf(q, __shfl_xor_sync(0xffffffffu, q, o));
-        RW = sqrtf(q) * 1.0001f + 1e-4f;
-    }
-
     float pre[R][NF], pim[R][NF];
-    int evr[R];
+    unsigned evp[R / 2] = {};  // evaluation counts of receivers 2i, 2i+1 (16-bit fields)
+    unsigned ties = 0, nbp = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        evr[j] = 0;
 #pragma unroll
         for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
     }
-    int ties = 0, nbp = 0;
-    unsigned pc[4] = {0, 0, 0, 0};
 
-    // ---- prologue: stage chunk 0; chunk bounds run one chunk ahead of staging
-    int64_t nb0 = 0;
-    int nnbc = chunk_len(seg_start, 0, a.n_beams);
-    if (nnbc > 0) stage_chunk(S.st[0], a, seg_start, nb0, nnbc, cen, RT, K, tid);
-    nb0 += nnbc;
-    nnbc = chunk_len(seg_start, nb0, a.n_beams);
-    __syncthreads();
-
-    for (int c = 0;; ++c) {
-        const Stage<NF> &G = S.st[c & 1];
-        const int nbc = G.nbc;
-        if (nnbc == 0 && c > 0 && nbc <= 0) break;
-        if (nbc <= 0) break;
-        const int64_t b0 = G.b0;
-        // stage the next chunk into the other buffer (free since the last barrier)
-        if (nnbc > 0) {
-            stage_chunk(S.st[(c + 1) & 1], a, seg_start, nb0, nnbc, cen, RT, K, tid);
-        } else if (tid == 0) {
-            S.st[(c + 1) & 1].nbc = 0;
-        }
-        nb0 += nnbc;
-        nnbc = chunk_len(seg_start, nb0, a.n_beams);
-        // ---- warp work generation on this chunk: one lane per beam bounds the
-        //      warp patch against the beam's segments (cut / behind / dominated)
-        for (int g = 0; 32 * g < nbc; ++g) {
-            const int jb = 32 * g + lane;
-            unsigned word = 0;
-            if (jb < nbc) {
-                const int r0 = G.brow[jb], ns = G.brow[jb + 1] - r0;
-                float D = 0.f;
-                for (int k = 0; k < ns; ++k) D = fmaxf(D, G.aux[r0 + k].w);
-                const int64_t gb = b0 + jb;  // tile-level work list (exact fp64 test)
-                if ((tl.wl_bits[tile * tl.wl_words + (gb >> 5)] >> (gb & 31)) & 1u)
-                    word = classify(G, r0, ns, cwx, cwy, cwz, RW, D);
-                S.surv[warp][jb] = word;
-                S.btie[warp][jb] = TIE_ABS * D * D;
-                const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
-                pc[word == 0 ? 0 : (word & WEDGE) ? 2 : (m & (m - 1)) ? 3 : 1] += 1;
+    const uint32_t *wl = tl.wl_bits + (p / (TILE / PATCH)) * tl.wl_words;
+    int64_t b = q * w.range_beams;
+    const int64_t bend = b + w.range_beams < a.n_beams ? b + w.range_beams : a.n_beams;
+    const unsigned lt = (1u << lane) - 1u;
+    while (b < bend) {
+        // ---- gather the next <= CB candidate beams of the tile (work-list bits)
+        int nbc = 0;
+#pragma unroll 1
+        while (nbc < CB && b < bend) {
+            const int64_t wi = b >> 5;
+            unsigned word = wl[wi] & (~0u << (b & 31));
+            const int64_t rem = bend - 32 * wi;
+            if (rem < 32) word &= (1u << rem) - 1u;
+            const int cnt = __popc(word);
+            const int take = min(cnt, CB - nbc);
+            const bool mine = (word >> lane) & 1u;
+            const int rank = __popc(word & lt);
+            if (mine && rank < take) S.gbeam[nbc + rank] = (int)(32 * wi + lane);
+            nbc += take;
+            if (take < cnt) {
+                const unsigned nx = __ballot_sync(0xffffffffu, mine && rank == take);
+                b = 32 * wi + __ffs(nx) - 1;
+            } else {
+                b = 32 * (wi + 1);
             }
-            const unsigned live = __ballot_sync(0xffffffffu, word != 0);
-            if (lane == 0) S.live[warp][g] = live;
+        }
+        if (b > bend) b = bend;
+        if (nbc == 0) break;
+        __syncwarp();
+        // ---- row capacity: keep the prefix of beams whose rows fit ROWCAP
+        int ns = 0;
+        if (lane < nbc) ns = a.n_segs[S.gbeam[lane]];
+        int incl = ns;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbc && incl <= ROWCAP);
+        const int nacc = __popc(fit);
+        if (nacc < nbc) b = __shfl_sync(0xffffffffu, lane < nbc ? S.gbeam[lane] : 0, nacc);
+        nbc = nacc;
+        const int nrows = __shfl_sync(0xffffffffu, incl, nbc - 1);
+        if (lane < nbc) {
+            S.brow[lane] = incl - ns;
+#pragma unroll 1
+            for (int k = incl - ns; k < incl; ++k) S.rowbeam[k] = lane;
+        }
+        if (lane == 0) S.brow[nbc] = nrows;
+        __syncwarp();
+        stage_rows<NF>(S, w, a.max_seg, nrows, pcen.x, pcen.y, pcen.z, RW, K, lane);
+        __syncwarp();
+        // ---- work generation: one lane per beam bounds the patch against the
+        //      beam's segments (cut / behind / dominated)
+        unsigned word = 0;
+        if (lane < nbc) {
+            const int r0 = S.brow[lane], nsb = S.brow[lane + 1] - r0;
+            float D = 0.f;
+#pragma unroll 1
+            for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.aux[r0 + k].w);
+            word = classify<NF>(S, r0, nsb, RW, D);
+            S.surv[lane] = word;
+            S.btie[lane] = TIE_ABS * D * D;
+        }
+        const unsigned live = __ballot_sync(0xffffffffu, word != 0);
+        {
+            const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
+            wc.items += nbc;
+            wc.pc0 += nbc - __popc(live);
+            wc.pc2 += __popc(__ballot_sync(0xffffffffu, (word & WEDGE) != 0));
+            wc.pc3 += __popc(__ballot_sync(0xffffffffu, word != 0 && !(word & WEDGE) &&
+                                                            (m & (m - 1)) != 0));
         }
         __syncwarp();
-        // ---- summation over the chunk's live beams, ascending (culled beams,
-        //      where every pair of the patch is cut or behind, are never visited)
-        for (int g = 0; 32 * g < nbc; ++g)
-        for (unsigned lm = S.live[warp][g]; lm;) {
-            const int jb = 32 * g + __ffs(lm) - 1;
+        // ---- summation over the chunk's live beams, ascending.  Each path yields
+        //      the nearest point of every receiver (s, q^2, row, proj, r.d) and the
+        //      mask of non-behind receivers; one shared tail applies the cutoff and
+        //      evaluates the contributions.
+#pragma unroll 1
+        for (unsigned lm = live; lm;) {
+            const int jb = __ffs(lm) - 1;
             lm &= lm - 1;
-            const unsigned word = S.surv[warp][jb];
-            const unsigned surv = word & ~(BEHIND_CHECK | WEDGE);
-            const int r0 = G.brow[jb];
+            const int64_t beam = S.gbeam[jb];
+            const unsigned bword = S.surv[jb];
+            const unsigned surv = bword & ~(BEHIND_CHECK | WEDGE);
+            const int r0 = S.brow[jb];
+            float sj[R], q2j[R], pj[R], dlj[R];
+            int rowj[R];
+            unsigned lvm;
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
                 const int k = __ffs(surv) - 1;
                 const int row = r0 + k;
-                const float4 g0 = G.geo0[row];
-                const float4 g1 = G.geo1[row];
-                const float4 g2 = G.geo2[row];
-                const float4 ax = G.aux[row];
-                float anc[3 * NF];
-#pragma unroll
-                for (int q = 0; q < 3 * NF; ++q) anc[q] = G.anc[q][row];
-                // geometry of all R receivers, branch-free (independent chains)
-                float sj[R], q2j[R], pj[R], m2j[R], base[R][NF];
+                const float4 g0 = S.geo0[row];
+                const float4 g1 = S.geo1[row];
+                const float4 g2 = S.geo2[row];
+                const float s0 = S.aux[row].x;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
-                    const float rr = fmaf(rx[j], rx[j], fmaf(ry[j], ry[j], rz[j] * rz[j]));
+                    rowj[j] = row;
+                    dlj[j] = dl;
                     pj[j] = proj;
-                    sj[j] = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
+                    sj[j] = s0 + fminf(fmaxf(proj, 0.f), g0.w);
                     q2j[j] = fmaxf(
-                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
+                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                         0.f);
-                    m2j[j] = fmaf(sj[j], sj[j], K.b2);
-                    phase_base<NF>(K, proj, dl, g0.w, anc, base[j]);
                 }
-                unsigned lvm = (1u << R) - 1;
-                if (word & BEHIND_CHECK) lvm = behind_mask(a, K, pj, oi, ax.w, b0 + jb, k, ties);
-                nbp += __popc(lvm);
-                if (NF == 1 && a.use_cutoff) {
-#pragma unroll
-                    for (int j = 0; j < R; ++j)
-                        if (q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);  // ex_re < -36
-                }
-#pragma unroll
-                for (int j = 0; j < R; ++j)
-                    if (lvm & (1u << j))
-                        eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], ax.y, base[j],
-                                      pre[j], pim[j], evr[j]);
-            } else if (word & WEDGE) {
+                lvm = (1u << R) - 1;
+                if (bword & BEHIND_CHECK)
+                    lvm = behind_mask(a, pj, perm, nvalid, S.aux[row].w, beam, k, ties);
+            } else if (bword & WEDGE) {
                 // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
                 //      the reference picks by fp64 rounding, reproduced exactly here
                 const int k = __ffs(surv) - 1;
                 const int ra = r0 + k, rb = ra + 1;
-                const int64_t grow = (b0 + jb) * a.max_seg + k;
+                const int64_t grow = beam * a.max_seg + k;
                 const double lena = a.seg_len[grow];
                 const double oax = a.seg_origin[3 * grow], oay = a.seg_origin[3 * grow + 1],
                              oaz = a.seg_origin[3 * grow + 2];
@@ -551,13 +556,13 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                 const double ldz = __dmul_rn(lena, a.seg_dir[3 * grow + 2]);
                 const float sa = (float)(a.seg_s0[grow] + lena);  // s0_k + t, t = len
                 const float sb = (float)a.seg_s0[grow + 1];       // s0_{k+1} + 0
-                const float4 g1a = G.geo1[ra], g2a = G.geo2[ra];
-                const float4 g1b = G.geo1[rb], g2b = G.geo2[rb];
-                const float Aa = G.aux[ra].y, Ab = G.aux[rb].y;
+                const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
+                const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
+                lvm = 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    if (oi[j] < 0) continue;
-                    const int64_t gi = 3 * (int64_t)oi[j];
+                    if (j >= nvalid) continue;
+                    const int64_t gi = 3 * (int64_t)perm[j];
                     const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
                     const double vx = __dsub_rn(__dsub_rn(px, oax), ldx);
                     const double vy = __dsub_rn(__dsub_rn(py, oay), ldy);
@@ -571,22 +576,20 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                     const bool wb = db < da;  // strict: equal distances keep segment k
                     const float4 g1 = wb ? g1b : g1a;
                     const float4 g2 = wb ? g2b : g2a;
-                    const float rr = fmaf(rx[j], rx[j], fmaf(ry[j], ry[j], rz[j] * rz[j]));
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                    const float q2 = fmaxf(
-                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
+                    q2j[j] = fmaxf(
+                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                         0.f);
-                    float base[NF];
-#pragma unroll
-                    for (int f = 0; f < NF; ++f) base[f] = wb ? G.anc[3 * f + 1][rb] : G.anc[3 * f + 2][ra];
-                    ++ties;
-                    ++nbp;
-                    contribute<NF>(K, a.use_cutoff, wb ? sb : sa, q2, wb ? Ab : Aa, base, pre[j],
-                                   pim[j], evr[j]);
+                    sj[j] = wb ? sb : sa;
+                    rowj[j] = wb ? rb : ra;
+                    pj[j] = wb ? -1.f : INFINITY;  // start anchor of k+1 / end anchor of k
+                    dlj[j] = 0.f;
+                    lvm |= 1u << j;
                 }
+                ties += __popc(lvm);
             } else {
                 // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
-                const float tie_abs = S.btie[warp][jb];
+                const float tie_abs = S.btie[jb];
                 float best[R], second[R];
                 int kb[R];
 #pragma unroll
@@ -595,10 +598,11 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                     second[j] = INFINITY;
                     kb[j] = 0;
                 }
+#pragma unroll 1
                 for (unsigned m = surv; m; m &= m - 1) {
                     const int k = __ffs(m) - 1;
-                    const float4 g0 = G.geo0[r0 + k];
-                    const float4 g1 = G.geo1[r0 + k];
+                    const float4 g0 = S.geo0[r0 + k];
+                    const float4 g1 = S.geo1[r0 + k];
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
@@ -611,136 +615,229 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
                         best[j] = fminf(best[j], d2);
                     }
                 }
+                lvm = 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    const int k = kb[j];
+                    int k = kb[j];
                     bool exact = second[j] - best[j] <= fmaf(TIE_REL, second[j], tie_abs);
-                    const float4 g0 = G.geo0[r0 + k];
-                    const float4 g1 = G.geo1[r0 + k];
-                    const float4 ax = G.aux[r0 + k];
-                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                    const float proj = dl + g1.w;
-                    const float rr = fmaf(rx[j], rx[j], fmaf(ry[j], ry[j], rz[j] * rz[j]));
-                    if (k == 0 && fabsf(proj) <= PROJ_ERR * ax.w) exact = true;
-                    float s, q2, A, base[NF];
+                    float4 g1 = S.geo1[r0 + k];
+                    float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
+                    float proj = dl + g1.w;
+                    if (k == 0 && fabsf(proj) <= PROJ_ERR * S.aux[r0].w) exact = true;
+                    float s;
                     if (!exact) {
                         if (k == 0 && proj < 0.f) continue;  // behind the source
-                        const float4 g2 = G.geo2[r0 + k];
-                        s = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
-                        A = ax.y;
-                        q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr)))),
-                                   0.f);
-                        float anc[3 * NF];
-#pragma unroll
-                        for (int q = 0; q < 3 * NF; ++q) anc[q] = G.anc[q][r0 + k];
-                        phase_base<NF>(K, proj, dl, g0.w, anc, base);
+                        s = S.aux[r0 + k].x + fminf(fmaxf(proj, 0.f), S.geo0[r0 + k].w);
                     } else {
                         // exact re-decision among the contenders, ascending k, strict <
-                        if (oi[j] < 0) continue;
+                        if (j >= nvalid) continue;
                         ++ties;
-                        const int64_t gi = 3 * (int64_t)oi[j];
-                        const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
-                        double bd = INFINITY, bt = 0.0, bp = 0.0;
-                        int bk = -1;
-                        for (unsigned m = surv; m; m &= m - 1) {
-                            const int kk = __ffs(m) - 1;
-                            // a segment can beat the fp32 winner only within the error bound
-                            const float4 h0 = G.geo0[r0 + kk];
-                            const float4 h1 = G.geo1[r0 + kk];
-                            const float vx0 = rx[j] + h0.x, vy0 = ry[j] + h0.y, vz0 = rz[j] + h0.z;
-                            const float pjj = vx0 * h1.x + vy0 * h1.y + vz0 * h1.z;
-                            const float tt = fminf(fmaxf(pjj, 0.f), h0.w);
-                            const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y,
-                                        ez = vz0 - tt * h1.z;
-                            const float d2k = ex * ex + ey * ey + ez * ez;
-                            if (kk != k && fmaf(-TIE_REL, d2k, d2k - best[j]) > tie_abs) continue;
-                            double p64, t64;
-                            const double d2 = exact_d2(a, (b0 + jb) * a.max_seg + kk, px, py, pz,
-                                                       &p64, &t64);
-                            if (d2 < bd) {
-                                bd = d2;
-                                bk = kk;
-                                bt = t64;
-                                bp = p64;
-                            }
-                        }
-                        if (bk == 0 && bt == 0.0 && bp < 0.0) continue;  // behind
-                        const int64_t grow = (b0 + jb) * a.max_seg + bk;
-                        const double s_ref = a.seg_s0[grow] + bt;  // reference s (kernels.py:344)
-                        s = (float)s_ref;
-                        const float4 h1 = G.geo1[r0 + bk];
-                        const float4 h2 = G.geo2[r0 + bk];
-                        A = G.aux[r0 + bk].y;
-                        const float dk = fmaf(rx[j], h1.x, fmaf(ry[j], h1.y, rz[j] * h1.z));
-                        q2 = fmaxf(fmaf(-dk, dk, fmaf(h2.x, rx[j], fmaf(h2.y, ry[j], fmaf(h2.z, rz[j], h2.w + rr)))),
-                                   0.f);
-#pragma unroll
-                        for (int f = 0; f < NF; ++f) base[f] = (float)frac_turns(K.kappa64[f] * s_ref);
+                        const ExactPick e = exact_pick(a.seg_origin, a.seg_dir, a.seg_len,
+                                                       beam * a.max_seg, S.geo0 + r0, S.geo1 + r0,
+                                                       surv, k, rx[j], ry[j], rz[j], best[j],
+                                                       tie_abs, a.obs + 3 * (int64_t)perm[j]);
+                        if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
+                        k = e.bk;
+                        s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
+                        g1 = S.geo1[r0 + k];
+                        dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
+                        // anchor choice follows the exact clamp
+                        proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
                     }
-                    ++nbp;
-                    contribute<NF>(K, a.use_cutoff, s, q2, A, base, pre[j], pim[j], evr[j]);
+                    const float4 g2 = S.geo2[r0 + k];
+                    q2j[j] = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                                   0.f);
+                    sj[j] = s;
+                    rowj[j] = r0 + k;
+                    pj[j] = proj;
+                    dlj[j] = dl;
+                    lvm |= 1u << j;
                 }
             }
+            // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
+            nbp += __popc(lvm);
+            float m2j[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                m2j[j] = fmaf(sj[j], sj[j], K.b2);
+                if (NF == 1 && a.use_cutoff && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);
+            }
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                if (lvm & (1u << j)) {
+                    const int row = rowj[j];
+                    float base[NF];
+                    phase_base<NF>(K, pj[j], dlj[j], S.geo0[row].w, S, row, base);
+                    eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], S.aux[row].y, base,
+                                  pre[j], pim[j], evp[j >> 1], 16 * (j & 1));
+                }
         }
         // flush fp32 partial sums into the fp64 accumulators
 #pragma unroll
         for (int j = 0; j < R; ++j)
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-                S.acc[R * tid + j][f][0] += (double)pre[j][f];
-                S.acc[R * tid + j][f][1] += (double)pim[j][f];
+                S.acc[R * lane + j][f][0] += (double)pre[j][f];
+                S.acc[R * lane + j][f][1] += (double)pim[j][f];
                 pre[j][f] = pim[j][f] = 0.f;
             }
-        __syncthreads();  // next chunk staged; this chunk's buffer may be reused
+#pragma unroll
+        for (int j = 0; j < R; ++j) S.evc[R * lane + j] += (evp[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+#pragma unroll
+        for (int i = 0; i < R / 2; ++i) evp[i] = 0;
+        __syncwarp();  // every lane is done with this chunk's shared rows
     }
-    // ---- write back (in-place continuation) and evaluation counts (kernels.py:399)
+    // ---- fold into the caller's acc after the previous beam range of this patch
+    //      (ascending ranges: deterministic, kernels.py:358-359 continuation)
+    if (lane == 0)
+        while (ld_acquire(&w.done[p]) != (int)q) __nanosleep(100);
+    __syncwarp();
+    (void)ld_acquire(&w.done[p]);
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        if (oi[j] < 0) continue;
+        if (j >= nvalid) continue;
+        const int64_t oi = perm[j];
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-            a.acc[2 * ((int64_t)oi[j] * NF + f)] = S.acc[R * tid + j][f][0];
-            a.acc[2 * ((int64_t)oi[j] * NF + f) + 1] = S.acc[R * tid + j][f][1];
+            a.acc[2 * (oi * NF + f)] += S.acc[R * lane + j][f][0];
+            a.acc[2 * (oi * NF + f) + 1] += S.acc[R * lane + j][f][1];
         }
-        a.evals[oi[j]] += evr[j];
+        a.evals[oi] += S.evc[R * lane + j];
     }
-    unsigned long long t[6] = {(unsigned long long)ties, (unsigned long long)nbp, pc[0], pc[1],
-                               pc[2], pc[3]};
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t[i] += __shfl_xor_sync(0xffffffffu, t[i], o);
-    }
-    if (lane == 0) {
-        if (t[0]) atomicAdd(&stats->tie_pairs, t[0]);
-        if (t[1]) atomicAdd(&stats->nb_pairs, t[1]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (t[2 + i]) atomicAdd(&stats->paths[i], t[2 + i]);
-    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(&w.done[p], (int)q + 1);
+    wc.ties += ties;
+    wc.nbp += nbp;
 }
 
 template <int NF>
-int launch_nf(const GbsArgs &a, const Tiling &t, const int32_t *seg_start, const Fp32Consts &K,
+__global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
+    gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w, const Fp32Consts K,
+                    GbsStats *stats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSmem<NF> &S = reinterpret_cast<WarpSmem<NF> *>(smem_raw)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned n_units = (unsigned)(w.n_patches * w.n_ranges);
+    const unsigned n_patches = (unsigned)w.n_patches;
+    WarpCounters wc;
+    for (;;) {
+        unsigned u = 0;
+        if (lane == 0) u = atomicAdd(w.unit_ctr, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= n_units) break;
+        const unsigned q = u / n_patches;  // range-major: one L2-resident slice
+        const unsigned p = u - q * n_patches;
+        run_unit<NF>(a, tl, w, K, S, p, q, lane, wc);
+    }
+    // per-lane counters straight into the device statistics
+    if (wc.ties) atomicAdd(&stats->tie_pairs, wc.ties);
+    if (wc.nbp) atomicAdd(&stats->nb_pairs, wc.nbp);
+    if (lane == 0) {
+        atomicAdd(&stats->paths[0], wc.pc0);
+        atomicAdd(&stats->paths[1], wc.items - wc.pc0 - wc.pc2 - wc.pc3);
+        atomicAdd(&stats->paths[2], wc.pc2);
+        atomicAdd(&stats->paths[3], wc.pc3);
+    }
+}
+
+// ------------------------------------------------------------ preparation ----
+
+// Row SoA of the padded reference bundle (beamtrace.py:274-288), tile-independent
+// parts of the staging computed once: p0 = (o, len), p1 = (d, s0) in fp64,
+// p2 = (A = phi sqrt(c)/(2 pi c) refl w_b, R_cut), pa = fp64-exact anchors
+// frac(omega/(2 pi c) s) at s0 and s0 + len, per frequency.
+__global__ void pack_kernel(const GbsArgs a, const Fp32Consts K, double4 *p0, double4 *p1,
+                            float2 *p2, float2 *pa) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= a.n_beams * a.max_seg) return;
+    const int64_t b = row / a.max_seg;
+    const int k = (int)(row - b * a.max_seg);
+    if (k >= a.n_segs[b]) return;
+    const double len = a.seg_len[row], s0 = a.seg_s0[row];
+    p0[row] = make_double4(a.seg_origin[3 * row], a.seg_origin[3 * row + 1],
+                           a.seg_origin[3 * row + 2], len);
+    p1[row] = make_double4(a.seg_dir[3 * row], a.seg_dir[3 * row + 1], a.seg_dir[3 * row + 2], s0);
+    const double se = s0 + len;
+    const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
+    const double A = K.amp_scale * a.seg_refl[row] * a.weights[b];
+    p2[row] = make_float2((float)A, (float)rcut);
+    for (int f = 0; f < a.nf; ++f)
+        pa[row * a.nf + f] = make_float2((float)frac_turns(K.kappa64[f] * s0),
+                                         (float)frac_turns(K.kappa64[f] * se));
+}
+
+// One warp per patch: fp64 bounding-box centre c_P, patch-local r = p - c_P in
+// fp32 (w = |r|^2) and the patch radius (max |r|, padded).
+__global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
+                             int64_t n_patches, float4 *prl, double4 *pcen) {
+    const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= n_patches) return;
+    double px[R], py[R], pz[R];
+    bool valid[R];
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int64_t si = p * PATCH + R * lane + j;
+        valid[j] = si < n;
+        px[j] = py[j] = pz[j] = 0.0;
+        if (valid[j]) {
+            const int64_t oi = perm[si];
+            px[j] = obs[3 * oi];
+            py[j] = obs[3 * oi + 1];
+            pz[j] = obs[3 * oi + 2];
+            mn[0] = fmin(mn[0], px[j]); mx[0] = fmax(mx[0], px[j]);
+            mn[1] = fmin(mn[1], py[j]); mx[1] = fmax(mx[1], py[j]);
+            mn[2] = fmin(mn[2], pz[j]); mx[2] = fmax(mx[2], pz[j]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+            mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+        }
+    const double cx = 0.5 * (mn[0] + mx[0]), cy = 0.5 * (mn[1] + mx[1]),
+                 cz = 0.5 * (mn[2] + mx[2]);
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (!valid[j]) continue;
+        const float rx = (float)(px[j] - cx), ry = (float)(py[j] - cy), rz = (float)(pz[j] - cz);
+        const float r2 = rx * rx + ry * ry + rz * rz;
+        prl[p * PATCH + R * lane + j] = make_float4(rx, ry, rz, r2);
+        q = fmaxf(q, r2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q = fmaxf(q, __shfl_xor_sync(0xffffffffu, q, o));
+    if (lane == 0) pcen[p] = make_double4(cx, cy, cz, (double)(sqrtf(q) * 1.0001f + 1e-4f));
+}
+
+template <int NF>
+int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
               GbsStats *stats, cudaStream_t st) {
-    const size_t smem = sizeof(Smem<NF>);
+    const size_t smem = WARPS * sizeof(WarpSmem<NF>);
     BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    gbs_fp32_kernel<NF><<<(unsigned)t.n_tiles, THREADS, smem, st>>>(a, t, seg_start, K, stats);
+    int dev = 0, sms = 0, per_sm = 0;
+    BF_TRY_CUDA(cudaGetDevice(&dev));
+    BF_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gbs_fp32_kernel<NF>,
+                                                              THREADS, smem));
+    if (per_sm < 1) return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
+    const int64_t units = w.n_patches * w.n_ranges;
+    int64_t grid = (int64_t)sms * per_sm;
+    const int64_t need = (units + WARPS - 1) / WARPS;
+    if (grid > need) grid = need;
+    gbs_fp32_kernel<NF><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
 }
 
-}  // namespace
-
-int gbs_fp32_tile() { return TILE; }
-
-int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
-                    GbsStats *d_stats, cudaStream_t st) {
-    if (t.n <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
-    if (a.max_seg > 32)
-        return fail(BF_EINVAL, "max_seg %lld exceeds 32 (r_max <= 31)", (long long)a.max_seg);
+Fp32Consts make_consts(const GbsArgs &a) {
     Fp32Consts K;
     const double two_pi = 2.0 * 3.141592653589793;
     double wmin = INFINITY;
@@ -749,7 +846,6 @@ int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
         if (f < a.nf && w < wmin) wmin = w;
         K.kappa64[f] = w / (two_pi * a.c);
         K.kappa[f] = (float)K.kappa64[f];
-        K.hk[f] = (float)(w * 0.5 / a.c);
         K.omega[f] = (float)w;
         K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
         K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
@@ -759,17 +855,57 @@ int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const int32_t *seg_start,
     K.b2 = (float)(a.width_b * a.width_b);
     K.b2_64 = a.width_b * a.width_b;
     K.amp_scale = a.phi_amp * sqrt(a.c) / (two_pi * a.c);
-    // Cut radius for the warp-patch prepass; without the cutoff nothing is ever cut.
+    // Cut radius for the patch prepass; without the cutoff nothing is ever cut.
     K.rcut_scale = (a.use_cutoff && wmin > 0) ? 72.0 * a.c / (wmin * a.width_b) : INFINITY;
+    return K;
+}
+
+}  // namespace
+
+int gbs_fp32_tile() { return TILE; }
+int gbs_fp32_patch() { return PATCH; }
+
+// Beams per range unit: depends on the beam count only, so the per-receiver
+// summation order (and result bits) does not depend on how receivers are
+// sharded over ranks.
+int64_t gbs_fp32_range_beams(int64_t n_beams) {
+    int64_t rb = (n_beams + BF_RANGES - 1) / BF_RANGES;
+    rb = (rb + 31) / 32 * 32;
+    return rb < 256 ? 256 : rb;
+}
+
+int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st) {
+    const Fp32Consts K = make_consts(a);
+    const int64_t rows = a.n_beams * a.max_seg;
+    if (rows > 0) {
+        pack_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(a, K, w.p0, w.p1, w.p2,
+                                                                    reinterpret_cast<float2 *>(w.pa));
+        note_launch();
+    }
+    if (w.n_patches > 0) {
+        patch_kernel<<<(unsigned)((w.n_patches * 32 + 127) / 128), 128, 0, st>>>(
+            a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen);
+        note_launch();
+    }
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
+                    cudaStream_t st) {
+    if (t.n <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
+    if (a.max_seg > 32)
+        return fail(BF_EINVAL, "max_seg %lld exceeds 32 (r_max <= 31)", (long long)a.max_seg);
+    const Fp32Consts K = make_consts(a);
     switch (a.nf) {
-        case 1: return launch_nf<1>(a, t, seg_start, K, d_stats, st);
-        case 2: return launch_nf<2>(a, t, seg_start, K, d_stats, st);
-        case 3: return launch_nf<3>(a, t, seg_start, K, d_stats, st);
-        case 4: return launch_nf<4>(a, t, seg_start, K, d_stats, st);
-        case 5: return launch_nf<5>(a, t, seg_start, K, d_stats, st);
-        case 6: return launch_nf<6>(a, t, seg_start, K, d_stats, st);
-        case 7: return launch_nf<7>(a, t, seg_start, K, d_stats, st);
-        case 8: return launch_nf<8>(a, t, seg_start, K, d_stats, st);
+        case 1: return launch_nf<1>(a, t, w, K, d_stats, st);
+        case 2: return launch_nf<2>(a, t, w, K, d_stats, st);
+        case 3: return launch_nf<3>(a, t, w, K, d_stats, st);
+        case 4: return launch_nf<4>(a, t, w, K, d_stats, st);
+        case 5: return launch_nf<5>(a, t, w, K, d_stats, st);
+        case 6: return launch_nf<6>(a, t, w, K, d_stats, st);
+        case 7: return launch_nf<7>(a, t, w, K, d_stats, st);
+        case 8: return launch_nf<8>(a, t, w, K, d_stats, st);
         default: return fail(BF_EINVAL, "nf=%d outside 1..%d", a.nf, BF_MAXF);
     }
 }
