@@ -52,6 +52,14 @@ constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk
 constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
 constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
 constexpr float PROJ_ERR = 3.814697265625e-06f;     // 2^-18 (x D): bound on |fp32 proj error|
+constexpr float TIE_DD = 3.814697265625e-06f;       // 2^-18 (x d D)   tight tie bound terms
+constexpr float TIE_D2 = 4.76837158203125e-07f;     // 2^-21 (x d^2)
+constexpr float TIE_DSQ = 1.8189894035458565e-12f;  // 2^-39 (x D^2)
+
+template <typename T>
+__device__ __forceinline__ T pick4(const T (&v)[4], int j) {
+    return j == 0 ? v[0] : j == 1 ? v[1] : j == 2 ? v[2] : v[3];
+}
 
 struct Fp32Consts {
     float kappa[BF_MAXF];    // omega/(2 pi c), turns per metre
@@ -102,30 +110,6 @@ __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Exact fp64 clamped distance of kernels.py:328-340 for padded row `row`,
-// reference operation order, no FMA.
-__device__ __forceinline__ double exact_d2(const GbsArgs &a, int64_t row, double px, double py,
-                                           double pz, double *proj_out, double *t_out) {
-    const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
-                 oz = a.seg_origin[3 * row + 2];
-    const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1], dz = a.seg_dir[3 * row + 2];
-    const double len = a.seg_len[row];
-    const double wx = __dsub_rn(px, ox), wy = __dsub_rn(py, oy), wz = __dsub_rn(pz, oz);
-    const double proj =
-        __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
-    double t = proj;
-    if (t < 0.0)
-        t = 0.0;
-    else if (t > len)
-        t = len;
-    const double vx = __dsub_rn(wx, __dmul_rn(t, dx));
-    const double vy = __dsub_rn(wy, __dmul_rn(t, dy));
-    const double vz = __dsub_rn(wz, __dmul_rn(t, dz));
-    *proj_out = proj;
-    *t_out = t;
-    return __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-}
-
 constexpr unsigned BEHIND_CHECK = 0x80000000u;
 constexpr unsigned WEDGE = 0x40000000u;
 
@@ -138,13 +122,14 @@ struct WarpSmem {
     float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
     float4 aux[ROWCAP];      // s0, A (amplitude factor), R_cut, D (error scale)
     float4 anc[NF][ROWCAP];  // phase anchors (turns): centre proj, start, end, -
-    int rowbeam[ROWCAP];     // chunk row -> chunk beam
-    int brow[CB + 1];        // chunk beam -> first chunk row
+    unsigned char rowbeam[ROWCAP];  // chunk row -> chunk beam
+    short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
     unsigned surv[CB];       // surviving segments + flags (0 = culled)
-    float btie[CB];          // absolute tie tolerance of the beam
+    float bD[CB];            // error scale D of the beam (max over its rows)
     double acc[PATCH][NF][2];
     int evc[PATCH];          // evaluation counts of the unit
+    double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
 };
 
 // Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
@@ -286,7 +271,7 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, int r0, int 
 // launch plane: behind = proj < 0 (kernels.py:348,375); |proj| within the fp32
 // error bound is re-decided with the reference's exact fp64 projection.
 __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&pj)[R],
-                                             const int32_t *perm, int nvalid, float D,
+                                             const double (*p64)[3], int nvalid, float D,
                                              int64_t beam, int k, unsigned &ties) {
     const float tolp = PROJ_ERR * D;
     unsigned m = 0;
@@ -297,11 +282,16 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&
             continue;
         }
         if (pj[j] < -tolp || j >= nvalid) continue;
-        const int64_t gi = 3 * (int64_t)perm[j];
-        double p64, t64;
-        exact_d2(a, beam * a.max_seg + k, a.obs[gi], a.obs[gi + 1], a.obs[gi + 2], &p64, &t64);
+        // proj of kernels.py:328-331, reference operation order, no FMA
+        const int64_t row = beam * a.max_seg + k;
+        const double wx = __dsub_rn(p64[j][0], a.seg_origin[3 * row]);
+        const double wy = __dsub_rn(p64[j][1], a.seg_origin[3 * row + 1]);
+        const double wz = __dsub_rn(p64[j][2], a.seg_origin[3 * row + 2]);
+        const double proj = __dadd_rn(__dadd_rn(__dmul_rn(wx, a.seg_dir[3 * row]),
+                                                __dmul_rn(wy, a.seg_dir[3 * row + 1])),
+                                      __dmul_rn(wz, a.seg_dir[3 * row + 2]));
         ++ties;
-        if (!(p64 < 0.0)) m |= 1u << j;
+        if (!(proj < 0.0)) m |= 1u << j;
     }
     return m;
 }
@@ -320,7 +310,7 @@ __device__ __noinline__ ExactPick exact_pick(const double *__restrict__ seg_orig
                                              const double *__restrict__ seg_len, int64_t row0,
                                              const float4 *geo0, const float4 *geo1,
                                              unsigned surv, int kf, float rx, float ry, float rz,
-                                             float best, float tie_abs, const double *p) {
+                                             float best, float tie_abs, const double (&p)[3]) {
     const double px = p[0], py = p[1], pz = p[2];
     ExactPick e{0.0, 0.0, 0.0, -1};
     double bd = INFINITY;
@@ -418,6 +408,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
         for (int f = 0; f < NF; ++f) S.acc[R * lane + j][f][0] = S.acc[R * lane + j][f][1] = 0.0;
         S.evc[R * lane + j] = 0;
+        if (j < nvalid) {
+            const int64_t oi = perm[j];
+            S.p64[R * lane + j][0] = a.obs[3 * oi];
+            S.p64[R * lane + j][1] = a.obs[3 * oi + 1];
+            S.p64[R * lane + j][2] = a.obs[3 * oi + 2];
+        }
     }
     float pre[R][NF], pim[R][NF];
     unsigned evp[R / 2] = {};  // evaluation counts of receivers 2i, 2i+1 (16-bit fields)
@@ -490,7 +486,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.aux[r0 + k].w);
             word = classify<NF>(S, r0, nsb, RW, D);
             S.surv[lane] = word;
-            S.btie[lane] = TIE_ABS * D * D;
+            S.bD[lane] = D;
         }
         const unsigned live = __ballot_sync(0xffffffffu, word != 0);
         {
@@ -539,7 +535,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 lvm = (1u << R) - 1;
                 if (bword & BEHIND_CHECK)
-                    lvm = behind_mask(a, pj, perm, nvalid, S.aux[row].w, beam, k, ties);
+                    lvm = behind_mask(a, pj, S.p64 + R * lane, nvalid, S.aux[row].w, beam, k, ties);
             } else if (bword & WEDGE) {
                 // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
                 //      the reference picks by fp64 rounding, reproduced exactly here
@@ -562,8 +558,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     if (j >= nvalid) continue;
-                    const int64_t gi = 3 * (int64_t)perm[j];
-                    const double px = a.obs[gi], py = a.obs[gi + 1], pz = a.obs[gi + 2];
+                    const double px = S.p64[R * lane + j][0], py = S.p64[R * lane + j][1],
+                                 pz = S.p64[R * lane + j][2];
                     const double vx = __dsub_rn(__dsub_rn(px, oax), ldx);
                     const double vy = __dsub_rn(__dsub_rn(py, oay), ldy);
                     const double vz = __dsub_rn(__dsub_rn(pz, oaz), ldz);
@@ -589,7 +585,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 ties += __popc(lvm);
             } else {
                 // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
-                const float tie_abs = S.btie[jb];
+                const float Db = S.bD[jb];
+                const float tie_abs = TIE_ABS * Db * Db;
                 float best[R], second[R];
                 int kb[R];
 #pragma unroll
@@ -616,41 +613,67 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     }
                 }
                 lvm = 0;
+                unsigned pend = 0;  // receivers whose winner is re-decided in fp64
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
-                    int k = kb[j];
-                    bool exact = second[j] - best[j] <= fmaf(TIE_REL, second[j], tie_abs);
-                    float4 g1 = S.geo1[r0 + k];
-                    float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                    float proj = dl + g1.w;
+                    const int k = kb[j];
+                    const float gap = second[j] - best[j];
+                    // fp32 error of the two distances: loose test first,
+                    // then 2^-18 d D + 2^-21 d^2 + 2^-39 D^2 with d^2 <= second
+                    bool exact = gap <= fmaf(TIE_REL, second[j], tie_abs);
+                    if (exact)
+                        exact = gap <= fmaf(TIE_DD * Db, sqrt_approx(second[j]) * 1.0001f,
+                                            fmaf(TIE_D2, second[j], TIE_DSQ * Db * Db));
+                    const float4 g1 = S.geo1[r0 + k];
+                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
+                    const float proj = dl + g1.w;
                     if (k == 0 && fabsf(proj) <= PROJ_ERR * S.aux[r0].w) exact = true;
-                    float s;
-                    if (!exact) {
-                        if (k == 0 && proj < 0.f) continue;  // behind the source
-                        s = S.aux[r0 + k].x + fminf(fmaxf(proj, 0.f), S.geo0[r0 + k].w);
-                    } else {
-                        // exact re-decision among the contenders, ascending k, strict <
-                        if (j >= nvalid) continue;
-                        ++ties;
-                        const ExactPick e = exact_pick(a.seg_origin, a.seg_dir, a.seg_len,
-                                                       beam * a.max_seg, S.geo0 + r0, S.geo1 + r0,
-                                                       surv, k, rx[j], ry[j], rz[j], best[j],
-                                                       tie_abs, a.obs + 3 * (int64_t)perm[j]);
-                        if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
-                        k = e.bk;
-                        s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
-                        g1 = S.geo1[r0 + k];
-                        dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                        // anchor choice follows the exact clamp
-                        proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
+                    if (exact) {
+                        if (j < nvalid) pend |= 1u << j;
+                        continue;
                     }
+                    if (k == 0 && proj < 0.f) continue;  // behind the source
                     const float4 g2 = S.geo2[r0 + k];
                     q2j[j] = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                                    0.f);
-                    sj[j] = s;
+                    sj[j] = S.aux[r0 + k].x + fminf(fmaxf(proj, 0.f), S.geo0[r0 + k].w);
                     rowj[j] = r0 + k;
                     pj[j] = proj;
                     dlj[j] = dl;
+                    lvm |= 1u << j;
+                }
+                // exact re-decision among the contenders (ascending k, strict <), one
+                // pending receiver per lane per round
+                ties += __popc(pend);
+#pragma unroll 1
+                while (__any_sync(0xffffffffu, pend != 0)) {
+                    if (!pend) continue;
+                    const int j = __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
+                    const ExactPick e = exact_pick(a.seg_origin, a.seg_dir, a.seg_len,
+                                                   beam * a.max_seg, S.geo0 + r0, S.geo1 + r0,
+                                                   surv, pick4(kb, j), x, y, z, pick4(best, j),
+                                                   tie_abs, S.p64[R * lane + j]);
+                    if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
+                    const int k = e.bk;
+                    const float4 g1 = S.geo1[r0 + k];
+                    const float4 g2 = S.geo2[r0 + k];
+                    const float dl = fmaf(x, g1.x, fmaf(y, g1.y, z * g1.z));
+                    const float q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
+                                           0.f);
+                    const float s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
+                    // anchor choice follows the exact clamp
+                    const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
+#pragma unroll
+                    for (int jj = 0; jj < R; ++jj)
+                        if (jj == j) {
+                            q2j[jj] = q2;
+                            sj[jj] = s;
+                            rowj[jj] = r0 + k;
+                            pj[jj] = proj;
+                            dlj[jj] = dl;
+                        }
                     lvm |= 1u << j;
                 }
             }
