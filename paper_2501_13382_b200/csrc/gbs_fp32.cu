@@ -71,6 +71,7 @@ struct Fp32Consts {
     float b, b2;             // width_b, width_b^2
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
     double rcut_scale;       // 72 c / (omega_min b): R_cut^2 = rcut_scale * (s_end^2 + b^2)
+    float rscale;            // (float) rcut_scale
     double b2_64;
 };
 
@@ -178,8 +179,9 @@ __device__ __forceinline__ void phase_base(const Fp32Consts &K, float proj, floa
 // segment row `r` (fp32), the unit vector from the nearest point, whether the
 // whole patch (radius RW) is cut for this segment, and the centre's projection.
 template <int NF>
-__device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, int r, float RW, float *ux,
-                                            float *uy, float *uz, bool *cut, float *proj_out) {
+__device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, const Fp32Consts &K, int r,
+                                            float RW, float *ux, float *uy, float *uz, bool *cut,
+                                            float *proj_out) {
     const float4 g0 = S.geo0[r];
     const float4 g1 = S.geo1[r];
     const float wx = g0.x, wy = g0.y, wz = g0.z;
@@ -191,8 +193,12 @@ __device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, int r, float 
     *ux = vx * inv;
     *uy = vy * inv;
     *uz = vz * inv;
-    // |u_c|^2 is the centre's squared distance to the infinite line
-    const float rc = (S.aux[r].z + RW) * 1.00002f + 2e-3f;
+    // cut for every receiver if this segment wins (kernels.py:382-385): q >= |u_c| - RW
+    // (|u_c|: the centre's distance to the infinite line) and s <= s_hi, so the
+    // patch is cut when |u_c| > R_cut(s_hi) + RW, R_cut(s)^2 = 72 c (s^2 + b^2)/(omega_min b)
+    const float s_hi = S.aux[r].x + fminf(fmaxf(proj + RW * 1.00002f + 2e-3f, 0.f), g0.w);
+    const float rk = sqrt_approx(K.rscale * fmaf(s_hi, s_hi, K.b2)) * 1.00002f + 1e-3f;
+    const float rc = (rk + RW) * 1.00002f + 2e-3f;
     *cut = S.geo2[r].w > rc * rc;
     *proj_out = proj;
     return dc;
@@ -208,8 +214,8 @@ __device__ __forceinline__ float sweep(float RW, float d) {
 
 // Work generation for one (patch, beam): survivor mask + flags (0 = culled).
 template <int NF>
-__device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, int r0, int ns, float RW,
-                                             float D) {
+__device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Consts &K, int r0,
+                                             int ns, float RW, float D) {
     if (ns <= 0) return 0u;
     // pass 1: nearest segment at the patch centre
     float best = INFINITY;
@@ -232,7 +238,7 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, int r0, int 
     // segments never win, so then no pair of the patch contributes
     float ujx, ujy, ujz, pj;
     bool cj;
-    const float dj = patch_dist(S, r0 + kj, RW, &ujx, &ujy, &ujz, &cj, &pj);
+    const float dj = patch_dist(S, K, r0 + kj, RW, &ujx, &ujy, &ujz, &cj, &pj);
     const float sj = sweep(RW, dj);
     const bool behind0 = p0 + RW * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
     unsigned mask = 1u << kj;
@@ -242,7 +248,7 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, int r0, int 
         if (k == kj) continue;
         float ux, uy, uz, proj;
         bool cut;
-        const float dk = patch_dist(S, r0 + k, RW, &ux, &uy, &uz, &cut, &proj);
+        const float dk = patch_dist(S, K, r0 + k, RW, &ux, &uy, &uz, &cut, &proj);
         // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * sup|grad d_k - grad d_j|
         const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
         const float lip = fminf(sqrt_approx(ex * ex + ey * ey + ez * ez) + sweep(RW, dk) + sj, 2.f);
@@ -484,7 +490,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             float D = 0.f;
 #pragma unroll 1
             for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.aux[r0 + k].w);
-            word = classify<NF>(S, r0, nsb, RW, D);
+            word = classify<NF>(S, K, r0, nsb, RW, D);
             S.surv[lane] = word;
             S.bD[lane] = D;
         }
@@ -880,6 +886,7 @@ Fp32Consts make_consts(const GbsArgs &a) {
     K.amp_scale = a.phi_amp * sqrt(a.c) / (two_pi * a.c);
     // Cut radius for the patch prepass; without the cutoff nothing is ever cut.
     K.rcut_scale = (a.use_cutoff && wmin > 0) ? 72.0 * a.c / (wmin * a.width_b) : INFINITY;
+    K.rscale = (float)K.rcut_scale;
     return K;
 }
 
