@@ -39,8 +39,11 @@ namespace {
 #ifndef BF_MINB
 #define BF_MINB 4
 #endif
+#ifndef BF_STAGE_BATCH
+#define BF_STAGE_BATCH 0
+#endif
 #ifndef BF_RANGES
-#define BF_RANGES 32
+#define BF_RANGES 64
 #endif
 constexpr int R = 4;                    // receivers per lane
 constexpr int PATCH = 32 * R;           // receivers per warp patch
@@ -131,6 +134,7 @@ struct WarpSmem {
     double acc[PATCH][NF][2];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
+    unsigned long long cnt[6];  // statistics: ties, non-behind, culled/single/wedge/multi items
 };
 
 // Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
@@ -361,42 +365,61 @@ template <int NF>
 __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, int64_t max_seg,
                                            int nrows, double cx, double cy, double cz, float RW,
                                            const Fp32Consts &K, int lane) {
+#if BF_STAGE_BATCH
+    // all of this lane's row loads first (<= SR rows): one L2 round trip per chunk
+    constexpr int SR = (ROWCAP + 31) / 32;
+    double4 P0[SR], P1[SR];
+#pragma unroll
+    for (int i = 0; i < SR; ++i) {
+        const int r = lane + 32 * i;
+        if (r < nrows) {
+            const int jb = S.rowbeam[r];
+            const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
+            P0[i] = w.p0[g];  // o.xyz, len
+            P1[i] = w.p1[g];  // d.xyz, s0
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < SR; ++i) {
+        const int r = lane + 32 * i;
+        if (r >= nrows) break;
+        const double4 p0 = P0[i], p1 = P1[i];
+        const int jb = S.rowbeam[r];
+        const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
+#else
 #pragma unroll 1
     for (int r = lane; r < nrows; r += 32) {
         const int jb = S.rowbeam[r];
-        const int64_t grow = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
-        const double4 P0 = w.p0[grow];  // o.xyz, len
-        const double4 P1 = w.p1[grow];  // d.xyz, s0
-        const float2 P2 = w.p2[grow];   // A, R_cut
-        const double wcx = cx - P0.x, wcy = cy - P0.y, wcz = cz - P0.z;
-        const double pc = wcx * P1.x + wcy * P1.y + wcz * P1.z;
-        const double ucx = wcx - pc * P1.x, ucy = wcy - pc * P1.y, ucz = wcz - pc * P1.z;
-        S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)P0.w);
-        S.geo1[r] = make_float4((float)P1.x, (float)P1.y, (float)P1.z, (float)pc);
+        const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
+        const double4 p0 = w.p0[g];  // o.xyz, len
+        const double4 p1 = w.p1[g];  // d.xyz, s0
+#endif
+        const float2 p2 = w.p2[g];   // A, R_cut
+        const double wcx = cx - p0.x, wcy = cy - p0.y, wcz = cz - p0.z;
+        const double pc = wcx * p1.x + wcy * p1.y + wcz * p1.z;
+        const double ucx = wcx - pc * p1.x, ucy = wcy - pc * p1.y, ucz = wcz - pc * p1.z;
+        S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)p0.w);
+        S.geo1[r] = make_float4((float)p1.x, (float)p1.y, (float)p1.z, (float)pc);
         S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
                                 (float)(ucx * ucx + ucy * ucy + ucz * ucz));
-        const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + P0.w) + RW + 1.f;
-        S.aux[r] = make_float4((float)P1.w, P2.x, P2.y, D);
+        const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + p0.w) + RW + 1.f;
+        S.aux[r] = make_float4((float)p1.w, p2.x, p2.y, D);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-            const float2 ae = reinterpret_cast<const float2 *>(w.pa)[grow * NF + f];
-            S.anc[f][r] = make_float4((float)frac_turns(K.kappa64[f] * (P1.w + pc)), ae.x, ae.y, 0.f);
+            const float2 ae = reinterpret_cast<const float2 *>(w.pa)[g * NF + f];
+            S.anc[f][r] =
+                make_float4((float)frac_turns(K.kappa64[f] * (p1.w + pc)), ae.x, ae.y, 0.f);
         }
     }
 }
 
-struct WarpCounters {
-    unsigned long long ties = 0, nbp = 0;  // per lane: fp64 re-decided / non-behind pairs
-    unsigned long long pc0 = 0, pc2 = 0, pc3 = 0, items = 0;  // (patch, beam) items (uniform)
-};
 
 // One (patch, beam range) unit.
 template <int NF>
 __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, const Fp32Work &w,
                                          const Fp32Consts &K, WarpSmem<NF> &S, int64_t p,
-                                         int64_t q, int lane, WarpCounters &wc) {
-    const double4 pcen = w.pcen[p];
-    const float RW = (float)pcen.w;
+                                         int64_t q, int lane) {
+    const float RW = (float)w.pcen[p].w;
     // ---- receivers (patch-local); padding receivers sit at the centre and are
     //      computed but never written back
     float rx[R], ry[R], rz[R], rr[R];
@@ -480,7 +503,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         }
         if (lane == 0) S.brow[nbc] = nrows;
         __syncwarp();
-        stage_rows<NF>(S, w, a.max_seg, nrows, pcen.x, pcen.y, pcen.z, RW, K, lane);
+        {
+            const double4 c = w.pcen[p];  // re-read (L1) rather than held in registers
+            stage_rows<NF>(S, w, a.max_seg, nrows, c.x, c.y, c.z, RW, K, lane);
+        }
         __syncwarp();
         // ---- work generation: one lane per beam bounds the patch against the
         //      beam's segments (cut / behind / dominated)
@@ -497,11 +523,15 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         const unsigned live = __ballot_sync(0xffffffffu, word != 0);
         {
             const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
-            wc.items += nbc;
-            wc.pc0 += nbc - __popc(live);
-            wc.pc2 += __popc(__ballot_sync(0xffffffffu, (word & WEDGE) != 0));
-            wc.pc3 += __popc(__ballot_sync(0xffffffffu, word != 0 && !(word & WEDGE) &&
-                                                            (m & (m - 1)) != 0));
+            const unsigned nw = __popc(__ballot_sync(0xffffffffu, (word & WEDGE) != 0));
+            const unsigned nm = __popc(__ballot_sync(0xffffffffu, word != 0 && !(word & WEDGE) &&
+                                                                      (m & (m - 1)) != 0));
+            if (lane == 0) {
+                S.cnt[2] += nbc - __popc(live);
+                S.cnt[3] += __popc(live) - nw - nm;
+                S.cnt[4] += nw;
+                S.cnt[5] += nm;
+            }
         }
         __syncwarp();
         // ---- summation over the chunk's live beams, ascending.  Each path yields
@@ -736,8 +766,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(&w.done[p], (int)q + 1);
-    wc.ties += ties;
-    wc.nbp += nbp;
+    ties = __reduce_add_sync(0xffffffffu, ties);
+    nbp = __reduce_add_sync(0xffffffffu, nbp);
+    if (lane == 0) {
+        S.cnt[0] += ties;
+        S.cnt[1] += nbp;
+    }
 }
 
 template <int NF>
@@ -749,7 +783,8 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
     const int lane = threadIdx.x & 31;
     const unsigned n_units = (unsigned)(w.n_patches * w.n_ranges);
     const unsigned n_patches = (unsigned)w.n_patches;
-    WarpCounters wc;
+    if (lane < 6) S.cnt[lane] = 0;
+    __syncwarp();
     for (;;) {
         unsigned u = 0;
         if (lane == 0) u = atomicAdd(w.unit_ctr, 1u);
@@ -757,16 +792,15 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
         if (u >= n_units) break;
         const unsigned q = u / n_patches;  // range-major: one L2-resident slice
         const unsigned p = u - q * n_patches;
-        run_unit<NF>(a, tl, w, K, S, p, q, lane, wc);
+        run_unit<NF>(a, tl, w, K, S, p, q, lane);
     }
     // per-lane counters straight into the device statistics
-    if (wc.ties) atomicAdd(&stats->tie_pairs, wc.ties);
-    if (wc.nbp) atomicAdd(&stats->nb_pairs, wc.nbp);
+    __syncwarp();
     if (lane == 0) {
-        atomicAdd(&stats->paths[0], wc.pc0);
-        atomicAdd(&stats->paths[1], wc.items - wc.pc0 - wc.pc2 - wc.pc3);
-        atomicAdd(&stats->paths[2], wc.pc2);
-        atomicAdd(&stats->paths[3], wc.pc3);
+        atomicAdd(&stats->tie_pairs, S.cnt[0]);
+        atomicAdd(&stats->nb_pairs, S.cnt[1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) atomicAdd(&stats->paths[i], S.cnt[2 + i]);
     }
 }
 
