@@ -42,6 +42,9 @@ namespace {
 #ifndef BF_STAGE_BATCH
 #define BF_STAGE_BATCH 0
 #endif
+#ifndef BF_EVG
+#define BF_EVG 4
+#endif
 #ifndef BF_RANGES
 #define BF_RANGES 64
 #endif
@@ -52,6 +55,7 @@ constexpr int WARPS = 4;                // independent warps per CTA
 constexpr int THREADS = 32 * WARPS;
 constexpr int CB = 32;                  // max beams per staged chunk
 constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk
+constexpr int EVG = BF_EVG;             // receivers evaluated per branch of the tail
 constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
 constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
 constexpr float PROJ_ERR = 3.814697265625e-06f;     // 2^-18 (x D): bound on |fp32 proj error|
@@ -145,22 +149,25 @@ template <int NF>
 __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
                                           float m2, float A, const float *base,
                                           float (&pre)[NF], float (&pim)[NF], unsigned &ev,
-                                          int shift) {
+                                          int shift, bool live) {
     const float inv = rcp_approx(m2);
     const float gq = q2 * inv;
     const float ainv = A * inv;
     const float gqs = gq * s;
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-        if (NF > 1 && use_cutoff && q2 * K.cutk[f] > m2) continue;  // ex_re < -36
+        const bool lf = live && !(NF > 1 && use_cutoff && q2 * K.cutk[f] > m2);  // ex_re < -36
         float turns = fmaf(gqs, K.hk2pi[f], base[f]);
         turns -= rintf(turns);
         const float ph = turns * 6.283185307179586f;
         const float sn = sin_approx(ph), cs = cos_approx(ph);
         const float amp = ainv * K.omega[f] * ex2_approx(gq * K.nhkbl2e[f]);
-        pre[f] = fmaf(-amp, fmaf(s, sn, K.b * cs), pre[f]);
-        pim[f] = fmaf(amp, fmaf(s, cs, -K.b * sn), pim[f]);
-        ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
+        const float dre = -amp * fmaf(s, sn, K.b * cs), dim = amp * fmaf(s, cs, -K.b * sn);
+        if (lf) {
+            pre[f] += dre;
+            pim[f] += dim;
+            ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
+        }
     }
 }
 
@@ -548,6 +555,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             const int r0 = S.brow[jb];
             float sj[R], q2j[R], pj[R], dlj[R];
             int rowj[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) rowj[j] = r0;  // a valid row for masked lanes
             unsigned lvm;
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
@@ -721,14 +730,19 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 m2j[j] = fmaf(sj[j], sj[j], K.b2);
                 if (NF == 1 && a.use_cutoff && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);
             }
+            // receivers evaluated in groups of EVG (one branch, EVG independent chains)
 #pragma unroll
-            for (int j = 0; j < R; ++j)
-                if (lvm & (1u << j)) {
-                    const int row = rowj[j];
-                    float base[NF];
-                    phase_base<NF>(K, pj[j], dlj[j], S.geo0[row].w, S, row, base);
-                    eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], S.aux[row].y, base,
-                                  pre[j], pim[j], evp[j >> 1], 16 * (j & 1));
+            for (int g = 0; g < R; g += EVG)
+                if (lvm & (((1u << EVG) - 1u) << g)) {
+#pragma unroll
+                    for (int j = g; j < g + EVG; ++j) {
+                        const int row = rowj[j];
+                        float base[NF];
+                        phase_base<NF>(K, pj[j], dlj[j], S.geo0[row].w, S, row, base);
+                        eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], S.aux[row].y, base,
+                                      pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
+                                      EVG == 1 || ((lvm >> j) & 1u));
+                    }
                 }
         }
         // flush fp32 partial sums into the fp64 accumulators
