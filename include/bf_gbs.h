@@ -111,14 +111,16 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
  * Morton receiver order perm (n_obs), tile centres/radii centre (n_tiles x 4:
  * x, y, z, R_T) and the candidate bitmask bits (n_tiles x ceil(n_beams/32)
  * uint32, bit b%32 of word b/32 = beam b may contribute to some receiver of the
- * tile).  Host buffers; exact fp64 test, reproduced bit for bit by
- * oracle/worklist_oracle.c.
+ * tile).  tight_bits (same shape, may be NULL) is the subset the fp32 kernel
+ * walks: R_k from the largest arc length s_hi = s0 + clamp(w.d + R_T, 0, len)
+ * the tile reaches instead of s_end.  Host buffers; exact fp64 tests, reproduced
+ * bit for bit by oracle/worklist_oracle.c.
  */
 int bf_worklist(const double *seg_origin, const double *seg_dir, const double *seg_len,
                 const double *seg_s0, const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
                 const double *obs, int64_t n_obs, const double *omegas, int64_t nf, double c,
                 double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
-                int64_t n_tiles_cap, int64_t *n_tiles_out, int device);
+                uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out, int device);
 
 /* Receivers per tile of the fp32 summation kernel. */
 int bf_tile_size(void);

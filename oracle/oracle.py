@@ -150,13 +150,15 @@ def trace(v0, v1, v2, refl, bounds, diameter, origin, dirs, e1s, e2s, length_cap
 
 
 def worklist(seg_origin, seg_dir, seg_len, seg_s0, n_segs, max_seg, centre, c, width_b,
-             omega_min, use_cutoff=True):
-    """Tile-level candidate bitmask (worklist_oracle.c); centre is (n_tiles, 4)."""
+             omega_min, use_cutoff=True, tight=False):
+    """Tile-level candidate bitmask (worklist_oracle.c); centre is (n_tiles, 4).
+    tight=True: the tight list the fp32 kernel walks (subset of the a9 list)."""
     lib = _load()
     if not hasattr(lib, "_wl_declared"):
         lib.oracle_worklist.argtypes = [_d, _d, _d, _d, _i32, _i64, _i64, _d, _i64,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                        ctypes.c_int, ctypes.POINTER(ctypes.c_uint32)]
+                                        ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_uint32)]
         lib.oracle_worklist.restype = None
         lib._wl_declared = True
     f = lambda a: np.ascontiguousarray(a, dtype=np.float64)  # noqa: E731
@@ -167,5 +169,5 @@ def worklist(seg_origin, seg_dir, seg_len, seg_s0, n_segs, max_seg, centre, c, w
     bits = np.zeros((nt, (nb + 31) // 32), np.uint32)
     lib.oracle_worklist(_p(so), _p(sd), _p(sl), _p(ss0), _p(n_segs, _i32), nb, int(max_seg),
                         _p(centre), nt, float(c), float(width_b), float(omega_min),
-                        int(bool(use_cutoff)), bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
+                        int(bool(use_cutoff)), int(bool(tight)), bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
     return bits

@@ -7,13 +7,17 @@
  * R_k + R_T, R_k^2 = 72 c (s_end^2 + b^2)/(omega_min b), kernels.py:377-385) or,
  * for k == 0, the tile lies behind the launch plane (kernels.py:348,375).
  * Same fp64 operation order, no FMA (-ffp-contract=off), IEEE sqrt.
+ *
+ * tight = 1 restates the TIGHT list the fp32 kernel walks (a subset): R_k uses the
+ * largest arc length the tile reaches on k, s_hi = s0 + clamp(w.d + R_T, 0, len),
+ * instead of s_end.
  */
 #include <math.h>
 #include <stdint.h>
 
 static int beam_dead(const double *so, const double *sd, const double *sl, const double *ss0,
                      const int32_t *n_segs, int64_t max_seg, double width_b, int64_t b,
-                     double cx, double cy, double cz, double rt, double rscale) {
+                     double cx, double cy, double cz, double rt, double rscale, int tight) {
     int ns = n_segs[b];
     for (int k = 0; k < ns; ++k) {
         int64_t row = b * max_seg + k;
@@ -23,6 +27,11 @@ static int beam_dead(const double *so, const double *sd, const double *sl, const
         double ux = wx - proj * dx, uy = wy - proj * dy, uz = wz - proj * dz;
         double qp = sqrt(ux * ux + uy * uy + uz * uz);
         double se = ss0[row] + sl[row];
+        if (tight) {
+            double reach = proj + rt;
+            reach = reach < 0.0 ? 0.0 : (reach > sl[row] ? sl[row] : reach);
+            se = ss0[row] + reach;
+        }
         double rk = sqrt(rscale * (se * se + width_b * width_b));
         int dead = qp - rt > rk * (1.0 + 1e-6) + 1e-6;
         if (k == 0) dead = dead || (proj + rt < -1e-6);
@@ -35,7 +44,7 @@ static int beam_dead(const double *so, const double *sd, const double *sl, const
 void oracle_worklist(const double *so, const double *sd, const double *sl, const double *ss0,
                      const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
                      const double *centre, int64_t n_tiles, double c, double width_b,
-                     double omega_min, int use_cutoff, uint32_t *bits) {
+                     double omega_min, int use_cutoff, int tight, uint32_t *bits) {
     const double rscale = use_cutoff ? 72.0 * c / (omega_min * width_b) : INFINITY;
     const int64_t n_words = (n_beams + 31) / 32;
     for (int64_t t = 0; t < n_tiles; ++t) {
@@ -46,7 +55,7 @@ void oracle_worklist(const double *so, const double *sd, const double *sl, const
                 int64_t b = 32 * w + j;
                 if (b < n_beams &&
                     !beam_dead(so, sd, sl, ss0, n_segs, max_seg, width_b, b, ct[0], ct[1], ct[2],
-                               ct[3], rscale))
+                               ct[3], rscale, tight))
                     m |= 1u << j;
             }
             bits[t * n_words + w] = m;

@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_COUNT
 };
 
 struct DeviceCtx {
@@ -299,15 +299,17 @@ int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_
 int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st,
                    unsigned long long **cand_out) {
     const int64_t n_words = (a.n_beams + 31) / 32;
-    uint32_t *bits;
+    uint32_t *bits, *tbits;
     unsigned long long *cand;
     BF_TRY(c->get(B_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
+    BF_TRY(c->get(B_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
     BF_TRY(c->get(B_WLCNT, (size_t)(2 * t.n_tiles), &cand));
     BF_TRY_CUDA(cudaMemsetAsync(cand, 0, 2 * sizeof(unsigned long long) * t.n_tiles, st));
     double wmin = INFINITY;
     for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
-    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, cand, cand + t.n_tiles, st));
+    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, tbits, cand, cand + t.n_tiles, st));
     t.wl_bits = bits;
+    t.wl_tight = tbits;
     t.wl_words = n_words;
     if (cand_out) *cand_out = cand;
     return BF_OK;
@@ -648,7 +650,7 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
                 const double *seg_s0, const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
                 const double *obs, int64_t n_obs, const double *omegas, int64_t nf, double c,
                 double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
-                int64_t n_tiles_cap, int64_t *n_tiles_out, int device) {
+                uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out, int device) {
     if (max_seg < 1 || n_beams < 1 || n_obs < 1 || nf < 1 || nf > BF_MAXF)
         return fail(BF_EINVAL, "bad sizes");
     const int64_t T = gbs_fp32_tile(), n_tiles = (n_obs + T - 1) / T;
@@ -698,6 +700,8 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     BF_TRY_CUDA(cudaMemcpyAsync(perm, t.perm, 4 * n_obs, D2H, st));
     BF_TRY_CUDA(cudaMemcpyAsync(centre, t.centre, 32 * n_tiles, D2H, st));
     BF_TRY_CUDA(cudaMemcpyAsync(bits, t.wl_bits, 4 * n_tiles * n_words, D2H, st));
+    if (tight_bits)
+        BF_TRY_CUDA(cudaMemcpyAsync(tight_bits, t.wl_tight, 4 * n_tiles * n_words, D2H, st));
     BF_TRY_CUDA(cudaStreamSynchronize(st));
     return BF_OK;
 }

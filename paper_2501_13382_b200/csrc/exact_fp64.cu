@@ -376,11 +376,17 @@ __global__ void __launch_bounds__(128) trace_kernel(const TraceArgs a) {
 //     wins it is `behind`, kernels.py:348,375).
 // Fixed fp64 operation order, no FMA (this file is -fmad=false), IEEE sqrt/div:
 // oracle/worklist_oracle.c reproduces the bitmask bit for bit.
-__device__ __forceinline__ bool beam_dead_for_tile(const GbsArgs &a, int64_t b, double cx,
-                                                   double cy, double cz, double rt,
-                                                   double rscale) {
+// Returns bit 0 = dead under the a9 bound above (R_k from s_end), bit 1 = dead under
+// the TIGHT bound that uses the largest arc length the tile can reach on segment k,
+// s_hi = s0 + clamp(w.d + R_T, 0, len) <= s_end (every receiver's nearest point on k
+// projects within R_T of the centre's), R_k(s_hi)^2 = 72 c (s_hi^2 + b^2)/(omega_min b).
+// Tight-dead implies nothing about a9; a9-dead implies tight-dead.
+__device__ __forceinline__ unsigned beam_dead_for_tile(const GbsArgs &a, int64_t b, double cx,
+                                                       double cy, double cz, double rt,
+                                                       double rscale) {
     const int ns = a.n_segs[b];
-    for (int k = 0; k < ns; ++k) {
+    bool loose = true, tight = true;
+    for (int k = 0; k < ns && tight; ++k) {
         const int64_t row = b * a.max_seg + k;
         const double wx = cx - a.seg_origin[3 * row], wy = cy - a.seg_origin[3 * row + 1],
                      wz = cz - a.seg_origin[3 * row + 2];
@@ -389,18 +395,24 @@ __device__ __forceinline__ bool beam_dead_for_tile(const GbsArgs &a, int64_t b, 
         const double proj = wx * dx + wy * dy + wz * dz;
         const double ux = wx - proj * dx, uy = wy - proj * dy, uz = wz - proj * dz;
         const double qp = sqrt(ux * ux + uy * uy + uz * uz);
-        const double se = a.seg_s0[row] + a.seg_len[row];
+        const double s0 = a.seg_s0[row], len = a.seg_len[row];
+        const double se = s0 + len;
         const double rk = sqrt(rscale * (se * se + a.width_b * a.width_b));
-        bool dead = qp - rt > rk * (1.0 + 1e-6) + 1e-6;
-        if (k == 0) dead = dead || (proj + rt < -1e-6);
-        if (!dead) return false;
+        double reach = proj + rt;
+        reach = reach < 0.0 ? 0.0 : (reach > len ? len : reach);
+        const double sh = s0 + reach;
+        const double rh = sqrt(rscale * (sh * sh + a.width_b * a.width_b));
+        const bool behind = k == 0 && proj + rt < -1e-6;
+        loose = loose && (qp - rt > rk * (1.0 + 1e-6) + 1e-6 || behind);
+        tight = tight && (qp - rt > rh * (1.0 + 1e-6) + 1e-6 || behind);
     }
-    return true;
+    return (loose ? 1u : 0u) | (tight ? 2u : 0u);
 }
 
-// One warp per (tile, 32-beam word): bit j = beam 32*word + j is a candidate.
+// One warp per (tile, 32-beam word): bit j = beam 32*word + j is a candidate
+// (bits: a9 bound, tbits: tight bound, tbits subset of bits).
 __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t n_tiles,
-                                int64_t n_words, double rscale, uint32_t *bits,
+                                int64_t n_words, double rscale, uint32_t *bits, uint32_t *tbits,
                                 unsigned long long *cand_beams, unsigned long long *cand_segs) {
     const int64_t tile = blockIdx.x;
     const int64_t word = (int64_t)blockIdx.y * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -408,14 +420,17 @@ __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t 
     if (tile >= n_tiles || word >= n_words) return;
     const double4 c = centre[tile];
     const int64_t b = 32 * word + lane;
-    bool cand = false;
-    if (b < a.n_beams) cand = !beam_dead_for_tile(a, b, c.x, c.y, c.z, c.w, rscale);
+    unsigned dead = 3u;
+    if (b < a.n_beams) dead = beam_dead_for_tile(a, b, c.x, c.y, c.z, c.w, rscale);
+    const bool cand = !(dead & 1u);
     const unsigned m = __ballot_sync(0xffffffffu, cand);
+    const unsigned mt = __ballot_sync(0xffffffffu, !(dead & 2u));
     int segs = cand ? a.n_segs[b] : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) segs += __shfl_xor_sync(0xffffffffu, segs, o);
     if (lane == 0) {
         bits[tile * n_words + word] = m;
+        tbits[tile * n_words + word] = mt;
         if (m) {
             atomicAdd(&cand_beams[tile], (unsigned long long)__popc(m));
             atomicAdd(&cand_segs[tile], (unsigned long long)segs);
@@ -486,14 +501,14 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
 }
 
 int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
-                    uint32_t *bits, unsigned long long *cand_beams,
+                    uint32_t *bits, uint32_t *tbits, unsigned long long *cand_beams,
                     unsigned long long *cand_segs, cudaStream_t st) {
     if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
     const int64_t n_words = (a.n_beams + 31) / 32;
     // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
     const double rscale = a.use_cutoff ? 72.0 * a.c / (omega_min * a.width_b) : INFINITY;
     dim3 grid((unsigned)n_tiles, (unsigned)((n_words + 3) / 4));
-    worklist_kernel<<<grid, 128, 0, st>>>(a, centre, n_tiles, n_words, rscale, bits, cand_beams,
+    worklist_kernel<<<grid, 128, 0, st>>>(a, centre, n_tiles, n_words, rscale, bits, tbits, cand_beams,
                                           cand_segs);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());

@@ -460,7 +460,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
     }
 
-    const uint32_t *wl = tl.wl_bits + (p / (TILE / PATCH)) * tl.wl_words;
+    const uint32_t *wl = tl.wl_tight + (p / (TILE / PATCH)) * tl.wl_words;
     int64_t b = q * w.range_beams;
     const int64_t bend = b + w.range_beams < a.n_beams ? b + w.range_beams : a.n_beams;
     const unsigned lt = (1u << lane) - 1u;

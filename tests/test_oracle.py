@@ -89,8 +89,9 @@ def test_oracle_tracer_bitexact_vs_reference(name):
         assert np.array_equal(out[f].view(np.uint64), b[f].view(np.uint64)), f
 
 
+@pytest.mark.parametrize("tight", [False, True])
 @pytest.mark.parametrize("name", ["city_street", "city_corner_f5", "cfg1_open_plane"])
-def test_worklist_is_sound(name):
+def test_worklist_is_sound(name, tight):
     """Culled (tile, beam) pairs are pairs the reference skips: no receiver of a culled
     tile gets an evaluation from that beam (kernels.py:375,384-385)."""
     b = load_case(name)
@@ -108,7 +109,7 @@ def test_worklist_is_sound(name):
     om = b["omegas"]
     bits = oracle.worklist(b["seg_origin"], b["seg_dir"], b["seg_len"], b["seg_s0"],
                            b["n_segs"], b["max_seg"], centre, float(b["c"]),
-                           -float(b["beam_param_im"]), om.min(), True)
+                           -float(b["beam_param_im"]), om.min(), True, tight=tight)
     nb = b["n_segs"].shape[0]
     cand = np.unpackbits(bits.view(np.uint8), bitorder="little").reshape(len(tiles), -1)[:, :nb]
     assert 0 < cand.mean() < 1
