@@ -82,9 +82,10 @@ struct Fp32Work {
     float *pa;                // per row and frequency: phase anchors at s0, s0+len (turns)
     float4 *prl;              // sorted receiver -> patch-local fp32 coordinates, |r|^2
     double4 *pcen;            // per patch: centre xyz, radius
-    int *done;                // per patch: beam ranges already folded into acc
+    double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum
+    int *part_ev;             // per (beam range, sorted receiver): unit evaluation count
     unsigned *unit_ctr;       // persistent-kernel work queue head
-    int64_t n_patches, n_ranges, range_beams;
+    int64_t n_patches, n_ranges, range_beams, n_pad;  // n_pad = n_patches * patch
 };
 
 // Launchers (return BF_OK or an error status).

@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_COUNT
 };
 
 struct DeviceCtx {
@@ -122,14 +122,18 @@ int get_ctx(int device, DeviceCtx **out) {
 
 // ------------------------------------------------------------ tiling ----
 
-__global__ void bbox_kernel(const double *obs, int64_t n, double *bbox) {
+// Bounding box of n observers: grid-stride partial boxes per block (pass 1, out =
+// 6 x gridDim doubles), then one block reduces the partials (pass 2).
+__global__ void bbox_kernel(const double *obs, int64_t n, int stride3, double *out) {
     __shared__ double smin[3][256], smax[3][256];
     double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
         for (int d = 0; d < 3; ++d) {
-            const double v = obs[3 * i + d];
-            mn[d] = fmin(mn[d], v);
-            mx[d] = fmax(mx[d], v);
+            const double lo = obs[stride3 ? 3 * i + d : d * n + i];
+            const double hi = stride3 ? lo : obs[3 * n + d * n + i];
+            mn[d] = fmin(mn[d], lo);
+            mx[d] = fmax(mx[d], hi);
         }
     for (int d = 0; d < 3; ++d) {
         smin[d][threadIdx.x] = mn[d];
@@ -146,8 +150,8 @@ __global__ void bbox_kernel(const double *obs, int64_t n, double *bbox) {
     }
     if (threadIdx.x == 0)
         for (int d = 0; d < 3; ++d) {
-            bbox[d] = smin[d][0];
-            bbox[3 + d] = smax[d][0];
+            out[d * gridDim.x + blockIdx.x] = smin[d][0];
+            out[3 * gridDim.x + d * gridDim.x + blockIdx.x] = smax[d][0];
         }
 }
 
@@ -223,14 +227,16 @@ int morton_order(DeviceCtx *c, const double *obs, int64_t n, cudaStream_t st,
     double *bbox;
     uint64_t *k1, *k2;
     int32_t *v1, *v2;
-    BF_TRY(c->get(B_BBOX, 6, &bbox));
+    BF_TRY(c->get(B_BBOX, 6 + 6 * 256, &bbox));
     BF_TRY(c->get(B_KEYS, n, &k1));
     BF_TRY(c->get(B_KEYS2, n, &k2));
     BF_TRY(c->get(B_VALS, n, &v1));
     BF_TRY(c->get(B_VALS2, n, &v2));
-    bbox_kernel<<<1, 256, 0, st>>>(obs, n, bbox);
+    // pass 1: 256 partial boxes (min block-major in bbox[6..], max after); pass 2: final
+    bbox_kernel<<<256, 256, 0, st>>>(obs, n, 1, bbox + 6);
+    bbox_kernel<<<1, 256, 0, st>>>(bbox + 6, 256, 0, bbox);
     morton_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(obs, n, bbox, k1, v1);
-    note_launch(2);
+    note_launch(3);
     BF_TRY_CUDA(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(k1, k2);
     cub::DoubleBuffer<int32_t> dv(v1, v2);
@@ -340,9 +346,10 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     BF_TRY(c->get(B_PA, 2 * rows * a.nf, &w.pa));
     BF_TRY(c->get(B_PRL, a.n_obs, &w.prl));
     BF_TRY(c->get(B_PCEN, w.n_patches, &w.pcen));
-    BF_TRY(c->get(B_DONE, w.n_patches, &w.done));
+    w.n_pad = w.n_patches * P;
+    BF_TRY(c->get(B_DONE, (size_t)(w.n_ranges * w.n_pad * a.nf), &w.part));
+    BF_TRY(c->get(B_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
     BF_TRY(c->get(B_UCTR, 1, &w.unit_ctr));
-    BF_TRY_CUDA(cudaMemsetAsync(w.done, 0, sizeof(int) * w.n_patches, st));
     BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, sizeof(unsigned), st));
     BF_TRY(launch_fp32_prepare(a, t, w, st));
     GbsStats *d_stats;

@@ -22,10 +22,10 @@
 //    (cut / behind / dominated segments), then sum the live
 //    beams in ascending order through the single / corner-wedge / multi paths.
 //  * fp32 partial sums are flushed per chunk into fp64 accumulators; a unit
-//    folds its fp64 partial into the caller's acc (in-place continuation,
-//    kernels.py:358-359) only after the unit of the previous beam range of the
-//    same patch did (acquire/release flag per patch) -- the result is
-//    deterministic and independent of scheduling and of the number of ranks.
+//    stores its fp64 partial per (beam range, receiver) and fold_kernel adds the
+//    ranges in ascending order to the caller's acc (in-place continuation,
+//    kernels.py:358-359) -- the result is deterministic and independent of
+//    scheduling and of the number of ranks.
 #include <math.h>
 
 #include "common.cuh"
@@ -109,14 +109,6 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 __device__ __forceinline__ double frac_turns(double x) { return x - rint(x); }
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(int *p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 constexpr unsigned BEHIND_CHECK = 0x80000000u;
 constexpr unsigned WEDGE = 0x40000000u;
@@ -760,26 +752,18 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         for (int i = 0; i < R / 2; ++i) evp[i] = 0;
         __syncwarp();  // every lane is done with this chunk's shared rows
     }
-    // ---- fold into the caller's acc after the previous beam range of this patch
-    //      (ascending ranges: deterministic, kernels.py:358-359 continuation)
-    if (lane == 0)
-        while (ld_acquire(&w.done[p]) != (int)q) __nanosleep(100);
-    __syncwarp();
-    (void)ld_acquire(&w.done[p]);
+    // ---- the unit's partial sums (fp64) for fold_kernel, which adds the beam
+    //      ranges in ascending order: deterministic, kernels.py:358-359 continuation
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         if (j >= nvalid) continue;
-        const int64_t oi = perm[j];
+        const int64_t slot = q * w.n_pad + sb + j;
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            a.acc[2 * (oi * NF + f)] += S.acc[R * lane + j][f][0];
-            a.acc[2 * (oi * NF + f) + 1] += S.acc[R * lane + j][f][1];
-        }
-        a.evals[oi] += S.evc[R * lane + j];
+        for (int f = 0; f < NF; ++f)
+            w.part[slot * NF + f] =
+                make_double2(S.acc[R * lane + j][f][0], S.acc[R * lane + j][f][1]);
+        w.part_ev[slot] = S.evc[R * lane + j];
     }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(&w.done[p], (int)q + 1);
     ties = __reduce_add_sync(0xffffffffu, ties);
     nbp = __reduce_add_sync(0xffffffffu, nbp);
     if (lane == 0) {
@@ -892,6 +876,27 @@ __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
     if (lane == 0) pcen[p] = make_double4(cx, cy, cz, (double)(sqrtf(q) * 1.0001f + 1e-4f));
 }
 
+// acc[oi] += sum over beam ranges q (ascending) of the units' partials; evals alike.
+__global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, double *acc,
+                            int64_t *evals) {
+    const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (si >= tl.n) return;
+    const int64_t oi = tl.perm[si];
+    for (int f = 0; f < nf; ++f) {
+        double re = acc[2 * (oi * nf + f)], im = acc[2 * (oi * nf + f) + 1];
+        for (int64_t q = 0; q < w.n_ranges; ++q) {
+            const double2 v = w.part[(q * w.n_pad + si) * nf + f];
+            re += v.x;
+            im += v.y;
+        }
+        acc[2 * (oi * nf + f)] = re;
+        acc[2 * (oi * nf + f) + 1] = im;
+    }
+    int64_t ev = 0;
+    for (int64_t q = 0; q < w.n_ranges; ++q) ev += w.part_ev[q * w.n_pad + si];
+    evals[oi] += ev;
+}
+
 template <int NF>
 int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
               GbsStats *stats, cudaStream_t st) {
@@ -909,7 +914,8 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
     const int64_t need = (units + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
     gbs_fp32_kernel<NF><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
-    note_launch();
+    fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, st>>>(t, w, a.nf, a.acc, a.evals);
+    note_launch(2);
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
 }
