@@ -42,6 +42,9 @@ namespace {
 #ifndef BF_STAGE_BATCH
 #define BF_STAGE_BATCH 0
 #endif
+#ifndef BF_NORED
+#define BF_NORED 1
+#endif
 #ifndef BF_EVG
 #define BF_EVG 4
 #endif
@@ -72,6 +75,7 @@ struct Fp32Consts {
     float kappa[BF_MAXF];    // omega/(2 pi c), turns per metre
     double kappa64[BF_MAXF];
     float omega[BF_MAXF];
+    float omrel[BF_MAXF];    // omega_f / omega_0 (the staged amplitude carries omega_0)
     float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36)
     float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
     float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
@@ -150,14 +154,18 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
     for (int f = 0; f < NF; ++f) {
         const bool lf = live && !(NF > 1 && use_cutoff && q2 * K.cutk[f] > m2);  // ex_re < -36
         float turns = fmaf(gqs, K.hk2pi[f], base[f]);
+#if !BF_NORED
         turns -= rintf(turns);
+#endif
         const float ph = turns * 6.283185307179586f;
         const float sn = sin_approx(ph), cs = cos_approx(ph);
-        const float amp = ainv * K.omega[f] * ex2_approx(gq * K.nhkbl2e[f]);
-        const float dre = -amp * fmaf(s, sn, K.b * cs), dim = amp * fmaf(s, cs, -K.b * sn);
-        if (lf) {
-            pre[f] += dre;
-            pim[f] += dim;
+        // A carries omega_0 (staging); omrel[f] = omega_f / omega_0
+        float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]);
+        if (f > 0) amp *= K.omrel[f];
+        const float as = amp * s, ab = amp * K.b;
+        if (lf) {  // i * amp * (s + i b) * (cos + i sin)
+            pre[f] = fmaf(-as, sn, fmaf(-ab, cs, pre[f]));
+            pim[f] = fmaf(as, cs, fmaf(-ab, sn, pim[f]));
             ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
         }
     }
@@ -402,7 +410,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, i
         S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
                                 (float)(ucx * ucx + ucy * ucy + ucz * ucz));
         const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + p0.w) + RW + 1.f;
-        S.aux[r] = make_float4((float)p1.w, p2.x, p2.y, D);
+        S.aux[r] = make_float4((float)p1.w, p2.x * K.omega[0], p2.y, D);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             const float2 ae = reinterpret_cast<const float2 *>(w.pa)[g * NF + f];
@@ -930,6 +938,7 @@ Fp32Consts make_consts(const GbsArgs &a) {
         K.kappa64[f] = w / (two_pi * a.c);
         K.kappa[f] = (float)K.kappa64[f];
         K.omega[f] = (float)w;
+        K.omrel[f] = f < a.nf ? (float)(w / a.omegas[0]) : 0.f;
         K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
         K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
         K.nhkbl2e[f] = (float)(-(w * 0.5 / a.c) * a.width_b * 1.4426950408889634);
