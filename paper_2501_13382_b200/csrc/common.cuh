@@ -57,6 +57,7 @@ struct GbsStats {
     unsigned long long nb_pairs;         // non-behind pairs (P_nb of SURVEY 8(d))
     unsigned long long cand_pair_segs;   // sum over candidate pairs of the beam's n_segs
     unsigned long long paths[4];         // (warp patch, beam) items: culled, single, wedge, multi
+    unsigned long long multi_surv[4];    // multi items with 2, 3, 4, >= 5 surviving segments
     float kernel_ms;                     // CUDA-event duration of the summation kernel
 };
 

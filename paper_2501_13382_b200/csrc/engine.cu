@@ -378,6 +378,11 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     h.candidate_pairs = cp;
     h.cand_pair_segs = cs;
     g_last_stats = h;
+    if (getenv("BF_DEBUG_STATS"))
+        fprintf(stderr, "bf stats: items culled %llu single %llu wedge %llu multi %llu "
+                "(surv 2:%llu 3:%llu 4:%llu 5+:%llu) ties %llu\n", h.paths[0], h.paths[1],
+                h.paths[2], h.paths[3], h.multi_surv[0], h.multi_surv[1], h.multi_surv[2],
+                h.multi_surv[3], h.tie_pairs);
     g_last_tiles = t.n_tiles;
     return BF_OK;
 }

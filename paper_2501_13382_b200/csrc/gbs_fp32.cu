@@ -42,6 +42,9 @@ namespace {
 #ifndef BF_STAGE_BATCH
 #define BF_STAGE_BATCH 0
 #endif
+#ifndef BF_HIST
+#define BF_HIST 0
+#endif
 #ifndef BF_NORED
 #define BF_NORED 1
 #endif
@@ -367,6 +370,52 @@ __device__ __noinline__ ExactPick exact_pick(const double *__restrict__ seg_orig
     return e;
 }
 
+// Exact re-decision (fp64, reference operation order) of the receivers in `pend`
+// among the surviving segments `surv` (ascending k, strict <), one pending
+// receiver per lane per round; fills the nearest point of each decided receiver.
+template <int NF>
+__device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<NF> &S,
+                                              int64_t beam, int r0, unsigned surv, unsigned pend,
+                                              const float (&rx)[R], const float (&ry)[R],
+                                              const float (&rz)[R], const float (&rr)[R],
+                                              const float (&best)[R], const int (&kb)[R],
+                                              float tie_abs, int lane, float (&sj)[R],
+                                              float (&q2j)[R], float (&pj)[R], float (&dlj)[R],
+                                              int (&rowj)[R], unsigned &lvm, unsigned &ties) {
+    ties += __popc(pend);
+#pragma unroll 1
+    while (__any_sync(0xffffffffu, pend != 0)) {
+        if (!pend) continue;
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
+        const ExactPick e = exact_pick(a.seg_origin, a.seg_dir, a.seg_len, beam * a.max_seg,
+                                       S.geo0 + r0, S.geo1 + r0, surv, pick4(kb, j), x, y, z,
+                                       pick4(best, j), tie_abs, S.p64[R * lane + j]);
+        if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
+        const int k = e.bk;
+        const float4 g1 = S.geo1[r0 + k];
+        const float4 g2 = S.geo2[r0 + k];
+        const float dl = fmaf(x, g1.x, fmaf(y, g1.y, z * g1.z));
+        const float q2 =
+            fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
+                  0.f);
+        const float s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
+        // anchor choice follows the exact clamp
+        const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
+#pragma unroll
+        for (int jj = 0; jj < R; ++jj)
+            if (jj == j) {
+                q2j[jj] = q2;
+                sj[jj] = s;
+                rowj[jj] = r0 + k;
+                pj[jj] = proj;
+                dlj[jj] = dl;
+            }
+        lvm |= 1u << j;
+    }
+}
+
 // Stage chunk rows [0, nrows) into warp-private shared memory, patch-local.
 template <int NF>
 __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, int64_t max_seg,
@@ -425,7 +474,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, i
 template <int NF>
 __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, const Fp32Work &w,
                                          const Fp32Consts &K, WarpSmem<NF> &S, int64_t p,
-                                         int64_t q, int lane) {
+                                         int64_t q, int lane, GbsStats *stats) {
     const float RW = (float)w.pcen[p].w;
     // ---- receivers (patch-local); padding receivers sit at the centre and are
     //      computed but never written back
@@ -533,6 +582,22 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             const unsigned nw = __popc(__ballot_sync(0xffffffffu, (word & WEDGE) != 0));
             const unsigned nm = __popc(__ballot_sync(0xffffffffu, word != 0 && !(word & WEDGE) &&
                                                                       (m & (m - 1)) != 0));
+#if BF_HIST
+            {
+                const bool mul = word != 0 && !(word & WEDGE) && (m & (m - 1)) != 0;
+                const int ns_ = __popc(m);
+                const unsigned h2 = __popc(__ballot_sync(0xffffffffu, mul && ns_ == 2));
+                const unsigned h3 = __popc(__ballot_sync(0xffffffffu, mul && ns_ == 3));
+                const unsigned h4 = __popc(__ballot_sync(0xffffffffu, mul && ns_ == 4));
+                const unsigned h5 = __popc(__ballot_sync(0xffffffffu, mul && ns_ >= 5));
+                if (lane == 0) {
+                    atomicAdd(&stats->multi_surv[0], (unsigned long long)h2);
+                    atomicAdd(&stats->multi_surv[1], (unsigned long long)h3);
+                    atomicAdd(&stats->multi_surv[2], (unsigned long long)h4);
+                    atomicAdd(&stats->multi_surv[3], (unsigned long long)h5);
+                }
+            }
+#endif
             if (lane == 0) {
                 S.cnt[2] += nbc - __popc(live);
                 S.cnt[3] += __popc(live) - nw - nm;
@@ -629,11 +694,14 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 ties += __popc(lvm);
             } else {
-                // ---- several candidate segments: fp32 scan, fp64 re-decision of ties
+                // ---- several candidate segments: fp32 distances, fp64 re-decision of ties
                 const float Db = S.bD[jb];
                 const float tie_abs = TIE_ABS * Db * Db;
-                float best[R], second[R];
+                float best[R];
                 int kb[R];
+                unsigned pend = 0;  // receivers whose winner is re-decided in fp64
+                lvm = 0;
+                float second[R];
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     best[j] = INFINITY;
@@ -657,8 +725,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         best[j] = fminf(best[j], d2);
                     }
                 }
-                lvm = 0;
-                unsigned pend = 0;  // receivers whose winner is re-decided in fp64
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const int k = kb[j];
@@ -687,40 +753,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     dlj[j] = dl;
                     lvm |= 1u << j;
                 }
-                // exact re-decision among the contenders (ascending k, strict <), one
-                // pending receiver per lane per round
-                ties += __popc(pend);
-#pragma unroll 1
-                while (__any_sync(0xffffffffu, pend != 0)) {
-                    if (!pend) continue;
-                    const int j = __ffs(pend) - 1;
-                    pend &= pend - 1;
-                    const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
-                    const ExactPick e = exact_pick(a.seg_origin, a.seg_dir, a.seg_len,
-                                                   beam * a.max_seg, S.geo0 + r0, S.geo1 + r0,
-                                                   surv, pick4(kb, j), x, y, z, pick4(best, j),
-                                                   tie_abs, S.p64[R * lane + j]);
-                    if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
-                    const int k = e.bk;
-                    const float4 g1 = S.geo1[r0 + k];
-                    const float4 g2 = S.geo2[r0 + k];
-                    const float dl = fmaf(x, g1.x, fmaf(y, g1.y, z * g1.z));
-                    const float q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
-                                           0.f);
-                    const float s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
-                    // anchor choice follows the exact clamp
-                    const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
-#pragma unroll
-                    for (int jj = 0; jj < R; ++jj)
-                        if (jj == j) {
-                            q2j[jj] = q2;
-                            sj[jj] = s;
-                            rowj[jj] = r0 + k;
-                            pj[jj] = proj;
-                            dlj[jj] = dl;
-                        }
-                    lvm |= 1u << j;
-                }
+                exact_pending<NF>(a, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb, tie_abs,
+                                  lane, sj, q2j, pj, dlj, rowj, lvm, ties);
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
@@ -798,7 +832,7 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
         if (u >= n_units) break;
         const unsigned q = u / n_patches;  // range-major: one L2-resident slice
         const unsigned p = u - q * n_patches;
-        run_unit<NF>(a, tl, w, K, S, p, q, lane);
+        run_unit<NF>(a, tl, w, K, S, p, q, lane, stats);
     }
     // per-lane counters straight into the device statistics
     __syncwarp();
