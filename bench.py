@@ -20,6 +20,7 @@ threads on a bounded receiver sample of the same workload; rank 0 only.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -292,6 +293,12 @@ def run_ours(args):
         # FLOP model over the work-list survivors: candidate pairs only
         flop, mufu = flop_model(float(st["candidate_pair_segs"]), p_nb, ev_sum, nf)
         kernel_s = kern_max / 1e3
+        traffic = None  # DRAM bytes of the summation kernel from the committed ncu capture
+        for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_*_traffic.json"))):
+            with open(tf) as fh:
+                tj = json.load(fh)
+            if tj.get("config") == args.config and world == 1:
+                traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
         ach = flop / kernel_s / 1e12
         clocks = clk.summary()
         peak = peaks["fp32_tflops"]
@@ -313,7 +320,9 @@ def run_ours(args):
                     "path": "kernels.gbs_accumulate(host numpy, pinned) -> bf_gbs_accumulate"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                         "frac": ach / peak, "traffic": None,
+                         "frac": ach / peak, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per launch (ncu --set full, committed "
+                                         "profile of this config)" if traffic else None,
                          "peak_source": "measured FFMA stream (bf_probe_peaks), this GPU",
                          "kernel": "gbs_fp32_kernel", "kernel_ms": kern_max,
                          "flop_per_launch": flop, "mufu_per_launch": mufu,
