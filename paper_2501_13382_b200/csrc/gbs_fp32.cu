@@ -27,6 +27,8 @@
 //    kernels.py:358-359) -- the result is deterministic and independent of
 //    scheduling and of the number of ranks.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -127,8 +129,8 @@ struct WarpSmem {
     float4 geo0[ROWCAP];     // wc.xyz (c_P - o), len
     float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_P)
     float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
-    float4 aux[ROWCAP];      // s0, A (amplitude factor), R_cut, D (error scale)
-    float4 anc[NF][ROWCAP];  // phase anchors (turns): centre proj, start, end, -
+    float2 aux[ROWCAP];      // s0, A (amplitude factor x omega_0)
+    float4 anc[NF][ROWCAP];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
     unsigned char rowbeam[ROWCAP];  // chunk row -> chunk beam
     short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
@@ -459,12 +461,12 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, i
         S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
                                 (float)(ucx * ucx + ucy * ucy + ucz * ucz));
         const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + p0.w) + RW + 1.f;
-        S.aux[r] = make_float4((float)p1.w, p2.x * K.omega[0], p2.y, D);
+        S.aux[r] = make_float2((float)p1.w, p2.x * K.omega[0]);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             const float2 ae = reinterpret_cast<const float2 *>(w.pa)[g * NF + f];
             S.anc[f][r] =
-                make_float4((float)frac_turns(K.kappa64[f] * (p1.w + pc)), ae.x, ae.y, 0.f);
+                make_float4((float)frac_turns(K.kappa64[f] * (p1.w + pc)), ae.x, ae.y, f ? 0.f : D);
         }
     }
 }
@@ -571,7 +573,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             const int r0 = S.brow[lane], nsb = S.brow[lane + 1] - r0;
             float D = 0.f;
 #pragma unroll 1
-            for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.aux[r0 + k].w);
+            for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.anc[0][r0 + k].w);
             word = classify<NF>(S, K, r0, nsb, RW, D);
             S.surv[lane] = word;
             S.bD[lane] = D;
@@ -645,7 +647,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 lvm = (1u << R) - 1;
                 if (bword & BEHIND_CHECK)
-                    lvm = behind_mask(a, pj, S.p64 + R * lane, nvalid, S.aux[row].w, beam, k, ties);
+                    lvm = behind_mask(a, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, beam, k, ties);
             } else if (bword & WEDGE) {
                 // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
                 //      the reference picks by fp64 rounding, reproduced exactly here
@@ -738,7 +740,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g1 = S.geo1[r0 + k];
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
-                    if (k == 0 && fabsf(proj) <= PROJ_ERR * S.aux[r0].w) exact = true;
+                    if (k == 0 && fabsf(proj) <= PROJ_ERR * S.anc[0][r0].w) exact = true;
                     if (exact) {
                         if (j < nvalid) pend |= 1u << j;
                         continue;
@@ -951,6 +953,9 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
     BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gbs_fp32_kernel<NF>,
                                                               THREADS, smem));
     if (per_sm < 1) return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
+    if (getenv("BF_DEBUG_STATS"))
+        fprintf(stderr, "bf fp32 kernel: %zu B shared per CTA (%zu per warp), %d CTAs/SM\n", smem,
+                sizeof(WarpSmem<NF>), per_sm);
     const int64_t units = w.n_patches * w.n_ranges;
     int64_t grid = (int64_t)sms * per_sm;
     const int64_t need = (units + WARPS - 1) / WARPS;
