@@ -290,8 +290,11 @@ def run_ours(args):
         st = stats[-1]
         ev_sum = int(evals.sum().item())
         p_nb = st["nonbehind_pairs"]
-        # FLOP model over the work-list survivors: candidate pairs only
-        flop, mufu = flop_model(float(st["candidate_pair_segs"]), p_nb, ev_sum, nf)
+        # FLOP model over the pairs of the tight work list the kernel walks
+        # (bit-exact, oracle-pinned); the a9 list and the evaluated items are reported too
+        flop, mufu = flop_model(float(st["tight_pair_segs"]), p_nb, ev_sum, nf)
+        flop_a9, _ = flop_model(float(st["candidate_pair_segs"]), p_nb, ev_sum, nf)
+        flop_live, _ = flop_model(float(st["live_pair_segs"]), p_nb, ev_sum, nf)
         kernel_s = kern_max / 1e3
         traffic = None  # DRAM bytes of the summation kernel from the committed ncu capture
         for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_*_traffic.json"))):
@@ -321,6 +324,9 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak, "traffic": traffic,
+                         "work_list": "tight (tile, beam) list walked by the kernel",
+                         "frac_a9_list": flop_a9 / kernel_s / 1e12 / peak,
+                         "frac_evaluated_items": flop_live / kernel_s / 1e12 / peak,
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, committed "
                                          "profile of this config)" if traffic else None,
                          "peak_source": "measured FFMA stream (bf_probe_peaks), this GPU",
@@ -329,11 +335,14 @@ def run_ours(args):
                          "mufu_tops": mufu / kernel_s / 1e12,
                          "mufu_peak_tops": peaks["mufu_tops"],
                          "mufu_frac": mufu / kernel_s / 1e12 / peaks["mufu_tops"],
-                         "algorithmic_model": "SURVEY.md 8(d): 19*N_r*sum(n_segs) + "
-                                              "(16+5F)*P_nb + 22*E FLOP; P_nb + 3E MUFU",
+                         "algorithmic_model": "SURVEY.md 8(d): 19*sum over work-list pairs of "
+                                              "n_segs + (16+5F)*P_nb + 22*E FLOP; P_nb + 3E "
+                                              "MUFU",
                          "nonbehind_pairs": p_nb, "evaluations": ev_sum,
                          "tie_pairs": st["tie_pairs"], "patch_beams": st["patch_beams"],
-                         "candidate_pairs": st["candidate_pairs"],
+                         "candidate_pairs_a9": st["candidate_pairs"],
+                         "candidate_pairs_tight": st["tight_pairs"],
+                         "evaluated_item_pairs": st["live_pairs"],
                          "dense_pairs": int(nb) * int(n_loc)},
             "clocks": clocks,
         }

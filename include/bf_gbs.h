@@ -122,6 +122,15 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
                 double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
                 uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out, int device);
 
+/*
+ * Pair counts of the last fp32 summation on this thread (FLOP model of the roofline,
+ * SURVEY 8(d)): (beam, receiver) pairs and pair-segments (sum of the beam's n_segs)
+ * on the a9 work list, on the tight work list the kernel walks, and in the
+ * (patch, beam) items the kernel evaluated (after its own patch-level culling).
+ */
+int bf_last_pair_stats(int64_t *a9_pairs, int64_t *a9_pair_segs, int64_t *tight_pairs,
+                       int64_t *tight_pair_segs, int64_t *live_pairs, int64_t *live_pair_segs);
+
 /* Receivers per tile of the fp32 summation kernel. */
 int bf_tile_size(void);
 

@@ -25,6 +25,7 @@ EXPORTS = (
     "bf_gbs_accumulate", "bf_gbs_accumulate_dev", "bf_nearest_on_segments",
     "bf_trace_range_dev", "bf_field_finalize_dev", "bf_plan_chunks", "bf_last_stats",
     "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats", "bf_worklist",
+    "bf_last_pair_stats",
 )
 FLAG_OBS_PRESORTED = 1
 
@@ -63,6 +64,7 @@ def _declare(lib):
     lib.bf_last_stats.argtypes = [I64P, I64P, I64P, I64P, I64P, D, I64P]
     lib.bf_probe_peaks.argtypes = [INT, D, D]
     lib.bf_last_path_stats.argtypes = [I64P] * 4
+    lib.bf_last_pair_stats.argtypes = [I64P] * 6
     lib.bf_worklist.argtypes = [VP, VP, VP, VP, VP, I64, I64, VP, I64, VP, I64, F64, F64, INT,
                                 VP, VP, VP, VP, I64, I64P, INT]
     for name in EXPORTS:
@@ -113,7 +115,11 @@ def last_stats() -> dict:
     cand, total, ties, tiles, nbp = (v.value for v in vals)
     paths = [ctypes.c_int64(0) for _ in range(4)]
     check(load().bf_last_path_stats(*[ctypes.byref(v) for v in paths]))
+    pairs = [ctypes.c_int64(0) for _ in range(6)]
+    check(load().bf_last_pair_stats(*[ctypes.byref(v) for v in pairs]))
+    a9p, a9s, tp, ts, lp, ls = (v.value for v in pairs)
     return {"candidate_pairs": cand, "total_pairs": total, "tie_pairs": ties, "n_tiles": tiles,
+            "tight_pairs": tp, "tight_pair_segs": ts, "live_pairs": lp, "live_pair_segs": ls,
             "nonbehind_pairs": nbp, "kernel_ms": ms.value, "candidate_pair_segs": cps.value,
             "patch_beams": dict(zip(("culled", "single", "wedge", "multi"),
                                     (v.value for v in paths)))}

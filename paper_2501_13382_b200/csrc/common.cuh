@@ -58,6 +58,10 @@ struct GbsStats {
     unsigned long long cand_pair_segs;   // sum over candidate pairs of the beam's n_segs
     unsigned long long paths[4];         // (warp patch, beam) items: culled, single, wedge, multi
     unsigned long long multi_surv[4];    // multi items with 2, 3, 4, >= 5 surviving segments
+    unsigned long long tight_pairs;      // (beam, receiver) pairs on the tight work list
+    unsigned long long tight_pair_segs;  // sum over those pairs of the beam's n_segs
+    unsigned long long live_pairs;       // pairs of the (patch, beam) items the kernel evaluates
+    unsigned long long live_pair_segs;   // sum over those pairs of the beam's n_segs
     float kernel_ms;                     // CUDA-event duration of the summation kernel
 };
 
@@ -108,7 +112,8 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                  int64_t row_base, cudaStream_t st);
 int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
                     uint32_t *bits, uint32_t *tbits, unsigned long long *cand_beams,
-                    unsigned long long *cand_segs, cudaStream_t st);
+                    unsigned long long *cand_segs, unsigned long long *tight_beams,
+                    unsigned long long *tight_segs, cudaStream_t st);
 int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
                     double *spl, cudaStream_t st);
 

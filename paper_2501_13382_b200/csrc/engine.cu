@@ -309,11 +309,12 @@ int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st,
     unsigned long long *cand;
     BF_TRY(c->get(B_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
     BF_TRY(c->get(B_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
-    BF_TRY(c->get(B_WLCNT, (size_t)(2 * t.n_tiles), &cand));
-    BF_TRY_CUDA(cudaMemsetAsync(cand, 0, 2 * sizeof(unsigned long long) * t.n_tiles, st));
+    BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &cand));
+    BF_TRY_CUDA(cudaMemsetAsync(cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
     double wmin = INFINITY;
     for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
-    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, tbits, cand, cand + t.n_tiles, st));
+    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, tbits, cand, cand + t.n_tiles,
+                           cand + 2 * t.n_tiles, cand + 3 * t.n_tiles, st));
     t.wl_bits = bits;
     t.wl_tight = tbits;
     t.wl_words = n_words;
@@ -366,17 +367,22 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     BF_TRY_CUDA(cudaMemcpyAsync(&h, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost, st));
     BF_TRY_CUDA(cudaStreamSynchronize(st));
     BF_TRY_CUDA(cudaEventElapsedTime(&h.kernel_ms, c->ev0, c->ev1));
-    std::vector<unsigned long long> cand((size_t)(2 * t.n_tiles));
-    BF_TRY_CUDA(cudaMemcpy(cand.data(), d_cand, 2 * sizeof(unsigned long long) * t.n_tiles,
+    std::vector<unsigned long long> cand((size_t)(4 * t.n_tiles));
+    BF_TRY_CUDA(cudaMemcpy(cand.data(), d_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
                            cudaMemcpyDeviceToHost));
-    unsigned long long cp = 0, cs = 0;
+    unsigned long long cp = 0, cs = 0, tp = 0, ts = 0;
     for (int64_t i = 0; i < t.n_tiles; ++i) {
-        const int64_t in_tile = (i + 1 < t.n_tiles) ? t.tile : a.n_obs - i * t.tile;
-        cp += cand[(size_t)i] * (unsigned long long)in_tile;
-        cs += cand[(size_t)(t.n_tiles + i)] * (unsigned long long)in_tile;
+        const unsigned long long in_tile =
+            (unsigned long long)((i + 1 < t.n_tiles) ? t.tile : a.n_obs - i * t.tile);
+        cp += cand[(size_t)i] * in_tile;
+        cs += cand[(size_t)(t.n_tiles + i)] * in_tile;
+        tp += cand[(size_t)(2 * t.n_tiles + i)] * in_tile;
+        ts += cand[(size_t)(3 * t.n_tiles + i)] * in_tile;
     }
     h.candidate_pairs = cp;
     h.cand_pair_segs = cs;
+    h.tight_pairs = tp;
+    h.tight_pair_segs = ts;
     g_last_stats = h;
     if (getenv("BF_DEBUG_STATS"))
         fprintf(stderr, "bf stats: items culled %llu single %llu wedge %llu multi %llu "
@@ -419,6 +425,17 @@ int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_p
     if (total_pairs) *total_pairs = g_last_total_pairs;
     if (tie_pairs) *tie_pairs = (int64_t)g_last_stats.tie_pairs;
     if (n_tiles) *n_tiles = g_last_tiles;
+    return BF_OK;
+}
+
+int bf_last_pair_stats(int64_t *a9_pairs, int64_t *a9_pair_segs, int64_t *tight_pairs,
+                       int64_t *tight_pair_segs, int64_t *live_pairs, int64_t *live_pair_segs) {
+    if (a9_pairs) *a9_pairs = (int64_t)g_last_stats.candidate_pairs;
+    if (a9_pair_segs) *a9_pair_segs = (int64_t)g_last_stats.cand_pair_segs;
+    if (tight_pairs) *tight_pairs = (int64_t)g_last_stats.tight_pairs;
+    if (tight_pair_segs) *tight_pair_segs = (int64_t)g_last_stats.tight_pair_segs;
+    if (live_pairs) *live_pairs = (int64_t)g_last_stats.live_pairs;
+    if (live_pair_segs) *live_pair_segs = (int64_t)g_last_stats.live_pair_segs;
     return BF_OK;
 }
 

@@ -413,7 +413,8 @@ __device__ __forceinline__ unsigned beam_dead_for_tile(const GbsArgs &a, int64_t
 // (bits: a9 bound, tbits: tight bound, tbits subset of bits).
 __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t n_tiles,
                                 int64_t n_words, double rscale, uint32_t *bits, uint32_t *tbits,
-                                unsigned long long *cand_beams, unsigned long long *cand_segs) {
+                                unsigned long long *cand_beams, unsigned long long *cand_segs,
+                                unsigned long long *tight_beams, unsigned long long *tight_segs) {
     const int64_t tile = blockIdx.x;
     const int64_t word = (int64_t)blockIdx.y * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -425,15 +426,23 @@ __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t 
     const bool cand = !(dead & 1u);
     const unsigned m = __ballot_sync(0xffffffffu, cand);
     const unsigned mt = __ballot_sync(0xffffffffu, !(dead & 2u));
-    int segs = cand ? a.n_segs[b] : 0;
+    const int ns = b < a.n_beams ? a.n_segs[b] : 0;
+    int segs = cand ? ns : 0, tsegs = !(dead & 2u) ? ns : 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) segs += __shfl_xor_sync(0xffffffffu, segs, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        segs += __shfl_xor_sync(0xffffffffu, segs, o);
+        tsegs += __shfl_xor_sync(0xffffffffu, tsegs, o);
+    }
     if (lane == 0) {
         bits[tile * n_words + word] = m;
         tbits[tile * n_words + word] = mt;
         if (m) {
             atomicAdd(&cand_beams[tile], (unsigned long long)__popc(m));
             atomicAdd(&cand_segs[tile], (unsigned long long)segs);
+        }
+        if (mt) {
+            atomicAdd(&tight_beams[tile], (unsigned long long)__popc(mt));
+            atomicAdd(&tight_segs[tile], (unsigned long long)tsegs);
         }
     }
 }
@@ -502,14 +511,15 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
 
 int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
                     uint32_t *bits, uint32_t *tbits, unsigned long long *cand_beams,
-                    unsigned long long *cand_segs, cudaStream_t st) {
+                    unsigned long long *cand_segs, unsigned long long *tight_beams,
+                    unsigned long long *tight_segs, cudaStream_t st) {
     if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
     const int64_t n_words = (a.n_beams + 31) / 32;
     // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
     const double rscale = a.use_cutoff ? 72.0 * a.c / (omega_min * a.width_b) : INFINITY;
     dim3 grid((unsigned)n_tiles, (unsigned)((n_words + 3) / 4));
     worklist_kernel<<<grid, 128, 0, st>>>(a, centre, n_tiles, n_words, rscale, bits, tbits, cand_beams,
-                                          cand_segs);
+                                          cand_segs, tight_beams, tight_segs);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

@@ -139,7 +139,8 @@ struct WarpSmem {
     double acc[PATCH][NF][2];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
-    unsigned long long cnt[6];  // statistics: ties, non-behind, culled/single/wedge/multi items
+    unsigned long long cnt[8];  // statistics: ties, non-behind, culled/single/wedge/multi
+                                // items, live pairs, live pair-segments
 };
 
 // Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
@@ -600,7 +601,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
             }
 #endif
+            // pairs of the evaluated items and their segment counts (FLOP model)
+            const unsigned lsegs = __reduce_add_sync(
+                0xffffffffu, word != 0 ? (unsigned)(S.brow[lane + 1] - S.brow[lane]) : 0u);
+            const unsigned long long pv = (unsigned long long)min((int64_t)PATCH, tl.n - p * PATCH);
             if (lane == 0) {
+                S.cnt[6] += pv * __popc(live);
+                S.cnt[7] += pv * lsegs;
                 S.cnt[2] += nbc - __popc(live);
                 S.cnt[3] += __popc(live) - nw - nm;
                 S.cnt[4] += nw;
@@ -825,7 +832,7 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
     const int lane = threadIdx.x & 31;
     const unsigned n_units = (unsigned)(w.n_patches * w.n_ranges);
     const unsigned n_patches = (unsigned)w.n_patches;
-    if (lane < 6) S.cnt[lane] = 0;
+    if (lane < 8) S.cnt[lane] = 0;
     __syncwarp();
     for (;;) {
         unsigned u = 0;
@@ -843,6 +850,8 @@ __global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
         atomicAdd(&stats->nb_pairs, S.cnt[1]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) atomicAdd(&stats->paths[i], S.cnt[2 + i]);
+        atomicAdd(&stats->live_pairs, S.cnt[6]);
+        atomicAdd(&stats->live_pair_segs, S.cnt[7]);
     }
 }
 
