@@ -44,6 +44,9 @@ namespace {
 #ifndef BF_STAGE_BATCH
 #define BF_STAGE_BATCH 0
 #endif
+#ifndef BF_JUNC
+#define BF_JUNC 1
+#endif
 #ifndef BF_HIST
 #define BF_HIST 0
 #endif
@@ -297,24 +300,31 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&
                                              const double (*p64)[3], int nvalid, float D,
                                              int64_t beam, int k, unsigned &ties) {
     const float tolp = PROJ_ERR * D;
-    unsigned m = 0;
+    unsigned m = 0, amb = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        if (pj[j] >= tolp) {
+        if (pj[j] >= tolp)
             m |= 1u << j;
-            continue;
-        }
-        if (pj[j] < -tolp || j >= nvalid) continue;
-        // proj of kernels.py:328-331, reference operation order, no FMA
+        else if (pj[j] >= -tolp && j < nvalid)
+            amb |= 1u << j;
+    }
+    if (amb) {  // rare: one copy of the fp64 code
         const int64_t row = beam * a.max_seg + k;
-        const double wx = __dsub_rn(p64[j][0], a.seg_origin[3 * row]);
-        const double wy = __dsub_rn(p64[j][1], a.seg_origin[3 * row + 1]);
-        const double wz = __dsub_rn(p64[j][2], a.seg_origin[3 * row + 2]);
-        const double proj = __dadd_rn(__dadd_rn(__dmul_rn(wx, a.seg_dir[3 * row]),
-                                                __dmul_rn(wy, a.seg_dir[3 * row + 1])),
-                                      __dmul_rn(wz, a.seg_dir[3 * row + 2]));
-        ++ties;
-        if (!(proj < 0.0)) m |= 1u << j;
+        const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
+                     oz = a.seg_origin[3 * row + 2];
+        const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
+                     dz = a.seg_dir[3 * row + 2];
+        ties += __popc(amb);
+#pragma unroll 1
+        for (; amb; amb &= amb - 1) {
+            const int j = __ffs(amb) - 1;
+            // proj of kernels.py:328-331, reference operation order, no FMA
+            const double wx = __dsub_rn(p64[j][0], ox), wy = __dsub_rn(p64[j][1], oy),
+                         wz = __dsub_rn(p64[j][2], oz);
+            const double proj =
+                __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
+            if (!(proj < 0.0)) m |= 1u << j;
+        }
     }
     return m;
 }
@@ -373,6 +383,39 @@ __device__ __noinline__ ExactPick exact_pick(const double *__restrict__ seg_orig
     return e;
 }
 
+// Segments k, k+1 meeting at a reflection point, in fp64 (packed rows): when a
+// receiver projects beyond the end of k and before the start of k+1, both clamped
+// distances (kernels.py:332-340) are distances to the reflection point and the
+// reference's choice is decided by fp64 rounding, reproduced here op for op.
+struct Junction {
+    double ox, oy, oz;  // o_k
+    double lx, ly, lz;  // len_k * d_k (t = len, kernels.py:337-339)
+    double bx, by, bz;  // o_{k+1}
+    float sa, sb;       // s of either winner: s0_k + len_k, s0_{k+1}
+};
+
+__device__ __forceinline__ Junction load_junction(const Fp32Work &w, int64_t grow) {
+    const double4 a0 = w.p0[grow], a1 = w.p1[grow], b0 = w.p0[grow + 1], b1 = w.p1[grow + 1];
+    Junction J;
+    J.ox = a0.x, J.oy = a0.y, J.oz = a0.z;
+    J.lx = __dmul_rn(a0.w, a1.x), J.ly = __dmul_rn(a0.w, a1.y), J.lz = __dmul_rn(a0.w, a1.z);
+    J.bx = b0.x, J.by = b0.y, J.bz = b0.z;
+    J.sa = (float)(a1.w + a0.w);
+    J.sb = (float)b1.w;
+    return J;
+}
+
+// true -> segment k+1 is the reference's nearest segment (strict <: ties keep k)
+__device__ __forceinline__ bool junction_pick(const Junction &J, const double (&p)[3]) {
+    const double vx = __dsub_rn(__dsub_rn(p[0], J.ox), J.lx);
+    const double vy = __dsub_rn(__dsub_rn(p[1], J.oy), J.ly);
+    const double vz = __dsub_rn(__dsub_rn(p[2], J.oz), J.lz);
+    const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    const double wx = __dsub_rn(p[0], J.bx), wy = __dsub_rn(p[1], J.by), wz = __dsub_rn(p[2], J.bz);
+    const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
+    return db < da;
+}
+
 // Exact re-decision (fp64, reference operation order) of the receivers in `pend`
 // among the surviving segments `surv` (ascending k, strict <), one pending
 // receiver per lane per round; fills the nearest point of each decided receiver.
@@ -384,8 +427,55 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<N
                                               const float (&best)[R], const int (&kb)[R],
                                               float tie_abs, int lane, float (&sj)[R],
                                               float (&q2j)[R], float (&pj)[R], float (&dlj)[R],
-                                              int (&rowj)[R], unsigned &lvm, unsigned &ties) {
+                                              int (&rowj)[R], unsigned &lvm, unsigned &ties,
+                                              const Fp32Work &w) {
     ties += __popc(pend);
+    // two adjacent candidates k, k+1 (most multi items): a receiver that projects
+    // beyond the end of k and before the start of k+1 is decided like the corner wedge
+#if BF_JUNC
+    const int ka = __ffs(surv) - 1;
+    if (surv == (3u << ka) && __any_sync(0xffffffffu, pend != 0)) {
+        const float4 a0 = S.geo0[r0 + ka], a1 = S.geo1[r0 + ka], b0 = S.geo0[r0 + ka + 1],
+                     b1 = S.geo1[r0 + ka + 1];
+        const float tol = PROJ_ERR * fmaxf(S.anc[0][r0 + ka].w, S.anc[0][r0 + ka + 1].w);
+        unsigned jp = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const float pa = (rx[j] + a0.x) * a1.x + (ry[j] + a0.y) * a1.y + (rz[j] + a0.z) * a1.z;
+            const float pb = (rx[j] + b0.x) * b1.x + (ry[j] + b0.y) * b1.y + (rz[j] + b0.z) * b1.z;
+            if (((pend >> j) & 1u) && pa - a0.w >= tol && pb <= -tol) jp |= 1u << j;
+        }
+        if (__any_sync(0xffffffffu, jp != 0)) {
+            pend &= ~jp;
+            const Junction J = load_junction(w, beam * a.max_seg + ka);
+#pragma unroll 1
+            while (__any_sync(0xffffffffu, jp != 0)) {
+                if (!jp) continue;
+                const int j = __ffs(jp) - 1;
+                jp &= jp - 1;
+                const bool wb = junction_pick(J, S.p64[R * lane + j]);
+                const int row = r0 + ka + (wb ? 1 : 0);
+                const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
+                const float4 g1 = wb ? b1 : a1;
+                const float4 g2 = S.geo2[row];
+                const float dl = fmaf(x, g1.x, fmaf(y, g1.y, z * g1.z));
+                const float q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
+                                       0.f);
+                const float sv = wb ? J.sb : J.sa;
+#pragma unroll
+                for (int jj = 0; jj < R; ++jj)
+                    if (jj == j) {
+                        q2j[jj] = q2;
+                        sj[jj] = sv;
+                        rowj[jj] = row;
+                        pj[jj] = wb ? -1.f : INFINITY;  // start anchor of k+1 / end anchor of k
+                        dlj[jj] = 0.f;
+                    }
+                lvm |= 1u << j;
+            }
+        }
+    }
+#endif
 #pragma unroll 1
     while (__any_sync(0xffffffffu, pend != 0)) {
         if (!pend) continue;
@@ -660,42 +750,21 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 //      the reference picks by fp64 rounding, reproduced exactly here
                 const int k = __ffs(surv) - 1;
                 const int ra = r0 + k, rb = ra + 1;
-                const int64_t grow = beam * a.max_seg + k;
-                const double lena = a.seg_len[grow];
-                const double oax = a.seg_origin[3 * grow], oay = a.seg_origin[3 * grow + 1],
-                             oaz = a.seg_origin[3 * grow + 2];
-                const double obx = a.seg_origin[3 * grow + 3], oby = a.seg_origin[3 * grow + 4],
-                             obz = a.seg_origin[3 * grow + 5];
-                const double ldx = __dmul_rn(lena, a.seg_dir[3 * grow]);
-                const double ldy = __dmul_rn(lena, a.seg_dir[3 * grow + 1]);
-                const double ldz = __dmul_rn(lena, a.seg_dir[3 * grow + 2]);
-                const float sa = (float)(a.seg_s0[grow] + lena);  // s0_k + t, t = len
-                const float sb = (float)a.seg_s0[grow + 1];       // s0_{k+1} + 0
+                const Junction J = load_junction(w, beam * a.max_seg + k);
                 const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
                 const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                 lvm = 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     if (j >= nvalid) continue;
-                    const double px = S.p64[R * lane + j][0], py = S.p64[R * lane + j][1],
-                                 pz = S.p64[R * lane + j][2];
-                    const double vx = __dsub_rn(__dsub_rn(px, oax), ldx);
-                    const double vy = __dsub_rn(__dsub_rn(py, oay), ldy);
-                    const double vz = __dsub_rn(__dsub_rn(pz, oaz), ldz);
-                    const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)),
-                                                __dmul_rn(vz, vz));
-                    const double wx = __dsub_rn(px, obx), wy = __dsub_rn(py, oby),
-                                 wz = __dsub_rn(pz, obz);
-                    const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)),
-                                                __dmul_rn(wz, wz));
-                    const bool wb = db < da;  // strict: equal distances keep segment k
+                    const bool wb = junction_pick(J, S.p64[R * lane + j]);
                     const float4 g1 = wb ? g1b : g1a;
                     const float4 g2 = wb ? g2b : g2a;
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     q2j[j] = fmaxf(
                         fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                         0.f);
-                    sj[j] = wb ? sb : sa;
+                    sj[j] = wb ? J.sb : J.sa;
                     rowj[j] = wb ? rb : ra;
                     pj[j] = wb ? -1.f : INFINITY;  // start anchor of k+1 / end anchor of k
                     dlj[j] = 0.f;
@@ -763,7 +832,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     lvm |= 1u << j;
                 }
                 exact_pending<NF>(a, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb, tie_abs,
-                                  lane, sj, q2j, pj, dlj, rowj, lvm, ties);
+                                  lane, sj, q2j, pj, dlj, rowj, lvm, ties, w);
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
