@@ -44,6 +44,12 @@ namespace {
 #ifndef BF_STAGE_BATCH
 #define BF_STAGE_BATCH 0
 #endif
+#ifndef BF_PREFETCH
+#define BF_PREFETCH 0
+#endif
+#ifndef BF_ABL
+#define BF_ABL 0
+#endif
 #ifndef BF_JUNC
 #define BF_JUNC 1
 #endif
@@ -536,6 +542,16 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, i
         const int jb = S.rowbeam[r];
         const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
 #else
+#if BF_PREFETCH
+    // rows after this lane's first: start their L2 -> L1 transfers now
+#pragma unroll 1
+    for (int r = lane + 32; r < nrows; r += 32) {
+        const int jb = S.rowbeam[r];
+        const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g));
+    }
+#endif
 #pragma unroll 1
     for (int r = lane; r < nrows; r += 32) {
         const int jb = S.rowbeam[r];
@@ -654,7 +670,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         __syncwarp();
         {
             const double4 c = w.pcen[p];  // re-read (L1) rather than held in registers
+#if !(BF_ABL & 64)
             stage_rows<NF>(S, w, a.max_seg, nrows, c.x, c.y, c.z, RW, K, lane);
+#endif
         }
         __syncwarp();
         // ---- work generation: one lane per beam bounds the patch against the
@@ -665,7 +683,11 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             float D = 0.f;
 #pragma unroll 1
             for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.anc[0][r0 + k].w);
+#if BF_ABL & 32
+            word = 0;  // ablation: no classification
+#else
             word = classify<NF>(S, K, r0, nsb, RW, D);
+#endif
             S.surv[lane] = word;
             S.bD[lane] = D;
         }
@@ -710,13 +732,26 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         //      mask of non-behind receivers; one shared tail applies the cutoff and
         //      evaluates the contributions.
 #pragma unroll 1
+#if BF_ABL & 16
+        for (unsigned lm = 0; lm;) {  // ablation: no summation at all
+#else
         for (unsigned lm = live; lm;) {
+#endif
             const int jb = __ffs(lm) - 1;
             lm &= lm - 1;
             const int64_t beam = S.gbeam[jb];
             const unsigned bword = S.surv[jb];
             const unsigned surv = bword & ~(BEHIND_CHECK | WEDGE);
             const int r0 = S.brow[jb];
+#if BF_ABL
+            // ablation (timing experiments only; results are wrong): skip item kinds
+            {
+                const bool is_single = (surv & (surv - 1)) == 0, is_wedge = (bword & WEDGE) != 0;
+                if ((BF_ABL & 1) && is_single) continue;
+                if ((BF_ABL & 2) && !is_single && is_wedge) continue;
+                if ((BF_ABL & 4) && !is_single && !is_wedge) continue;
+            }
+#endif
             float sj[R], q2j[R], pj[R], dlj[R];
             int rowj[R];
 #pragma unroll
@@ -836,6 +871,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
+#if BF_ABL & 8
+            if (lvm != 0x7u) continue;  // ablation: no evaluation
+#endif
             float m2j[R];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
