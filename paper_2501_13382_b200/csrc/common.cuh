@@ -90,6 +90,9 @@ struct Fp32Work {
     double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum
     int *part_ev;             // per (beam range, sorted receiver): unit evaluation count
     unsigned *unit_ctr;       // persistent-kernel work queue head
+    uint32_t *wl_items;       // compacted tight work list: per (tile, beam range), ascending
+                              // beams, entry = (n_segs - 1) << 27 | beam
+    int64_t *wl_off;          // n_tiles * n_ranges + 1 offsets into wl_items
     int64_t n_patches, n_ranges, range_beams, n_pad;  // n_pad = n_patches * patch
 };
 
@@ -99,6 +102,13 @@ int gbs_fp32_tile();
 int gbs_fp32_patch();
 int64_t gbs_fp32_range_beams(int64_t n_beams);
 int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st);
+// Work-list compaction (north star: prefix-sum compaction into (beam, tile) lists):
+// counts per (tile, range) into w.wl_off (pass 1), then, after an exclusive scan of
+// the counts, the entries (pass 2).
+int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
+                         cudaStream_t st);
+int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
+                           cudaStream_t st);
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
                     cudaStream_t st);
 int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam,

@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_COUNT
 };
 
 struct DeviceCtx {
@@ -341,6 +341,8 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     w.n_ranges = (a.n_beams + w.range_beams - 1) / w.range_beams;
     if (w.n_patches * w.n_ranges >= (int64_t)1 << 31)
         return fail(BF_EINVAL, "too many (patch, beam range) units; split the call");
+    if (a.n_beams >= ((int64_t)1 << 27))
+        return fail(BF_EINVAL, "more than 2^27 beams in one call; split the beam range");
     BF_TRY(c->get(B_P0, rows, &w.p0));
     BF_TRY(c->get(B_P1, rows, &w.p1));
     BF_TRY(c->get(B_P2, rows, &w.p2));
@@ -352,6 +354,25 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     BF_TRY(c->get(B_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
     BF_TRY(c->get(B_UCTR, 1, &w.unit_ctr));
     BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, sizeof(unsigned), st));
+    {   // compacted tight work list: counts -> exclusive scan -> entries
+        const int64_t nu = t.n_tiles * w.n_ranges;
+        int64_t *cnt;
+        BF_TRY(c->get(B_WLTMP, (size_t)(nu + 1), &cnt));
+        BF_TRY(c->get(B_WLOFF, (size_t)(nu + 1), &w.wl_off));
+        BF_TRY_CUDA(cudaMemsetAsync(cnt + nu, 0, sizeof(int64_t), st));
+        BF_TRY(launch_fp32_wl_count(a, t, w, cnt, st));
+        size_t tmp_bytes = 0;
+        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, w.wl_off, (int)(nu + 1), st));
+        void *tmp;
+        BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
+        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, w.wl_off, (int)(nu + 1), st));
+        note_launch();
+        int64_t total = 0;  // entries: bounded by the tight candidate count (stats)
+        BF_TRY_CUDA(cudaMemcpyAsync(&total, w.wl_off + nu, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        BF_TRY_CUDA(cudaStreamSynchronize(st));
+        BF_TRY(c->get(B_WLITEMS, (size_t)(total + 1), &w.wl_items));
+        BF_TRY(launch_fp32_wl_compact(a, t, w, st));
+    }
     BF_TRY(launch_fp32_prepare(a, t, w, st));
     GbsStats *d_stats;
     BF_TRY(c->get(B_STATS, 1, &d_stats));

@@ -618,54 +618,35 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
     }
 
-    const uint32_t *wl = tl.wl_tight + (p / (TILE / PATCH)) * tl.wl_words;
-    int64_t b = q * w.range_beams;
-    const int64_t bend = b + w.range_beams < a.n_beams ? b + w.range_beams : a.n_beams;
-    const unsigned lt = (1u << lane) - 1u;
-    while (b < bend) {
-        // ---- gather the next <= CB candidate beams of the tile (work-list bits)
-        int nbc = 0;
-#pragma unroll 1
-        while (nbc < CB && b < bend) {
-            const int64_t wi = b >> 5;
-            unsigned word = wl[wi] & (~0u << (b & 31));
-            const int64_t rem = bend - 32 * wi;
-            if (rem < 32) word &= (1u << rem) - 1u;
-            const int cnt = __popc(word);
-            const int take = min(cnt, CB - nbc);
-            const bool mine = (word >> lane) & 1u;
-            const int rank = __popc(word & lt);
-            if (mine && rank < take) S.gbeam[nbc + rank] = (int)(32 * wi + lane);
-            nbc += take;
-            if (take < cnt) {
-                const unsigned nx = __ballot_sync(0xffffffffu, mine && rank == take);
-                b = 32 * wi + __ffs(nx) - 1;
-            } else {
-                b = 32 * (wi + 1);
-            }
-        }
-        if (b > bend) b = bend;
-        if (nbc == 0) break;
-        __syncwarp();
+    // ---- candidate beams: the unit's slice of the compacted tight work list
+    const int64_t ui = (p / (TILE / PATCH)) * w.n_ranges + q;
+    const uint32_t *items = w.wl_items + w.wl_off[ui];
+    const int n_items = (int)(w.wl_off[ui + 1] - w.wl_off[ui]);
+    int cur = 0;
+    uint32_t e = lane < n_items ? items[lane] : 0u;  // entries of the next chunk
+    while (cur < n_items) {
+        const int nbn = min(CB, n_items - cur);
+        const int ns = lane < nbn ? (int)(e >> 27) + 1 : 0;
+        const int beam_l = (int)(e & 0x7ffffffu);
         // ---- row capacity: keep the prefix of beams whose rows fit ROWCAP
-        int ns = 0;
-        if (lane < nbc) ns = a.n_segs[S.gbeam[lane]];
         int incl = ns;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
-        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbc && incl <= ROWCAP);
-        const int nacc = __popc(fit);
-        if (nacc < nbc) b = __shfl_sync(0xffffffffu, lane < nbc ? S.gbeam[lane] : 0, nacc);
-        nbc = nacc;
+        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbn && incl <= ROWCAP);
+        const int nbc = __popc(fit);
         const int nrows = __shfl_sync(0xffffffffu, incl, nbc - 1);
         if (lane < nbc) {
+            S.gbeam[lane] = beam_l;
             S.brow[lane] = incl - ns;
 #pragma unroll 1
             for (int k = incl - ns; k < incl; ++k) S.rowbeam[k] = lane;
         }
+        cur += nbc;
+        // the next chunk's entries: in flight during this chunk
+        e = cur + lane < n_items ? items[cur + lane] : 0u;
         if (lane == 0) S.brow[nbc] = nrows;
         __syncwarp();
         {
@@ -1057,6 +1038,53 @@ __global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, double *a
     evals[oi] += ev;
 }
 
+// One warp per (tile, beam range): candidate count of the tight work list.
+__global__ void wl_count_kernel(const Tiling tl, const Fp32Work w, int64_t *counts) {
+    const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (u >= tl.n_tiles * w.n_ranges) return;
+    const int64_t tile = u / w.n_ranges, q = u - tile * w.n_ranges;
+    const int64_t w0 = q * w.range_beams / 32;
+    const int64_t w1 = min(tl.wl_words, (q + 1) * w.range_beams / 32);
+    const uint32_t *bits = tl.wl_tight + tile * tl.wl_words;
+    int c = 0;
+    for (int64_t i = w0 + lane; i < w1; i += 32) c += __popc(bits[i]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) counts[u] = c;
+}
+
+// One warp per (tile, beam range): ascending candidate beams with their segment
+// counts, (n_segs - 1) << 27 | beam, at the scanned offset.
+__global__ void wl_compact_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w) {
+    const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (u >= tl.n_tiles * w.n_ranges) return;
+    const int64_t tile = u / w.n_ranges, q = u - tile * w.n_ranges;
+    const int64_t w0 = q * w.range_beams / 32;
+    const int64_t w1 = min(tl.wl_words, (q + 1) * w.range_beams / 32);
+    const uint32_t *bits = tl.wl_tight + tile * tl.wl_words;
+    uint32_t *out = w.wl_items + w.wl_off[u];
+    int64_t base = 0;
+    for (int64_t i0 = w0; i0 < w1; i0 += 32) {
+        const int64_t i = i0 + lane;
+        unsigned m = i < w1 ? bits[i] : 0u;
+        const int c = __popc(m);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int64_t pos = base + incl - c;
+        for (; m; m &= m - 1) {
+            const int64_t beam = 32 * i + __ffs(m) - 1;
+            const uint32_t ns = (uint32_t)a.n_segs[beam];
+            out[pos++] = ((ns - 1u) << 27) | (uint32_t)beam;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 template <int NF>
 int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
               GbsStats *stats, cudaStream_t st) {
@@ -1133,6 +1161,29 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
     if (w.n_patches > 0) {
         patch_kernel<<<(unsigned)((w.n_patches * 32 + 127) / 128), 128, 0, st>>>(
             a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen);
+        note_launch();
+    }
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
+                         cudaStream_t st) {
+    (void)a;
+    const int64_t nu = t.n_tiles * w.n_ranges;
+    if (nu > 0) {
+        wl_count_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(t, w, counts);
+        note_launch();
+    }
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
+                           cudaStream_t st) {
+    const int64_t nu = t.n_tiles * w.n_ranges;
+    if (nu > 0) {
+        wl_compact_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(a, t, w);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
