@@ -47,6 +47,9 @@ namespace {
 #ifndef BF_PREFETCH
 #define BF_PREFETCH 0
 #endif
+#ifndef BF_PREFETCH_EXACT
+#define BF_PREFETCH_EXACT 0
+#endif
 #ifndef BF_ABL
 #define BF_ABL 0
 #endif
@@ -344,9 +347,8 @@ struct ExactPick {
 // beam (kernels.py:320-348 with the reference's fp64 operations): only segments
 // whose fp32 distance is within the tie bound of the fp32 best can win.  Out of
 // line: one copy of the code serves every call site of the multi path.
-__device__ __noinline__ ExactPick exact_pick(const double *__restrict__ seg_origin,
-                                             const double *__restrict__ seg_dir,
-                                             const double *__restrict__ seg_len, int64_t row0,
+__device__ __noinline__ ExactPick exact_pick(const double4 *__restrict__ p0,
+                                             const double4 *__restrict__ p1, int64_t row0,
                                              const float4 *geo0, const float4 *geo1,
                                              unsigned surv, int kf, float rx, float ry, float rz,
                                              float best, float tie_abs, const double (&p)[3]) {
@@ -364,11 +366,9 @@ __device__ __noinline__ ExactPick exact_pick(const double *__restrict__ seg_orig
         const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y, ez = vz0 - tt * h1.z;
         const float d2k = ex * ex + ey * ey + ez * ez;
         if (kk != kf && fmaf(-TIE_REL, d2k, d2k - best) > tie_abs) continue;
-        const int64_t row = row0 + kk;
-        const double ox = seg_origin[3 * row], oy = seg_origin[3 * row + 1],
-                     oz = seg_origin[3 * row + 2];
-        const double dx = seg_dir[3 * row], dy = seg_dir[3 * row + 1], dz = seg_dir[3 * row + 2];
-        const double len = seg_len[row];
+        const double4 o = p0[row0 + kk], d = p1[row0 + kk];  // packed fp64 rows (exact copies)
+        const double ox = o.x, oy = o.y, oz = o.z, len = o.w;
+        const double dx = d.x, dy = d.y, dz = d.z;
         const double wx = __dsub_rn(px, ox), wy = __dsub_rn(py, oy), wz = __dsub_rn(pz, oz);
         const double proj =
             __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
@@ -488,7 +488,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<N
         const int j = __ffs(pend) - 1;
         pend &= pend - 1;
         const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
-        const ExactPick e = exact_pick(a.seg_origin, a.seg_dir, a.seg_len, beam * a.max_seg,
+        const ExactPick e = exact_pick(w.p0, w.p1, beam * a.max_seg,
                                        S.geo0 + r0, S.geo1 + r0, surv, pick4(kb, j), x, y, z,
                                        pick4(best, j), tie_abs, S.p64[R * lane + j]);
         if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
@@ -671,6 +671,19 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #endif
             S.surv[lane] = word;
             S.bD[lane] = D;
+#if BF_PREFETCH_EXACT
+            // wedge / several-candidate items read fp64 rows later: start the transfers
+            const unsigned mw = word & ~(BEHIND_CHECK | WEDGE);
+            if (word && (mw & (mw - 1))) {
+                const int64_t g0 = (int64_t)S.gbeam[lane] * a.max_seg;
+#pragma unroll 1
+                for (unsigned m = mw; m; m &= m - 1) {
+                    const int k = __ffs(m) - 1;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g0 + k));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g0 + k));
+                }
+            }
+#endif
         }
         const unsigned live = __ballot_sync(0xffffffffu, word != 0);
         {
