@@ -50,6 +50,12 @@ namespace {
 #ifndef BF_PREFETCH_EXACT
 #define BF_PREFETCH_EXACT 0
 #endif
+#ifndef BF_EXACT_INLINE
+#define BF_EXACT_INLINE 1
+#endif
+#ifndef BF_ABLM
+#define BF_ABLM 0
+#endif
 #ifndef BF_ABL
 #define BF_ABL 0
 #endif
@@ -347,7 +353,12 @@ struct ExactPick {
 // beam (kernels.py:320-348 with the reference's fp64 operations): only segments
 // whose fp32 distance is within the tie bound of the fp32 best can win.  Out of
 // line: one copy of the code serves every call site of the multi path.
-__device__ __noinline__ ExactPick exact_pick(const double4 *__restrict__ p0,
+#if BF_EXACT_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+ExactPick exact_pick(const double4 *__restrict__ p0,
                                              const double4 *__restrict__ p1, int64_t row0,
                                              const float4 *geo0, const float4 *geo1,
                                              unsigned surv, int kf, float rx, float ry, float rz,
@@ -438,50 +449,6 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<N
     ties += __popc(pend);
     // two adjacent candidates k, k+1 (most multi items): a receiver that projects
     // beyond the end of k and before the start of k+1 is decided like the corner wedge
-#if BF_JUNC
-    const int ka = __ffs(surv) - 1;
-    if (surv == (3u << ka) && __any_sync(0xffffffffu, pend != 0)) {
-        const float4 a0 = S.geo0[r0 + ka], a1 = S.geo1[r0 + ka], b0 = S.geo0[r0 + ka + 1],
-                     b1 = S.geo1[r0 + ka + 1];
-        const float tol = PROJ_ERR * fmaxf(S.anc[0][r0 + ka].w, S.anc[0][r0 + ka + 1].w);
-        unsigned jp = 0;
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const float pa = (rx[j] + a0.x) * a1.x + (ry[j] + a0.y) * a1.y + (rz[j] + a0.z) * a1.z;
-            const float pb = (rx[j] + b0.x) * b1.x + (ry[j] + b0.y) * b1.y + (rz[j] + b0.z) * b1.z;
-            if (((pend >> j) & 1u) && pa - a0.w >= tol && pb <= -tol) jp |= 1u << j;
-        }
-        if (__any_sync(0xffffffffu, jp != 0)) {
-            pend &= ~jp;
-            const Junction J = load_junction(w, beam * a.max_seg + ka);
-#pragma unroll 1
-            while (__any_sync(0xffffffffu, jp != 0)) {
-                if (!jp) continue;
-                const int j = __ffs(jp) - 1;
-                jp &= jp - 1;
-                const bool wb = junction_pick(J, S.p64[R * lane + j]);
-                const int row = r0 + ka + (wb ? 1 : 0);
-                const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
-                const float4 g1 = wb ? b1 : a1;
-                const float4 g2 = S.geo2[row];
-                const float dl = fmaf(x, g1.x, fmaf(y, g1.y, z * g1.z));
-                const float q2 = fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
-                                       0.f);
-                const float sv = wb ? J.sb : J.sa;
-#pragma unroll
-                for (int jj = 0; jj < R; ++jj)
-                    if (jj == j) {
-                        q2j[jj] = q2;
-                        sj[jj] = sv;
-                        rowj[jj] = row;
-                        pj[jj] = wb ? -1.f : INFINITY;  // start anchor of k+1 / end anchor of k
-                        dlj[jj] = 0.f;
-                    }
-                lvm |= 1u << j;
-            }
-        }
-    }
-#endif
 #pragma unroll 1
     while (__any_sync(0xffffffffu, pend != 0)) {
         if (!pend) continue;
@@ -590,7 +557,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     float rx[R], ry[R], rz[R], rr[R];
     const int64_t sb = p * PATCH + R * lane;  // sorted position of receiver j = sb + j
     const int32_t *perm = tl.perm + sb;       // observer index of receiver j = perm[j]
-    const int nvalid = tl.n - sb < R ? (int)(tl.n - sb) : R;  // receivers j < nvalid are real
+    const int nvalid =  // receivers j < nvalid are real
+        tl.n - sb < R ? (tl.n - sb > 0 ? (int)(tl.n - sb) : 0) : R;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         float4 rl = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -774,39 +742,25 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 lvm = (1u << R) - 1;
                 if (bword & BEHIND_CHECK)
                     lvm = behind_mask(a, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, beam, k, ties);
-            } else if (bword & WEDGE) {
-                // ---- corner wedge of segments k, k+1: both clamp to the reflection point;
-                //      the reference picks by fp64 rounding, reproduced exactly here
-                const int k = __ffs(surv) - 1;
-                const int ra = r0 + k, rb = ra + 1;
-                const Junction J = load_junction(w, beam * a.max_seg + k);
-                const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
-                const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
-                lvm = 0;
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    if (j >= nvalid) continue;
-                    const bool wb = junction_pick(J, S.p64[R * lane + j]);
-                    const float4 g1 = wb ? g1b : g1a;
-                    const float4 g2 = wb ? g2b : g2a;
-                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                    q2j[j] = fmaxf(
-                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
-                        0.f);
-                    sj[j] = wb ? J.sb : J.sa;
-                    rowj[j] = wb ? rb : ra;
-                    pj[j] = wb ? -1.f : INFINITY;  // start anchor of k+1 / end anchor of k
-                    dlj[j] = 0.f;
-                    lvm |= 1u << j;
-                }
-                ties += __popc(lvm);
             } else {
-                // ---- several candidate segments: fp32 distances, fp64 re-decision of ties
-                const float Db = S.bD[jb];
-                const float tie_abs = TIE_ABS * Db * Db;
+                // receivers decided at the junction of segments ka, ka+1 (corner wedge):
+                // both clamped distances are distances to the reflection point, an exact
+                // tie the reference breaks by fp64 rounding, reproduced op for op
+                unsigned jp;
+                int ka = __ffs(surv) - 1;
+                unsigned pend = 0;  // receivers re-decided by the general fp64 search
                 float best[R];
                 int kb[R];
-                unsigned pend = 0;  // receivers whose winner is re-decided in fp64
+                float tie_abs = 0.f;
+                if (bword & WEDGE) {
+                    // ---- corner wedge: every receiver of the patch is at the junction
+                    jp = (1u << nvalid) - 1u;
+                    lvm = 0;
+                } else {
+                // ---- several candidate segments: fp32 distances, fp64 re-decision of ties
+                const float Db = S.bD[jb];
+                tie_abs = TIE_ABS * Db * Db;
+                jp = 0;
                 lvm = 0;
                 float second[R];
 #pragma unroll
@@ -832,6 +786,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         best[j] = fminf(best[j], d2);
                     }
                 }
+#if BF_ABLM == 1
+                if (best[0] >= 0.f) continue;  // ablation: scan only
+#endif
+                // two adjacent candidates: ties at the junction go to the wedge decision
+                const bool pair = surv == (3u << ka);
+                const float jtol =
+                    pair ? PROJ_ERR * fmaxf(S.anc[0][r0 + ka].w, S.anc[0][r0 + ka + 1].w) : 0.f;
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const int k = kb[j];
@@ -847,7 +808,19 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float proj = dl + g1.w;
                     if (k == 0 && fabsf(proj) <= PROJ_ERR * S.anc[0][r0].w) exact = true;
                     if (exact) {
-                        if (j < nvalid) pend |= 1u << j;
+                        if (j >= nvalid) continue;
+                        if (pair) {
+                            // beyond the end of ka and before the start of ka+1?
+                            const float4 a0 = S.geo0[r0 + ka], a1 = S.geo1[r0 + ka];
+                            const float4 b1 = S.geo1[r0 + ka + 1];
+                            const float pa = fmaf(rx[j], a1.x, fmaf(ry[j], a1.y, rz[j] * a1.z)) + a1.w;
+                            const float pb = fmaf(rx[j], b1.x, fmaf(ry[j], b1.y, rz[j] * b1.z)) + b1.w;
+                            if (pa - a0.w >= jtol && pb <= -jtol) {
+                                jp |= 1u << j;
+                                continue;
+                            }
+                        }
+                        pend |= 1u << j;
                         continue;
                     }
                     if (k == 0 && proj < 0.f) continue;  // behind the source
@@ -860,8 +833,38 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     dlj[j] = dl;
                     lvm |= 1u << j;
                 }
-                exact_pending<NF>(a, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb, tie_abs,
-                                  lane, sj, q2j, pj, dlj, rowj, lvm, ties, w);
+#if BF_ABLM == 2
+                if (best[0] >= 0.f) continue;  // ablation: scan + decision only
+#endif
+                }
+                if (__any_sync(0xffffffffu, jp != 0)) {
+                    const int ra = r0 + ka, rb = ra + 1;
+                    const Junction J = load_junction(w, beam * a.max_seg + ka);
+                    const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
+                    const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
+                    ties += __popc(jp);
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        if (!((jp >> j) & 1u)) continue;
+                        const bool wb = junction_pick(J, S.p64[R * lane + j]);
+                        const float4 g1 = wb ? g1b : g1a;
+                        const float4 g2 = wb ? g2b : g2a;
+                        const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
+                        q2j[j] = fmaxf(
+                            fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
+                            0.f);
+                        sj[j] = wb ? J.sb : J.sa;
+                        rowj[j] = wb ? rb : ra;
+                        pj[j] = wb ? -1.f : INFINITY;  // start anchor of ka+1 / end anchor of ka
+                        dlj[j] = 0.f;
+                        lvm |= 1u << j;
+                    }
+                }
+#if BF_ABLM != 3
+                if (__any_sync(0xffffffffu, pend != 0))
+                    exact_pending<NF>(a, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
+                                      tie_abs, lane, sj, q2j, pj, dlj, rowj, lvm, ties, w);
+#endif
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
