@@ -362,7 +362,7 @@ ExactPick exact_pick(const double4 *__restrict__ p0,
                                              const double4 *__restrict__ p1, int64_t row0,
                                              const float4 *geo0, const float4 *geo1,
                                              unsigned surv, int kf, float rx, float ry, float rz,
-                                             float best, float tie_abs, const double (&p)[3]) {
+                                             float best, float Db, const double (&p)[3]) {
     const double px = p[0], py = p[1], pz = p[2];
     ExactPick e{0.0, 0.0, 0.0, -1};
     double bd = INFINITY;
@@ -376,7 +376,10 @@ ExactPick exact_pick(const double4 *__restrict__ p0,
         const float tt = fminf(fmaxf(pjj, 0.f), h0.w);
         const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y, ez = vz0 - tt * h1.z;
         const float d2k = ex * ex + ey * ey + ez * ez;
-        if (kk != kf && fmaf(-TIE_REL, d2k, d2k - best) > tie_abs) continue;
+        // a contender only within the fp32 error of two distances (tight bound, DESIGN 5.8)
+        if (kk != kf && d2k - best > fmaf(TIE_DD * Db, sqrt_approx(d2k) * 1.0001f,
+                                          fmaf(TIE_D2, d2k, TIE_DSQ * Db * Db)))
+            continue;
         const double4 o = p0[row0 + kk], d = p1[row0 + kk];  // packed fp64 rows (exact copies)
         const double ox = o.x, oy = o.y, oz = o.z, len = o.w;
         const double dx = d.x, dy = d.y, dz = d.z;
@@ -404,6 +407,9 @@ ExactPick exact_pick(const double4 *__restrict__ p0,
 // receiver projects beyond the end of k and before the start of k+1, both clamped
 // distances (kernels.py:332-340) are distances to the reflection point and the
 // reference's choice is decided by fp64 rounding, reproduced here op for op.
+#if BF_HIST
+__device__ unsigned long long g_hist[4];  // debug: junction, pending, pending rounds, non-pair
+#endif
 struct Junction {
     double ox, oy, oz;  // o_k
     double lx, ly, lz;  // len_k * d_k (t = len, kernels.py:337-339)
@@ -442,7 +448,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<N
                                               const float (&rx)[R], const float (&ry)[R],
                                               const float (&rz)[R], const float (&rr)[R],
                                               const float (&best)[R], const int (&kb)[R],
-                                              float tie_abs, int lane, float (&sj)[R],
+                                              float Db, int lane, float (&sj)[R],
                                               float (&q2j)[R], float (&pj)[R], float (&dlj)[R],
                                               int (&rowj)[R], unsigned &lvm, unsigned &ties,
                                               const Fp32Work &w) {
@@ -451,13 +457,16 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<N
     // beyond the end of k and before the start of k+1 is decided like the corner wedge
 #pragma unroll 1
     while (__any_sync(0xffffffffu, pend != 0)) {
+#if BF_HIST
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_hist[2], 1ull);
+#endif
         if (!pend) continue;
         const int j = __ffs(pend) - 1;
         pend &= pend - 1;
         const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
         const ExactPick e = exact_pick(w.p0, w.p1, beam * a.max_seg,
                                        S.geo0 + r0, S.geo1 + r0, surv, pick4(kb, j), x, y, z,
-                                       pick4(best, j), tie_abs, S.p64[R * lane + j]);
+                                       pick4(best, j), Db, S.p64[R * lane + j]);
         if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
         const int k = e.bk;
         const float4 g1 = S.geo1[r0 + k];
@@ -751,15 +760,15 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 unsigned pend = 0;  // receivers re-decided by the general fp64 search
                 float best[R];
                 int kb[R];
-                float tie_abs = 0.f;
+                float Db = 0.f;
                 if (bword & WEDGE) {
                     // ---- corner wedge: every receiver of the patch is at the junction
                     jp = (1u << nvalid) - 1u;
                     lvm = 0;
                 } else {
                 // ---- several candidate segments: fp32 distances, fp64 re-decision of ties
-                const float Db = S.bD[jb];
-                tie_abs = TIE_ABS * Db * Db;
+                Db = S.bD[jb];
+                const float tie_abs = TIE_ABS * Db * Db;
                 jp = 0;
                 lvm = 0;
                 float second[R];
@@ -837,6 +846,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (best[0] >= 0.f) continue;  // ablation: scan + decision only
 #endif
                 }
+#if BF_HIST
+                if (!(bword & WEDGE)) {
+                    if (jp) atomicAdd(&g_hist[0], (unsigned long long)__popc(jp));
+                    if (pend) atomicAdd(&g_hist[1], (unsigned long long)__popc(pend));
+                    if (pend && surv != (3u << ka)) atomicAdd(&g_hist[3], (unsigned long long)__popc(pend));
+                }
+#endif
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
                     const Junction J = load_junction(w, beam * a.max_seg + ka);
@@ -863,7 +879,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #if BF_ABLM != 3
                 if (__any_sync(0xffffffffu, pend != 0))
                     exact_pending<NF>(a, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
-                                      tie_abs, lane, sj, q2j, pj, dlj, rowj, lvm, ties, w);
+                                      Db, lane, sj, q2j, pj, dlj, rowj, lvm, ties, w);
 #endif
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
@@ -1120,7 +1136,22 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
     int64_t grid = (int64_t)sms * per_sm;
     const int64_t need = (units + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
+#if BF_HIST
+    {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbolAsync(g_hist, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+    }
+#endif
     gbs_fp32_kernel<NF><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
+#if BF_HIST
+    {
+        unsigned long long h[4];
+        cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "bf hist: multi junction %llu pending %llu (non-pair %llu) rounds %llu\n",
+                h[0], h[1], h[3], h[2]);
+    }
+#endif
     fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, st>>>(t, w, a.nf, a.acc, a.evals);
     note_launch(2);
     BF_TRY_CUDA(cudaGetLastError());
