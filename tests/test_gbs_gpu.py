@@ -321,3 +321,51 @@ def test_worklist_bitexact_vs_oracle(name, dense):
     assert not (tbits & ~bits).any()  # tight list is a subset of the a9 list
     if dense:
         assert 0 < np.unpackbits(bits.view(np.uint8)).mean() < 1
+
+
+@pytest.mark.parametrize("freqs,src,corner", [((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0)),
+                                              ((63.0, 250.0, 1000.0), (0.0, 20.0, 2.0),
+                                               (-30.0, 5.0))])
+def test_fp32_dense_city_vs_oracle(freqs, src, corner, threads):
+    """Config-3 receiver density (0.25 m) around street corners of the city scene: every
+    fp32 path (single survivor, corner wedge, several candidates with junction and
+    general fp64 re-decisions, behind plane) against the C oracle on the same traced
+    bundle (device tracer, bit-exact with the reference tracer)."""
+    import torch
+
+    from paper_2501_13382_b200 import _lib, engine, kernels
+    from paper_2501_13382_b200.beamtrace import (Atmosphere, LaunchGrid, SourceSpec,
+                                                 TraceConfig, launch_directions)
+    from paper_2501_13382_b200.scene import make_city
+    dev = torch.device("cuda", 0)
+    sc = make_city(5, 10, 40.0, 20.0, 300.0)
+    source = SourceSpec(position=np.array(src), frequencies=freqs, beam_param_im=-10.0)
+    launch = launch_directions(LaunchGrid(0.0, 180.0, 0.0, 360.0, 60, 120))
+    cfg = TraceConfig(5000, 1e-4, 8)
+    c = Atmosphere(20.0).sound_speed
+    tr = engine.trace_device_rows(engine.DeviceScene.from_scene(sc, dev), source, launch, cfg,
+                                  c, 0, len(launch), dev)
+    hb = tr["bundle"].to_host()
+    x = corner[0] + np.arange(96) * 0.25
+    y = corner[1] + np.arange(96) * 0.25
+    X, Y = np.meshgrid(x, y, indexing="xy")
+    obs = np.ascontiguousarray(np.stack([X.ravel(), Y.ravel(), np.full(X.size, 1.8)], axis=1))
+    om = source.omegas
+    args = [hb.seg_origin, hb.seg_dir, hb.seg_e1, hb.seg_e2, hb.seg_len, hb.seg_s0,
+            hb.seg_refl, hb.n_segs, hb.max_seg, hb.weights, obs, om, float(c),
+            -float(source.beam_param_im), float(source.amplitude_phi), True]
+    nb = hb.n_segs.shape[0]
+    ref = np.zeros((obs.shape[0], om.shape[0]), np.complex128)
+    rev = np.zeros(obs.shape[0], np.int64)
+    oracle.gbs_accumulate(*args, ref, rev, 0, obs.shape[0], 0, nb, threads=threads)
+    acc = np.zeros_like(ref)
+    ev = np.zeros_like(rev)
+    kernels.gbs_accumulate(*args, acc, ev, 0, obs.shape[0], 0, nb, precision="fp32")
+    st = _lib.last_stats()
+    assert rel_l2(acc, ref) <= FP32_L2
+    assert tl_db(acc, ref, floor_db=-60.0) <= FP32_TL_DB
+    assert tl_db(acc, ref) <= FP32_TL_ALL_DB
+    assert abs(int(ev.sum()) - int(rev.sum())) <= 1e-4 * int(rev.sum()) + 10
+    # the scene exercises the exact-decision paths
+    assert st["patch_beams"]["wedge"] > 0 and st["patch_beams"]["multi"] > 0
+    assert st["tie_pairs"] > 0
