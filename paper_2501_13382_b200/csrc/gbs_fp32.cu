@@ -149,7 +149,7 @@ struct WarpSmem {
     float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
     float2 aux[ROWCAP];      // s0, A (amplitude factor x omega_0)
     float4 anc[NF][ROWCAP];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
-    unsigned char rowbeam[ROWCAP];  // chunk row -> chunk beam
+    unsigned rowinfo[ROWCAP];  // chunk row -> beam << 5 | segment
     short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
     unsigned surv[CB];       // surviving segments + flags (0 = culled)
@@ -250,13 +250,15 @@ __device__ __forceinline__ float sweep(float RW, float d) {
 // Work generation for one (patch, beam): survivor mask + flags (0 = culled).
 template <int NF>
 __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Consts &K, int r0,
-                                             int ns, float RW, float D) {
+                                             int ns, float RW, float &D) {
+    D = 0.f;
     if (ns <= 0) return 0u;
-    // pass 1: nearest segment at the patch centre
+    // pass 1: nearest segment at the patch centre; error scale D of the beam
     float best = INFINITY;
     int kj = 0;
 #pragma unroll 1
     for (int k = 0; k < ns; ++k) {
+        D = fmaxf(D, S.anc[0][r0 + k].w);
         const float4 g0 = S.geo0[r0 + k];
         const float4 g1 = S.geo1[r0 + k];
         const float t = fminf(fmaxf(g1.w, 0.f), g0.w);
@@ -496,46 +498,36 @@ template <int NF>
 __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, int64_t max_seg,
                                            int nrows, double cx, double cy, double cz, float RW,
                                            const Fp32Consts &K, int lane) {
-#if BF_STAGE_BATCH
-    // all of this lane's row loads first (<= SR rows): one L2 round trip per chunk
-    constexpr int SR = (ROWCAP + 31) / 32;
-    double4 P0[SR], P1[SR];
-#pragma unroll
-    for (int i = 0; i < SR; ++i) {
-        const int r = lane + 32 * i;
-        if (r < nrows) {
-            const int jb = S.rowbeam[r];
-            const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
-            P0[i] = w.p0[g];  // o.xyz, len
-            P1[i] = w.p1[g];  // d.xyz, s0
+    // software-pipelined: the next row's loads are in flight while this row converts
+    auto grow = [&](int r) {
+        const unsigned info = S.rowinfo[r];  // beam << 5 | k
+        return (int64_t)(info >> 5) * max_seg + (info & 31);
+    };
+    const float2 *pa2 = reinterpret_cast<const float2 *>(w.pa);
+    int r = lane;
+    int64_t g = 0;
+    double4 p0 = make_double4(0, 0, 0, 0), p1 = p0;
+    float2 p2 = make_float2(0.f, 0.f), ae0 = p2;
+    if (r < nrows) {
+        g = grow(r);
+        p0 = w.p0[g];  // o.xyz, len
+        p1 = w.p1[g];  // d.xyz, s0
+        p2 = w.p2[g];  // A, R_cut
+        ae0 = pa2[g * NF];
+    }
+#pragma unroll 1
+    for (; r < nrows; r += 32) {
+        const int rn = r + 32;
+        int64_t gn = 0;
+        double4 p0n = p0, p1n = p1;
+        float2 p2n = p2, aen = ae0;
+        if (rn < nrows) {
+            gn = grow(rn);
+            p0n = w.p0[gn];
+            p1n = w.p1[gn];
+            p2n = w.p2[gn];
+            aen = pa2[gn * NF];
         }
-    }
-#pragma unroll
-    for (int i = 0; i < SR; ++i) {
-        const int r = lane + 32 * i;
-        if (r >= nrows) break;
-        const double4 p0 = P0[i], p1 = P1[i];
-        const int jb = S.rowbeam[r];
-        const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
-#else
-#if BF_PREFETCH
-    // rows after this lane's first: start their L2 -> L1 transfers now
-#pragma unroll 1
-    for (int r = lane + 32; r < nrows; r += 32) {
-        const int jb = S.rowbeam[r];
-        const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g));
-    }
-#endif
-#pragma unroll 1
-    for (int r = lane; r < nrows; r += 32) {
-        const int jb = S.rowbeam[r];
-        const int64_t g = (int64_t)S.gbeam[jb] * max_seg + (r - S.brow[jb]);
-        const double4 p0 = w.p0[g];  // o.xyz, len
-        const double4 p1 = w.p1[g];  // d.xyz, s0
-#endif
-        const float2 p2 = w.p2[g];   // A, R_cut
         const double wcx = cx - p0.x, wcy = cy - p0.y, wcz = cz - p0.z;
         const double pc = wcx * p1.x + wcy * p1.y + wcz * p1.z;
         const double ucx = wcx - pc * p1.x, ucy = wcy - pc * p1.y, ucz = wcz - pc * p1.z;
@@ -547,10 +539,15 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, i
         S.aux[r] = make_float2((float)p1.w, p2.x * K.omega[0]);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-            const float2 ae = reinterpret_cast<const float2 *>(w.pa)[g * NF + f];
+            const float2 ae = f ? pa2[g * NF + f] : ae0;
             S.anc[f][r] =
                 make_float4((float)frac_turns(K.kappa64[f] * (p1.w + pc)), ae.x, ae.y, f ? 0.f : D);
         }
+        g = gn;
+        p0 = p0n;
+        p1 = p1n;
+        p2 = p2n;
+        ae0 = aen;
     }
 }
 
@@ -619,7 +616,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             S.gbeam[lane] = beam_l;
             S.brow[lane] = incl - ns;
 #pragma unroll 1
-            for (int k = incl - ns; k < incl; ++k) S.rowbeam[k] = lane;
+            for (int k = 0; k < ns; ++k) S.rowinfo[incl - ns + k] = ((unsigned)beam_l << 5) | k;
         }
         cur += nbc;
         // the next chunk's entries: in flight during this chunk
@@ -639,8 +636,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         if (lane < nbc) {
             const int r0 = S.brow[lane], nsb = S.brow[lane + 1] - r0;
             float D = 0.f;
-#pragma unroll 1
-            for (int k = 0; k < nsb; ++k) D = fmaxf(D, S.anc[0][r0 + k].w);
 #if BF_ABL & 32
             word = 0;  // ablation: no classification
 #else
