@@ -77,7 +77,10 @@ namespace {
 constexpr int R = 4;                    // receivers per lane
 constexpr int PATCH = 32 * R;           // receivers per warp patch
 constexpr int TILE = 4 * PATCH;         // receivers per work-list tile
-constexpr int WARPS = 4;                // independent warps per CTA
+#ifndef BF_WARPS
+#define BF_WARPS 4
+#endif
+constexpr int WARPS = BF_WARPS;         // independent warps per CTA
 constexpr int THREADS = 32 * WARPS;
 constexpr int CB = 32;                  // max beams per staged chunk
 constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk
