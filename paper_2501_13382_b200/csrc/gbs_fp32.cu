@@ -200,18 +200,16 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
 
 // Phase anchor of the nearest point: interior -> centre anchor + kappa (r.d);
 // clamped -> exact start / end anchor (turns).
-template <int NF>
-__device__ __forceinline__ void phase_base(const Fp32Consts &K, float proj, float dl, float len,
-                                           const WarpSmem<NF> &G, int row, float *base) {
-#pragma unroll
-    for (int f = 0; f < NF; ++f) {
-        const float4 an = G.anc[f][row];
-        float bf = fmaf(K.kappa[f], dl, an.x);
-        bf = proj >= len ? an.z : bf;
-        bf = proj <= 0.f ? an.y : bf;
-        base[f] = bf;
-    }
+// Axial phase (turns) of the nearest point from the row's anchor `an` (centre
+// projection / start / end): interior -> an.x + kappa (r.d); clamped -> exact end anchor.
+__device__ __forceinline__ float anchor_phase(float kappa, float proj, float dl, float len,
+                                              const float4 &an) {
+    float bf = fmaf(kappa, dl, an.x);
+    bf = proj >= len ? an.z : bf;
+    bf = proj <= 0.f ? an.y : bf;
+    return bf;
 }
+
 
 // Distance of the patch centre (the origin of patch-local coordinates) to
 // segment row `r` (fp32), the unit vector from the nearest point, whether the
@@ -448,14 +446,15 @@ __device__ __forceinline__ bool junction_pick(const Junction &J, const double (&
 // among the surviving segments `surv` (ascending k, strict <), one pending
 // receiver per lane per round; fills the nearest point of each decided receiver.
 template <int NF>
-__device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<NF> &S,
+__device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts &K,
+                                              const WarpSmem<NF> &S,
                                               int64_t beam, int r0, unsigned surv, unsigned pend,
                                               const float (&rx)[R], const float (&ry)[R],
                                               const float (&rz)[R], const float (&rr)[R],
                                               const float (&best)[R], const int (&kb)[R],
                                               float Db, int lane, float (&sj)[R],
-                                              float (&q2j)[R], float (&pj)[R], float (&dlj)[R],
-                                              int (&rowj)[R], unsigned &lvm, unsigned &ties,
+                                              float (&q2j)[R], float (&Aj)[R],
+                                              float (&bj)[R][NF], unsigned &lvm, unsigned &ties,
                                               const Fp32Work &w) {
     ties += __popc(pend);
     // two adjacent candidates k, k+1 (most multi items): a receiver that projects
@@ -483,14 +482,19 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const WarpSmem<N
         const float s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
         // anchor choice follows the exact clamp
         const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
+        const float A = S.aux[r0 + k].y;
+        float b[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            b[f] = anchor_phase(K.kappa[f], proj, dl, S.geo0[r0 + k].w, S.anc[f][r0 + k]);
 #pragma unroll
         for (int jj = 0; jj < R; ++jj)
             if (jj == j) {
                 q2j[jj] = q2;
                 sj[jj] = s;
-                rowj[jj] = r0 + k;
-                pj[jj] = proj;
-                dlj[jj] = dl;
+                Aj[jj] = A;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) bj[jj][f] = b[f];
             }
         lvm |= 1u << j;
     }
@@ -721,10 +725,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if ((BF_ABL & 4) && !is_single && !is_wedge) continue;
             }
 #endif
-            float sj[R], q2j[R], pj[R], dlj[R];
-            int rowj[R];
-#pragma unroll
-            for (int j = 0; j < R; ++j) rowj[j] = r0;  // a valid row for masked lanes
+            // nearest point of every receiver: s, q^2, amplitude factor, axial phase base
+            float sj[R], q2j[R], Aj[R], bj[R][NF];
             unsigned lvm;
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
@@ -733,15 +735,21 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 const float4 g0 = S.geo0[row];
                 const float4 g1 = S.geo1[row];
                 const float4 g2 = S.geo2[row];
-                const float s0 = S.aux[row].x;
+                const float2 ax = S.aux[row];
+                float4 an[NF];
+#pragma unroll
+                for (int f = 0; f < NF; ++f) an[f] = S.anc[f][row];
+                float pj[R];
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
-                    rowj[j] = row;
-                    dlj[j] = dl;
                     pj[j] = proj;
-                    sj[j] = s0 + fminf(fmaxf(proj, 0.f), g0.w);
+                    Aj[j] = ax.y;
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        bj[j][f] = anchor_phase(K.kappa[f], proj, dl, g0.w, an[f]);
+                    sj[j] = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
                     q2j[j] = fmaxf(
                         fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                         0.f);
@@ -834,10 +842,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g2 = S.geo2[r0 + k];
                     q2j[j] = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                                    0.f);
-                    sj[j] = S.aux[r0 + k].x + fminf(fmaxf(proj, 0.f), S.geo0[r0 + k].w);
-                    rowj[j] = r0 + k;
-                    pj[j] = proj;
-                    dlj[j] = dl;
+                    const float2 ax = S.aux[r0 + k];
+                    const float len = S.geo0[r0 + k].w;
+                    sj[j] = ax.x + fminf(fmaxf(proj, 0.f), len);
+                    Aj[j] = ax.y;
+#pragma unroll
+                    for (int f = 0; f < NF; ++f)
+                        bj[j][f] = anchor_phase(K.kappa[f], proj, dl, len, S.anc[f][r0 + k]);
                     lvm |= 1u << j;
                 }
 #if BF_ABLM == 2
@@ -856,6 +867,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const Junction J = load_junction(w, beam * a.max_seg + ka);
                     const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
                     const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
+                    const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
+                    float ea[NF], sb_[NF];  // end anchor of ka, start anchor of ka+1
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        ea[f] = S.anc[f][ra].z;
+                        sb_[f] = S.anc[f][rb].y;
+                    }
                     ties += __popc(jp);
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
@@ -868,16 +886,16 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                             fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                             0.f);
                         sj[j] = wb ? J.sb : J.sa;
-                        rowj[j] = wb ? rb : ra;
-                        pj[j] = wb ? -1.f : INFINITY;  // start anchor of ka+1 / end anchor of ka
-                        dlj[j] = 0.f;
+                        Aj[j] = wb ? Ab : Aa;
+#pragma unroll
+                        for (int f = 0; f < NF; ++f) bj[j][f] = wb ? sb_[f] : ea[f];
                         lvm |= 1u << j;
                     }
                 }
 #if BF_ABLM != 3
                 if (__any_sync(0xffffffffu, pend != 0))
-                    exact_pending<NF>(a, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
-                                      Db, lane, sj, q2j, pj, dlj, rowj, lvm, ties, w);
+                    exact_pending<NF>(a, K, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
+                                      Db, lane, sj, q2j, Aj, bj, lvm, ties, w);
 #endif
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
@@ -896,14 +914,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             for (int g = 0; g < R; g += EVG)
                 if (lvm & (((1u << EVG) - 1u) << g)) {
 #pragma unroll
-                    for (int j = g; j < g + EVG; ++j) {
-                        const int row = rowj[j];
-                        float base[NF];
-                        phase_base<NF>(K, pj[j], dlj[j], S.geo0[row].w, S, row, base);
-                        eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], S.aux[row].y, base,
+                    for (int j = g; j < g + EVG; ++j)
+                        eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], Aj[j], bj[j],
                                       pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
                                       EVG == 1 || ((lvm >> j) & 1u));
-                    }
                 }
         }
         // flush fp32 partial sums into the fp64 accumulators
