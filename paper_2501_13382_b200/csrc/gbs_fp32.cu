@@ -155,8 +155,7 @@ struct WarpSmem {
     unsigned rowinfo[ROWCAP];  // chunk row -> beam << 5 | segment
     short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
-    unsigned surv[CB];       // surviving segments + flags (0 = culled)
-    float bD[CB];            // error scale D of the beam (max over its rows)
+    int4 desc[CB];           // chunk beam -> (beam, survivor word, first row, D bits)
     double acc[PATCH][NF][2];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
@@ -648,8 +647,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #else
             word = classify<NF>(S, K, r0, nsb, RW, D);
 #endif
-            S.surv[lane] = word;
-            S.bD[lane] = D;
+            S.desc[lane] = make_int4(S.gbeam[lane], (int)word, r0, __float_as_int(D));
 #if BF_PREFETCH_EXACT
             // wedge / several-candidate items read fp64 rows later: start the transfers
             const unsigned mw = word & ~(BEHIND_CHECK | WEDGE);
@@ -710,12 +708,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #else
         for (unsigned lm = live; lm;) {
 #endif
-            const int jb = __ffs(lm) - 1;
+            const int4 dsc = S.desc[__ffs(lm) - 1];
             lm &= lm - 1;
-            const int64_t beam = S.gbeam[jb];
-            const unsigned bword = S.surv[jb];
+            const int64_t beam = dsc.x;
+            const unsigned bword = (unsigned)dsc.y;
             const unsigned surv = bword & ~(BEHIND_CHECK | WEDGE);
-            const int r0 = S.brow[jb];
+            const int r0 = dsc.z;
 #if BF_ABL
             // ablation (timing experiments only; results are wrong): skip item kinds
             {
@@ -773,7 +771,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     lvm = 0;
                 } else {
                 // ---- several candidate segments: fp32 distances, fp64 re-decision of ties
-                Db = S.bD[jb];
+                Db = __int_as_float(dsc.w);
                 const float tie_abs = TIE_ABS * Db * Db;
                 jp = 0;
                 lvm = 0;
