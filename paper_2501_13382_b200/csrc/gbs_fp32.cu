@@ -346,6 +346,43 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&
     return m;
 }
 
+// Segments k, k+1 meeting at a reflection point, in fp64 (packed rows): when a
+// receiver projects beyond the end of k and before the start of k+1, both clamped
+// distances (kernels.py:332-340) are distances to the reflection point and the
+// reference's choice is decided by fp64 rounding, reproduced here op for op.
+#if BF_HIST
+__device__ unsigned long long g_hist[4];  // debug: junction, pending, pending rounds, non-pair
+#endif
+struct Junction {
+    double ox, oy, oz;  // o_k
+    double lx, ly, lz;  // len_k * d_k (t = len, kernels.py:337-339)
+    double bx, by, bz;  // o_{k+1}
+    float sa, sb;       // s of either winner: s0_k + len_k, s0_{k+1}
+};
+
+__device__ __forceinline__ Junction load_junction(const double4 *__restrict__ p0,
+                                                  const double4 *__restrict__ p1, int64_t grow) {
+    const double4 a0 = p0[grow], a1 = p1[grow], b0 = p0[grow + 1], b1 = p1[grow + 1];
+    Junction J;
+    J.ox = a0.x, J.oy = a0.y, J.oz = a0.z;
+    J.lx = __dmul_rn(a0.w, a1.x), J.ly = __dmul_rn(a0.w, a1.y), J.lz = __dmul_rn(a0.w, a1.z);
+    J.bx = b0.x, J.by = b0.y, J.bz = b0.z;
+    J.sa = (float)(a1.w + a0.w);
+    J.sb = (float)b1.w;
+    return J;
+}
+
+// true -> segment k+1 is the reference's nearest segment (strict <: ties keep k)
+__device__ __forceinline__ bool junction_pick(const Junction &J, const double (&p)[3]) {
+    const double vx = __dsub_rn(__dsub_rn(p[0], J.ox), J.lx);
+    const double vy = __dsub_rn(__dsub_rn(p[1], J.oy), J.ly);
+    const double vz = __dsub_rn(__dsub_rn(p[2], J.oz), J.lz);
+    const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+    const double wx = __dsub_rn(p[0], J.bx), wy = __dsub_rn(p[1], J.by), wz = __dsub_rn(p[2], J.bz);
+    const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
+    return db < da;
+}
+
 struct ExactPick {
     double bt, bp, len;  // clamped t, projection and length of the winning segment
     int bk;              // winning segment (ascending k, strict <)
@@ -367,7 +404,9 @@ ExactPick exact_pick(const double4 *__restrict__ p0,
                                              float best, float Db, const double (&p)[3]) {
     const double px = p[0], py = p[1], pz = p[2];
     ExactPick e{0.0, 0.0, 0.0, -1};
-    double bd = INFINITY;
+    // pass 1 (fp32): contenders, the segments within the fp32 error of two distances of
+    // the fp32 best (tight bound, DESIGN 5.8)
+    unsigned cm = 0;
 #pragma unroll 1
     for (unsigned m = surv; m; m &= m - 1) {
         const int kk = __ffs(m) - 1;
@@ -378,10 +417,33 @@ ExactPick exact_pick(const double4 *__restrict__ p0,
         const float tt = fminf(fmaxf(pjj, 0.f), h0.w);
         const float ex = vx0 - tt * h1.x, ey = vy0 - tt * h1.y, ez = vz0 - tt * h1.z;
         const float d2k = ex * ex + ey * ey + ez * ez;
-        // a contender only within the fp32 error of two distances (tight bound, DESIGN 5.8)
-        if (kk != kf && d2k - best > fmaf(TIE_DD * Db, sqrt_approx(d2k) * 1.0001f,
-                                          fmaf(TIE_D2, d2k, TIE_DSQ * Db * Db)))
-            continue;
+        if (kk == kf || d2k - best <= fmaf(TIE_DD * Db, sqrt_approx(d2k) * 1.0001f,
+                                           fmaf(TIE_D2, d2k, TIE_DSQ * Db * Db)))
+            cm |= 1u << kk;
+    }
+    // two adjacent contenders k, k+1 and the receiver beyond the end of k and before the
+    // start of k+1: the junction decision (both clamped, kernels.py:332-336)
+    const int ka = __ffs(cm) - 1;
+    if (cm == (3u << ka)) {
+        const float4 a0 = geo0[ka], a1 = geo1[ka], b1 = geo1[ka + 1];
+        const float pa = fmaf(rx, a1.x, fmaf(ry, a1.y, rz * a1.z)) + a1.w;
+        const float pb = fmaf(rx, b1.x, fmaf(ry, b1.y, rz * b1.z)) + b1.w;
+        const float tol = PROJ_ERR * Db;
+        if (pa - a0.w >= tol && pb <= -tol) {
+            const Junction J = load_junction(p0, p1, row0 + ka);
+            const bool wb = junction_pick(J, p);
+            e.bk = ka + (wb ? 1 : 0);
+            e.len = wb ? p0[row0 + ka + 1].w : p0[row0 + ka].w;
+            e.bt = wb ? 0.0 : e.len;
+            e.bp = wb ? -1.0 : e.len;  // clamped at the start of k+1 / the end of k
+            return e;
+        }
+    }
+    // pass 2 (fp64, reference operation order): argmin over the contenders, strict <
+    double bd = INFINITY;
+#pragma unroll 1
+    for (unsigned m = cm; m; m &= m - 1) {
+        const int kk = __ffs(m) - 1;
         const double4 o = p0[row0 + kk], d = p1[row0 + kk];  // packed fp64 rows (exact copies)
         const double ox = o.x, oy = o.y, oz = o.z, len = o.w;
         const double dx = d.x, dy = d.y, dz = d.z;
@@ -405,41 +467,6 @@ ExactPick exact_pick(const double4 *__restrict__ p0,
     return e;
 }
 
-// Segments k, k+1 meeting at a reflection point, in fp64 (packed rows): when a
-// receiver projects beyond the end of k and before the start of k+1, both clamped
-// distances (kernels.py:332-340) are distances to the reflection point and the
-// reference's choice is decided by fp64 rounding, reproduced here op for op.
-#if BF_HIST
-__device__ unsigned long long g_hist[4];  // debug: junction, pending, pending rounds, non-pair
-#endif
-struct Junction {
-    double ox, oy, oz;  // o_k
-    double lx, ly, lz;  // len_k * d_k (t = len, kernels.py:337-339)
-    double bx, by, bz;  // o_{k+1}
-    float sa, sb;       // s of either winner: s0_k + len_k, s0_{k+1}
-};
-
-__device__ __forceinline__ Junction load_junction(const Fp32Work &w, int64_t grow) {
-    const double4 a0 = w.p0[grow], a1 = w.p1[grow], b0 = w.p0[grow + 1], b1 = w.p1[grow + 1];
-    Junction J;
-    J.ox = a0.x, J.oy = a0.y, J.oz = a0.z;
-    J.lx = __dmul_rn(a0.w, a1.x), J.ly = __dmul_rn(a0.w, a1.y), J.lz = __dmul_rn(a0.w, a1.z);
-    J.bx = b0.x, J.by = b0.y, J.bz = b0.z;
-    J.sa = (float)(a1.w + a0.w);
-    J.sb = (float)b1.w;
-    return J;
-}
-
-// true -> segment k+1 is the reference's nearest segment (strict <: ties keep k)
-__device__ __forceinline__ bool junction_pick(const Junction &J, const double (&p)[3]) {
-    const double vx = __dsub_rn(__dsub_rn(p[0], J.ox), J.lx);
-    const double vy = __dsub_rn(__dsub_rn(p[1], J.oy), J.ly);
-    const double vz = __dsub_rn(__dsub_rn(p[2], J.oz), J.lz);
-    const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-    const double wx = __dsub_rn(p[0], J.bx), wy = __dsub_rn(p[1], J.by), wz = __dsub_rn(p[2], J.bz);
-    const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
-    return db < da;
-}
 
 // Exact re-decision (fp64, reference operation order) of the receivers in `pend`
 // among the surviving segments `surv` (ascending k, strict <), one pending
@@ -862,7 +889,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #endif
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
-                    const Junction J = load_junction(w, beam * a.max_seg + ka);
+                    const Junction J = load_junction(w.p0, w.p1, beam * a.max_seg + ka);
                     const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
                     const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
