@@ -87,6 +87,7 @@ struct Fp32Work {
     float *pa;                // per row and frequency: phase anchors at s0, s0+len (turns)
     float4 *prl;              // sorted receiver -> patch-local fp32 coordinates, |r|^2
     double4 *pcen;            // per patch: centre xyz, radius
+    float4 *pbox;             // per patch: bounding-box half extents xyz, radius (patch-local)
     double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum
     int *part_ev;             // per (beam range, sorted receiver): unit evaluation count
     unsigned *unit_ctr;       // persistent-kernel work queue head

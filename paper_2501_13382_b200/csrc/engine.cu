@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_COUNT
 };
 
 struct DeviceCtx {
@@ -349,6 +349,7 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     BF_TRY(c->get(B_PA, 2 * rows * a.nf, &w.pa));
     BF_TRY(c->get(B_PRL, a.n_obs, &w.prl));
     BF_TRY(c->get(B_PCEN, w.n_patches, &w.pcen));
+    BF_TRY(c->get(B_PBOX, w.n_patches, &w.pbox));
     w.n_pad = w.n_patches * P;
     BF_TRY(c->get(B_DONE, (size_t)(w.n_ranges * w.n_pad * a.nf), &w.part));
     BF_TRY(c->get(B_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));

@@ -213,12 +213,19 @@ __device__ __forceinline__ float anchor_phase(float kappa, float proj, float dl,
 // Distance of the patch centre (the origin of patch-local coordinates) to
 // segment row `r` (fp32), the unit vector from the nearest point, whether the
 // whole patch (radius RW) is cut for this segment, and the centre's projection.
+// Largest |r.g| over the patch: min of the box bound sum_i h_i |g_i| and the ball bound
+// RW |g| (both hold for every receiver; the box is much tighter along a flat patch's normal).
+__device__ __forceinline__ float reach(const float4 &B, float gx, float gy, float gz, float gn) {
+    return fminf(fmaf(B.x, fabsf(gx), fmaf(B.y, fabsf(gy), B.z * fabsf(gz))), B.w * gn);
+}
+
 template <int NF>
 __device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, const Fp32Consts &K, int r,
-                                            float RW, float *ux, float *uy, float *uz, bool *cut,
-                                            float *proj_out) {
+                                            const float4 &B, float *ux, float *uy, float *uz,
+                                            bool *cut, float *proj_out) {
     const float4 g0 = S.geo0[r];
     const float4 g1 = S.geo1[r];
+    const float4 g2 = S.geo2[r];
     const float wx = g0.x, wy = g0.y, wz = g0.z;
     const float proj = g1.w;
     const float t = fminf(fmaxf(proj, 0.f), g0.w);
@@ -228,13 +235,18 @@ __device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, const Fp32Con
     *ux = vx * inv;
     *uy = vy * inv;
     *uz = vz * inv;
-    // cut for every receiver if this segment wins (kernels.py:382-385): q >= |u_c| - RW
-    // (|u_c|: the centre's distance to the infinite line) and s <= s_hi, so the
-    // patch is cut when |u_c| > R_cut(s_hi) + RW, R_cut(s)^2 = 72 c (s^2 + b^2)/(omega_min b)
-    const float s_hi = S.aux[r].x + fminf(fmaxf(proj + RW * 1.00002f + 2e-3f, 0.f), g0.w);
+    // cut for every receiver if this segment wins (kernels.py:382-385): q is convex with
+    // subgradient n = u_c/|u_c| at the centre, so q >= |u_c| - reach(n) (|u_c|: the
+    // centre's distance to the infinite line), and s <= s_hi = s0 + clamp(Pc + reach(d));
+    // the patch is cut when |u_c| > R_cut(s_hi) + reach(n),
+    // R_cut(s)^2 = 72 c (s^2 + b^2)/(omega_min b)
+    const float uc = sqrt_approx(g2.w);
+    const float hn = uc > 1e-6f ? 0.5f * rcp_approx(uc) : 0.f;
+    const float rn = uc > 1e-6f ? reach(B, g2.x * hn, g2.y * hn, g2.z * hn, 1.f) : B.w;
+    const float rd = reach(B, g1.x, g1.y, g1.z, 1.f);
+    const float s_hi = S.aux[r].x + fminf(fmaxf(proj + rd * 1.00002f + 2e-3f, 0.f), g0.w);
     const float rk = sqrt_approx(K.rscale * fmaf(s_hi, s_hi, K.b2)) * 1.00002f + 1e-3f;
-    const float rc = (rk + RW) * 1.00002f + 2e-3f;
-    *cut = S.geo2[r].w > rc * rc;
+    *cut = uc * 0.99999f > (rk + rn) * 1.00002f + 2e-3f;
     *proj_out = proj;
     return dc;
 }
@@ -250,7 +262,8 @@ __device__ __forceinline__ float sweep(float RW, float d) {
 // Work generation for one (patch, beam): survivor mask + flags (0 = culled).
 template <int NF>
 __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Consts &K, int r0,
-                                             int ns, float RW, float &D) {
+                                             int ns, const float4 &B, float &D) {
+    const float RW = B.w;
     D = 0.f;
     if (ns <= 0) return 0u;
     // pass 1: nearest segment at the patch centre; error scale D of the beam
@@ -275,9 +288,11 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Co
     // segments never win, so then no pair of the patch contributes
     float ujx, ujy, ujz, pj;
     bool cj;
-    const float dj = patch_dist(S, K, r0 + kj, RW, &ujx, &ujy, &ujz, &cj, &pj);
+    const float dj = patch_dist(S, K, r0 + kj, B, &ujx, &ujy, &ujz, &cj, &pj);
     const float sj = sweep(RW, dj);
-    const bool behind0 = p0 + RW * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
+    const float4 d0 = S.geo1[r0];
+    const float r0d = reach(B, d0.x, d0.y, d0.z, 1.f);  // max |r.d_0| over the patch
+    const bool behind0 = p0 + r0d * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
     unsigned mask = 1u << kj;
     bool all_dead = cj || (kj == 0 && behind0);
 #pragma unroll 1
@@ -285,11 +300,14 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Co
         if (k == kj) continue;
         float ux, uy, uz, proj;
         bool cut;
-        const float dk = patch_dist(S, K, r0 + k, RW, &ux, &uy, &uz, &cut, &proj);
-        // d_k - d_j over the patch >= (d_k - d_j)(c) - RW * sup|grad d_k - grad d_j|
+        const float dk = patch_dist(S, K, r0 + k, B, &ux, &uy, &uz, &cut, &proj);
+        // d_k - d_j over the patch >= (d_k - d_j)(c) + g.r - |r| sup|grad(d_k - d_j) - g|
+        // with g = grad(d_k - d_j)(c) = u_k - u_j; each gradient turns by at most the
+        // sweep angle over the ball, so the drop is <= reach(g) + RW (sweep_k + sweep_j)
         const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
-        const float lip = fminf(sqrt_approx(ex * ex + ey * ey + ez * ez) + sweep(RW, dk) + sj, 2.f);
-        if (!(dk - dj > RW * lip * 1.00002f + 2e-3f + 1e-5f * dk)) {
+        const float gn = sqrt_approx(ex * ex + ey * ey + ez * ez);
+        const float drop = fminf(reach(B, ex, ey, ez, gn) + RW * (sweep(RW, dk) + sj), 2.f * RW);
+        if (!(dk - dj > drop * 1.00002f + 2e-3f + 1e-5f * dk)) {
             mask |= 1u << k;
             all_dead = all_dead && (cut || (k == 0 && behind0));
         }
@@ -297,15 +315,16 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Co
     if (all_dead) return 0u;
     unsigned word = mask;
     // segment 0 survives and the patch reaches its launch plane
-    if ((mask & 1u) && p0 - RW * 1.00002f - 2e-3f <= PROJ_ERR * D) word |= BEHIND_CHECK;
+    if ((mask & 1u) && p0 - r0d * 1.00002f - 2e-3f <= PROJ_ERR * D) word |= BEHIND_CHECK;
     // corner wedge: exactly segments k, k+1 survive and every receiver projects
     // beyond the end of k and before the start of k+1, so both clamped
     // distances are distances to the shared reflection point
     const int kl = __ffs(mask) - 1;
     if (mask == (3u << kl)) {
-        const float pa = S.geo1[r0 + kl].w, pb = S.geo1[r0 + kl + 1].w;
-        const float m1 = PROJ_ERR * D + RW * 1.00002f + 2e-3f;
-        if (pa - S.geo0[r0 + kl].w >= m1 && pb <= -m1) word = mask | WEDGE;
+        const float4 da = S.geo1[r0 + kl], db = S.geo1[r0 + kl + 1];
+        const float ma = PROJ_ERR * D + reach(B, da.x, da.y, da.z, 1.f) * 1.00002f + 2e-3f;
+        const float mb = PROJ_ERR * D + reach(B, db.x, db.y, db.z, 1.f) * 1.00002f + 2e-3f;
+        if (da.w - S.geo0[r0 + kl].w >= ma && db.w <= -mb) word = mask | WEDGE;
     }
     return word;
 }
@@ -672,7 +691,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #if BF_ABL & 32
             word = 0;  // ablation: no classification
 #else
-            word = classify<NF>(S, K, r0, nsb, RW, D);
+            word = classify<NF>(S, K, r0, nsb, w.pbox[p], D);
 #endif
             S.desc[lane] = make_int4(S.gbeam[lane], (int)word, r0, __float_as_int(D));
 #if BF_PREFETCH_EXACT
@@ -1041,7 +1060,7 @@ __global__ void pack_kernel(const GbsArgs a, const Fp32Consts K, double4 *p0, do
 // One warp per patch: fp64 bounding-box centre c_P, patch-local r = p - c_P in
 // fp32 (w = |r|^2) and the patch radius (max |r|, padded).
 __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
-                             int64_t n_patches, float4 *prl, double4 *pcen) {
+                             int64_t n_patches, float4 *prl, double4 *pcen, float4 *pbox) {
     const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (p >= n_patches) return;
@@ -1072,7 +1091,7 @@ __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
         }
     const double cx = 0.5 * (mn[0] + mx[0]), cy = 0.5 * (mn[1] + mx[1]),
                  cz = 0.5 * (mn[2] + mx[2]);
-    float q = 0.f;
+    float q = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         if (!valid[j]) continue;
@@ -1080,10 +1099,22 @@ __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
         const float r2 = rx * rx + ry * ry + rz * rz;
         prl[p * PATCH + R * lane + j] = make_float4(rx, ry, rz, r2);
         q = fmaxf(q, r2);
+        hx = fmaxf(hx, fabsf(rx));
+        hy = fmaxf(hy, fabsf(ry));
+        hz = fmaxf(hz, fabsf(rz));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) q = fmaxf(q, __shfl_xor_sync(0xffffffffu, q, o));
-    if (lane == 0) pcen[p] = make_double4(cx, cy, cz, (double)(sqrtf(q) * 1.0001f + 1e-4f));
+    for (int o = 16; o > 0; o >>= 1) {
+        q = fmaxf(q, __shfl_xor_sync(0xffffffffu, q, o));
+        hx = fmaxf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+        hy = fmaxf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+        hz = fmaxf(hz, __shfl_xor_sync(0xffffffffu, hz, o));
+    }
+    const float RW = sqrtf(q) * 1.0001f + 1e-4f;
+    if (lane == 0) {
+        pcen[p] = make_double4(cx, cy, cz, (double)RW);
+        pbox[p] = make_float4(hx * 1.0001f + 1e-4f, hy * 1.0001f + 1e-4f, hz * 1.0001f + 1e-4f, RW);
+    }
 }
 
 // acc[oi] += sum over beam ranges q (ascending) of the units' partials; evals alike.
@@ -1244,7 +1275,7 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
     }
     if (w.n_patches > 0) {
         patch_kernel<<<(unsigned)((w.n_patches * 32 + 127) / 128), 128, 0, st>>>(
-            a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen);
+            a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen, w.pbox);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
