@@ -381,6 +381,17 @@ __global__ void __launch_bounds__(128) trace_kernel(const TraceArgs a) {
 // s_hi = s0 + clamp(w.d + R_T, 0, len) <= s_end (every receiver's nearest point on k
 // projects within R_T of the centre's), R_k(s_hi)^2 = 72 c (s_hi^2 + b^2)/(omega_min b).
 // Tight-dead implies nothing about a9; a9-dead implies tight-dead.
+// qp - rt > sqrt(r2) (1 + 1e-6) + 1e-6 with qp = sqrt(q2), decided in fp64 exactly as
+// the C restatement does, but the two square roots are only taken when an fp32
+// estimate (relative error ~1e-7) is within 1e-4 of the threshold.
+__device__ __forceinline__ bool cut_beyond(double q2, double r2, double rt) {
+    const float x = sqrtf((float)r2) * 1.000001f + 1e-6f + (float)rt;  // threshold for qp
+    const float x2 = x * x, qf = (float)q2;
+    if (qf > x2 * 1.0001f + 1e-12f) return true;
+    if (qf < x2 * 0.9999f - 1e-12f) return false;
+    return sqrt(q2) - rt > sqrt(r2) * (1.0 + 1e-6) + 1e-6;
+}
+
 __device__ __forceinline__ unsigned beam_dead_for_tile(const GbsArgs &a, int64_t b, double cx,
                                                        double cy, double cz, double rt,
                                                        double rscale) {
@@ -394,17 +405,17 @@ __device__ __forceinline__ unsigned beam_dead_for_tile(const GbsArgs &a, int64_t
                      dz = a.seg_dir[3 * row + 2];
         const double proj = wx * dx + wy * dy + wz * dz;
         const double ux = wx - proj * dx, uy = wy - proj * dy, uz = wz - proj * dz;
-        const double qp = sqrt(ux * ux + uy * uy + uz * uz);
+        const double q2 = ux * ux + uy * uy + uz * uz;
         const double s0 = a.seg_s0[row], len = a.seg_len[row];
         const double se = s0 + len;
-        const double rk = sqrt(rscale * (se * se + a.width_b * a.width_b));
         double reach = proj + rt;
         reach = reach < 0.0 ? 0.0 : (reach > len ? len : reach);
         const double sh = s0 + reach;
-        const double rh = sqrt(rscale * (sh * sh + a.width_b * a.width_b));
         const bool behind = k == 0 && proj + rt < -1e-6;
-        loose = loose && (qp - rt > rk * (1.0 + 1e-6) + 1e-6 || behind);
-        tight = tight && (qp - rt > rh * (1.0 + 1e-6) + 1e-6 || behind);
+        if (!behind) {
+            loose = loose && cut_beyond(q2, rscale * (se * se + a.width_b * a.width_b), rt);
+            tight = tight && cut_beyond(q2, rscale * (sh * sh + a.width_b * a.width_b), rt);
+        }
     }
     return (loose ? 1u : 0u) | (tight ? 2u : 0u);
 }
