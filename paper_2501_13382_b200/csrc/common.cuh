@@ -106,8 +106,10 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 // Work-list compaction (north star: prefix-sum compaction into (beam, tile) lists):
 // counts per (tile, range) into w.wl_off (pass 1), then, after an exclusive scan of
 // the counts, the entries (pass 2).
+// wstats (4 x n_tiles, zeroed): per tile a9 candidate beams, their segments, tight
+// candidate beams, their segments.
 int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
-                         cudaStream_t st);
+                         unsigned long long *wstats, cudaStream_t st);
 int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
                            cudaStream_t st);
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
@@ -122,9 +124,7 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                  double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
                  int64_t row_base, cudaStream_t st);
 int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
-                    uint32_t *bits, uint32_t *tbits, unsigned long long *cand_beams,
-                    unsigned long long *cand_segs, unsigned long long *tight_beams,
-                    unsigned long long *tight_segs, cudaStream_t st);
+                    uint32_t *bits, uint32_t *tbits, cudaStream_t st);
 int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
                     double *spl, cudaStream_t st);
 

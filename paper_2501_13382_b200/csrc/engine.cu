@@ -302,23 +302,17 @@ int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_
 }
 
 // Tile-level work list (exact fp64 candidate test, exact_fp64.cu) for tiling t.
-int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st,
-                   unsigned long long **cand_out) {
+int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st) {
     const int64_t n_words = (a.n_beams + 31) / 32;
     uint32_t *bits, *tbits;
-    unsigned long long *cand;
     BF_TRY(c->get(B_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
     BF_TRY(c->get(B_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
-    BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &cand));
-    BF_TRY_CUDA(cudaMemsetAsync(cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
     double wmin = INFINITY;
     for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
-    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, tbits, cand, cand + t.n_tiles,
-                           cand + 2 * t.n_tiles, cand + 3 * t.n_tiles, st));
+    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, tbits, st));
     t.wl_bits = bits;
     t.wl_tight = tbits;
     t.wl_words = n_words;
-    if (cand_out) *cand_out = cand;
     return BF_OK;
 }
 
@@ -331,8 +325,10 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     if (precision == BF_PRECISION_FP64) return launch_gbs_fp64(a, st);
     Tiling t;
     BF_TRY(build_tiling(c, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
-    unsigned long long *d_cand;
-    BF_TRY(build_worklist(c, a, t, st, &d_cand));
+    BF_TRY(build_worklist(c, a, t, st));
+    unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
+    BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &d_cand));
+    BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
     Fp32Work w{};
     const int64_t rows = a.n_beams * a.max_seg;
     const int P = gbs_fp32_patch();
@@ -361,7 +357,7 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         BF_TRY(c->get(B_WLTMP, (size_t)(nu + 1), &cnt));
         BF_TRY(c->get(B_WLOFF, (size_t)(nu + 1), &w.wl_off));
         BF_TRY_CUDA(cudaMemsetAsync(cnt + nu, 0, sizeof(int64_t), st));
-        BF_TRY(launch_fp32_wl_count(a, t, w, cnt, st));
+        BF_TRY(launch_fp32_wl_count(a, t, w, cnt, d_cand, st));
         size_t tmp_bytes = 0;
         BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, w.wl_off, (int)(nu + 1), st));
         void *tmp;
@@ -745,7 +741,7 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     a.use_cutoff = use_cutoff ? 1 : 0;
     Tiling t;
     BF_TRY(build_tiling(ctx, d_obs, n_obs, false, st, &t));
-    BF_TRY(build_worklist(ctx, a, t, st, nullptr));
+    BF_TRY(build_worklist(ctx, a, t, st));
     const int64_t n_words = (n_beams + 31) / 32;
     const auto D2H = cudaMemcpyDeviceToHost;
     BF_TRY_CUDA(cudaMemcpyAsync(perm, t.perm, 4 * n_obs, D2H, st));

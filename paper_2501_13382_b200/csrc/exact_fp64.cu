@@ -392,68 +392,76 @@ __device__ __forceinline__ bool cut_beyond(double q2, double r2, double rt) {
     return sqrt(q2) - rt > sqrt(r2) * (1.0 + 1e-6) + 1e-6;
 }
 
-__device__ __forceinline__ unsigned beam_dead_for_tile(const GbsArgs &a, int64_t b, double cx,
-                                                       double cy, double cz, double rt,
-                                                       double rscale) {
-    const int ns = a.n_segs[b];
+// The rows of one 32-beam word, staged in shared memory as [segment][beam] arrays.
+struct WordRows {
+    const double *ox, *oy, *oz, *dx, *dy, *dz, *s0, *len;
+};
+
+__device__ __forceinline__ unsigned beam_dead_for_tile(const WordRows &w, int jb, int ns,
+                                                       double width_b, double cx, double cy,
+                                                       double cz, double rt, double rscale) {
     bool loose = true, tight = true;
     for (int k = 0; k < ns && tight; ++k) {
-        const int64_t row = b * a.max_seg + k;
-        const double wx = cx - a.seg_origin[3 * row], wy = cy - a.seg_origin[3 * row + 1],
-                     wz = cz - a.seg_origin[3 * row + 2];
-        const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
-                     dz = a.seg_dir[3 * row + 2];
+        const int i = 32 * k + jb;
+        const double wx = cx - w.ox[i], wy = cy - w.oy[i], wz = cz - w.oz[i];
+        const double dx = w.dx[i], dy = w.dy[i], dz = w.dz[i];
         const double proj = wx * dx + wy * dy + wz * dz;
         const double ux = wx - proj * dx, uy = wy - proj * dy, uz = wz - proj * dz;
         const double q2 = ux * ux + uy * uy + uz * uz;
-        const double s0 = a.seg_s0[row], len = a.seg_len[row];
+        const double s0 = w.s0[i], len = w.len[i];
         const double se = s0 + len;
         double reach = proj + rt;
         reach = reach < 0.0 ? 0.0 : (reach > len ? len : reach);
         const double sh = s0 + reach;
         const bool behind = k == 0 && proj + rt < -1e-6;
         if (!behind) {
-            loose = loose && cut_beyond(q2, rscale * (se * se + a.width_b * a.width_b), rt);
-            tight = tight && cut_beyond(q2, rscale * (sh * sh + a.width_b * a.width_b), rt);
+            loose = loose && cut_beyond(q2, rscale * (se * se + width_b * width_b), rt);
+            tight = tight && cut_beyond(q2, rscale * (sh * sh + width_b * width_b), rt);
         }
     }
     return (loose ? 1u : 0u) | (tight ? 2u : 0u);
 }
 
-// One warp per (tile, 32-beam word): bit j = beam 32*word + j is a candidate
-// (bits: a9 bound, tbits: tight bound, tbits subset of bits).
+// One block per 32-beam word: the word's rows are read once into shared memory and
+// every warp sweeps a share of the tiles; bit j of (tile, word) = beam 32*word + j is a
+// candidate (bits: a9 bound, tbits: tight bound, tbits subset of bits).
 __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t n_tiles,
-                                int64_t n_words, double rscale, uint32_t *bits, uint32_t *tbits,
-                                unsigned long long *cand_beams, unsigned long long *cand_segs,
-                                unsigned long long *tight_beams, unsigned long long *tight_segs) {
-    const int64_t tile = blockIdx.x;
-    const int64_t word = (int64_t)blockIdx.y * (blockDim.x / 32) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (tile >= n_tiles || word >= n_words) return;
-    const double4 c = centre[tile];
-    const int64_t b = 32 * word + lane;
-    unsigned dead = 3u;
-    if (b < a.n_beams) dead = beam_dead_for_tile(a, b, c.x, c.y, c.z, c.w, rscale);
-    const bool cand = !(dead & 1u);
-    const unsigned m = __ballot_sync(0xffffffffu, cand);
-    const unsigned mt = __ballot_sync(0xffffffffu, !(dead & 2u));
-    const int ns = b < a.n_beams ? a.n_segs[b] : 0;
-    int segs = cand ? ns : 0, tsegs = !(dead & 2u) ? ns : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        segs += __shfl_xor_sync(0xffffffffu, segs, o);
-        tsegs += __shfl_xor_sync(0xffffffffu, tsegs, o);
+                                int64_t n_words, double rscale, uint32_t *bits, uint32_t *tbits) {
+    extern __shared__ double wsm[];
+    __shared__ int ns_s[32];
+    const int S = (int)a.max_seg;
+    const int64_t word = blockIdx.x;
+    WordRows w{wsm, wsm + 32 * S, wsm + 64 * S, wsm + 96 * S, wsm + 128 * S, wsm + 160 * S,
+               wsm + 192 * S, wsm + 224 * S};
+    for (int i = threadIdx.x; i < 32 * S; i += blockDim.x) {
+        const int jb = i / S, k = i - jb * S;  // padded rows are beam-major
+        const int64_t b = 32 * word + jb;
+        if (b >= a.n_beams || k >= a.n_segs[b]) continue;
+        const int64_t row = b * S + k;
+        const int o = 32 * k + jb;
+        const_cast<double *>(w.ox)[o] = a.seg_origin[3 * row];
+        const_cast<double *>(w.oy)[o] = a.seg_origin[3 * row + 1];
+        const_cast<double *>(w.oz)[o] = a.seg_origin[3 * row + 2];
+        const_cast<double *>(w.dx)[o] = a.seg_dir[3 * row];
+        const_cast<double *>(w.dy)[o] = a.seg_dir[3 * row + 1];
+        const_cast<double *>(w.dz)[o] = a.seg_dir[3 * row + 2];
+        const_cast<double *>(w.s0)[o] = a.seg_s0[row];
+        const_cast<double *>(w.len)[o] = a.seg_len[row];
     }
-    if (lane == 0) {
-        bits[tile * n_words + word] = m;
-        tbits[tile * n_words + word] = mt;
-        if (m) {
-            atomicAdd(&cand_beams[tile], (unsigned long long)__popc(m));
-            atomicAdd(&cand_segs[tile], (unsigned long long)segs);
-        }
-        if (mt) {
-            atomicAdd(&tight_beams[tile], (unsigned long long)__popc(mt));
-            atomicAdd(&tight_segs[tile], (unsigned long long)tsegs);
+    const int lane = threadIdx.x & 31;
+    const int64_t b = 32 * word + lane;
+    if (threadIdx.x < 32) ns_s[lane] = b < a.n_beams ? a.n_segs[b] : 0;
+    __syncthreads();
+    const int ns = ns_s[lane];
+    for (int64_t t = threadIdx.x >> 5; t < n_tiles; t += blockDim.x >> 5) {
+        const double4 c = centre[t];
+        unsigned dead = 3u;
+        if (b < a.n_beams) dead = beam_dead_for_tile(w, lane, ns, a.width_b, c.x, c.y, c.z, c.w, rscale);
+        const unsigned m = __ballot_sync(0xffffffffu, !(dead & 1u));
+        const unsigned mt = __ballot_sync(0xffffffffu, !(dead & 2u));
+        if (lane == 0) {
+            bits[t * n_words + word] = m;
+            tbits[t * n_words + word] = mt;
         }
     }
 }
@@ -521,16 +529,16 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
 }
 
 int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
-                    uint32_t *bits, uint32_t *tbits, unsigned long long *cand_beams,
-                    unsigned long long *cand_segs, unsigned long long *tight_beams,
-                    unsigned long long *tight_segs, cudaStream_t st) {
+                    uint32_t *bits, uint32_t *tbits, cudaStream_t st) {
     if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
     const int64_t n_words = (a.n_beams + 31) / 32;
     // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
     const double rscale = a.use_cutoff ? 72.0 * a.c / (omega_min * a.width_b) : INFINITY;
-    dim3 grid((unsigned)n_tiles, (unsigned)((n_words + 3) / 4));
-    worklist_kernel<<<grid, 128, 0, st>>>(a, centre, n_tiles, n_words, rscale, bits, tbits, cand_beams,
-                                          cand_segs, tight_beams, tight_segs);
+    const size_t smem = 8 * 32 * sizeof(double) * (size_t)a.max_seg;
+    BF_TRY_CUDA(cudaFuncSetAttribute(worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    worklist_kernel<<<(unsigned)n_words, 256, smem, st>>>(a, centre, n_tiles, n_words, rscale,
+                                                          bits, tbits);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

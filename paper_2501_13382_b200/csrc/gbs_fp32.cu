@@ -1138,19 +1138,45 @@ __global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, double *a
     evals[oi] += ev;
 }
 
-// One warp per (tile, beam range): candidate count of the tight work list.
-__global__ void wl_count_kernel(const Tiling tl, const Fp32Work w, int64_t *counts) {
+// One warp per (tile, beam range): candidate count of the tight work list (compaction
+// offsets) and the per-tile statistics of both lists (FLOP model).
+__global__ void wl_count_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w,
+                                int64_t *counts, unsigned long long *wstats) {
     const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (u >= tl.n_tiles * w.n_ranges) return;
     const int64_t tile = u / w.n_ranges, q = u - tile * w.n_ranges;
     const int64_t w0 = q * w.range_beams / 32;
     const int64_t w1 = min(tl.wl_words, (q + 1) * w.range_beams / 32);
-    const uint32_t *bits = tl.wl_tight + tile * tl.wl_words;
-    int c = 0;
-    for (int64_t i = w0 + lane; i < w1; i += 32) c += __popc(bits[i]);
+    const uint32_t *bits = tl.wl_bits + tile * tl.wl_words;
+    const uint32_t *tbits = tl.wl_tight + tile * tl.wl_words;
+    unsigned c = 0, ct = 0, sg = 0, sgt = 0;
+    for (int64_t i = w0 + lane; i < w1; i += 32) {
+        const unsigned m = bits[i], mt = tbits[i];
+        c += __popc(m);
+        ct += __popc(mt);
+        for (unsigned x = m; x; x &= x - 1) {
+            const int j = __ffs(x) - 1;
+            const unsigned ns = (unsigned)a.n_segs[32 * i + j];
+            sg += ns;
+            if ((mt >> j) & 1u) sgt += ns;
+        }
+    }
     c = __reduce_add_sync(0xffffffffu, c);
-    if (lane == 0) counts[u] = c;
+    ct = __reduce_add_sync(0xffffffffu, ct);
+    sg = __reduce_add_sync(0xffffffffu, sg);
+    sgt = __reduce_add_sync(0xffffffffu, sgt);
+    if (lane == 0) {
+        counts[u] = ct;
+        if (c) {
+            atomicAdd(&wstats[tile], (unsigned long long)c);
+            atomicAdd(&wstats[tl.n_tiles + tile], (unsigned long long)sg);
+        }
+        if (ct) {
+            atomicAdd(&wstats[2 * tl.n_tiles + tile], (unsigned long long)ct);
+            atomicAdd(&wstats[3 * tl.n_tiles + tile], (unsigned long long)sgt);
+        }
+    }
 }
 
 // One warp per (tile, beam range): ascending candidate beams with their segment
@@ -1283,11 +1309,11 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 }
 
 int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
-                         cudaStream_t st) {
-    (void)a;
+                         unsigned long long *wstats, cudaStream_t st) {
     const int64_t nu = t.n_tiles * w.n_ranges;
     if (nu > 0) {
-        wl_count_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(t, w, counts);
+        wl_count_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(a, t, w, counts,
+                                                                           wstats);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
