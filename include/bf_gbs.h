@@ -47,7 +47,8 @@ typedef enum {
     BF_ENOMEM = 2,  /* device or pinned-host allocation failed (MemoryError) */
     BF_ECUDA = 3,   /* CUDA runtime / launch failure (RuntimeError) */
     BF_ENODEV = 4,  /* no usable sm_100 device (RuntimeError) */
-    BF_EBUDGET = 5  /* memory budget cannot hold one ray (BudgetError, parallel.py:98-100) */
+    BF_EBUDGET = 5, /* memory budget cannot hold one ray (BudgetError, parallel.py:98-100) */
+    BF_EIO = 6      /* file output failed (OSError) */
 } bf_status;
 
 /* Arithmetic of the summation kernel. */
@@ -130,6 +131,18 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
  */
 int bf_last_pair_stats(int64_t *a9_pairs, int64_t *a9_pair_segs, int64_t *tight_pairs,
                        int64_t *tight_pair_segs, int64_t *live_pairs, int64_t *live_pair_segs);
+
+/*
+ * Field CSV writer, replaces beamfield.harness.write_field_csv (harness.py:197-208):
+ * header "x,y,z,freq_hz,re_p,im_p,spl_db", one row per (observer, frequency),
+ * observer-major, numbers as Python format(x, ".17g") (harness.py:39-40).  points is
+ * (n_obs, 3), pressure (n_obs, nf) complex128 interleaved, spl (n_obs, nf); host
+ * buffers.  Rows are formatted on `threads` host threads (<= 0: all) and written in
+ * order, byte-identical to the reference's row loop.
+ */
+int bf_write_field_csv(const char *path, const double *points, int64_t n_obs,
+                       const double *freqs, int64_t nf, const double *pressure,
+                       const double *spl, int threads);
 
 /* Receivers per tile of the fp32 summation kernel. */
 int bf_tile_size(void);

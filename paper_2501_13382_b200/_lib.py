@@ -16,7 +16,7 @@ from .errors import BudgetError
 LIB_PATH = pathlib.Path(os.environ.get(
     "BF_GBS_LIB", pathlib.Path(__file__).resolve().parent / "_lib" / "libbf_gbs.so"))
 
-BF_OK, BF_EINVAL, BF_ENOMEM, BF_ECUDA, BF_ENODEV, BF_EBUDGET = range(6)
+BF_OK, BF_EINVAL, BF_ENOMEM, BF_ECUDA, BF_ENODEV, BF_EBUDGET, BF_EIO = range(7)
 PRECISION = {"fp32": 0, "fp64": 1}
 
 # Every symbol include/bf_gbs.h declares.
@@ -25,7 +25,7 @@ EXPORTS = (
     "bf_gbs_accumulate", "bf_gbs_accumulate_dev", "bf_nearest_on_segments",
     "bf_trace_range_dev", "bf_field_finalize_dev", "bf_plan_chunks", "bf_last_stats",
     "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats", "bf_worklist",
-    "bf_last_pair_stats",
+    "bf_last_pair_stats", "bf_write_field_csv",
 )
 FLAG_OBS_PRESORTED = 1
 
@@ -65,6 +65,7 @@ def _declare(lib):
     lib.bf_probe_peaks.argtypes = [INT, D, D]
     lib.bf_last_path_stats.argtypes = [I64P] * 4
     lib.bf_last_pair_stats.argtypes = [I64P] * 6
+    lib.bf_write_field_csv.argtypes = [ctypes.c_char_p, VP, I64, VP, I64, VP, VP, INT]
     lib.bf_worklist.argtypes = [VP, VP, VP, VP, VP, I64, I64, VP, I64, VP, I64, F64, F64, INT,
                                 VP, VP, VP, VP, I64, I64P, INT]
     for name in EXPORTS:
@@ -98,6 +99,8 @@ def check(status: int) -> None:
         raise MemoryError(msg)
     if status == BF_EBUDGET:
         raise BudgetError(msg)
+    if status == BF_EIO:
+        raise OSError(msg)
     raise EngineError(f"[bf_status {status}] {msg}")
 
 

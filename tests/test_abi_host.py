@@ -144,3 +144,45 @@ def test_rank_tiles_partition(n, world):
     for r, p in enumerate(parts):  # whole tiles, dealt round-robin
         if p.size:
             assert set(np.unique(p // 256) % world) == {r}
+
+
+def test_field_csv_bytes_match_python_format(tmp_path):
+    """bf_write_field_csv == the reference's row loop (harness.py:197-208): '%.17g'
+    numbers incl. -inf SPL of null pressure, -0, tiny/huge magnitudes."""
+    from paper_2501_13382_b200 import harness
+    from paper_2501_13382_b200.gbs import FieldResult
+    rng = np.random.default_rng(7)
+    n, freqs = 40000, np.array([63.0, 125.0, 1000.0])
+    pts = rng.normal(size=(n, 3)) * 100.0
+    pts[0] = [-0.0, 1e-300, 1e300]
+    p = (rng.normal(size=(n, 3)) + 1j * rng.normal(size=(n, 3))) * 10.0 ** rng.integers(-12, 3, (n, 3))
+    p[5, 1] = 0.0
+    field = FieldResult.from_pressure(p, 1.0)
+    path = tmp_path / "field.csv"
+    harness.write_field_csv(path, pts, freqs, field, threads=4)
+    g = harness._g
+    rows = [harness.FIELD_CSV_HEADER]
+    for oi in range(n):
+        x, y, z = pts[oi]
+        for fi, f in enumerate(freqs):
+            q = field.pressure[oi, fi]
+            rows.append(f"{g(x)},{g(y)},{g(z)},{g(f)},{g(q.real)},{g(q.imag)},"
+                        f"{g(field.spl[oi, fi])}")
+    assert path.read_text() == "\n".join(rows) + "\n"
+    with pytest.raises(OSError):
+        harness.write_field_csv(tmp_path / "missing" / "x.csv", pts, freqs, field)
+
+
+def test_heatmap(tmp_path):
+    from paper_2501_13382_b200 import harness
+    from PIL import Image
+
+    class Grid:
+        n1, n2 = 5, 3
+    v = np.arange(15, dtype=float)
+    v[4] = -np.inf
+    meta = harness.emit_heatmap(v, Grid, tmp_path / "h.png")
+    img = np.asarray(Image.open(tmp_path / "h.png"))
+    assert img.shape == (3, 5) and img[0, 4] == 0 and img.max() == 255
+    assert meta["null_points"] == 1 and meta["spl_min_db"] == 0.0 and meta["spl_max_db"] == 14.0
+    assert (tmp_path / "h.png.txt").read_text().startswith("width=5\nheight=3\n")
