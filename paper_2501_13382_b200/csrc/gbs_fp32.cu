@@ -259,6 +259,12 @@ __device__ __forceinline__ float sweep(float RW, float d) {
     return x < 0.7f ? x * rsqrtf(1.f - x * x) * 1.0001f : 2.f;
 }
 
+// Second-order drop of the distance to a segment over the ball of radius RW around a
+// point at distance d > RW: RW^2 / (2 (d - RW)) (gradient 1/(d - RW)-Lipschitz there).
+__device__ __forceinline__ float curv(float RW, float d) {
+    return d > RW * 1.0001f + 1e-4f ? 0.5f * RW * RW * rcp_approx(d - RW) * 1.0001f : INFINITY;
+}
+
 // Work generation for one (patch, beam): survivor mask + flags (0 = culled).
 template <int NF>
 __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Consts &K, int r0,
@@ -290,6 +296,7 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Co
     bool cj;
     const float dj = patch_dist(S, K, r0 + kj, B, &ujx, &ujy, &ujz, &cj, &pj);
     const float sj = sweep(RW, dj);
+    const float hj = curv(RW, dj);
     const float4 d0 = S.geo1[r0];
     const float r0d = reach(B, d0.x, d0.y, d0.z, 1.f);  // max |r.d_0| over the patch
     const bool behind0 = p0 + r0d * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
@@ -306,7 +313,12 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Co
         // sweep angle over the ball, so the drop is <= reach(g) + RW (sweep_k + sweep_j)
         const float ex = ux - ujx, ey = uy - ujy, ez = uz - ujz;
         const float gn = sqrt_approx(ex * ex + ey * ey + ez * ez);
-        const float drop = fminf(reach(B, ex, ey, ez, gn) + RW * (sweep(RW, dk) + sj), 2.f * RW);
+        // second order: grad d is 1/delta-Lipschitz at distance >= delta from a convex
+        // set, delta >= d - RW in the ball, so the drop is also <= reach(g) +
+        // RW^2 (1/(d_k - RW) + 1/(d_j - RW)) / 2
+        const float rg = reach(B, ex, ey, ez, gn);
+        const float drop = fminf(fminf(rg + RW * (sweep(RW, dk) + sj), rg + curv(RW, dk) + hj),
+                                 2.f * RW);
         if (!(dk - dj > drop * 1.00002f + 2e-3f + 1e-5f * dk)) {
             mask |= 1u << k;
             all_dead = all_dead && (cut || (k == 0 && behind0));
