@@ -911,13 +911,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (best[0] >= 0.f) continue;  // ablation: scan + decision only
 #endif
                 }
-#if BF_HIST
-                if (!(bword & WEDGE)) {
-                    if (jp) atomicAdd(&g_hist[0], (unsigned long long)__popc(jp));
-                    if (pend) atomicAdd(&g_hist[1], (unsigned long long)__popc(pend));
-                    if (pend && surv != (3u << ka)) atomicAdd(&g_hist[3], (unsigned long long)__popc(pend));
-                }
-#endif
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
                     const Junction J = load_junction(w.p0, w.p1, beam * a.max_seg + ka);
@@ -1346,8 +1339,8 @@ int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
                     cudaStream_t st) {
     if (t.n <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
-    if (a.max_seg > 32)
-        return fail(BF_EINVAL, "max_seg %lld exceeds 32 (r_max <= 31)", (long long)a.max_seg);
+    if (a.max_seg > 30)  // survivor masks share the word with two flag bits
+        return fail(BF_EINVAL, "max_seg %lld exceeds 30 (r_max <= 29)", (long long)a.max_seg);
     const Fp32Consts K = make_consts(a);
     switch (a.nf) {
         case 1: return launch_nf<1>(a, t, w, K, d_stats, st);
