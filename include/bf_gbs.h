@@ -113,15 +113,18 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
  * x, y, z, R_T) and the candidate bitmask bits (n_tiles x ceil(n_beams/32)
  * uint32, bit b%32 of word b/32 = beam b may contribute to some receiver of the
  * tile).  tight_bits (same shape, may be NULL) is the subset the fp32 kernel
- * walks: R_k from the largest arc length s_hi = s0 + clamp(w.d + R_T, 0, len)
- * the tile reaches instead of s_end.  Host buffers; exact fp64 tests, reproduced
- * bit for bit by oracle/worklist_oracle.c.
+ * walks: with the tile's bounding box (half extents h, tile_box = n_tiles x 4:
+ * hx, hy, hz, R_T, may be NULL), R_k from the largest arc length
+ * s_hi = s0 + clamp(w.d + min(h.|d|, R_T), 0, len) the tile reaches and the line
+ * distance lowered by min(h.|u|/|u|, R_T) (u: the centre's offset from the line).
+ * Host buffers; exact fp64 tests, reproduced bit for bit by oracle/worklist_oracle.c.
  */
 int bf_worklist(const double *seg_origin, const double *seg_dir, const double *seg_len,
                 const double *seg_s0, const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
                 const double *obs, int64_t n_obs, const double *omegas, int64_t nf, double c,
-                double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
-                uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out, int device);
+                double width_b, int use_cutoff, int32_t *perm, double *centre, double *tile_box,
+                uint32_t *bits, uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out,
+                int device);
 
 /*
  * Pair counts of the last fp32 summation on this thread (FLOP model of the roofline,

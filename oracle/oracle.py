@@ -150,12 +150,13 @@ def trace(v0, v1, v2, refl, bounds, diameter, origin, dirs, e1s, e2s, length_cap
 
 
 def worklist(seg_origin, seg_dir, seg_len, seg_s0, n_segs, max_seg, centre, c, width_b,
-             omega_min, use_cutoff=True, tight=False):
+             omega_min, use_cutoff=True, tight=False, box=None):
     """Tile-level candidate bitmask (worklist_oracle.c); centre is (n_tiles, 4).
-    tight=True: the tight list the fp32 kernel walks (subset of the a9 list)."""
+    tight=True: the tight list the fp32 kernel walks (subset of the a9 list); needs the
+    tiles' bounding-box half extents box (n_tiles, 4: hx, hy, hz, R_T)."""
     lib = _load()
     if not hasattr(lib, "_wl_declared"):
-        lib.oracle_worklist.argtypes = [_d, _d, _d, _d, _i32, _i64, _i64, _d, _i64,
+        lib.oracle_worklist.argtypes = [_d, _d, _d, _d, _i32, _i64, _i64, _d, _d, _i64,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_int, ctypes.c_int,
                                         ctypes.POINTER(ctypes.c_uint32)]
@@ -166,8 +167,12 @@ def worklist(seg_origin, seg_dir, seg_len, seg_s0, n_segs, max_seg, centre, c, w
     n_segs = np.ascontiguousarray(n_segs, dtype=np.int32)
     nb = n_segs.shape[0]
     nt = centre.reshape(-1, 4).shape[0]
+    if tight and box is None:
+        raise ValueError("the tight list needs the tiles' bounding boxes")
+    bx = f(box).reshape(nt, 4) if box is not None else None
     bits = np.zeros((nt, (nb + 31) // 32), np.uint32)
     lib.oracle_worklist(_p(so), _p(sd), _p(sl), _p(ss0), _p(n_segs, _i32), nb, int(max_seg),
-                        _p(centre), nt, float(c), float(width_b), float(omega_min),
-                        int(bool(use_cutoff)), int(bool(tight)), bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
+                        _p(centre), _p(bx) if bx is not None else None, nt, float(c),
+                        float(width_b), float(omega_min), int(bool(use_cutoff)),
+                        int(bool(tight)), bits.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
     return bits

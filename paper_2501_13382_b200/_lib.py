@@ -67,7 +67,7 @@ def _declare(lib):
     lib.bf_last_pair_stats.argtypes = [I64P] * 6
     lib.bf_write_field_csv.argtypes = [ctypes.c_char_p, VP, I64, VP, I64, VP, VP, INT]
     lib.bf_worklist.argtypes = [VP, VP, VP, VP, VP, I64, I64, VP, I64, VP, I64, F64, F64, INT,
-                                VP, VP, VP, VP, I64, I64P, INT]
+                                VP, VP, VP, VP, VP, I64, I64P, INT]
     for name in EXPORTS:
         if name not in ("bf_version", "bf_last_error", "bf_device_count", "bf_launch_count"):
             getattr(lib, name).restype = INT

@@ -73,6 +73,7 @@ struct Tiling {
     const int32_t *perm;      // sorted position -> local observer index
     const float4 *rloc;       // sorted position -> (p - centre) fp32, w = unused
     const double4 *centre;    // per tile: centre xyz, radius
+    const double4 *tbox;      // per tile: bounding-box half extents xyz, radius
     const uint32_t *wl_bits;  // work list: (tile, beam) candidate bits, wl_words per tile
     const uint32_t *wl_tight; // tight work list (subset of wl_bits) the fp32 kernel walks
     int64_t wl_words;
@@ -123,8 +124,8 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                  double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
                  double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
                  int64_t row_base, cudaStream_t st);
-int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
-                    uint32_t *bits, uint32_t *tbits, cudaStream_t st);
+int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox, int64_t n_tiles,
+                    double omega_min, uint32_t *bits, uint32_t *tbits, cudaStream_t st);
 int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
                     double *spl, cudaStream_t st);
 

@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_TBOX, B_COUNT
 };
 
 struct DeviceCtx {
@@ -182,10 +182,10 @@ __global__ void morton_kernel(const double *obs, int64_t n, const double *bbox, 
 
 template <int T>
 __global__ void tile_kernel(const double *obs, int64_t n, const int32_t *perm, float4 *rloc,
-                            double4 *centre) {
+                            double4 *centre, double4 *tbox) {
     using BR = cub::BlockReduce<double, T>;
     __shared__ typename BR::TempStorage tmp;
-    __shared__ double s_c[3];
+    __shared__ double s_c[3], s_h[3];
     __shared__ float s_r;
     const int64_t si = (int64_t)blockIdx.x * T + threadIdx.x;
     const bool valid = si < n;
@@ -199,7 +199,10 @@ __global__ void tile_kernel(const double *obs, int64_t n, const int32_t *perm, f
         __syncthreads();
         const double mx = BR(tmp).Reduce(valid ? p[d] : -INFINITY, cub::Max());
         __syncthreads();
-        if (threadIdx.x == 0) s_c[d] = 0.5 * (mn + mx);
+        if (threadIdx.x == 0) {
+            s_c[d] = 0.5 * (mn + mx);
+            s_h[d] = 0.5 * (mx - mn);
+        }
     }
     __syncthreads();
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -213,7 +216,10 @@ __global__ void tile_kernel(const double *obs, int64_t n, const int32_t *perm, f
     const double rmax = BR(tmp).Reduce(rad, cub::Max());
     if (threadIdx.x == 0) s_r = (float)rmax;
     __syncthreads();
-    if (threadIdx.x == 0) centre[blockIdx.x] = make_double4(s_c[0], s_c[1], s_c[2], (double)s_r);
+    if (threadIdx.x == 0) {
+        centre[blockIdx.x] = make_double4(s_c[0], s_c[1], s_c[2], (double)s_r);
+        tbox[blockIdx.x] = make_double4(s_h[0], s_h[1], s_h[2], (double)s_r);
+    }
 }
 
 __global__ void iota_kernel(int32_t *v, int64_t n) {
@@ -259,9 +265,10 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
     if (n <= 0) return BF_OK;
     if (n > INT32_MAX) return fail(BF_EINVAL, "observer range too large (%lld)", (long long)n);
     float4 *rloc;
-    double4 *cen;
+    double4 *cen, *box;
     BF_TRY(c->get(B_RLOC, n, &rloc));
     BF_TRY(c->get(B_CENTRE, out->n_tiles, &cen));
+    BF_TRY(c->get(B_TBOX, out->n_tiles, &box));
     const int32_t *perm;
     if (presorted) {
         int32_t *id;
@@ -273,9 +280,9 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
         BF_TRY(morton_order(c, obs, n, st, &perm));
     }
     if (T == 512)
-        tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm, rloc, cen);
+        tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm, rloc, cen, box);
     else if (T == 256)
-        tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm, rloc, cen);
+        tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm, rloc, cen, box);
     else
         return fail(BF_EINVAL, "unsupported tile size %d", T);
     note_launch();
@@ -283,6 +290,7 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
     out->perm = perm;
     out->rloc = rloc;
     out->centre = cen;
+    out->tbox = box;
     return BF_OK;
 }
 
@@ -309,7 +317,7 @@ int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st) {
     BF_TRY(c->get(B_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
     double wmin = INFINITY;
     for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
-    BF_TRY(launch_worklist(a, t.centre, t.n_tiles, wmin, bits, tbits, st));
+    BF_TRY(launch_worklist(a, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, st));
     t.wl_bits = bits;
     t.wl_tight = tbits;
     t.wl_words = n_words;
@@ -696,8 +704,9 @@ int bf_tile_size(void) { return gbs_fp32_tile(); }
 int bf_worklist(const double *seg_origin, const double *seg_dir, const double *seg_len,
                 const double *seg_s0, const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
                 const double *obs, int64_t n_obs, const double *omegas, int64_t nf, double c,
-                double width_b, int use_cutoff, int32_t *perm, double *centre, uint32_t *bits,
-                uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out, int device) {
+                double width_b, int use_cutoff, int32_t *perm, double *centre, double *tile_box,
+                uint32_t *bits, uint32_t *tight_bits, int64_t n_tiles_cap, int64_t *n_tiles_out,
+                int device) {
     if (max_seg < 1 || n_beams < 1 || n_obs < 1 || nf < 1 || nf > BF_MAXF)
         return fail(BF_EINVAL, "bad sizes");
     const int64_t T = gbs_fp32_tile(), n_tiles = (n_obs + T - 1) / T;
@@ -746,6 +755,7 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     const auto D2H = cudaMemcpyDeviceToHost;
     BF_TRY_CUDA(cudaMemcpyAsync(perm, t.perm, 4 * n_obs, D2H, st));
     BF_TRY_CUDA(cudaMemcpyAsync(centre, t.centre, 32 * n_tiles, D2H, st));
+    if (tile_box) BF_TRY_CUDA(cudaMemcpyAsync(tile_box, t.tbox, 32 * n_tiles, D2H, st));
     BF_TRY_CUDA(cudaMemcpyAsync(bits, t.wl_bits, 4 * n_tiles * n_words, D2H, st));
     if (tight_bits)
         BF_TRY_CUDA(cudaMemcpyAsync(tight_bits, t.wl_tight, 4 * n_tiles * n_words, D2H, st));

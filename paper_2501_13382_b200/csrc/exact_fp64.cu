@@ -397,9 +397,28 @@ struct WordRows {
     const double *ox, *oy, *oz, *dx, *dy, *dz, *s0, *len;
 };
 
+// Tight cut: qn - min(hu/qn, rt) > sqrt(r2) (1 + 1e-6) + 1e-6 with qn = sqrt(q2), in
+// fp64 exactly as the C restatement, after an fp32 screen (relative margin 1e-4).
+__device__ __forceinline__ bool tight_cut(double q2, double hu, double rt, double r2) {
+    const float qf = sqrtf((float)q2);
+    const float rnf = qf > 0.f ? fminf((float)hu / qf, (float)rt) : (float)rt;
+    const float lhs = qf - rnf, rhs = sqrtf((float)r2) * 1.000001f + 1e-6f;
+    const float tol = 1e-4f * (qf + rnf + rhs) + 1e-6f;
+    if (lhs > rhs + tol) return true;
+    if (lhs < rhs - tol) return false;
+    const double qn = sqrt(q2);
+    double rn = rt;
+    if (qn > 0.0) {
+        rn = hu / qn;
+        rn = rn < rt ? rn : rt;
+    }
+    return qn - rn > sqrt(r2) * (1.0 + 1e-6) + 1e-6;
+}
+
 __device__ __forceinline__ unsigned beam_dead_for_tile(const WordRows &w, int jb, int ns,
                                                        double width_b, double cx, double cy,
-                                                       double cz, double rt, double rscale) {
+                                                       double cz, double rt, double hx, double hy,
+                                                       double hz, double rscale) {
     bool loose = true, tight = true;
     for (int k = 0; k < ns && tight; ++k) {
         const int i = 32 * k + jb;
@@ -410,14 +429,18 @@ __device__ __forceinline__ unsigned beam_dead_for_tile(const WordRows &w, int jb
         const double q2 = ux * ux + uy * uy + uz * uz;
         const double s0 = w.s0[i], len = w.len[i];
         const double se = s0 + len;
-        double reach = proj + rt;
+        // tight: the tile's bounding box bounds r.d and (q convex, subgradient u/|u| at
+        // the centre) the drop of q; each bound is also capped by the radius R_T
+        double rd = hx * fabs(dx) + hy * fabs(dy) + hz * fabs(dz);
+        rd = rd < rt ? rd : rt;
+        double reach = proj + rd;
         reach = reach < 0.0 ? 0.0 : (reach > len ? len : reach);
         const double sh = s0 + reach;
-        const bool behind = k == 0 && proj + rt < -1e-6;
-        if (!behind) {
+        if (!(k == 0 && proj + rt < -1e-6))
             loose = loose && cut_beyond(q2, rscale * (se * se + width_b * width_b), rt);
-            tight = tight && cut_beyond(q2, rscale * (sh * sh + width_b * width_b), rt);
-        }
+        if (!(k == 0 && proj + rd < -1e-6) && tight)
+            tight = tight_cut(q2, hx * fabs(ux) + hy * fabs(uy) + hz * fabs(uz), rt,
+                              rscale * (sh * sh + width_b * width_b));
     }
     return (loose ? 1u : 0u) | (tight ? 2u : 0u);
 }
@@ -425,8 +448,9 @@ __device__ __forceinline__ unsigned beam_dead_for_tile(const WordRows &w, int jb
 // One block per 32-beam word: the word's rows are read once into shared memory and
 // every warp sweeps a share of the tiles; bit j of (tile, word) = beam 32*word + j is a
 // candidate (bits: a9 bound, tbits: tight bound, tbits subset of bits).
-__global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t n_tiles,
-                                int64_t n_words, double rscale, uint32_t *bits, uint32_t *tbits) {
+__global__ void worklist_kernel(const GbsArgs a, const double4 *centre, const double4 *tbox,
+                                int64_t n_tiles, int64_t n_words, double rscale, uint32_t *bits,
+                                uint32_t *tbits) {
     extern __shared__ double wsm[];
     __shared__ int ns_s[32];
     const int S = (int)a.max_seg;
@@ -454,9 +478,11 @@ __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, int64_t 
     __syncthreads();
     const int ns = ns_s[lane];
     for (int64_t t = threadIdx.x >> 5; t < n_tiles; t += blockDim.x >> 5) {
-        const double4 c = centre[t];
+        const double4 c = centre[t], h = tbox[t];
         unsigned dead = 3u;
-        if (b < a.n_beams) dead = beam_dead_for_tile(w, lane, ns, a.width_b, c.x, c.y, c.z, c.w, rscale);
+        if (b < a.n_beams)
+            dead = beam_dead_for_tile(w, lane, ns, a.width_b, c.x, c.y, c.z, c.w, h.x, h.y, h.z,
+                                      rscale);
         const unsigned m = __ballot_sync(0xffffffffu, !(dead & 1u));
         const unsigned mt = __ballot_sync(0xffffffffu, !(dead & 2u));
         if (lane == 0) {
@@ -528,8 +554,8 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
     return BF_OK;
 }
 
-int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, double omega_min,
-                    uint32_t *bits, uint32_t *tbits, cudaStream_t st) {
+int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox, int64_t n_tiles,
+                    double omega_min, uint32_t *bits, uint32_t *tbits, cudaStream_t st) {
     if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
     const int64_t n_words = (a.n_beams + 31) / 32;
     // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
@@ -537,8 +563,8 @@ int launch_worklist(const GbsArgs &a, const double4 *centre, int64_t n_tiles, do
     const size_t smem = 8 * 32 * sizeof(double) * (size_t)a.max_seg;
     BF_TRY_CUDA(cudaFuncSetAttribute(worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    worklist_kernel<<<(unsigned)n_words, 256, smem, st>>>(a, centre, n_tiles, n_words, rscale,
-                                                          bits, tbits);
+    worklist_kernel<<<(unsigned)n_words, 256, smem, st>>>(a, centre, tbox, n_tiles, n_words,
+                                                          rscale, bits, tbits);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

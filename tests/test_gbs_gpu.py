@@ -290,6 +290,7 @@ def test_worklist_bitexact_vs_oracle(name, dense):
     nt = -(-n // T)
     perm = np.zeros(n, np.int32)
     centre = np.zeros((nt, 4))
+    box = np.zeros((nt, 4))
     bits = np.zeros((nt, -(-nb // 32)), np.uint32)
     tbits = np.zeros_like(bits)
     got = ctypes.c_int64(0)
@@ -306,6 +307,7 @@ def test_worklist_bitexact_vs_oracle(name, dense):
         p(b["n_segs"].astype(np.int32)), nb, int(b["max_seg"]), p(obs), n, p(b["omegas"]),
         b["omegas"].shape[0], float(b["c"]), -float(b["beam_param_im"]), int(use_cut),
         ctypes.c_void_p(perm.ctypes.data), ctypes.c_void_p(centre.ctypes.data),
+        ctypes.c_void_p(box.ctypes.data),
         ctypes.c_void_p(bits.ctypes.data), ctypes.c_void_p(tbits.ctypes.data), nt,
         ctypes.byref(got), 0))
     assert got.value == nt
@@ -316,7 +318,10 @@ def test_worklist_bitexact_vs_oracle(name, dense):
     assert np.array_equal(bits, ref)
     tref = oracle.worklist(b["seg_origin"], b["seg_dir"], b["seg_len"], b["seg_s0"],
                            b["n_segs"], b["max_seg"], centre, float(b["c"]),
-                           -float(b["beam_param_im"]), b["omegas"].min(), use_cut, tight=True)
+                           -float(b["beam_param_im"]), b["omegas"].min(), use_cut, tight=True,
+                           box=box)
+    # the boxes are the tiles' coordinate ranges about their centres
+    assert np.all(box[:, :3] >= 0) and np.all(box[:, :3] <= box[:, 3:4] * (1 + 1e-6) + 1e-9)
     assert np.array_equal(tbits, tref)
     assert not (tbits & ~bits).any()  # tight list is a subset of the a9 list
     if dense:

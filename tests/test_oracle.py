@@ -100,16 +100,19 @@ def test_worklist_is_sound(name, tight):
     # spatially compact 4x4 receiver blocks of the row-major grid
     tiles = [np.array([(j0 + dj) * n1 + i0 + di for dj in range(4) for di in range(4)])
              for j0 in range(0, 32, 4) for i0 in range(0, n1, 4)]
-    centre = []
+    centre, box = [], []
     for t in tiles:
         p = obs[t]
         c = 0.5 * (p.min(0) + p.max(0))
-        centre.append([*c, np.linalg.norm(p - c, axis=1).max()])
+        rt = np.linalg.norm(p - c, axis=1).max()
+        centre.append([*c, rt])
+        box.append([*(0.5 * (p.max(0) - p.min(0))), rt])
     centre = np.array(centre)
     om = b["omegas"]
     bits = oracle.worklist(b["seg_origin"], b["seg_dir"], b["seg_len"], b["seg_s0"],
                            b["n_segs"], b["max_seg"], centre, float(b["c"]),
-                           -float(b["beam_param_im"]), om.min(), True, tight=tight)
+                           -float(b["beam_param_im"]), om.min(), True, tight=tight,
+                           box=np.array(box))
     nb = b["n_segs"].shape[0]
     cand = np.unpackbits(bits.view(np.uint8), bitorder="little").reshape(len(tiles), -1)[:, :nb]
     assert 0 < cand.mean() < 1
