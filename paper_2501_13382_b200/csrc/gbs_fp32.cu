@@ -41,26 +41,8 @@ namespace {
 #ifndef BF_MINB
 #define BF_MINB 4
 #endif
-#ifndef BF_STAGE_BATCH
-#define BF_STAGE_BATCH 0
-#endif
-#ifndef BF_PREFETCH
-#define BF_PREFETCH 0
-#endif
-#ifndef BF_PREFETCH_EXACT
-#define BF_PREFETCH_EXACT 0
-#endif
-#ifndef BF_EXACT_INLINE
-#define BF_EXACT_INLINE 1
-#endif
-#ifndef BF_ABLM
-#define BF_ABLM 0
-#endif
 #ifndef BF_ABL
 #define BF_ABL 0
-#endif
-#ifndef BF_JUNC
-#define BF_JUNC 1
 #endif
 #ifndef BF_HIST
 #define BF_HIST 0
@@ -423,12 +405,7 @@ struct ExactPick {
 // beam (kernels.py:320-348 with the reference's fp64 operations): only segments
 // whose fp32 distance is within the tie bound of the fp32 best can win.  Out of
 // line: one copy of the code serves every call site of the multi path.
-#if BF_EXACT_INLINE
-__device__ __forceinline__
-#else
-__device__ __noinline__
-#endif
-ExactPick exact_pick(const double4 *__restrict__ p0,
+__device__ __forceinline__ ExactPick exact_pick(const double4 *__restrict__ p0,
                                              const double4 *__restrict__ p1, int64_t row0,
                                              const float4 *geo0, const float4 *geo1,
                                              unsigned surv, int kf, float rx, float ry, float rz,
@@ -706,19 +683,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             word = classify<NF>(S, K, r0, nsb, w.pbox[p], D);
 #endif
             S.desc[lane] = make_int4(S.gbeam[lane], (int)word, r0, __float_as_int(D));
-#if BF_PREFETCH_EXACT
-            // wedge / several-candidate items read fp64 rows later: start the transfers
-            const unsigned mw = word & ~(BEHIND_CHECK | WEDGE);
-            if (word && (mw & (mw - 1))) {
-                const int64_t g0 = (int64_t)S.gbeam[lane] * a.max_seg;
-#pragma unroll 1
-                for (unsigned m = mw; m; m &= m - 1) {
-                    const int k = __ffs(m) - 1;
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g0 + k));
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g0 + k));
-                }
-            }
-#endif
         }
         const unsigned live = __ballot_sync(0xffffffffu, word != 0);
         {
@@ -857,9 +821,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         best[j] = fminf(best[j], d2);
                     }
                 }
-#if BF_ABLM == 1
-                if (best[0] >= 0.f) continue;  // ablation: scan only
-#endif
                 // two adjacent candidates: ties at the junction go to the wedge decision
                 const bool pair = surv == (3u << ka);
                 const float jtol =
@@ -907,9 +868,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         bj[j][f] = anchor_phase(K.kappa[f], proj, dl, len, S.anc[f][r0 + k]);
                     lvm |= 1u << j;
                 }
-#if BF_ABLM == 2
-                if (best[0] >= 0.f) continue;  // ablation: scan + decision only
-#endif
                 }
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
@@ -941,11 +899,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         lvm |= 1u << j;
                     }
                 }
-#if BF_ABLM != 3
                 if (__any_sync(0xffffffffu, pend != 0))
                     exact_pending<NF>(a, K, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
                                       Db, lane, sj, q2j, Aj, bj, lvm, ties, w);
-#endif
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
