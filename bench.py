@@ -178,9 +178,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BF_BENCH_SHARE_DEVICE=1: every rank on cuda:0 with gloo (functional check of the
+    # multi-rank path on a one-GPU box; its timings are not a scaling measurement)
+    share = os.environ.get("BF_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if share else dev  # where the max-over-ranks reduce runs
     torch.cuda.set_device(dev)
     cfg = CONFIGS[args.config]
     sc, src, launch, tcfg, c, obs_np = make_inputs(cfg)
@@ -244,7 +253,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = float(np.mean(ms_steps))
-    t = torch.tensor([ms, float(np.mean(kern_ms))], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, float(np.mean(kern_ms))], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, kern_max = float(t[0]), float(t[1])
@@ -276,7 +285,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         e2e_step()
         e2e_t.append(time.perf_counter() - t0)
-    tt = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=dev)
+    tt = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s = float(tt[0])

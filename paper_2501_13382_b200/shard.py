@@ -83,8 +83,11 @@ def gather_field(acc, evals, order, rank: int, world_size: int, n_total: int, gr
     n_loc = acc.shape[0]
     pay[:n_loc, :2 * F] = torch.view_as_real(acc).reshape(n_loc, 2 * F)
     pay[:n_loc, 2 * F] = evals.view(torch.float64)
+    if pay.is_cuda and dist.get_backend(group) == "gloo":  # gloo gathers host tensors
+        pay = pay.cpu()
     bufs = [torch.empty_like(pay) for _ in range(world_size)]
     dist.all_gather(bufs, pay, group=group)
+    bufs = [b.to(acc.device) for b in bufs]
     if rank != 0:
         return None, None
     acc_full = torch.zeros((n_total, F), dtype=torch.complex128, device=acc.device)
