@@ -330,7 +330,9 @@ def test_worklist_bitexact_vs_oracle(name, dense):
 
 @pytest.mark.parametrize("freqs,src,corner", [((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0)),
                                               ((63.0, 250.0, 1000.0), (0.0, 20.0, 2.0),
-                                               (-30.0, 5.0))])
+                                               (-30.0, 5.0)),
+                                              ((50.0, 63.0, 80.0, 100.0, 125.0, 160.0, 200.0,
+                                                250.0), (20.0, 0.0, 2.0), (10.0, -5.0))])
 def test_fp32_dense_city_vs_oracle(freqs, src, corner, threads):
     """Config-3 receiver density (0.25 m) around street corners of the city scene: every
     fp32 path (single survivor, corner wedge, several candidates with junction and
@@ -374,3 +376,18 @@ def test_fp32_dense_city_vs_oracle(freqs, src, corner, threads):
     # the scene exercises the exact-decision paths
     assert st["patch_beams"]["wedge"] > 0 and st["patch_beams"]["multi"] > 0
     assert st["tie_pairs"] > 0
+
+
+def test_max_seg_limit():
+    """The fp32 path packs survivor masks with two flag bits: max_seg <= 30."""
+    from paper_2501_13382_b200 import kernels
+    b = load_case("cfg1_open_plane")
+    nb, S = b["n_segs"].shape[0], 31
+    pad = lambda a, w: np.zeros((nb * S,) + ((w,) if w else ()))  # noqa: E731
+    args = [pad(0, 3), pad(0, 3), pad(0, 3), pad(0, 3), pad(0, 0), pad(0, 0), pad(0, 0),
+            np.ones(nb, np.int32), S, b["weights"], b["obs"][:4], b["omegas"], float(b["c"]),
+            -float(b["beam_param_im"]), 1.0, True]
+    acc = np.zeros((4, 1), np.complex128)
+    ev = np.zeros(4, np.int64)
+    with pytest.raises(ValueError):
+        kernels.gbs_accumulate(*args, acc, ev, 0, 4, 0, nb, precision="fp32")
