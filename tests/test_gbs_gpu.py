@@ -391,3 +391,32 @@ def test_max_seg_limit():
     ev = np.zeros(4, np.int64)
     with pytest.raises(ValueError):
         kernels.gbs_accumulate(*args, acc, ev, 0, 4, 0, nb, precision="fp32")
+
+
+@pytest.mark.parametrize("kind", ["one", "coincident", "vertical", "on_source"])
+def test_fp32_degenerate_receiver_sets(kind):
+    """Patch geometry corner cases of the fp32 path (zero-extent boxes, a lone receiver,
+    non-planar patches, receivers at the source where segment 0's launch plane, ties and
+    q = 0 meet) against the oracle."""
+    from paper_2501_13382_b200 import kernels
+    b = load_case("city_street")
+    src = np.asarray(b["seg_origin"][0], float)  # segment 0 of beam 0 starts at the source
+    if kind == "one":
+        obs = np.array([[3.0, -4.0, 1.8]])
+    elif kind == "coincident":
+        obs = np.tile([[5.0, 1.0, 1.8]], (130, 1))
+    elif kind == "vertical":
+        obs = np.stack([np.full(200, 12.0), np.full(200, 3.0), np.linspace(0.1, 30.0, 200)], 1)
+    else:
+        obs = src[None, :] + np.linspace(-1e-3, 1e-3, 64)[:, None] * np.array([1.0, 0.5, 0.25])
+    obs = np.ascontiguousarray(obs)
+    nb = b["n_segs"].shape[0]
+    acc = np.zeros((obs.shape[0], 1), np.complex128)
+    ev = np.zeros(obs.shape[0], np.int64)
+    kernels.gbs_accumulate(*gbs_args(b, obs), acc, ev, 0, obs.shape[0], 0, nb, precision="fp32")
+    ref = np.zeros_like(acc)
+    rev = np.zeros_like(ev)
+    oracle.gbs_accumulate(*gbs_args(b, obs), ref, rev, 0, obs.shape[0], 0, nb)
+    assert np.all(np.isfinite(acc))
+    assert rel_l2(acc, ref) <= FP32_L2
+    assert abs(int(ev.sum()) - int(rev.sum())) <= 1e-4 * int(rev.sum()) + 10
