@@ -305,6 +305,12 @@ def run_ours(args):
         flop_a9, _ = flop_model(float(st["candidate_pair_segs"]), p_nb, ev_sum, nf)
         flop_live, _ = flop_model(float(st["live_pair_segs"]), p_nb, ev_sum, nf)
         kernel_s = kern_max / 1e3
+        if prec == "fp64":
+            # oracle mode: dense kernel, no work list or kernel statistics -> FLOP model
+            # over all pairs (segment scan + evaluations), timed by the step
+            flop = flop_a9 = flop_live = 19.0 * n_total * sum_segs + 22.0 * ev_sum
+            mufu = 3.0 * ev_sum
+            kernel_s = ms_max / 1e3
         traffic = None  # DRAM bytes of the summation kernel from the committed ncu capture
         for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_*_traffic.json"))):
             with open(tf) as fh:
@@ -339,7 +345,10 @@ def run_ours(args):
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, committed "
                                          "profile of this config)" if traffic else None,
                          "peak_source": "measured FFMA stream (bf_probe_peaks), this GPU",
-                         "kernel": "gbs_fp32_kernel", "kernel_ms": kern_max,
+                         "kernel": "gbs_fp32_kernel" if prec == "fp32" else
+                                   "gbs_fp64_kernel (oracle mode, dense; FP32 peak as a "
+                                   "common yardstick)",
+                         "kernel_ms": kernel_s * 1e3,
                          "flop_per_launch": flop, "mufu_per_launch": mufu,
                          "mufu_tops": mufu / kernel_s / 1e12,
                          "mufu_peak_tops": peaks["mufu_tops"],
