@@ -364,7 +364,7 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&
 // distances (kernels.py:332-340) are distances to the reflection point and the
 // reference's choice is decided by fp64 rounding, reproduced here op for op.
 #if BF_HIST
-__device__ unsigned long long g_hist[4];  // debug: junction, pending, pending rounds, non-pair
+__device__ unsigned long long g_hist[4];  // debug: exact re-decision rounds (warp-level) in [2]
 #endif
 struct Junction {
     double ox, oy, oz;  // o_k
@@ -1203,8 +1203,7 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
         unsigned long long h[4];
         cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        fprintf(stderr, "bf hist: multi junction %llu pending %llu (non-pair %llu) rounds %llu\n",
-                h[0], h[1], h[3], h[2]);
+        fprintf(stderr, "bf hist: exact re-decision rounds %llu\n", h[2]);
     }
 #endif
     fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, st>>>(t, w, a.nf, a.acc, a.evals);
