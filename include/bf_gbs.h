@@ -11,18 +11,18 @@
  *
  *   bf_gbs_accumulate        kernels.gbs_accumulate           kernels.py:352-399
  *                            (called by parallel.run_pipeline.gbs_range,
- *                             parallel.py:576-583, and gbs.sum_at_observer,
+ *                             parallel.py:320-327, and gbs.sum_at_observer,
  *                             gbs.py:196-201)
  *   bf_gbs_accumulate_dev    same operator, device-resident buffers (the
  *                            engine path used by run_pipeline on the GPU)
  *   bf_nearest_on_segments   kernels.nearest_on_segments      kernels.py:304-349
  *   bf_trace_range_dev       kernels.trace_range/trace_one    kernels.py:143-301
  *                            (+ bvh_nearest semantics kernels.py:54-116)
- *   bf_field_finalize_dev    parallel.py:599-600 (pressure = calibration*acc)
+ *   bf_field_finalize_dev    parallel.py:343-344 (pressure = calibration*acc)
  *                            + gbs.spl                        gbs.py:39-46
- *   bf_plan_chunks           parallel.plan_chunks             parallel.py:347-361
+ *   bf_plan_chunks           parallel.plan_chunks             parallel.py:91-105
  *   bf_tile_order_dev        parallel.block_partition/WorkerPool.flat observer split
- *                            (parallel.py:364-396), re-cut as spatial receiver tiles
+ *                            (parallel.py:108-140), re-cut as spatial receiver tiles
  *
  * Array layouts are exactly the reference PathBundle's (beamtrace.py:218-288):
  * seg_origin/seg_dir/seg_e1/seg_e2 are (n_beams*max_seg, 3) C-contiguous fp64,
@@ -188,13 +188,13 @@ int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
                        int64_t hi, int64_t row_base, int device, void *stream);
 
 /*
- * pressure = calibration * acc (parallel.py:599) and spl = 20 log10(|p|/2e-5),
+ * pressure = calibration * acc (parallel.py:343) and spl = 20 log10(|p|/2e-5),
  * -inf for |p| == 0 (gbs.py:39-46), over n complex values on the device.
  */
 int bf_field_finalize_dev(const double *acc, int64_t n, double calibration,
                           double *pressure, double *spl, int device, void *stream);
 
-/* parallel.plan_chunks (parallel.py:347-361): greedy maximal chunks.
+/* parallel.plan_chunks (parallel.py:91-105): greedy maximal chunks.
  * Writes up to max_chunks sizes, returns the count in *n_chunks. */
 int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_bytes,
                    int64_t *chunk_sizes, int64_t max_chunks, int64_t *n_chunks);

@@ -11,7 +11,7 @@
 //   trace_kernel      kernels.trace_one/range     kernels.py:143-301 (nearest hit of
 //                     bvh_nearest, kernels.py:54-116, by exhaustive search; same
 //                     (t, triangle index) lexicographic minimum)
-//   finalize_kernel   parallel.py:599-600 + gbs.spl (gbs.py:39-46)
+//   finalize_kernel   parallel.py:343-344 + gbs.spl (gbs.py:39-46)
 #include <math.h>
 
 #include "common.cuh"

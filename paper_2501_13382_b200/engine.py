@@ -1,7 +1,7 @@
 """Device-resident GBS engine: HBM buffers owned by torch, compute in libbf_gbs.
 
 This is the layer ``parallel.run_pipeline`` drives (the reference's per-chunk
-trace -> sum loop, parallel.py:553-594, moved onto the B200):
+trace -> sum loop, parallel.py:297-338, moved onto the B200):
 
 * :class:`DeviceScene` -- triangle soup in HBM for the tracer;
 * :func:`trace_device_rows` -- sm_100a tracer into a padded device bundle
@@ -11,7 +11,7 @@ trace -> sum loop, parallel.py:553-594, moved onto the B200):
 * :func:`accumulate` -- ``bf_gbs_accumulate_dev`` on device buffers;
 * :class:`ChunkStreamer` -- double-buffered pinned host -> HBM streaming of
   beam chunks for ray sets larger than one device pass (plan_chunks semantics,
-  parallel.py:347-361), copy of chunk i+1 overlapping the summation of chunk i.
+  parallel.py:91-105), copy of chunk i+1 overlapping the summation of chunk i.
 
 PyTorch is used for allocation, streams and events only.
 """
@@ -196,7 +196,7 @@ def accumulate(bundle: DeviceBundle, obs, omegas, width_b, use_cutoff, acc, eval
 
 
 def finalize(acc, calibration, stream=None):
-    """pressure = calibration*acc and SPL on the device (parallel.py:599, gbs.py:39-46)."""
+    """pressure = calibration*acc and SPL on the device (parallel.py:343, gbs.py:39-46)."""
     torch = _torch()
     lib = _lib.load()
     pressure = torch.empty_like(acc)
@@ -210,7 +210,7 @@ def finalize(acc, calibration, stream=None):
 class ChunkStreamer:
     """Double-buffered pinned-host -> HBM streaming of beam chunks.
 
-    The reference sizes chunks with plan_chunks (parallel.py:347-361) and runs
+    The reference sizes chunks with plan_chunks (parallel.py:91-105) and runs
     trace+sum per chunk.  Here a host-resident PathBundle larger than one device
     pass is cut into beam chunks; chunk i+1 is copied on a copy stream (pinned
     source, cudaMemcpyAsync) while chunk i is summed on the compute stream, with

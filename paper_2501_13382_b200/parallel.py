@@ -87,7 +87,7 @@ class PhaseTimings:
 
 
 def plan_chunks(total_rays: int, memory_budget: int, per_ray_bytes: int) -> ChunkPlan:
-    """Greedy maximal chunks under the budget (parallel.py:347-361), via bf_plan_chunks."""
+    """Greedy maximal chunks under the budget (parallel.py:91-105), via bf_plan_chunks."""
     import ctypes
     if total_rays < 1:
         raise ValueError("need at least one ray to plan chunks")
@@ -106,7 +106,7 @@ def plan_chunks(total_rays: int, memory_budget: int, per_ray_bytes: int) -> Chun
 
 
 def block_partition(n: int, workers: int):
-    """Contiguous near-even blocks of [0, n) (parallel.py:364-374)."""
+    """Contiguous near-even blocks of [0, n) (parallel.py:108-118)."""
     workers = max(1, workers)
     base, rem = divmod(n, workers)
     out, lo = [], 0
@@ -118,7 +118,7 @@ def block_partition(n: int, workers: int):
 
 
 def measure(run, baseline: PhaseTimings | None = None) -> PhaseTimings:
-    """Time a pipeline-style callable (parallel.py:484-502)."""
+    """Time a pipeline-style callable (parallel.py:228-246)."""
     t0 = time.perf_counter()
     out = run()
     total = time.perf_counter() - t0
@@ -135,7 +135,7 @@ def measure(run, baseline: PhaseTimings | None = None) -> PhaseTimings:
 
 def measure_per_ray_bytes(scene, source: SourceSpec, launch, cfg: TraceConfig,
                           atmosphere: Atmosphere, device=None) -> int:
-    """Ray-0 estimate x 1.5 with 120 B/row, as the reference (parallel.py:505-513).
+    """Ray-0 estimate x 1.5 with 120 B/row, as the reference (parallel.py:249-257).
 
     (Reference defect kept for drop-in chunk plans: a padded device row costs
     (r_max+1) x 120 B regardless of ray 0.)
@@ -160,7 +160,7 @@ def run_pipeline(scene, source: SourceSpec, grid: LaunchGrid, cfg: TraceConfig,
                  observers: ObserverSet, plan: ExecPlan, atmosphere: Atmosphere,
                  calibration: float | None = None, use_cutoff: bool = True, *,
                  precision: str | None = None, device=None, group=None):
-    """Trace-then-sum pipeline on the GPU, chunked to the plan's budget (parallel.py:516-607).
+    """Trace-then-sum pipeline on the GPU, chunked to the plan's budget (parallel.py:260-351).
 
     Returns (FieldResult, PhaseTimings) like the reference.  Under
     torch.distributed (or with ``group``) every rank sums its receiver tiles
@@ -243,7 +243,7 @@ def run_pipeline(scene, source: SourceSpec, grid: LaunchGrid, cfg: TraceConfig,
 
 def pipeline_calibration(source: SourceSpec, grid: LaunchGrid, cfg: TraceConfig,
                          atmosphere: Atmosphere, device=None) -> float:
-    """Free-field calibration traced on an empty scene (parallel.py:610-624)."""
+    """Free-field calibration traced on an empty scene (parallel.py:354-368)."""
     import torch
 
     from . import engine
