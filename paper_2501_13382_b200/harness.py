@@ -4,7 +4,7 @@ Reference: /root/reference/pkg/src/beamfield/harness.py.  Kept names, files and 
 ``write_field_csv`` (harness.py:197-208) writes the same CSV -- header
 ``x,y,z,freq_hz,re_p,im_p,spl_db``, observer-major rows, numbers as ``format(x,
 ".17g")`` (harness.py:39-40) -- through the native multithreaded formatter
-``bf_write_field_csv``; ``emit_heatmap`` (harness.py:218-249) writes the same 8-bit
+``bf_write_field_csv``; ``emit_heatmap`` (harness.py:224-255) writes the same 8-bit
 grayscale SPL raster and ``.txt`` sidecar.
 """
 from __future__ import annotations
@@ -39,7 +39,7 @@ def write_field_csv(path, observers, freqs, field, threads: int = 0) -> None:
 def emit_heatmap(spl_values, grid_spec, out_path) -> dict:
     """8-bit grayscale raster of the SPL grid (row-major n2 x n1): [min, max] of the
     finite values mapped linearly onto [0, 255] (rounded half to even), non-finite
-    (null) points 0; sidecar ``<out_path>.txt`` records the scale (harness.py:218-249)."""
+    (null) points 0; sidecar ``<out_path>.txt`` records the scale (harness.py:224-255)."""
     from PIL import Image
 
     n1, n2 = int(grid_spec.n1), int(grid_spec.n2)
