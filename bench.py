@@ -47,6 +47,12 @@ CONFIGS = {
                  scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0), src=(20.0, 0.0, 2.0),
                  freqs=(125.0,), im_b=-10.0, n_theta=500, n_phi=1000, n_steps=5000, r_max=8,
                  grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
+    # config-3 variant with the five-frequency set of the survey (63-1000 Hz)
+    "cfg3s_f5": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers, F=5 "
+                          "(63-1000 Hz variant)", scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0),
+                     src=(20.0, 0.0, 2.0), freqs=(63.0, 125.0, 250.0, 500.0, 1000.0), im_b=-10.0,
+                     n_theta=100, n_phi=200, n_steps=5000, r_max=8,
+                     grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
     # profiling variant of config 3: same scene/receivers, 20k rays (ncu replays stay short)
     "cfg3s": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers (cfg3 profile "
                        "variant)", scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0),

@@ -138,7 +138,10 @@ struct WarpSmem {
     short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
     int4 desc[CB];           // chunk beam -> (beam, survivor word, first row, D bits)
-    double acc[PATCH][NF][2];
+    // fp64 accumulators of the unit (NF == 1); with several frequencies they live in
+    // the unit's slice of the global partial buffer instead (shared memory is the
+    // occupancy limit there)
+    double acc[NF == 1 ? PATCH : 1][NF][2];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
     unsigned long long cnt[8];  // statistics: ties, non-behind, culled/single/wedge/multi
@@ -149,6 +152,23 @@ struct WarpSmem {
 // sqrt(c) (s + i b)/m2 exp(-g b) exp(i(omega s/c + g s)), contribution
 // i omega/(2 pi c) w_b field.  `base[f]` is the fp64-anchored axial phase
 // omega s/(2 pi c) reduced to turns.
+// One frequency of a pair's contribution (the several-frequency tail): gq = q^2/m2,
+// ainv = A/m2 shared across frequencies.
+__device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float s, float gq,
+                                          float ainv, float base, float &pre, float &pim,
+                                          unsigned &ev, int shift, bool live) {
+    const float turns = fmaf(gq * s, K.hk2pi[f], base);
+    const float ph = turns * 6.283185307179586f;
+    const float sn = sin_approx(ph), cs = cos_approx(ph);
+    const float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]) * K.omrel[f];
+    const float as = amp * s, ab = amp * K.b;
+    if (live) {  // i * amp * (s + i b) * (cos + i sin)
+        pre = fmaf(-as, sn, fmaf(-ab, cs, pre));
+        pim = fmaf(as, cs, fmaf(-ab, sn, pim));
+        ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
+    }
+}
+
 template <int NF>
 __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
                                           float m2, float A, const float *base,
@@ -614,8 +634,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         ry[j] = rl.y;
         rz[j] = rl.z;
         rr[j] = rl.w;
+        if (NF == 1) {
+            S.acc[R * lane + j][0][0] = S.acc[R * lane + j][0][1] = 0.0;
+        } else if (j < nvalid) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) S.acc[R * lane + j][f][0] = S.acc[R * lane + j][f][1] = 0.0;
+            for (int f = 0; f < NF; ++f)
+                w.part[((q * w.n_pad + sb + j) * NF) + f] = make_double2(0.0, 0.0);
+        }
         S.evc[R * lane + j] = 0;
         if (j < nvalid) {
             const int64_t oi = perm[j];
@@ -914,6 +939,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 m2j[j] = fmaf(sj[j], sj[j], K.b2);
                 if (NF == 1 && a.use_cutoff && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);
             }
+            if constexpr (NF == 1) {
             // receivers evaluated in groups of EVG (one branch, EVG independent chains)
 #pragma unroll
             for (int g = 0; g < R; g += EVG)
@@ -924,16 +950,48 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                                       pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
                                       EVG == 1 || ((lvm >> j) & 1u));
                 }
+            } else {
+            // several frequencies: the cutoff grows with omega, so each frequency is
+            // evaluated only if some receiver of the warp is live for it
+            float gq[R], ainv[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const float inv = rcp_approx(m2j[j]);
+                gq[j] = q2j[j] * inv;
+                ainv[j] = Aj[j] * inv;
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                unsigned lf = 0;
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    if (((lvm >> j) & 1u) && !(a.use_cutoff && q2j[j] * K.cutk[f] > m2j[j]))
+                        lf |= 1u << j;  // ex_re < -36 (kernels.py:384)
+                if (!__any_sync(0xffffffffu, lf != 0)) continue;
+#pragma unroll
+                for (int j = 0; j < R; ++j)
+                    eval_freq(K, f, sj[j], gq[j], ainv[j], bj[j][f], pre[j][f], pim[j][f],
+                              evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+            }
+            }
         }
         // flush fp32 partial sums into the fp64 accumulators
 #pragma unroll
-        for (int j = 0; j < R; ++j)
+        for (int j = 0; j < R; ++j) {
+            if (NF == 1) {
+                S.acc[R * lane + j][0][0] += (double)pre[j][0];
+                S.acc[R * lane + j][0][1] += (double)pim[j][0];
+            } else if (j < nvalid) {
+                double2 *pp = w.part + (q * w.n_pad + sb + j) * NF;
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-                S.acc[R * lane + j][f][0] += (double)pre[j][f];
-                S.acc[R * lane + j][f][1] += (double)pim[j][f];
-                pre[j][f] = pim[j][f] = 0.f;
+                for (int f = 0; f < NF; ++f) {
+                    const double2 v = pp[f];
+                    pp[f] = make_double2(v.x + (double)pre[j][f], v.y + (double)pim[j][f]);
+                }
             }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < R; ++j) S.evc[R * lane + j] += (evp[j >> 1] >> (16 * (j & 1))) & 0xffffu;
 #pragma unroll
@@ -946,10 +1004,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     for (int j = 0; j < R; ++j) {
         if (j >= nvalid) continue;
         const int64_t slot = q * w.n_pad + sb + j;
-#pragma unroll
-        for (int f = 0; f < NF; ++f)
-            w.part[slot * NF + f] =
-                make_double2(S.acc[R * lane + j][f][0], S.acc[R * lane + j][f][1]);
+        if (NF == 1) w.part[slot] = make_double2(S.acc[R * lane + j][0][0], S.acc[R * lane + j][0][1]);
         w.part_ev[slot] = S.evc[R * lane + j];
     }
     ties = __reduce_add_sync(0xffffffffu, ties);
@@ -961,7 +1016,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 }
 
 template <int NF>
-__global__ void __launch_bounds__(THREADS, (NF <= 2 ? BF_MINB : 2))
+__global__ void __launch_bounds__(THREADS, (NF == 1 ? BF_MINB : NF <= 5 ? 3 : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w, const Fp32Consts K,
                     GbsStats *stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
