@@ -960,18 +960,34 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 gq[j] = q2j[j] * inv;
                 ainv[j] = Aj[j] * inv;
             }
-#pragma unroll
+            // one copy of the code per receiver: frequency f is always in slot 0 of the
+            // per-frequency arrays, which rotate by one slot per iteration
+#pragma unroll 1
             for (int f = 0; f < NF; ++f) {
                 unsigned lf = 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j)
                     if (((lvm >> j) & 1u) && !(a.use_cutoff && q2j[j] * K.cutk[f] > m2j[j]))
                         lf |= 1u << j;  // ex_re < -36 (kernels.py:384)
-                if (!__any_sync(0xffffffffu, lf != 0)) continue;
+                if (__any_sync(0xffffffffu, lf != 0)) {
 #pragma unroll
-                for (int j = 0; j < R; ++j)
-                    eval_freq(K, f, sj[j], gq[j], ainv[j], bj[j][f], pre[j][f], pim[j][f],
-                              evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                    for (int j = 0; j < R; ++j)
+                        eval_freq(K, f, sj[j], gq[j], ainv[j], bj[j][0], pre[j][0], pim[j][0],
+                                  evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const float p0 = pre[j][0], i0 = pim[j][0], b0 = bj[j][0];
+#pragma unroll
+                    for (int g = 0; g + 1 < NF; ++g) {
+                        pre[j][g] = pre[j][g + 1];
+                        pim[j][g] = pim[j][g + 1];
+                        bj[j][g] = bj[j][g + 1];
+                    }
+                    pre[j][NF - 1] = p0;
+                    pim[j][NF - 1] = i0;
+                    bj[j][NF - 1] = b0;
+                }
             }
             }
         }
