@@ -260,3 +260,31 @@ def pipeline_calibration(source: SourceSpec, grid: LaunchGrid, cfg: TraceConfig,
     torch.cuda.synchronize(dev)
     bundle = out["bundle"].to_host()
     return calibrate_phi(bundle, atmosphere, source, device=dev.index)
+
+
+def run_snapshots(scene, sources, grid: LaunchGrid, cfg: TraceConfig, observers: ObserverSet,
+                  plan: ExecPlan, atmosphere: Atmosphere, calibration: float | None = None,
+                  use_cutoff: bool = True, **kw):
+    """Moving-source noise map: one run_pipeline field per source
+    position (snapshot) and the energy-mean SPL over the snapshots,
+    10 log10(mean_k |p_k|^2 / p_ref^2) per receiver and frequency.  Moving sources are a
+    reference non-goal; each snapshot is the reference's static problem.
+
+    Returns (fields, spl_energy_mean, timings) on rank 0; fields of other ranks are None.
+    """
+    from .gbs import P_REF
+    fields, timings = [], []
+    energy = None
+    for src in sources:
+        res, t = run_pipeline(scene, src, grid, cfg, observers, plan, atmosphere,
+                              calibration=calibration, use_cutoff=use_cutoff, **kw)
+        fields.append(res)
+        timings.append(t)
+        if res is not None:
+            e = np.abs(res.pressure) ** 2
+            energy = e if energy is None else energy + e
+    spl_mean = None
+    if energy is not None:
+        with np.errstate(divide="ignore"):
+            spl_mean = 10.0 * np.log10(energy / len(sources) / P_REF ** 2)
+    return fields, spl_mean, timings

@@ -420,3 +420,25 @@ def test_fp32_degenerate_receiver_sets(kind):
     assert np.all(np.isfinite(acc))
     assert rel_l2(acc, ref) <= FP32_L2
     assert abs(int(ev.sum()) - int(rev.sum())) <= 1e-4 * int(rev.sum()) + 10
+
+
+def test_run_snapshots_energy_mean():
+    """run_snapshots == one run_pipeline per source; energy-mean SPL of the fields."""
+    from paper_2501_13382_b200 import (Atmosphere, ExecPlan, LaunchGrid, ObserverSet,
+                                       SourceSpec, TraceConfig, make_city, parallel)
+    from paper_2501_13382_b200.gbs import P_REF
+    sc = make_city(5, 10, 40.0, 20.0, 300.0)
+    srcs = [SourceSpec(position=np.array([20.0 + 5 * k, 0.0, 2.0]), frequencies=(125.0,),
+                       beam_param_im=-10.0) for k in range(3)]
+    x = np.arange(40) * 0.5 - 10.0
+    X, Y = np.meshgrid(x, x, indexing="xy")
+    pts = np.stack([X.ravel(), Y.ravel(), np.full(X.size, 1.8)], 1)
+    args = (LaunchGrid(n_theta=32, n_phi=64), TraceConfig(5000, 1e-4, 8), ObserverSet(pts),
+            ExecPlan(), Atmosphere(20.0))
+    fields, spl_mean, tims = parallel.run_snapshots(sc, srcs, *args, calibration=1.0)
+    assert len(fields) == 3 and len(tims) == 3
+    for src, f in zip(srcs, fields):
+        res, _ = parallel.run_pipeline(sc, src, *args, calibration=1.0)
+        assert np.array_equal(res.pressure, f.pressure)
+    e = sum(np.abs(f.pressure) ** 2 for f in fields) / 3
+    assert np.allclose(spl_mean, 10 * np.log10(e / P_REF ** 2), equal_nan=True)
