@@ -15,12 +15,15 @@
 //  * The kernel is PERSISTENT: every warp is an independent worker that pulls
 //    (patch, beam range) units from an atomic queue (range-major, so all warps
 //    share one L2-resident slice of the bundle).  No CTA barriers at all.
-//  * Per unit the warp walks the candidate beams of its tile (the exact fp64
-//    work-list bitmask, exact_fp64.cu), <= 32 beams / ROWCAP rows per chunk:
-//    stage the rows into warp-private shared memory in patch-local fp32
-//    (fp64 conversion), classify each (patch, beam) with one lane per beam
-//    (cut / behind / dominated segments), then sum the live
-//    beams in ascending order through the single / corner-wedge / multi paths.
+//  * Per unit the warp reads its tile's slice of the compacted tight work list
+//    (entries (n_segs - 1) << 27 | beam, built by wl_count / scan / wl_compact from
+//    the exact fp64 bitmask of exact_fp64.cu), <= 32 beams / ROWCAP rows per chunk:
+//    stages the rows into warp-private shared memory in patch-local fp32 (fp64
+//    conversion), classifies each (patch, beam) with one lane per beam (cut / behind /
+//    dominated segments from the patch's bounding box, first- and second-order
+//    bounds), then sums the live beams in ascending order through the
+//    single-survivor path, the junction block (corner wedges and junction ties) and the
+//    several-candidate scan with fp64 re-decision of near ties (exact_pending).
 //  * fp32 partial sums are flushed per chunk into fp64 accumulators; a unit
 //    stores its fp64 partial per (beam range, receiver) and fold_kernel adds the
 //    ranges in ascending order to the caller's acc (in-place continuation,
@@ -32,6 +35,11 @@
 
 #include "common.cuh"
 
+// Compile-time switches (tuning and diagnostics; the defaults are the product):
+//   BF_ROWCAP rows per staged chunk, BF_MINB CTAs/SM for NF = 1, BF_RANGES beam ranges per
+//   call, BF_EVG receivers per evaluation branch, BF_WARPS warps per CTA, BF_NORED (no
+//   explicit turn reduction before MUFU sin/cos); BF_ABL skips work for ablation timings
+//   (results invalid), BF_HIST prints debug counters.
 namespace bf {
 namespace {
 
