@@ -102,7 +102,7 @@ struct Fp32Work {
 int launch_gbs_fp64(const GbsArgs &a, cudaStream_t st);
 int gbs_fp32_tile();
 int gbs_fp32_patch();
-int64_t gbs_fp32_range_beams(int64_t n_beams);
+int64_t gbs_fp32_range_beams(int64_t n_beams, int nf);
 int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st);
 // Work-list compaction (north star: prefix-sum compaction into (beam, tile) lists):
 // counts per (tile, range) into w.wl_off (pass 1), then, after an exclusive scan of

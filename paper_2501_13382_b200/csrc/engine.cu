@@ -341,7 +341,7 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     const int64_t rows = a.n_beams * a.max_seg;
     const int P = gbs_fp32_patch();
     w.n_patches = (a.n_obs + P - 1) / P;
-    w.range_beams = gbs_fp32_range_beams(a.n_beams);
+    w.range_beams = gbs_fp32_range_beams(a.n_beams, a.nf);
     w.n_ranges = (a.n_beams + w.range_beams - 1) / w.range_beams;
     if (w.n_patches * w.n_ranges >= (int64_t)1 << 31)
         return fail(BF_EINVAL, "too many (patch, beam range) units; split the call");

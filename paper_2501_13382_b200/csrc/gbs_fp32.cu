@@ -1321,11 +1321,14 @@ Fp32Consts make_consts(const GbsArgs &a) {
 int gbs_fp32_tile() { return TILE; }
 int gbs_fp32_patch() { return PATCH; }
 
-// Beams per range unit: depends on the beam count only, so the per-receiver
-// summation order (and result bits) does not depend on how receivers are
+// Beams per range unit: depends on the beam and frequency counts only, so the
+// per-receiver summation order (and result bits) does not depend on how receivers are
 // sharded over ranks.
-int64_t gbs_fp32_range_beams(int64_t n_beams) {
-    int64_t rb = (n_beams + BF_RANGES - 1) / BF_RANGES;
+int64_t gbs_fp32_range_beams(int64_t n_beams, int nf) {
+    // BF_RANGES ranges for one frequency, fewer with several (the partial buffer holds
+    // ranges x receivers x frequencies complex values)
+    const int64_t ranges = BF_RANGES / nf > 8 ? BF_RANGES / nf : 8;
+    int64_t rb = (n_beams + ranges - 1) / ranges;
     rb = (rb + 31) / 32 * 32;
     return rb < 256 ? 256 : rb;
 }
