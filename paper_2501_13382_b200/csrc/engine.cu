@@ -79,6 +79,11 @@ struct DeviceCtx {
     int dev = -1;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // Completion of the last call that used this context's workspaces.  Calls may come
+    // on different caller streams and return before their kernels finish; each call
+    // orders itself after the previous one (StreamOrder) so no workspace is reused early.
+    cudaEvent_t done = nullptr;
+    bool done_valid = false;
     std::mutex mu;
     Buf buf[B_COUNT];
     template <typename T>
@@ -87,6 +92,19 @@ struct DeviceCtx {
         BF_TRY(buf[id].get(n * sizeof(T) + 16, &p));
         *out = (T *)p;
         return BF_OK;
+    }
+};
+
+// Held (with ctx->mu) for the duration of an ABI call that uses the context's workspaces:
+// the call's stream waits for the previous such call, and records completion on exit.
+struct StreamOrder {
+    DeviceCtx *c;
+    cudaStream_t st;
+    StreamOrder(DeviceCtx *c_, cudaStream_t st_) : c(c_), st(st_) {
+        if (c->done_valid) cudaStreamWaitEvent(st, c->done, 0);
+    }
+    ~StreamOrder() {
+        if (cudaEventRecord(c->done, st) == cudaSuccess) c->done_valid = true;
     }
 };
 
@@ -114,6 +132,7 @@ int get_ctx(int device, DeviceCtx **out) {
         DeviceCtx *c = new DeviceCtx();
         c->dev = device;
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
         g_ctx[device] = c;
     }
     *out = g_ctx[device];
@@ -489,6 +508,7 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    StreamOrder order(ctx, st);
     GbsArgs a;
     const int64_t r0 = beam_lo * max_seg;
     a.seg_origin = seg_origin + 3 * r0;
@@ -535,6 +555,7 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = ctx->stream;
+    StreamOrder order(ctx, st);
     const bool need_frame = precision == BF_PRECISION_FP64;
     const int64_t rows = nb * max_seg, r0 = beam_lo * max_seg;
     double *d_or, *d_dir, *d_e1 = nullptr, *d_e2 = nullptr, *d_len, *d_s0, *d_refl, *d_w, *d_obs,
@@ -616,6 +637,7 @@ int bf_nearest_on_segments(const double *seg_origin, const double *seg_dir,
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = ctx->stream;
+    StreamOrder order(ctx, st);
     const int64_t rows = n_beams * max_seg;
     double *d_or, *d_dir, *d_e1, *d_e2, *d_len, *d_s0, *d_refl, *d_obs, *d_out;
     int32_t *d_ns;
@@ -717,6 +739,7 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = ctx->stream;
+    StreamOrder order(ctx, st);
     const int64_t rows = n_beams * max_seg;
     double *d_or, *d_dir, *d_len, *d_s0, *d_obs;
     int32_t *d_ns;
@@ -771,6 +794,7 @@ int bf_tile_order_dev(const double *obs, int64_t n, int32_t *perm, int device, v
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    StreamOrder order(ctx, st);
     const int32_t *p;
     BF_TRY(morton_order(ctx, obs, n, st, &p));
     BF_TRY_CUDA(cudaMemcpyAsync(perm, p, 4 * n, cudaMemcpyDeviceToDevice, st));

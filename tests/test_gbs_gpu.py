@@ -237,6 +237,41 @@ def test_chunk_streamer_equals_single_call():
     assert torch.equal(ev, rev)
 
 
+def test_async_calls_on_two_streams():
+    """Asynchronous device calls on different caller streams share the engine's
+    workspaces; each call is ordered after the previous one, so results equal the
+    synchronous ones bit for bit."""
+    import torch
+
+    from paper_2501_13382_b200 import engine
+    b = load_case("city_street")
+    dev = torch.device("cuda", 0)
+    db = engine.DeviceBundle.from_host(_pb(b), dev, with_frame=False)
+    obs = torch.from_numpy(b["obs"]).to(dev)
+    parts = [obs[0::2].contiguous(), obs[1::2].contiguous().flip(0).contiguous()]
+    want = []
+    for o in parts:
+        acc = torch.zeros((o.shape[0], 1), dtype=torch.complex128, device=dev)
+        ev = torch.zeros(o.shape[0], dtype=torch.int64, device=dev)
+        engine.accumulate(db, o, b["omegas"], 10.0, True, acc, ev, precision="fp32")
+        torch.cuda.synchronize()
+        want.append((acc.clone(), ev.clone()))
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    got = []
+    for rep in range(3):
+        for o, s in zip(parts, streams):
+            acc = torch.zeros((o.shape[0], 1), dtype=torch.complex128, device=dev)
+            ev = torch.zeros(o.shape[0], dtype=torch.int64, device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):
+                engine.accumulate(db, o, b["omegas"], 10.0, True, acc, ev, precision="fp32",
+                                  stream=s)
+            got.append((acc, ev))
+    torch.cuda.synchronize()
+    for i, (acc, ev) in enumerate(got):
+        assert torch.equal(acc, want[i % 2][0]) and torch.equal(ev, want[i % 2][1])
+
+
 def test_run_pipeline_city_vs_oracle():
     """run_pipeline (GPU trace + GPU sum, uncalibrated) vs the oracle on the same bundle."""
     from paper_2501_13382_b200 import (Atmosphere, ExecPlan, LaunchGrid, ObserverSet,
