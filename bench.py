@@ -53,6 +53,13 @@ CONFIGS = {
                      src=(20.0, 0.0, 2.0), freqs=(63.0, 125.0, 250.0, 500.0, 1000.0), im_b=-10.0,
                      n_theta=100, n_phi=200, n_steps=5000, r_max=8,
                      grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
+    # config-3 variant with the paper's beam parameter (im_b = -45874): the cutoff never
+    # fires, so every non-behind pair is evaluated (no work-list culling)
+    "cfg3s_pb": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers, "
+                          "im_b=-45874 (paper beam parameter variant)", scene="city",
+                     scene_args=(5, 10, 40.0, 20.0, 300.0), src=(20.0, 0.0, 2.0),
+                     freqs=(125.0,), im_b=-45874.0, n_theta=100, n_phi=200, n_steps=5000,
+                     r_max=8, grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
     # profiling variant of config 3: same scene/receivers, 20k rays (ncu replays stay short)
     "cfg3s": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers (cfg3 profile "
                        "variant)", scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0),

@@ -95,6 +95,8 @@ struct Fp32Work {
     uint32_t *wl_items;       // compacted tight work list: per (tile, beam range), ascending
                               // beams, entry = (n_segs - 1) << 27 | beam
     int64_t *wl_off;          // n_tiles * n_ranges + 1 offsets into wl_items
+    const int32_t *unit_order;  // queue position -> unit q * n_patches + p (longest-first
+                                // buckets, range-major inside; see unit_keys_kernel)
     int64_t n_patches, n_ranges, range_beams, n_pad;  // n_pad = n_patches * patch
 };
 
@@ -111,6 +113,9 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 // candidate beams, their segments.
 int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
                          unsigned long long *wstats, cudaStream_t st);
+// Queue order: keys (longest-first bucket << 32 | range) and unit values, radix-sorted.
+int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w, const int64_t *counts,
+                          uint64_t *keys, int32_t *vals, cudaStream_t st);
 int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
                            cudaStream_t st);
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,

@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_TBOX, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_TBOX, B_UKEYS, B_UKEYS2, B_UVALS, B_UVALS2, B_COUNT
 };
 
 struct DeviceCtx {
@@ -396,6 +396,35 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         BF_TRY_CUDA(cudaStreamSynchronize(st));
         BF_TRY(c->get(B_WLITEMS, (size_t)(total + 1), &w.wl_items));
         BF_TRY(launch_fp32_wl_compact(a, t, w, st));
+    }
+    {   // unit queue order (longest-first buckets, range-major inside a bucket);
+        // the counts (B_WLTMP) are still intact after the scan
+        const int64_t nu = w.n_patches * w.n_ranges;
+        const int64_t *cnt;
+        {
+            int64_t *cm;
+            BF_TRY(c->get(B_WLTMP, (size_t)(t.n_tiles * w.n_ranges + 1), &cm));
+            cnt = cm;
+        }
+        uint64_t *k0, *k1;
+        int32_t *v0, *v1;
+        BF_TRY(c->get(B_UKEYS, (size_t)nu, &k0));
+        BF_TRY(c->get(B_UKEYS2, (size_t)nu, &k1));
+        BF_TRY(c->get(B_UVALS, (size_t)nu, &v0));
+        BF_TRY(c->get(B_UVALS2, (size_t)nu, &v1));
+        BF_TRY(launch_fp32_unit_keys(t, w, cnt, k0, v0, st));
+        const int end_bit = 39;  // bucket (7 bits) << 32 | range
+        cub::DoubleBuffer<uint64_t> dk(k0, k1);
+        cub::DoubleBuffer<int32_t> dv(v0, v1);
+        size_t tmp_bytes = 0;
+        BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)nu, 0,
+                                                    end_bit, st));
+        void *tmp;
+        BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
+        BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, dv, (int)nu, 0,
+                                                    end_bit, st));
+        note_launch();
+        w.unit_order = dv.Current();
     }
     BF_TRY(launch_fp32_prepare(a, t, w, st));
     GbsStats *d_stats;

@@ -1055,8 +1055,9 @@ __global__ void __launch_bounds__(THREADS, (NF == 1 ? BF_MINB : NF <= 5 ? 3 : 2)
         if (lane == 0) u = atomicAdd(w.unit_ctr, 1u);
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= n_units) break;
-        const unsigned q = u / n_patches;  // range-major: one L2-resident slice
-        const unsigned p = u - q * n_patches;
+        const unsigned id = (unsigned)w.unit_order[u];  // longest-first, see unit_keys_kernel
+        const unsigned q = id / n_patches;
+        const unsigned p = id - q * n_patches;
         run_unit<NF>(a, tl, w, K, S, p, q, lane, stats);
     }
     // per-lane counters straight into the device statistics
@@ -1219,6 +1220,23 @@ __global__ void wl_count_kernel(const GbsArgs a, const Tiling tl, const Fp32Work
     }
 }
 
+// Sort keys of the unit queue: longest-first in half-octave buckets of the unit's
+// candidate count, range-major inside a bucket (concurrent units share a beam range, so
+// its rows stay L2-resident).  A unit near the source can run for ~10 ms; started late
+// it would be the launch's tail, which matters once ranks hold few receivers each.
+__global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_t *counts,
+                                 uint64_t *keys, int32_t *vals) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= w.n_patches * w.n_ranges) return;
+    const int64_t q = u / w.n_patches, p = u - q * w.n_patches;
+    const int64_t tile = p / (TILE / PATCH);
+    const uint64_t c = (uint64_t)counts[tile * w.n_ranges + q] + 1;
+    const int msb = 63 - __clzll((long long)c);
+    const int bucket = 2 * msb + (msb > 0 ? (int)((c >> (msb - 1)) & 1) : 0);  // < 128
+    keys[u] = ((uint64_t)(127 - bucket) << 32) | (uint64_t)q;
+    vals[u] = (int32_t)u;
+}
+
 // One warp per (tile, beam range): ascending candidate beams with their segment
 // counts, (n_segs - 1) << 27 | beam, at the scanned offset.
 __global__ void wl_compact_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w) {
@@ -1356,6 +1374,17 @@ int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, i
     if (nu > 0) {
         wl_count_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(a, t, w, counts,
                                                                            wstats);
+        note_launch();
+    }
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w, const int64_t *counts,
+                          uint64_t *keys, int32_t *vals, cudaStream_t st) {
+    const int64_t nu = w.n_patches * w.n_ranges;
+    if (nu > 0) {
+        unit_keys_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, st>>>(t, w, counts, keys, vals);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
