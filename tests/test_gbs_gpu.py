@@ -363,12 +363,14 @@ def test_worklist_bitexact_vs_oracle(name, dense):
         assert 0 < np.unpackbits(bits.view(np.uint8)).mean() < 1
 
 
-@pytest.mark.parametrize("freqs,src,corner", [((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0)),
-                                              ((63.0, 250.0, 1000.0), (0.0, 20.0, 2.0),
-                                               (-30.0, 5.0)),
-                                              ((50.0, 63.0, 80.0, 100.0, 125.0, 160.0, 200.0,
-                                                250.0), (20.0, 0.0, 2.0), (10.0, -5.0))])
-def test_fp32_dense_city_vs_oracle(freqs, src, corner, threads):
+@pytest.mark.parametrize("freqs,src,corner,im_b", [
+    ((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0), -10.0),
+    ((63.0, 250.0, 1000.0), (0.0, 20.0, 2.0), (-30.0, 5.0), -10.0),
+    ((50.0, 63.0, 80.0, 100.0, 125.0, 160.0, 200.0, 250.0), (20.0, 0.0, 2.0), (10.0, -5.0),
+     -10.0),
+    # the paper's beam parameter: the cutoff never fires, every non-behind pair evaluated
+    ((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0), -45874.0)])
+def test_fp32_dense_city_vs_oracle(freqs, src, corner, im_b, threads):
     """Config-3 receiver density (0.25 m) around street corners of the city scene: every
     fp32 path (single survivor, corner wedge, several candidates with junction and
     general fp64 re-decisions, behind plane) against the C oracle on the same traced
@@ -381,7 +383,7 @@ def test_fp32_dense_city_vs_oracle(freqs, src, corner, threads):
     from paper_2501_13382_b200.scene import make_city
     dev = torch.device("cuda", 0)
     sc = make_city(5, 10, 40.0, 20.0, 300.0)
-    source = SourceSpec(position=np.array(src), frequencies=freqs, beam_param_im=-10.0)
+    source = SourceSpec(position=np.array(src), frequencies=freqs, beam_param_im=im_b)
     launch = launch_directions(LaunchGrid(0.0, 180.0, 0.0, 360.0, 60, 120))
     cfg = TraceConfig(5000, 1e-4, 8)
     c = Atmosphere(20.0).sound_speed
