@@ -73,7 +73,10 @@ constexpr int TILE = 4 * PATCH;         // receivers per work-list tile
 constexpr int WARPS = BF_WARPS;         // independent warps per CTA
 constexpr int THREADS = 32 * WARPS;
 constexpr int CB = 32;                  // max beams per staged chunk
-constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk
+constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk (one frequency)
+constexpr int ROWCAP_MF = 64;           // ... several frequencies (power of two, see ROWS)
+template <int NF>
+constexpr int ROWS = NF == 1 ? ROWCAP : ROWCAP_MF;
 constexpr int EVG = BF_EVG;             // receivers evaluated per branch of the tail
 constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
 constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
@@ -137,12 +140,12 @@ constexpr unsigned WEDGE = 0x40000000u;
 // plus the patch's fp64 accumulators.
 template <int NF>
 struct WarpSmem {
-    float4 geo0[ROWCAP];     // wc.xyz (c_P - o), len
-    float4 geo1[ROWCAP];     // d.xyz, Pc (projection of c_P)
-    float4 geo2[ROWCAP];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
-    float2 aux[ROWCAP];      // s0, A (amplitude factor x omega_0)
-    float4 anc[NF][ROWCAP];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
-    unsigned rowinfo[ROWCAP];  // chunk row -> beam << 5 | segment
+    float4 geo0[ROWS<NF>];     // wc.xyz (c_P - o), len
+    float4 geo1[ROWS<NF>];     // d.xyz, Pc (projection of c_P)
+    float4 geo2[ROWS<NF>];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
+    float2 aux[ROWS<NF>];      // s0, A (amplitude factor x omega_0)
+    float4 anc[NF][ROWS<NF>];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
+    unsigned rowinfo[ROWS<NF>];  // chunk row -> beam << 5 | segment
     short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
     int4 desc[CB];           // chunk beam -> (beam, survivor word, first row, D bits)
@@ -150,6 +153,8 @@ struct WarpSmem {
     // the unit's slice of the global partial buffer instead (shared memory is the
     // occupancy limit there)
     double acc[NF == 1 ? PATCH : 1][NF][2];
+    // several frequencies: the chunk's fp32 partial sums, [f][receiver j][lane]
+    float2 facc[NF == 1 ? 1 : NF][NF == 1 ? 1 : R][32];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
     unsigned long long cnt[8];  // statistics: ties, non-behind, culled/single/wedge/multi
@@ -163,16 +168,18 @@ struct WarpSmem {
 // One frequency of a pair's contribution (the several-frequency tail): gq = q^2/m2,
 // ainv = A/m2 shared across frequencies.
 __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float s, float gq,
-                                          float ainv, float base, float &pre, float &pim,
-                                          unsigned &ev, int shift, bool live) {
+                                          float ainv, float base, float2 &acc, unsigned &ev,
+                                          int shift, bool live) {
     const float turns = fmaf(gq * s, K.hk2pi[f], base);
     const float ph = turns * 6.283185307179586f;
     const float sn = sin_approx(ph), cs = cos_approx(ph);
     const float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]) * K.omrel[f];
     const float as = amp * s, ab = amp * K.b;
     if (live) {  // i * amp * (s + i b) * (cos + i sin)
-        pre = fmaf(-as, sn, fmaf(-ab, cs, pre));
-        pim = fmaf(as, cs, fmaf(-ab, sn, pim));
+        float2 v = acc;
+        v.x = fmaf(-as, sn, fmaf(-ab, cs, v.x));
+        v.y = fmaf(as, cs, fmaf(-ab, sn, v.y));
+        acc = v;
         ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
     }
 }
@@ -219,6 +226,23 @@ __device__ __forceinline__ float anchor_phase(float kappa, float proj, float dl,
     return bf;
 }
 
+
+// Several frequencies: the nearest point's phase is kept as (row | clamp << 8, r.d) and
+// resolved per frequency in the tail; clamp 1 = start anchor, 2 = end anchor, 0 =
+// interior (anchor_phase's choice, same order of tests).
+__device__ __forceinline__ int phase_ref(int row, float proj, float len) {
+    int st = proj >= len ? 2 : 0;
+    st = proj <= 0.f ? 1 : st;
+    return row | (st << 8);
+}
+
+template <int NF>
+__device__ __forceinline__ float phase_of(const WarpSmem<NF> &S, const Fp32Consts &K, int f,
+                                          int ref, float dl) {
+    const float4 an = S.anc[f][ref & (ROWS<NF> - 1)];
+    const int st = ref >> 8;
+    return st == 1 ? an.y : st == 2 ? an.z : fmaf(K.kappa[f], dl, an.x);
+}
 
 // Distance of the patch centre (the origin of patch-local coordinates) to
 // segment row `r` (fp32), the unit vector from the nearest point, whether the
@@ -516,8 +540,8 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
                                               const float (&best)[R], const int (&kb)[R],
                                               float Db, int lane, float (&sj)[R],
                                               float (&q2j)[R], float (&Aj)[R],
-                                              float (&bj)[R][NF], unsigned &lvm, unsigned &ties,
-                                              const Fp32Work &w) {
+                                              float (&bj)[R][1], int (&pref)[R], unsigned &lvm,
+                                              unsigned &ties, const Fp32Work &w) {
     ties += __popc(pend);
     // two adjacent candidates k, k+1 (most multi items): a receiver that projects
     // beyond the end of k and before the start of k+1 is decided like the corner wedge
@@ -545,18 +569,22 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         // anchor choice follows the exact clamp
         const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
         const float A = S.aux[r0 + k].y;
-        float b[NF];
-#pragma unroll
-        for (int f = 0; f < NF; ++f)
-            b[f] = anchor_phase(K.kappa[f], proj, dl, S.geo0[r0 + k].w, S.anc[f][r0 + k]);
+        float b;
+        int ref = 0;
+        if constexpr (NF == 1) {
+            b = anchor_phase(K.kappa[0], proj, dl, S.geo0[r0 + k].w, S.anc[0][r0 + k]);
+        } else {
+            b = dl;
+            ref = phase_ref(r0 + k, proj, S.geo0[r0 + k].w);
+        }
 #pragma unroll
         for (int jj = 0; jj < R; ++jj)
             if (jj == j) {
                 q2j[jj] = q2;
                 sj[jj] = s;
                 Aj[jj] = A;
-#pragma unroll
-                for (int f = 0; f < NF; ++f) bj[jj][f] = b[f];
+                bj[jj][0] = b;
+                if constexpr (NF > 1) pref[jj] = ref;
             }
         lvm |= 1u << j;
     }
@@ -657,13 +685,18 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             S.p64[R * lane + j][2] = a.obs[3 * oi + 2];
         }
     }
-    float pre[R][NF], pim[R][NF];
+    // fp32 partial sums of the chunk: registers with one frequency, shared memory
+    // (S.facc) with several
+    float pre[R][1], pim[R][1];
     unsigned evp[R / 2] = {};  // evaluation counts of receivers 2i, 2i+1 (16-bit fields)
     unsigned ties = 0, nbp = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
+        pre[j][0] = pim[j][0] = 0.f;
+        if constexpr (NF > 1) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
+            for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
+        }
     }
 
     // ---- candidate beams: the unit's slice of the compacted tight work list
@@ -676,14 +709,14 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         const int nbn = min(CB, n_items - cur);
         const int ns = lane < nbn ? (int)(e >> 27) + 1 : 0;
         const int beam_l = (int)(e & 0x7ffffffu);
-        // ---- row capacity: keep the prefix of beams whose rows fit ROWCAP
+        // ---- row capacity: keep the prefix of beams whose rows fit ROWS<NF>
         int incl = ns;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
-        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbn && incl <= ROWCAP);
+        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbn && incl <= ROWS<NF>);
         const int nbc = __popc(fit);
         const int nrows = __shfl_sync(0xffffffffu, incl, nbc - 1);
         if (lane < nbc) {
@@ -779,7 +812,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             }
 #endif
             // nearest point of every receiver: s, q^2, amplitude factor, axial phase base
-            float sj[R], q2j[R], Aj[R], bj[R][NF];
+            // (one frequency) or its (row, clamp) reference and r.d (several, pref/bj)
+            float sj[R], q2j[R], Aj[R], bj[R][1];
+            int pref[R] = {};
             unsigned lvm;
             if ((surv & (surv - 1)) == 0) {
                 // ---- single surviving segment: it is the nearest for every receiver
@@ -789,9 +824,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 const float4 g1 = S.geo1[row];
                 const float4 g2 = S.geo2[row];
                 const float2 ax = S.aux[row];
-                float4 an[NF];
-#pragma unroll
-                for (int f = 0; f < NF; ++f) an[f] = S.anc[f][row];
+                float4 an[1];
+                if constexpr (NF == 1) an[0] = S.anc[0][row];
                 float pj[R];
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
@@ -799,9 +833,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float proj = dl + g1.w;
                     pj[j] = proj;
                     Aj[j] = ax.y;
-#pragma unroll
-                    for (int f = 0; f < NF; ++f)
-                        bj[j][f] = anchor_phase(K.kappa[f], proj, dl, g0.w, an[f]);
+                    if constexpr (NF == 1) {
+                        bj[j][0] = anchor_phase(K.kappa[0], proj, dl, g0.w, an[0]);
+                    } else {
+                        bj[j][0] = dl;
+                        pref[j] = phase_ref(row, proj, g0.w);
+                    }
                     sj[j] = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
                     q2j[j] = fmaxf(
                         fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
@@ -896,9 +933,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float len = S.geo0[r0 + k].w;
                     sj[j] = ax.x + fminf(fmaxf(proj, 0.f), len);
                     Aj[j] = ax.y;
-#pragma unroll
-                    for (int f = 0; f < NF; ++f)
-                        bj[j][f] = anchor_phase(K.kappa[f], proj, dl, len, S.anc[f][r0 + k]);
+                    if constexpr (NF == 1) {
+                        bj[j][0] = anchor_phase(K.kappa[0], proj, dl, len, S.anc[0][r0 + k]);
+                    } else {
+                        bj[j][0] = dl;
+                        pref[j] = phase_ref(r0 + k, proj, len);
+                    }
                     lvm |= 1u << j;
                 }
                 }
@@ -908,11 +948,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
                     const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
-                    float ea[NF], sb_[NF];  // end anchor of ka, start anchor of ka+1
-#pragma unroll
-                    for (int f = 0; f < NF; ++f) {
-                        ea[f] = S.anc[f][ra].z;
-                        sb_[f] = S.anc[f][rb].y;
+                    float ea[1], sb_[1];  // end anchor of ka, start anchor of ka+1
+                    if constexpr (NF == 1) {
+                        ea[0] = S.anc[0][ra].z;
+                        sb_[0] = S.anc[0][rb].y;
                     }
                     ties += __popc(jp);
 #pragma unroll
@@ -927,14 +966,18 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                             0.f);
                         sj[j] = wb ? J.sb : J.sa;
                         Aj[j] = wb ? Ab : Aa;
-#pragma unroll
-                        for (int f = 0; f < NF; ++f) bj[j][f] = wb ? sb_[f] : ea[f];
+                        if constexpr (NF == 1) {
+                            bj[j][0] = wb ? sb_[0] : ea[0];
+                        } else {
+                            bj[j][0] = 0.f;
+                            pref[j] = wb ? (rb | (1 << 8)) : (ra | (2 << 8));
+                        }
                         lvm |= 1u << j;
                     }
                 }
                 if (__any_sync(0xffffffffu, pend != 0))
                     exact_pending<NF>(a, K, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
-                                      Db, lane, sj, q2j, Aj, bj, lvm, ties, w);
+                                      Db, lane, sj, q2j, Aj, bj, pref, lvm, ties, w);
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
@@ -954,9 +997,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (lvm & (((1u << EVG) - 1u) << g)) {
 #pragma unroll
                     for (int j = g; j < g + EVG; ++j)
-                        eval_pair<NF>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], Aj[j], bj[j],
-                                      pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
-                                      EVG == 1 || ((lvm >> j) & 1u));
+                        eval_pair<1>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], Aj[j], bj[j],
+                                     pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
+                                     EVG == 1 || ((lvm >> j) & 1u));
                 }
             } else {
             // several frequencies: the cutoff grows with omega, so each frequency is
@@ -968,8 +1011,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 gq[j] = q2j[j] * inv;
                 ainv[j] = Aj[j] * inv;
             }
-            // one copy of the code per receiver: frequency f is always in slot 0 of the
-            // per-frequency arrays, which rotate by one slot per iteration
+            // per frequency: the phase base from the (row, clamp) reference, partial sums
+            // in shared memory (no per-frequency registers)
 #pragma unroll 1
             for (int f = 0; f < NF; ++f) {
                 unsigned lf = 0;
@@ -980,21 +1023,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (__any_sync(0xffffffffu, lf != 0)) {
 #pragma unroll
                     for (int j = 0; j < R; ++j)
-                        eval_freq(K, f, sj[j], gq[j], ainv[j], bj[j][0], pre[j][0], pim[j][0],
-                                  evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
-                }
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const float p0 = pre[j][0], i0 = pim[j][0], b0 = bj[j][0];
-#pragma unroll
-                    for (int g = 0; g + 1 < NF; ++g) {
-                        pre[j][g] = pre[j][g + 1];
-                        pim[j][g] = pim[j][g + 1];
-                        bj[j][g] = bj[j][g + 1];
-                    }
-                    pre[j][NF - 1] = p0;
-                    pim[j][NF - 1] = i0;
-                    bj[j][NF - 1] = b0;
+                        eval_freq(K, f, sj[j], gq[j], ainv[j], phase_of<NF>(S, K, f, pref[j], bj[j][0]),
+                                  S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
                 }
             }
             }
@@ -1005,16 +1035,20 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             if (NF == 1) {
                 S.acc[R * lane + j][0][0] += (double)pre[j][0];
                 S.acc[R * lane + j][0][1] += (double)pim[j][0];
-            } else if (j < nvalid) {
-                double2 *pp = w.part + (q * w.n_pad + sb + j) * NF;
+            } else {
+                if (j < nvalid) {
+                    double2 *pp = w.part + (q * w.n_pad + sb + j) * NF;
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    const double2 v = pp[f];
-                    pp[f] = make_double2(v.x + (double)pre[j][f], v.y + (double)pim[j][f]);
+                    for (int f = 0; f < NF; ++f) {
+                        const double2 v = pp[f];
+                        const float2 c = S.facc[f][j][lane];
+                        pp[f] = make_double2(v.x + (double)c.x, v.y + (double)c.y);
+                    }
                 }
-            }
 #pragma unroll
-            for (int f = 0; f < NF; ++f) pre[j][f] = pim[j][f] = 0.f;
+                for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
+            }
+            pre[j][0] = pim[j][0] = 0.f;
         }
 #pragma unroll
         for (int j = 0; j < R; ++j) S.evc[R * lane + j] += (evp[j >> 1] >> (16 * (j & 1))) & 0xffffu;
