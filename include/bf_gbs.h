@@ -3,8 +3,11 @@
  *
  * Plain pointers and sizes only (no torch / C++ types).  Every entry point
  * returns a bf_status; on failure bf_last_error() returns a thread-local
- * message.  All functions are thread-safe; calls on one device serialise on
- * that device's engine stream unless a caller stream is given.
+ * message.  All functions are thread-safe.  Calls on one device serialise on
+ * that device's engine stream; a *_dev call given a caller stream returns once its
+ * work is enqueued, and the next call that uses the device's workspaces (on any
+ * stream) is ordered after it by an event, so concurrent callers on different
+ * streams never see each other's scratch buffers.
  *
  * Reference interface each entry point replaces (paths relative to
  * /root/reference/pkg/src/beamfield/):
