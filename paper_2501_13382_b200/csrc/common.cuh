@@ -92,12 +92,20 @@ struct Fp32Work {
     double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum
     int *part_ev;             // per (beam range, sorted receiver): unit evaluation count
     unsigned *unit_ctr;       // persistent-kernel work queue head
+    unsigned *n_wide;         // statistics: units of wide patches
+    float wide_k, wide_q;     // patch radius RW is wide iff RW wide_k > 1 or RW^2 wide_q > 1
     uint32_t *wl_items;       // compacted tight work list: per (tile, beam range), ascending
                               // beams, entry = (n_segs - 1) << 27 | beam
     int64_t *wl_off;          // n_tiles * n_ranges + 1 offsets into wl_items
     const int32_t *unit_order;  // queue position -> unit q * n_patches + p (longest-first
                                 // buckets, range-major inside; see unit_keys_kernel)
     int64_t n_patches, n_ranges, range_beams, n_pad;  // n_pad = n_patches * patch
+};
+
+// A launch's stream plus an auxiliary stream and two events for a fork/join inside it.
+struct StreamPair {
+    cudaStream_t st, aux;
+    cudaEvent_t fork, join;
 };
 
 // Launchers (return BF_OK or an error status).
@@ -114,12 +122,12 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
                          unsigned long long *wstats, cudaStream_t st);
 // Queue order: keys (longest-first bucket << 32 | range) and unit values, radix-sorted.
-int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w, const int64_t *counts,
-                          uint64_t *keys, int32_t *vals, cudaStream_t st);
+int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
+                          const int64_t *counts, uint64_t *keys, int32_t *vals, cudaStream_t st);
 int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
                            cudaStream_t st);
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
-                    cudaStream_t st);
+                    const StreamPair &st);
 int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam,
                    int64_t n_query, double *out, cudaStream_t st);
 int launch_trace(const double *v0, const double *v1, const double *v2, const double *refl,

@@ -84,6 +84,8 @@ struct DeviceCtx {
     // orders itself after the previous one (StreamOrder) so no workspace is reused early.
     cudaEvent_t done = nullptr;
     bool done_valid = false;
+    cudaStream_t aux = nullptr;              // second stream for the wide-patch kernel
+    cudaEvent_t fork = nullptr, join = nullptr;
     std::mutex mu;
     Buf buf[B_COUNT];
     template <typename T>
@@ -133,6 +135,9 @@ int get_ctx(int device, DeviceCtx **out) {
         c->dev = device;
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
+        BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         g_ctx[device] = c;
     }
     *out = g_ctx[device];
@@ -376,8 +381,19 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     w.n_pad = w.n_patches * P;
     BF_TRY(c->get(B_DONE, (size_t)(w.n_ranges * w.n_pad * a.nf), &w.part));
     BF_TRY(c->get(B_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
-    BF_TRY(c->get(B_UCTR, 1, &w.unit_ctr));
-    BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, sizeof(unsigned), st));
+    BF_TRY(c->get(B_UCTR, 3, &w.unit_ctr));
+    w.n_wide = w.unit_ctr + 2;
+    BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), st));
+    {   // wide patches (fp64 tail, see unit_keys_kernel): kappa_max RW > 16 turns or
+        // omega_max RW^2 / (2 c b) > 200 (the fp32 error of r.d and q^2 grows with RW;
+        // at these bounds it stays ~5x below the 0.01 dB gate at 50 dB below the maximum)
+        double wmax = 0.0;
+        for (int f = 0; f < a.nf; ++f) wmax = a.omegas[f] > wmax ? a.omegas[f] : wmax;
+        const char *ek = getenv("BF_WIDE_TURNS"), *eq = getenv("BF_WIDE_Q");  // tuning
+        const double lk = ek ? atof(ek) : 16.0, lq = eq ? atof(eq) : 200.0;
+        w.wide_k = (float)(wmax / (2.0 * 3.141592653589793 * a.c) / lk);
+        w.wide_q = (float)(wmax / (2.0 * a.c * a.width_b) / lq);
+    }
     {   // compacted tight work list: counts -> exclusive scan -> entries
         const int64_t nu = t.n_tiles * w.n_ranges;
         int64_t *cnt;
@@ -397,8 +413,11 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         BF_TRY(c->get(B_WLITEMS, (size_t)(total + 1), &w.wl_items));
         BF_TRY(launch_fp32_wl_compact(a, t, w, st));
     }
-    {   // unit queue order (longest-first buckets, range-major inside a bucket);
-        // the counts (B_WLTMP) are still intact after the scan
+    BF_TRY(launch_fp32_prepare(a, t, w, st));
+    {   // unit queue order (wide patches last; longest-first buckets, range-major inside
+        // a bucket);
+        // the counts (B_WLTMP) are still intact after the scan; the patch radii come
+        // from launch_fp32_prepare
         const int64_t nu = w.n_patches * w.n_ranges;
         const int64_t *cnt;
         {
@@ -413,7 +432,7 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         BF_TRY(c->get(B_UVALS, (size_t)nu, &v0));
         BF_TRY(c->get(B_UVALS2, (size_t)nu, &v1));
         BF_TRY(launch_fp32_unit_keys(t, w, cnt, k0, v0, st));
-        const int end_bit = 39;  // bucket (7 bits) << 32 | range
+        const int end_bit = 40;  // wide << 39 | bucket (7 bits) << 32 | range
         cub::DoubleBuffer<uint64_t> dk(k0, k1);
         cub::DoubleBuffer<int32_t> dv(v0, v1);
         size_t tmp_bytes = 0;
@@ -426,7 +445,6 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         note_launch();
         w.unit_order = dv.Current();
     }
-    BF_TRY(launch_fp32_prepare(a, t, w, st));
     GbsStats *d_stats;
     BF_TRY(c->get(B_STATS, 1, &d_stats));
     BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
@@ -435,7 +453,7 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         BF_TRY_CUDA(cudaEventCreate(&c->ev1));
     }
     BF_TRY_CUDA(cudaEventRecord(c->ev0, st));
-    BF_TRY(launch_gbs_fp32(a, t, w, d_stats, st));
+    BF_TRY(launch_gbs_fp32(a, t, w, d_stats, StreamPair{st, c->aux, c->fork, c->join}));
     BF_TRY_CUDA(cudaEventRecord(c->ev1, st));
     GbsStats h;
     BF_TRY_CUDA(cudaMemcpyAsync(&h, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost, st));
@@ -458,6 +476,12 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     h.tight_pairs = tp;
     h.tight_pair_segs = ts;
     g_last_stats = h;
+    if (getenv("BF_DEBUG_STATS")) {
+        unsigned nw = 0;
+        cudaMemcpy(&nw, w.n_wide, sizeof(unsigned), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "bf units: %lld, of wide patches %u\n",
+                (long long)(w.n_patches * w.n_ranges), nw);
+    }
     if (getenv("BF_DEBUG_STATS"))
         fprintf(stderr, "bf stats: items culled %llu single %llu wedge %llu multi %llu "
                 "(surv 2:%llu 3:%llu 4:%llu 5+:%llu) ties %llu\n", h.paths[0], h.paths[1],

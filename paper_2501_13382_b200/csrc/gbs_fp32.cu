@@ -75,8 +75,8 @@ constexpr int THREADS = 32 * WARPS;
 constexpr int CB = 32;                  // max beams per staged chunk
 constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk (one frequency)
 constexpr int ROWCAP_MF = 64;           // ... several frequencies (power of two, see ROWS)
-template <int NF>
-constexpr int ROWS = NF == 1 ? ROWCAP : ROWCAP_MF;
+template <bool MF>
+constexpr int ROWS = MF ? ROWCAP_MF : ROWCAP;
 constexpr int EVG = BF_EVG;             // receivers evaluated per branch of the tail
 constexpr float TIE_REL = 3.0517578125e-05f;        // 2^-15 (x d2)
 constexpr float TIE_ABS = 1.1920928955078125e-07f;  // 2^-23 (x D^2)
@@ -138,27 +138,31 @@ constexpr unsigned WEDGE = 0x40000000u;
 
 // Warp-private shared memory: one staged chunk of beams as seen from the patch,
 // plus the patch's fp64 accumulators.
-template <int NF>
+// MF: the several-frequency representation of the summation (phase references, fp32
+// chunk sums in shared memory, fp64 partials in the global buffer); also used with one
+// frequency by the wide-patch kernel.
+template <int NF, bool MF = (NF > 1)>
 struct WarpSmem {
-    float4 geo0[ROWS<NF>];     // wc.xyz (c_P - o), len
-    float4 geo1[ROWS<NF>];     // d.xyz, Pc (projection of c_P)
-    float4 geo2[ROWS<NF>];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
-    float2 aux[ROWS<NF>];      // s0, A (amplitude factor x omega_0)
-    float4 anc[NF][ROWS<NF>];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
-    unsigned rowinfo[ROWS<NF>];  // chunk row -> beam << 5 | segment
+    // first, at the same offset in both layouts (a wide unit aliases the warp's memory):
+    unsigned long long cnt[8];  // statistics: ties, non-behind, culled/single/wedge/multi
+                                // items, live pairs, live pair-segments
+    float4 geo0[ROWS<MF>];     // wc.xyz (c_P - o), len
+    float4 geo1[ROWS<MF>];     // d.xyz, Pc (projection of c_P)
+    float4 geo2[ROWS<MF>];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
+    float2 aux[ROWS<MF>];      // s0, A (amplitude factor x omega_0)
+    float4 anc[NF][ROWS<MF>];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
+    unsigned rowinfo[ROWS<MF>];  // chunk row -> beam << 5 | segment
     short brow[CB + 1];      // chunk beam -> first chunk row
     int gbeam[CB];           // chunk beam -> local beam index
     int4 desc[CB];           // chunk beam -> (beam, survivor word, first row, D bits)
     // fp64 accumulators of the unit (NF == 1); with several frequencies they live in
     // the unit's slice of the global partial buffer instead (shared memory is the
     // occupancy limit there)
-    double acc[NF == 1 ? PATCH : 1][NF][2];
+    double acc[MF ? 1 : PATCH][NF][2];
     // several frequencies: the chunk's fp32 partial sums, [f][receiver j][lane]
-    float2 facc[NF == 1 ? 1 : NF][NF == 1 ? 1 : R][32];
+    float2 facc[MF ? NF : 1][MF ? R : 1][32];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
-    unsigned long long cnt[8];  // statistics: ties, non-behind, culled/single/wedge/multi
-                                // items, live pairs, live pair-segments
 };
 
 // Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
@@ -236,10 +240,10 @@ __device__ __forceinline__ int phase_ref(int row, float proj, float len) {
     return row | (st << 8);
 }
 
-template <int NF>
-__device__ __forceinline__ float phase_of(const WarpSmem<NF> &S, const Fp32Consts &K, int f,
+template <int NF, bool MF>
+__device__ __forceinline__ float phase_of(const WarpSmem<NF, MF> &S, const Fp32Consts &K, int f,
                                           int ref, float dl) {
-    const float4 an = S.anc[f][ref & (ROWS<NF> - 1)];
+    const float4 an = S.anc[f][ref & (ROWS<MF> - 1)];
     const int st = ref >> 8;
     return st == 1 ? an.y : st == 2 ? an.z : fmaf(K.kappa[f], dl, an.x);
 }
@@ -253,8 +257,8 @@ __device__ __forceinline__ float reach(const float4 &B, float gx, float gy, floa
     return fminf(fmaf(B.x, fabsf(gx), fmaf(B.y, fabsf(gy), B.z * fabsf(gz))), B.w * gn);
 }
 
-template <int NF>
-__device__ __forceinline__ float patch_dist(const WarpSmem<NF> &S, const Fp32Consts &K, int r,
+template <int NF, bool MF>
+__device__ __forceinline__ float patch_dist(const WarpSmem<NF, MF> &S, const Fp32Consts &K, int r,
                                             const float4 &B, float *ux, float *uy, float *uz,
                                             bool *cut, float *proj_out) {
     const float4 g0 = S.geo0[r];
@@ -300,8 +304,8 @@ __device__ __forceinline__ float curv(float RW, float d) {
 }
 
 // Work generation for one (patch, beam): survivor mask + flags (0 = culled).
-template <int NF>
-__device__ __forceinline__ unsigned classify(const WarpSmem<NF> &S, const Fp32Consts &K, int r0,
+template <int NF, bool MF>
+__device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp32Consts &K, int r0,
                                              int ns, const float4 &B, float &D) {
     const float RW = B.w;
     D = 0.f;
@@ -531,9 +535,9 @@ __device__ __forceinline__ ExactPick exact_pick(const double4 *__restrict__ p0,
 // Exact re-decision (fp64, reference operation order) of the receivers in `pend`
 // among the surviving segments `surv` (ascending k, strict <), one pending
 // receiver per lane per round; fills the nearest point of each decided receiver.
-template <int NF>
+template <int NF, bool MF>
 __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts &K,
-                                              const WarpSmem<NF> &S,
+                                              const WarpSmem<NF, MF> &S,
                                               int64_t beam, int r0, unsigned surv, unsigned pend,
                                               const float (&rx)[R], const float (&ry)[R],
                                               const float (&rz)[R], const float (&rr)[R],
@@ -571,7 +575,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         const float A = S.aux[r0 + k].y;
         float b;
         int ref = 0;
-        if constexpr (NF == 1) {
+        if constexpr (!MF) {
             b = anchor_phase(K.kappa[0], proj, dl, S.geo0[r0 + k].w, S.anc[0][r0 + k]);
         } else {
             b = dl;
@@ -584,15 +588,15 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
                 sj[jj] = s;
                 Aj[jj] = A;
                 bj[jj][0] = b;
-                if constexpr (NF > 1) pref[jj] = ref;
+                if constexpr (MF) pref[jj] = ref;
             }
         lvm |= 1u << j;
     }
 }
 
 // Stage chunk rows [0, nrows) into warp-private shared memory, patch-local.
-template <int NF>
-__device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, int64_t max_seg,
+template <int NF, bool MF>
+__device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &w, int64_t max_seg,
                                            int nrows, double cx, double cy, double cz, float RW,
                                            const Fp32Consts &K, int lane) {
     // software-pipelined: the next row's loads are in flight while this row converts
@@ -650,9 +654,9 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF> &S, const Fp32Work &w, i
 
 
 // One (patch, beam range) unit.
-template <int NF>
+template <int NF, bool WIDE, bool MF = (NF > 1 || WIDE)>
 __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, const Fp32Work &w,
-                                         const Fp32Consts &K, WarpSmem<NF> &S, int64_t p,
+                                         const Fp32Consts &K, WarpSmem<NF, MF> &S, int64_t p,
                                          int64_t q, int lane, GbsStats *stats) {
     const float RW = (float)w.pcen[p].w;
     // ---- receivers (patch-local); padding receivers sit at the centre and are
@@ -670,7 +674,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         ry[j] = rl.y;
         rz[j] = rl.z;
         rr[j] = rl.w;
-        if (NF == 1) {
+        if (!MF) {
             S.acc[R * lane + j][0][0] = S.acc[R * lane + j][0][1] = 0.0;
         } else if (j < nvalid) {
 #pragma unroll
@@ -693,7 +697,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         pre[j][0] = pim[j][0] = 0.f;
-        if constexpr (NF > 1) {
+        if constexpr (MF) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
         }
@@ -709,14 +713,14 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         const int nbn = min(CB, n_items - cur);
         const int ns = lane < nbn ? (int)(e >> 27) + 1 : 0;
         const int beam_l = (int)(e & 0x7ffffffu);
-        // ---- row capacity: keep the prefix of beams whose rows fit ROWS<NF>
+        // ---- row capacity: keep the prefix of beams whose rows fit ROWS<MF>
         int incl = ns;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
-        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbn && incl <= ROWS<NF>);
+        const unsigned fit = __ballot_sync(0xffffffffu, lane < nbn && incl <= ROWS<MF>);
         const int nbc = __popc(fit);
         const int nrows = __shfl_sync(0xffffffffu, incl, nbc - 1);
         if (lane < nbc) {
@@ -733,7 +737,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         {
             const double4 c = w.pcen[p];  // re-read (L1) rather than held in registers
 #if !(BF_ABL & 64)
-            stage_rows<NF>(S, w, a.max_seg, nrows, c.x, c.y, c.z, RW, K, lane);
+            stage_rows<NF, MF>(S, w, a.max_seg, nrows, c.x, c.y, c.z, RW, K, lane);
 #endif
         }
         __syncwarp();
@@ -746,7 +750,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #if BF_ABL & 32
             word = 0;  // ablation: no classification
 #else
-            word = classify<NF>(S, K, r0, nsb, w.pbox[p], D);
+            word = classify<NF, MF>(S, K, r0, nsb, w.pbox[p], D);
 #endif
             S.desc[lane] = make_int4(S.gbeam[lane], (int)word, r0, __float_as_int(D));
         }
@@ -825,7 +829,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 const float4 g2 = S.geo2[row];
                 const float2 ax = S.aux[row];
                 float4 an[1];
-                if constexpr (NF == 1) an[0] = S.anc[0][row];
+                if constexpr (!MF) an[0] = S.anc[0][row];
                 float pj[R];
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
@@ -833,7 +837,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float proj = dl + g1.w;
                     pj[j] = proj;
                     Aj[j] = ax.y;
-                    if constexpr (NF == 1) {
+                    if constexpr (!MF) {
                         bj[j][0] = anchor_phase(K.kappa[0], proj, dl, g0.w, an[0]);
                     } else {
                         bj[j][0] = dl;
@@ -933,7 +937,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float len = S.geo0[r0 + k].w;
                     sj[j] = ax.x + fminf(fmaxf(proj, 0.f), len);
                     Aj[j] = ax.y;
-                    if constexpr (NF == 1) {
+                    if constexpr (!MF) {
                         bj[j][0] = anchor_phase(K.kappa[0], proj, dl, len, S.anc[0][r0 + k]);
                     } else {
                         bj[j][0] = dl;
@@ -949,7 +953,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
                     float ea[1], sb_[1];  // end anchor of ka, start anchor of ka+1
-                    if constexpr (NF == 1) {
+                    if constexpr (!MF) {
                         ea[0] = S.anc[0][ra].z;
                         sb_[0] = S.anc[0][rb].y;
                     }
@@ -966,7 +970,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                             0.f);
                         sj[j] = wb ? J.sb : J.sa;
                         Aj[j] = wb ? Ab : Aa;
-                        if constexpr (NF == 1) {
+                        if constexpr (!MF) {
                             bj[j][0] = wb ? sb_[0] : ea[0];
                         } else {
                             bj[j][0] = 0.f;
@@ -976,7 +980,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     }
                 }
                 if (__any_sync(0xffffffffu, pend != 0))
-                    exact_pending<NF>(a, K, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
+                    exact_pending<NF, MF>(a, K, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
                                       Db, lane, sj, q2j, Aj, bj, pref, lvm, ties, w);
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
@@ -984,13 +988,39 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #if BF_ABL & 8
             if (lvm != 0x7u) continue;  // ablation: no evaluation
 #endif
+            double s64[WIDE ? R : 1];
+            if constexpr (WIDE) {
+                // wide patch: the winner's arc length, q^2 and axial phase from the fp64
+                // rows and receiver positions (patch-local fp32 loses ~eps RW in r.d and
+                // eps RW^2 in q^2); clamp as kernels.py:331-336, q^2 to the infinite line
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    s64[j] = 0.0;
+                    if ((lvm >> j) & 1u) {
+                        const unsigned info = S.rowinfo[pref[j] & (ROWS<MF> - 1)];
+                        const int64_t g = (int64_t)(info >> 5) * a.max_seg + (info & 31);
+                        const double4 o = w.p0[g], d = w.p1[g];
+                        const double *P = S.p64[R * lane + j];
+                        const double wx = __dsub_rn(P[0], o.x), wy = __dsub_rn(P[1], o.y),
+                                     wz = __dsub_rn(P[2], o.z);
+                        const double proj = __dadd_rn(
+                            __dadd_rn(__dmul_rn(wx, d.x), __dmul_rn(wy, d.y)), __dmul_rn(wz, d.z));
+                        const double t = proj < 0.0 ? 0.0 : (proj > o.w ? o.w : proj);
+                        const double ux = wx - proj * d.x, uy = wy - proj * d.y,
+                                     uz = wz - proj * d.z;
+                        s64[j] = __dadd_rn(d.w, t);  // kernels.py:344
+                        sj[j] = (float)s64[j];
+                        q2j[j] = (float)(ux * ux + uy * uy + uz * uz);
+                    }
+                }
+            }
             float m2j[R];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 m2j[j] = fmaf(sj[j], sj[j], K.b2);
-                if (NF == 1 && a.use_cutoff && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);
+                if (!MF && a.use_cutoff && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);
             }
-            if constexpr (NF == 1) {
+            if constexpr (!MF) {
             // receivers evaluated in groups of EVG (one branch, EVG independent chains)
 #pragma unroll
             for (int g = 0; g < R; g += EVG)
@@ -1023,7 +1053,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (__any_sync(0xffffffffu, lf != 0)) {
 #pragma unroll
                     for (int j = 0; j < R; ++j)
-                        eval_freq(K, f, sj[j], gq[j], ainv[j], phase_of<NF>(S, K, f, pref[j], bj[j][0]),
+                        eval_freq(K, f, sj[j], gq[j], ainv[j],
+                                  WIDE ? (float)frac_turns(K.kappa64[f] * s64[j])
+                                       : phase_of<NF, MF>(S, K, f, pref[j], bj[j][0]),
                                   S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
                 }
             }
@@ -1032,7 +1064,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         // flush fp32 partial sums into the fp64 accumulators
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-            if (NF == 1) {
+            if (!MF) {
                 S.acc[R * lane + j][0][0] += (double)pre[j][0];
                 S.acc[R * lane + j][0][1] += (double)pim[j][0];
             } else {
@@ -1062,7 +1094,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     for (int j = 0; j < R; ++j) {
         if (j >= nvalid) continue;
         const int64_t slot = q * w.n_pad + sb + j;
-        if (NF == 1) w.part[slot] = make_double2(S.acc[R * lane + j][0][0], S.acc[R * lane + j][0][1]);
+        if (!MF) w.part[slot] = make_double2(S.acc[R * lane + j][0][0], S.acc[R * lane + j][0][1]);
         w.part_ev[slot] = S.evc[R * lane + j];
     }
     ties = __reduce_add_sync(0xffffffffu, ties);
@@ -1073,26 +1105,36 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     }
 }
 
-template <int NF>
-__global__ void __launch_bounds__(THREADS, (NF == 1 ? BF_MINB : NF <= 5 ? 3 : 2))
+__device__ __forceinline__ bool wide_patch(const Fp32Work &w, int64_t p) {
+    const float RW = (float)w.pcen[p].w;
+    return !(RW * w.wide_k <= 1.f && RW * RW * w.wide_q <= 1.f);
+}
+
+// One launch per patch class, on two streams: WIDE = false takes queue positions
+// [0, n_units - n_wide), WIDE = true the rest (unit_keys_kernel sorts wide patches last).
+template <int NF, bool WIDE>
+__global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5 ? 3 : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w, const Fp32Consts K,
                     GbsStats *stats) {
+    constexpr bool MF = NF > 1 || WIDE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpSmem<NF> &S = reinterpret_cast<WarpSmem<NF> *>(smem_raw)[threadIdx.x >> 5];
+    WarpSmem<NF, MF> &S = reinterpret_cast<WarpSmem<NF, MF> *>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const unsigned n_units = (unsigned)(w.n_patches * w.n_ranges);
+    const unsigned n_split = n_units - *w.n_wide;
+    const unsigned u0 = WIDE ? n_split : 0u, u1 = WIDE ? n_units : n_split;
     const unsigned n_patches = (unsigned)w.n_patches;
     if (lane < 8) S.cnt[lane] = 0;
     __syncwarp();
     for (;;) {
         unsigned u = 0;
-        if (lane == 0) u = atomicAdd(w.unit_ctr, 1u);
+        if (lane == 0) u = u0 + atomicAdd(w.unit_ctr + (WIDE ? 1 : 0), 1u);
         u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= n_units) break;
+        if (u >= u1) break;
         const unsigned id = (unsigned)w.unit_order[u];  // longest-first, see unit_keys_kernel
         const unsigned q = id / n_patches;
         const unsigned p = id - q * n_patches;
-        run_unit<NF>(a, tl, w, K, S, p, q, lane, stats);
+        run_unit<NF, WIDE>(a, tl, w, K, S, p, q, lane, stats);
     }
     // per-lane counters straight into the device statistics
     __syncwarp();
@@ -1258,6 +1300,11 @@ __global__ void wl_count_kernel(const GbsArgs a, const Tiling tl, const Fp32Work
 // candidate count, range-major inside a bucket (concurrent units share a beam range, so
 // its rows stay L2-resident).  A unit near the source can run for ~10 ms; started late
 // it would be the launch's tail, which matters once ranks hold few receivers each.
+// Units of WIDE patches sort last and are summed by the wide-patch kernel: with
+// patch-local fp32 geometry the nearest point's r.d carries an error ~eps RW and q^2
+// ~eps RW^2, which with strong cancellation between beams (a receiver 50 dB below the
+// field maximum) reaches the 0.01 dB gate once kappa RW is tens of turns (sparse
+// receiver sets); the wide kernel recomputes s, q^2 and the phase in fp64.
 __global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_t *counts,
                                  uint64_t *keys, int32_t *vals) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1267,7 +1314,9 @@ __global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_
     const uint64_t c = (uint64_t)counts[tile * w.n_ranges + q] + 1;
     const int msb = 63 - __clzll((long long)c);
     const int bucket = 2 * msb + (msb > 0 ? (int)((c >> (msb - 1)) & 1) : 0);  // < 128
-    keys[u] = ((uint64_t)(127 - bucket) << 32) | (uint64_t)q;
+    const bool wide = wide_patch(w, p);
+    if (wide) atomicAdd(w.n_wide, 1u);
+    keys[u] = ((uint64_t)wide << 39) | ((uint64_t)(127 - bucket) << 32) | (uint64_t)q;
     vals[u] = (int32_t)u;
 }
 
@@ -1303,42 +1352,62 @@ __global__ void wl_compact_kernel(const GbsArgs a, const Tiling tl, const Fp32Wo
     }
 }
 
-template <int NF>
-int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
-              GbsStats *stats, cudaStream_t st) {
-    const size_t smem = WARPS * sizeof(WarpSmem<NF>);
-    BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF>,
+template <int NF, bool WIDE>
+int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
+                 GbsStats *stats, cudaStream_t st) {
+    constexpr bool MF = NF > 1 || WIDE;
+    const size_t smem = WARPS * sizeof(WarpSmem<NF, MF>);
+    BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF, WIDE>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 0, per_sm = 0;
     BF_TRY_CUDA(cudaGetDevice(&dev));
     BF_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gbs_fp32_kernel<NF>,
+    BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gbs_fp32_kernel<NF, WIDE>,
                                                               THREADS, smem));
     if (per_sm < 1) return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
     if (getenv("BF_DEBUG_STATS"))
-        fprintf(stderr, "bf fp32 kernel: %zu B shared per CTA (%zu per warp), %d CTAs/SM\n", smem,
-                sizeof(WarpSmem<NF>), per_sm);
+        fprintf(stderr, "bf fp32 kernel%s: %zu B shared per CTA (%zu per warp), %d CTAs/SM\n",
+                WIDE ? " (wide patches)" : "", smem, sizeof(WarpSmem<NF, MF>), per_sm);
     const int64_t units = w.n_patches * w.n_ranges;
     int64_t grid = (int64_t)sms * per_sm;
     const int64_t need = (units + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
+    gbs_fp32_kernel<NF, WIDE><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+// The wide-patch kernel goes first on the auxiliary stream; the common kernel's CTAs
+// take the SM slots as the wide ones retire (no tail of a second sequential launch).
+template <int NF>
+int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
+              GbsStats *stats, const StreamPair &sp) {
 #if BF_HIST
     {
         unsigned long long z[4] = {0, 0, 0, 0};
-        cudaMemcpyToSymbolAsync(g_hist, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+        cudaMemcpyToSymbolAsync(g_hist, z, sizeof(z), 0, cudaMemcpyHostToDevice, sp.st);
     }
 #endif
-    gbs_fp32_kernel<NF><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
+    // the wide kernel is submitted first on the launch stream, the common one right
+    // after on the auxiliary stream (forked before the wide launch), so the wide CTAs
+    // are dispatched first and the common kernel fills the remaining SM slots
+    BF_TRY_CUDA(cudaEventRecord(sp.fork, sp.st));
+    BF_TRY_CUDA(cudaStreamWaitEvent(sp.aux, sp.fork, 0));
+    BF_TRY((launch_class<NF, true>(a, t, w, K, stats, sp.st)));
+    BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.aux)));
+    BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
+    BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
 #if BF_HIST
     {
         unsigned long long h[4];
-        cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, sp.st);
+        cudaStreamSynchronize(sp.st);
         fprintf(stderr, "bf hist: exact re-decision rounds %llu\n", h[2]);
     }
 #endif
-    fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, st>>>(t, w, a.nf, a.acc, a.evals);
-    note_launch(2);
+    fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, sp.st>>>(t, w, a.nf, a.acc, a.evals);
+    note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
 }
@@ -1414,8 +1483,8 @@ int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, i
     return BF_OK;
 }
 
-int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w, const int64_t *counts,
-                          uint64_t *keys, int32_t *vals, cudaStream_t st) {
+int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
+                          const int64_t *counts, uint64_t *keys, int32_t *vals, cudaStream_t st) {
     const int64_t nu = w.n_patches * w.n_ranges;
     if (nu > 0) {
         unit_keys_kernel<<<(unsigned)((nu + 255) / 256), 256, 0, st>>>(t, w, counts, keys, vals);
@@ -1437,7 +1506,7 @@ int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
 }
 
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
-                    cudaStream_t st) {
+                    const StreamPair &st) {
     if (t.n <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
     if (a.max_seg > 30)  // survivor masks share the word with two flag bits
         return fail(BF_EINVAL, "max_seg %lld exceeds 30 (r_max <= 29)", (long long)a.max_seg);
