@@ -112,7 +112,7 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
 
 /*
  * Work list of the fp32 path, exposed for verification: the
- * Morton receiver order perm (n_obs), tile centres/radii centre (n_tiles x 4:
+ * Hilbert receiver order perm (n_obs), tile centres/radii centre (n_tiles x 4:
  * x, y, z, R_T) and the candidate bitmask bits (n_tiles x ceil(n_beams/32)
  * uint32, bit b%32 of word b/32 = beam b may contribute to some receiver of the
  * tile).  tight_bits (same shape, may be NULL) is the subset the fp32 kernel
@@ -154,8 +154,9 @@ int bf_write_field_csv(const char *path, const double *points, int64_t n_obs,
 int bf_tile_size(void);
 
 /*
- * Spatial (Morton, 21 bits/axis over the bounding box) order of n device
- * observers: perm[i] = index of the i-th receiver in tile order.  Deterministic,
+ * Spatial order of n device observers (Hilbert curve, 21 bits per axis, isotropic
+ * over the bounding box; the 2-D curve for planar sets): perm[i] = index of the i-th
+ * receiver in tile order.  Deterministic,
  * so every rank of a multi-GPU run derives the same receiver-tile partition.
  */
 int bf_tile_order_dev(const double *obs, int64_t n, int32_t *perm, int device, void *stream);

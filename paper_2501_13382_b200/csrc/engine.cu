@@ -4,7 +4,7 @@
 // kernels.gbs_accumulate (kernels.py:352-399) and its neighbours; this file
 // owns everything between that boundary and the kernels: argument checks that
 // mirror the reference's contracts, per-device streams and grow-only
-// workspaces, host<->device staging of the caller's ranges, the Morton
+// workspaces, host<->device staging of the caller's ranges, the Hilbert
 // receiver tiling used by the fp32 kernel, and the beam segment prefix sums.
 #include <cuda_runtime.h>
 
@@ -189,18 +189,74 @@ __device__ __forceinline__ uint64_t spread3(uint64_t x) {
     return x;
 }
 
-__global__ void morton_kernel(const double *obs, int64_t n, const double *bbox, uint64_t *keys,
-                              int32_t *vals) {
+// Hilbert index of a receiver (the tiling order: consecutive receivers are spatial
+// neighbours with no jumps, so 128-receiver patches and 512-receiver tiles are compact).
+// Isotropic quantisation to 21 bits per axis over the bounding box; a planar set (third
+// extent < 1/64 of the largest) uses the 2-D curve of its two largest axes.
+__device__ __forceinline__ uint64_t hilbert2(uint64_t x, uint64_t y) {
+    const uint64_t n = 1ull << 21;
+    uint64_t d = 0;
+    for (uint64_t s = n >> 1; s > 0; s >>= 1) {
+        const uint64_t rx = (x & s) ? 1 : 0, ry = (y & s) ? 1 : 0;
+        d += s * s * ((3 * rx) ^ ry);
+        if (ry == 0) {  // rotate the quadrant
+            if (rx == 1) {
+                x = n - 1 - x;
+                y = n - 1 - y;
+            }
+            const uint64_t t = x;
+            x = y;
+            y = t;
+        }
+    }
+    return d;
+}
+
+// 3-D curve: axes -> transposed Hilbert index (Skilling's construction), bit-interleaved.
+__device__ __forceinline__ uint64_t hilbert3(uint64_t x0, uint64_t x1, uint64_t x2) {
+    uint64_t X[3] = {x0, x1, x2};
+    for (uint64_t Q = 1ull << 20; Q > 1; Q >>= 1) {
+        const uint64_t P = Q - 1;
+        for (int i = 0; i < 3; ++i) {
+            if (X[i] & Q) {
+                X[0] ^= P;
+            } else {
+                const uint64_t t = (X[0] ^ X[i]) & P;
+                X[0] ^= t;
+                X[i] ^= t;
+            }
+        }
+    }
+    X[1] ^= X[0];
+    X[2] ^= X[1];
+    uint64_t t = 0;
+    for (uint64_t Q = 1ull << 20; Q > 1; Q >>= 1)
+        if (X[2] & Q) t ^= Q - 1;
+    for (int i = 0; i < 3; ++i) X[i] ^= t;
+    return spread3(X[2]) | (spread3(X[1]) << 1) | (spread3(X[0]) << 2);
+}
+
+__global__ void order_key_kernel(const double *obs, int64_t n, const double *bbox,
+                                 uint64_t *keys, int32_t *vals) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    double ext[3], emax = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        ext[d] = bbox[3 + d] - bbox[d];
+        emax = fmax(emax, ext[d]);
+    }
     uint64_t q[3];
     for (int d = 0; d < 3; ++d) {
-        const double ext = bbox[3 + d] - bbox[d];
-        double u = ext > 0 ? (obs[3 * i + d] - bbox[d]) / ext : 0.0;
+        double u = emax > 0 ? (obs[3 * i + d] - bbox[d]) / emax : 0.0;
         u = fmin(fmax(u, 0.0), 1.0);
         q[d] = (uint64_t)(u * 2097151.0);
     }
-    keys[i] = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+    // axes by decreasing extent (ties: lower axis first)
+    int a0 = 0, a1 = 1, a2 = 2;
+    if (ext[a1] > ext[a0]) { const int t = a0; a0 = a1; a1 = t; }
+    if (ext[a2] > ext[a1]) { const int t = a1; a1 = a2; a2 = t; }
+    if (ext[a1] > ext[a0]) { const int t = a0; a0 = a1; a1 = t; }
+    keys[i] = ext[a2] * 64.0 < emax ? hilbert2(q[a0], q[a1]) : hilbert3(q[a0], q[a1], q[a2]);
     vals[i] = (int32_t)i;
 }
 
@@ -251,8 +307,8 @@ __global__ void iota_kernel(int32_t *v, int64_t n) {
     if (i < n) v[i] = (int32_t)i;
 }
 
-// Morton order of n observers into *perm (a workspace buffer).
-int morton_order(DeviceCtx *c, const double *obs, int64_t n, cudaStream_t st,
+// Hilbert order of n observers into *perm (a workspace buffer).
+int hilbert_order(DeviceCtx *c, const double *obs, int64_t n, cudaStream_t st,
                  const int32_t **perm) {
     double *bbox;
     uint64_t *k1, *k2;
@@ -265,7 +321,7 @@ int morton_order(DeviceCtx *c, const double *obs, int64_t n, cudaStream_t st,
     // pass 1: 256 partial boxes (min block-major in bbox[6..], max after); pass 2: final
     bbox_kernel<<<256, 256, 0, st>>>(obs, n, 1, bbox + 6);
     bbox_kernel<<<1, 256, 0, st>>>(bbox + 6, 256, 0, bbox);
-    morton_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(obs, n, bbox, k1, v1);
+    order_key_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(obs, n, bbox, k1, v1);
     note_launch(3);
     BF_TRY_CUDA(cudaGetLastError());
     cub::DoubleBuffer<uint64_t> dk(k1, k2);
@@ -301,7 +357,7 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
         note_launch();
         perm = id;
     } else {
-        BF_TRY(morton_order(c, obs, n, st, &perm));
+        BF_TRY(hilbert_order(c, obs, n, st, &perm));
     }
     if (T == 512)
         tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm, rloc, cen, box);
@@ -849,7 +905,7 @@ int bf_tile_order_dev(const double *obs, int64_t n, int32_t *perm, int device, v
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
     StreamOrder order(ctx, st);
     const int32_t *p;
-    BF_TRY(morton_order(ctx, obs, n, st, &p));
+    BF_TRY(hilbert_order(ctx, obs, n, st, &p));
     BF_TRY_CUDA(cudaMemcpyAsync(perm, p, 4 * n, cudaMemcpyDeviceToDevice, st));
     if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
     return BF_OK;

@@ -4,7 +4,7 @@
 // nearest_on_segments (kernels.py:304-349), re-designed for the B200 FP32/MUFU
 // pipes.  DESIGN.md holds the error analysis behind every tolerance here.
 //
-//  * Receivers are Morton-sorted (engine.cu); 128 consecutive receivers form a
+//  * Receivers are Hilbert-sorted (engine.cu); 128 consecutive receivers form a
 //    warp PATCH (lane l holds receivers 4l..4l+3), four patches a work-list
 //    TILE.  patch_kernel stores every receiver in PATCH-LOCAL fp32
 //    coordinates r = p - c_P (fp64 subtraction) with |r|^2, so fp32 never

@@ -3,7 +3,7 @@
 SURVEY.md 8(e): each receiver's sum depends on all beams and on nothing else
 (kernels.py:364-399), so receivers shard with no data-path exchange -- the
 reference's observer-range split across workers (parallel.py:108-140), re-cut
-as SPATIAL tiles: the global Morton order (bf_tile_order_dev) is cut into
+as SPATIAL tiles: the global Hilbert order (bf_tile_order_dev) is cut into
 tiles of bf_tile_size() receivers, dealt round-robin to the ranks (balancing
 the spatially varying tie-path / cutoff density), and every rank sums its
 tiles with the presorted flag so the kernel's tiles ARE the global tiles.

@@ -28,7 +28,7 @@ def _worker(rank, world, port, n, F, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2501_13382_b200 import shard
-    # a deterministic stand-in for the device Morton order
+    # a deterministic stand-in for the device Hilbert order
     order = torch.from_numpy(np.random.default_rng(7).permutation(n)).long()
     mine = shard.rank_indices(order, rank, world, tile=64)
     acc, ev = field_of(mine, F)
