@@ -382,9 +382,10 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
 // Live mask of the R receivers of a single-segment-0 beam whose patch reaches the
 // launch plane: behind = proj < 0 (kernels.py:348,375); |proj| within the fp32
 // error bound is re-decided with the reference's exact fp64 projection.
-__device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&pj)[R],
-                                             const double (*p64)[3], int nvalid, float D,
-                                             int64_t beam, int k, unsigned &ties) {
+__device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Work &w,
+                                             const float (&pj)[R], const double (*p64)[3],
+                                             int nvalid, float D, int64_t beam, int k,
+                                             unsigned &ties) {
     const float tolp = PROJ_ERR * D;
     unsigned m = 0, amb = 0;
 #pragma unroll
@@ -396,10 +397,9 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const float (&
     }
     if (amb) {  // rare: one copy of the fp64 code
         const int64_t row = beam * a.max_seg + k;
-        const double ox = a.seg_origin[3 * row], oy = a.seg_origin[3 * row + 1],
-                     oz = a.seg_origin[3 * row + 2];
-        const double dx = a.seg_dir[3 * row], dy = a.seg_dir[3 * row + 1],
-                     dz = a.seg_dir[3 * row + 2];
+        const double4 o4 = w.p0[row], d4 = w.p1[row];  // packed fp64 rows (exact copies)
+        const double ox = o4.x, oy = o4.y, oz = o4.z;
+        const double dx = d4.x, dy = d4.y, dz = d4.z;
         ties += __popc(amb);
 #pragma unroll 1
         for (; amb; amb &= amb - 1) {
@@ -569,7 +569,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         const float q2 =
             fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
                   0.f);
-        const float s = (float)(a.seg_s0[beam * a.max_seg + k] + e.bt);  // kernels.py:344
+        const float s = (float)(w.p1[beam * a.max_seg + k].w + e.bt);  // kernels.py:344
         // anchor choice follows the exact clamp
         const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
         const float A = S.aux[r0 + k].y;
@@ -752,6 +752,20 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #else
             word = classify<NF, MF>(S, K, r0, nsb, w.pbox[p], D);
 #endif
+#if !BF_NOPF
+            {   // corner wedges and two-adjacent-survivor items read the fp64 rows of the
+                // junction (load_junction): start those loads now, into L1
+                const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
+                const int ka = __ffs(m) - 1;
+                if ((word & WEDGE) || (m != 0 && m == (3u << ka))) {
+                    const int64_t g = (int64_t)S.gbeam[lane] * a.max_seg + ka;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g + 1));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g + 1));
+                }
+            }
+#endif
             S.desc[lane] = make_int4(S.gbeam[lane], (int)word, r0, __float_as_int(D));
         }
         const unsigned live = __ballot_sync(0xffffffffu, word != 0);
@@ -850,7 +864,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 lvm = (1u << R) - 1;
                 if (bword & BEHIND_CHECK)
-                    lvm = behind_mask(a, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, beam, k, ties);
+                    lvm = behind_mask(a, w, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, beam, k, ties);
             } else {
                 // receivers decided at the junction of segments ka, ka+1 (corner wedge):
                 // both clamped distances are distances to the reflection point, an exact
