@@ -95,7 +95,7 @@ struct Fp32Consts {
     double kappa64[BF_MAXF];
     float omega[BF_MAXF];
     float omrel[BF_MAXF];    // omega_f / omega_0 (the staged amplitude carries omega_0)
-    float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36)
+    float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36); 0 without cutoff
     float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
     float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
     float b, b2;             // width_b, width_b^2
@@ -199,7 +199,7 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
     const float gqs = gq * s;
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-        const bool lf = live && !(NF > 1 && use_cutoff && q2 * K.cutk[f] > m2);  // ex_re < -36
+        const bool lf = live && !(NF > 1 && q2 * K.cutk[f] > m2);  // ex_re < -36
         float turns = fmaf(gqs, K.hk2pi[f], base[f]);
 #if !BF_NORED
         turns -= rintf(turns);
@@ -1032,7 +1032,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 m2j[j] = fmaf(sj[j], sj[j], K.b2);
-                if (!MF && a.use_cutoff && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);
+                if (!MF && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);  // cutk 0: no cutoff
             }
             if constexpr (!MF) {
             // receivers evaluated in groups of EVG (one branch, EVG independent chains)
@@ -1062,7 +1062,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 unsigned lf = 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j)
-                    if (((lvm >> j) & 1u) && !(a.use_cutoff && q2j[j] * K.cutk[f] > m2j[j]))
+                    if (((lvm >> j) & 1u) && !(q2j[j] * K.cutk[f] > m2j[j]))
                         lf |= 1u << j;  // ex_re < -36 (kernels.py:384)
                 if (__any_sync(0xffffffffu, lf != 0)) {
 #pragma unroll
@@ -1437,7 +1437,7 @@ Fp32Consts make_consts(const GbsArgs &a) {
         K.kappa[f] = (float)K.kappa64[f];
         K.omega[f] = (float)w;
         K.omrel[f] = f < a.nf ? (float)(w / a.omegas[0]) : 0.f;
-        K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
+        K.cutk[f] = a.use_cutoff ? (float)(w * a.width_b / (72.0 * a.c)) : 0.f;  // 0: never cut
         K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
         K.nhkbl2e[f] = (float)(-(w * 0.5 / a.c) * a.width_b * 1.4426950408889634);
     }
