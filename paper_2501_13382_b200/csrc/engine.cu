@@ -191,8 +191,11 @@ __device__ __forceinline__ uint64_t spread3(uint64_t x) {
 
 // Hilbert index of a receiver (the tiling order: consecutive receivers are spatial
 // neighbours with no jumps, so 128-receiver patches and 512-receiver tiles are compact).
-// Isotropic quantisation to 21 bits per axis over the bounding box; a planar set (third
-// extent < 1/64 of the largest) uses the 2-D curve of its two largest axes.
+// A planar set (third extent < 1/64 of the largest) is cut along its longest axis into
+// square blocks of the second extent, each traversed by the 2-D curve (which enters a
+// block at its lower-left and leaves at its lower-right corner, so consecutive blocks
+// join up); key = block << 42 | 2-D index.  Otherwise the 3-D curve over the isotropic
+// bounding cube.  21 bits per axis within a block / the cube.
 __device__ __forceinline__ uint64_t hilbert2(uint64_t x, uint64_t y) {
     const uint64_t n = 1ull << 21;
     uint64_t d = 0;
@@ -256,7 +259,22 @@ __global__ void order_key_kernel(const double *obs, int64_t n, const double *bbo
     if (ext[a1] > ext[a0]) { const int t = a0; a0 = a1; a1 = t; }
     if (ext[a2] > ext[a1]) { const int t = a1; a1 = a2; a2 = t; }
     if (ext[a1] > ext[a0]) { const int t = a0; a0 = a1; a1 = t; }
-    keys[i] = ext[a2] * 64.0 < emax ? hilbert2(q[a0], q[a1]) : hilbert3(q[a0], q[a1], q[a2]);
+    if (ext[a2] * 64.0 < emax) {
+        const double L = fmax(ext[a1], ext[a0] * 0x1p-20);  // block side, <= 2^20 blocks
+        if (!(L > 0.0)) {
+            keys[i] = 0;
+        } else {
+            const double nbl = ceil(ext[a0] / L);
+            const double u0 = (obs[3 * i + a0] - bbox[a0]) / L;
+            const double blk = fmin(floor(u0), fmax(nbl - 1.0, 0.0));
+            const double f0 = fmin(fmax(u0 - blk, 0.0), 1.0);
+            const double f1 = fmin(fmax((obs[3 * i + a1] - bbox[a1]) / L, 0.0), 1.0);
+            keys[i] = ((uint64_t)blk << 42) |
+                      hilbert2((uint64_t)(f0 * 2097151.0), (uint64_t)(f1 * 2097151.0));
+        }
+    } else {
+        keys[i] = hilbert3(q[a0], q[a1], q[a2]);
+    }
     vals[i] = (int32_t)i;
 }
 

@@ -538,3 +538,22 @@ def test_fp32_random_city_vs_oracle(seed, threads):
     assert tl_db(acc, ref, floor_db=-60.0) <= FP32_TL_DB
     assert tl_db(acc, ref) <= FP32_TL_ALL_DB
     assert abs(int(ev.sum()) - int(rev.sum())) <= 1e-4 * int(rev.sum()) + 10
+
+
+@pytest.mark.parametrize("n1,n2", [(100, 37), (1000, 40), (333, 333), (37, 100)])
+def test_tile_order_compact_patches(n1, n2):
+    """The receiver order (bf_tile_order_dev) has no jumps on rectangular grids, so every
+    128-receiver patch is a compact blob (0.25 m grid: radius <= 4 m; Morton order and an
+    isotropic single Hilbert square left 12-60 m patches across jumps)."""
+    import torch
+
+    from paper_2501_13382_b200 import shard
+    X, Y = np.meshgrid(np.arange(n1) * 0.25 - 7.0, np.arange(n2) * 0.25 + 3.0, indexing="xy")
+    P = np.stack([X.ravel(), Y.ravel(), np.full(X.size, 1.5)], axis=1)
+    order = shard.tile_order(torch.from_numpy(P).to("cuda:0")).cpu().numpy()
+    assert np.array_equal(np.sort(order), np.arange(P.shape[0]))
+    Q = P[order]
+    for p in range(Q.shape[0] // 128):
+        B = Q[128 * p:128 * (p + 1)]
+        c = 0.5 * (B.min(0) + B.max(0))
+        assert np.sqrt(((B - c) ** 2).sum(1).max()) <= 4.0
