@@ -1,7 +1,8 @@
 #!/bin/bash
-# Build kernel-configuration variants of libbf_gbs.so (tuning sweeps only).
+# Build kernel-configuration variants of libbf_gbs.so (tuning sweeps only):
+#   bash scripts/build_variants.sh "-DBF_ROWCAP=64" "-DBF_RANGES=32" ...
 set -e
-cd "$(dirname "$0")/paper_2501_13382_b200/csrc"
+cd "$(dirname "$0")/../paper_2501_13382_b200/csrc"
 mkdir -p ../_lib/variants
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
