@@ -1,7 +1,9 @@
 """Broad randomized parity fuzz of the fp32 path against the C oracle (GPU; test
 infrastructure, not collected by pytest):
 
-    python tests/fuzz_parity.py FIRST_SEED LAST_SEED
+    python tests/fuzz_parity.py FIRST_SEED LAST_SEED          (fp32 mode)
+    FUZZ_PREC=fp64 python tests/fuzz_parity.py FIRST LAST     (fp64 mode: rel <= 1e-12,
+                                                              evaluation counts bit-exact)
 
 Per seed: ground plane or city, source anywhere in a street (0.3-40 m high), 1-8
 frequencies in 40-2000 Hz, beam parameter -1.5 .. -50000 (log-uniform), cutoff on/off,
@@ -22,6 +24,7 @@ from paper_2501_13382_b200 import engine, kernels
 from paper_2501_13382_b200.beamtrace import Atmosphere, LaunchGrid, SourceSpec, TraceConfig, launch_directions
 from paper_2501_13382_b200.scene import make_city, make_ground_plane
 dev = torch.device("cuda", 0)
+PREC = os.environ.get("FUZZ_PREC", "fp32")
 fails = []; worst = 0.0
 for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     rng = np.random.default_rng(5000 + seed)
@@ -61,7 +64,7 @@ for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     oracle.gbs_accumulate(*args, ref, rev, 0, obs.shape[0], 0, nb, threads=16)
     acc = np.zeros_like(ref); ev = np.zeros_like(rev)
     try:
-        kernels.gbs_accumulate(*args, acc, ev, 0, obs.shape[0], 0, nb, precision="fp32")
+        kernels.gbs_accumulate(*args, acc, ev, 0, obs.shape[0], 0, nb, precision=PREC)
     except Exception as e:
         fails.append((seed, "ERR " + repr(e)[:200])); continue
     if not np.any(ref):
@@ -74,7 +77,11 @@ for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     l2 = rel_l2(acc, ref); t60 = tl_db(acc, ref, floor_db=-60.0); tall = tl_db(acc, ref)
     evd = abs(int(ev.sum()) - int(rev.sum()))
     worst = max(worst, t60)
-    if l2 > 1e-4 or t60 > 0.01 or evd > 1e-4 * int(rev.sum()) + 10:
+    if PREC == "fp64":
+        bad = l2 > 1e-12 or not np.array_equal(ev, rev)
+    else:
+        bad = l2 > 1e-4 or t60 > 0.01 or evd > 1e-4 * int(rev.sum()) + 10
+    if bad:
         fails.append((seed, dict(kind=int(kind), nf=nf, im_b=round(im_b, 2), cut=use_cutoff, sp=round(sp, 3), R=round(R, 1), rmax=cfg.r_max if hasattr(cfg, 'r_max') else None, l2=l2, t60=t60, tall=tall, evd=evd, evsum=int(rev.sum()))))
 print("fuzz2", sys.argv[1:], "failures", len(fails), "worst t60 %.4f" % worst)
 for f in fails: print(f)
