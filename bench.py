@@ -229,13 +229,16 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     prec = args.precision
 
+    # the gather's index plan is part of the partition, built once (not per step)
+    plan = shard.GatherPlan(order, world, n_total) if world > 1 else None
+
     def step():
         acc.zero_()
         evals.zero_()
         engine.accumulate(bundle, obs, omegas, width_b, True, acc, evals, precision=prec,
                           stream=stream, presorted=True)
         if world > 1:
-            shard.gather_field(acc, evals, order, rank, world, n_total)
+            shard.gather_field(acc, evals, order, rank, world, n_total, plan=plan)
 
     for _ in range(args.warmup):
         step()

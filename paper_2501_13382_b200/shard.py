@@ -65,37 +65,62 @@ def rank_indices(order, rank: int, world_size: int, tile: int | None = None):
     return np.asarray(order)[pos]
 
 
+class GatherPlan:
+    """Where every row of the gathered per-rank payloads goes in the global order.
+
+    Built once per (order, world size); the gather itself is then one collective plus
+    one device scatter (no host index work inside a timed step).
+    sizes[r] = receivers of rank r, cap = max(sizes); dest (world*cap,) holds the global
+    receiver index of each gathered row, n_total for padding rows.
+    """
+
+    def __init__(self, order, world_size: int, n_total: int, tile: int | None = None):
+        import torch
+        tile = tile_size() if tile is None else tile
+        self.world_size, self.n_total = world_size, n_total
+        self.sizes = [rank_tiles(n_total, r, world_size, tile).size for r in range(world_size)]
+        self.cap = max(self.sizes) if self.sizes else 0
+        dev = order.device if hasattr(order, "device") else "cpu"
+        dest = torch.full((world_size * self.cap,), n_total, dtype=torch.long, device=dev)
+        for r in range(world_size):
+            idx = rank_indices(order, r, world_size, tile)
+            idx = torch.as_tensor(idx, device=dev).long()
+            dest[r * self.cap:r * self.cap + self.sizes[r]] = idx
+        self.dest = dest
+
+
 def gather_field(acc, evals, order, rank: int, world_size: int, n_total: int, group=None,
-                 tile: int | None = None):
+                 tile: int | None = None, plan: GatherPlan | None = None):
     """Gather per-rank (acc, evals) to rank 0 and scatter them into global order.
 
     acc is (n_local, F) complex128, evals (n_local,) int64, both in the rank's
     tile order.  Returns (acc_full, evals_full) on rank 0, (None, None) elsewhere.
-    Works for NCCL (CUDA tensors) and gloo (CPU tensors).
+    Works for NCCL (CUDA tensors, one all_gather_into_tensor) and gloo (CPU tensors).
+    `plan` (GatherPlan of the same order/world) is built on the fly if not given.
     """
     import torch
     import torch.distributed as dist
+    if plan is None:
+        plan = GatherPlan(order, world_size, n_total, tile)
     F = acc.shape[1]
-    sizes = [rank_tiles(n_total, r, world_size, tile).size for r in range(world_size)]
-    cap = max(sizes)
+    cap = plan.cap
     # complex -> float64 (NCCL has no complex type); evals ride as float64 bits
     pay = torch.zeros((cap, 2 * F + 1), dtype=torch.float64, device=acc.device)
     n_loc = acc.shape[0]
     pay[:n_loc, :2 * F] = torch.view_as_real(acc).reshape(n_loc, 2 * F)
     pay[:n_loc, 2 * F] = evals.view(torch.float64)
-    if pay.is_cuda and dist.get_backend(group) == "gloo":  # gloo gathers host tensors
-        pay = pay.cpu()
-    bufs = [torch.empty_like(pay) for _ in range(world_size)]
-    dist.all_gather(bufs, pay, group=group)
-    bufs = [b.to(acc.device) for b in bufs]
+    if dist.get_backend(group) == "gloo":  # gloo gathers host tensors, as a list
+        bufs = [torch.empty_like(pay.cpu()) for _ in range(world_size)]
+        dist.all_gather(bufs, pay.cpu(), group=group)
+        allp = torch.cat(bufs).to(acc.device)
+    else:
+        allp = torch.empty((world_size * cap, 2 * F + 1), dtype=torch.float64, device=acc.device)
+        dist.all_gather_into_tensor(allp, pay, group=group)
     if rank != 0:
         return None, None
-    acc_full = torch.zeros((n_total, F), dtype=torch.complex128, device=acc.device)
-    evals_full = torch.zeros(n_total, dtype=torch.int64, device=acc.device)
-    for r in range(world_size):
-        idx = rank_indices(order, r, world_size, tile)
-        idx = torch.as_tensor(idx, device=acc.device).long()
-        k = sizes[r]
-        acc_full[idx] = torch.view_as_complex(bufs[r][:k, :2 * F].reshape(k, F, 2).contiguous())
-        evals_full[idx] = bufs[r][:k, 2 * F].contiguous().view(torch.int64)
+    dest = plan.dest.to(acc.device)
+    out = torch.zeros((n_total + 1, 2 * F + 1), dtype=torch.float64, device=acc.device)
+    out[dest] = allp  # padding rows land in the extra row n_total
+    acc_full = torch.view_as_complex(out[:n_total, :2 * F].reshape(n_total, F, 2).contiguous())
+    evals_full = out[:n_total, 2 * F].contiguous().view(torch.int64)
     return acc_full, evals_full

@@ -32,7 +32,8 @@ def _worker(rank, world, port, n, F, q):
     order = torch.from_numpy(np.random.default_rng(7).permutation(n)).long()
     mine = shard.rank_indices(order, rank, world, tile=64)
     acc, ev = field_of(mine, F)
-    full, evf = shard.gather_field(acc, ev.long(), order, rank, world, n, tile=64)
+    plan = shard.GatherPlan(order, world, n, tile=64) if F > 1 else None
+    full, evf = shard.gather_field(acc, ev.long(), order, rank, world, n, tile=64, plan=plan)
     if rank == 0:
         want, want_ev = field_of(torch.arange(n), F)
         q.put((bool(torch.equal(full, want)), bool(torch.equal(evf, want_ev))))
@@ -40,12 +41,12 @@ def _worker(rank, world, port, n, F, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,F", [(1000, 1), (333, 5)])
-def test_gather_field_world2(n, F):
+@pytest.mark.parametrize("n,F,world", [(1000, 1, 2), (333, 5, 2), (1000, 3, 3)])
+def test_gather_field_world2(n, F, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, F, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, F, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
