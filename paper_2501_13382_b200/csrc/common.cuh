@@ -130,8 +130,11 @@ int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsSta
                     const StreamPair &st);
 int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam,
                    int64_t n_query, double *out, cudaStream_t st);
+// cbox: scratch for ceil(n_tri/16) cluster boxes (6 doubles each), or null for the
+// exhaustive hit search.
+int trace_cluster_count(int64_t n_tri);
 int launch_trace(const double *v0, const double *v1, const double *v2, const double *refl,
-                 int64_t n_tri, const double *bounds, double diameter, const double *origin,
+                 int64_t n_tri, double *cbox, const double *bounds, double diameter, const double *origin,
                  const double *dirs, const double *e1s, const double *e2s, double length_cap,
                  int64_t r_max, int64_t max_seg, double *seg_origin, double *seg_dir,
                  double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,

@@ -72,7 +72,7 @@ enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
     B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_TBOX, B_UKEYS, B_UKEYS2, B_UVALS, B_UVALS2, B_COUNT
+    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_TBOX, B_UKEYS, B_UKEYS2, B_UVALS, B_UVALS2, B_CBOX, B_COUNT
 };
 
 struct DeviceCtx {
@@ -828,7 +828,14 @@ int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
-    BF_TRY(launch_trace(v0, v1, v2, refl_coef, n_tri, bounds, diameter, origin, dirs, e1s, e2s,
+    StreamOrder order(ctx, st);
+    // triangle-cluster boxes for the hit search; BF_TRACE_EXHAUSTIVE=1 tests every
+    // triangle (the self-check of the culling, same bits)
+    double *cbox = nullptr;
+    const char *ex = getenv("BF_TRACE_EXHAUSTIVE");
+    if (n_tri > 0 && !(ex && ex[0] == '1'))
+        BF_TRY(ctx->get(B_CBOX, (size_t)(6 * trace_cluster_count(n_tri)), &cbox));
+    BF_TRY(launch_trace(v0, v1, v2, refl_coef, n_tri, cbox, bounds, diameter, origin, dirs, e1s, e2s,
                         length_cap, r_max, max_seg, seg_origin, seg_dir, seg_e1, seg_e2, seg_len,
                         seg_s0, seg_refl, n_segs, n_refls, lo, hi, row_base, st));
     if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));

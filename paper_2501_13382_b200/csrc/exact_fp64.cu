@@ -215,6 +215,8 @@ __device__ __forceinline__ double ray_box_exit(const double *bounds, double ox, 
 struct TraceArgs {
     const double *v0, *v1, *v2, *refl;
     int64_t n_tri;
+    const double *cbox;  // per cluster of TRI_CLUSTER consecutive triangles: expanded AABB
+    int64_t n_clu;       // 0: exhaustive search
     const double *bounds;
     double diameter;
     const double *origin, *dirs, *e1s, *e2s;
@@ -247,6 +249,60 @@ __device__ __forceinline__ void write_row(const TraceArgs &a, int64_t row, doubl
     a.seg_refl[row] = refl;
 }
 
+// Triangle clusters for the hit search: TRI_CLUSTER consecutive triangles (the scene
+// generators emit a building's faces contiguously) share an axis-aligned box, expanded
+// by 1e-7 + 1e-9 |x| so that it contains every point the exact intersection test can
+// accept.  A cluster is skipped when the ray misses its box or enters it beyond the best
+// hit so far; the selection -- lexicographic minimum of (t, triangle index) over the
+// accepted hits -- does not depend on the order triangles are visited, so the result is
+// bit-identical to the exhaustive search (tests/test_gbs_gpu.py checks both).
+constexpr int TRI_CLUSTER = 16;
+
+__global__ void cluster_box_kernel(const double *v0, const double *v1, const double *v2,
+                                   int64_t n_tri, int64_t n_clu, double *cbox) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_clu) return;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    const int64_t t1 = min(n_tri, (c + 1) * TRI_CLUSTER);
+    for (int64_t t = c * TRI_CLUSTER; t < t1; ++t)
+        for (int d = 0; d < 3; ++d) {
+            const double a = v0[3 * t + d], b = v1[3 * t + d], e = v2[3 * t + d];
+            lo[d] = fmin(lo[d], fmin(a, fmin(b, e)));
+            hi[d] = fmax(hi[d], fmax(a, fmax(b, e)));
+        }
+    for (int d = 0; d < 3; ++d) {
+        cbox[6 * c + d] = lo[d] - (1e-7 + 1e-9 * fabs(lo[d]));
+        cbox[6 * c + 3 + d] = hi[d] + (1e-7 + 1e-9 * fabs(hi[d]));
+    }
+}
+
+// Can the ray (o, d) meet box B at a parameter t <= tmax_allowed?  Conservative: slab
+// intervals widened by a relative 1e-9 (the box itself is already expanded).
+__device__ __forceinline__ bool ray_may_hit_box(const double *B, double ox, double oy,
+                                                double oz, double dx, double dy, double dz,
+                                                double tmax_allowed) {
+    double tmin = -INFINITY, tmax = INFINITY;
+    const double o[3] = {ox, oy, oz}, dd[3] = {dx, dy, dz};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (fabs(dd[k]) < 1e-300) {
+            if (o[k] < B[k] || o[k] > B[3 + k]) return false;
+            continue;
+        }
+        const double inv = 1.0 / dd[k];
+        double t1 = (B[k] - o[k]) * inv, t2 = (B[3 + k] - o[k]) * inv;
+        if (t1 > t2) {
+            const double t = t1;
+            t1 = t2;
+            t2 = t;
+        }
+        tmin = fmax(tmin, t1);
+        tmax = fmin(tmax, t2);
+    }
+    const double slack = 1e-9 * (1.0 + fabs(tmin) + fabs(tmax));
+    return tmax >= -slack && tmin <= tmax + slack && tmin <= tmax_allowed + slack;
+}
+
 // One thread per ray (kernels.py:282-301 / 143-279).
 __global__ void __launch_bounds__(128) trace_kernel(const TraceArgs a) {
     const int64_t i = a.lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -267,15 +323,24 @@ __global__ void __launch_bounds__(128) trace_kernel(const TraceArgs a) {
         // Nearest hit with t in (EPS_HIT, remaining]; ties -> lower triangle index.
         double best_t = remaining;
         int64_t best_i = -1;
-        for (int64_t tri = 0; tri < a.n_tri; ++tri) {
-            const double t = tri_intersect(px, py, pz, dx, dy, dz, a.v0 + 3 * tri,
-                                           a.v1 + 3 * tri, a.v2 + 3 * tri);
-            if (t > BF_EPS_HIT && t <= best_t) {
-                if (t < best_t || best_i < 0 || tri < best_i) {
-                    best_t = t;
-                    best_i = tri;
+        auto visit = [&](int64_t t0, int64_t t1) {
+            for (int64_t tri = t0; tri < t1; ++tri) {
+                const double t = tri_intersect(px, py, pz, dx, dy, dz, a.v0 + 3 * tri,
+                                               a.v1 + 3 * tri, a.v2 + 3 * tri);
+                if (t > BF_EPS_HIT && t <= best_t) {
+                    if (t < best_t || best_i < 0 || tri < best_i) {
+                        best_t = t;
+                        best_i = tri;
+                    }
                 }
             }
+        };
+        if (a.n_clu > 0) {
+            for (int64_t c = 0; c < a.n_clu; ++c)
+                if (ray_may_hit_box(a.cbox + 6 * c, px, py, pz, dx, dy, dz, best_t))
+                    visit(c * TRI_CLUSTER, min(a.n_tri, (c + 1) * TRI_CLUSTER));
+        } else {
+            visit(0, a.n_tri);
         }
         if (best_i < 0) {
             double seg = remaining;
@@ -536,15 +601,24 @@ int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam
     return BF_OK;
 }
 
+int trace_cluster_count(int64_t n_tri) { return (int)((n_tri + TRI_CLUSTER - 1) / TRI_CLUSTER); }
+
 int launch_trace(const double *v0, const double *v1, const double *v2, const double *refl,
-                 int64_t n_tri, const double *bounds, double diameter, const double *origin,
+                 int64_t n_tri, double *cbox, const double *bounds, double diameter,
+                 const double *origin,
                  const double *dirs, const double *e1s, const double *e2s, double length_cap,
                  int64_t r_max, int64_t max_seg, double *seg_origin, double *seg_dir,
                  double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
                  double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
                  int64_t row_base, cudaStream_t st) {
     if (hi <= lo) return BF_OK;
-    TraceArgs a{v0, v1, v2, refl, n_tri, bounds, diameter, origin, dirs, e1s, e2s,
+    const int64_t n_clu = cbox ? (n_tri + TRI_CLUSTER - 1) / TRI_CLUSTER : 0;
+    if (n_clu > 0) {
+        cluster_box_kernel<<<(unsigned)((n_clu + 127) / 128), 128, 0, st>>>(v0, v1, v2, n_tri,
+                                                                           n_clu, cbox);
+        note_launch();
+    }
+    TraceArgs a{v0, v1, v2, refl, n_tri, cbox, n_clu, bounds, diameter, origin, dirs, e1s, e2s,
                 length_cap, r_max, max_seg, seg_origin, seg_dir, seg_e1, seg_e2, seg_len,
                 seg_s0, seg_refl, n_segs, n_refls, lo, hi, row_base};
     const unsigned blocks = (unsigned)((hi - lo + 127) / 128);

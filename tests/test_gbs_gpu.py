@@ -557,3 +557,32 @@ def test_tile_order_compact_patches(n1, n2):
         B = Q[128 * p:128 * (p + 1)]
         c = 0.5 * (B.min(0) + B.max(0))
         assert np.sqrt(((B - c) ** 2).sum(1).max()) <= 4.0
+
+
+@pytest.mark.parametrize("src", [(0.0, 20.0, 2.0), (-37.0, 3.0, 25.0), (150.0, -260.0, 1.0)])
+def test_tracer_cluster_culling_equals_exhaustive(src, monkeypatch):
+    """The tracer's triangle-cluster culling returns the same bits as testing every
+    triangle (config-4 city: 500 buildings, 5002 triangles, up to 8 reflections)."""
+    import torch
+
+    from paper_2501_13382_b200 import engine
+    from paper_2501_13382_b200.beamtrace import (Atmosphere, LaunchGrid, SourceSpec,
+                                                 TraceConfig, launch_directions)
+    from paper_2501_13382_b200.scene import make_city
+    dev = torch.device("cuda", 0)
+    sc = make_city(20, 25, 40.0, 20.0, 600.0)
+    source = SourceSpec(position=np.array(src), frequencies=(125.0,), beam_param_im=-10.0)
+    launch = launch_directions(LaunchGrid(0.0, 180.0, 0.0, 360.0, 90, 180))
+    cfg = TraceConfig(5000, 1e-4, 8)
+    c = Atmosphere(20.0).sound_speed
+    ds = engine.DeviceScene.from_scene(sc, dev)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BF_TRACE_EXHAUSTIVE", mode)
+        out[mode] = engine.trace_device_rows(ds, source, launch, cfg, c, 0, len(launch), dev)
+        torch.cuda.synchronize()
+    a, b = out["0"]["bundle"], out["1"]["bundle"]
+    for name in ("seg_origin", "seg_dir", "seg_e1", "seg_e2", "seg_len", "seg_s0", "seg_refl",
+                 "n_segs", "n_refls"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    assert int(a.n_refls.max()) >= 2  # the rays do bounce between buildings
