@@ -64,6 +64,9 @@ namespace {
 #ifndef BF_RANGES
 #define BF_RANGES 64
 #endif
+#ifndef BF_FLUSHN
+#define BF_FLUSHN 4  // several frequencies: chunks per fp64 flush of the partials (power of 2)
+#endif
 constexpr int R = 4;                    // receivers per lane
 constexpr int PATCH = 32 * R;           // receivers per warp patch
 constexpr int TILE = 4 * PATCH;         // receivers per work-list tile
@@ -707,7 +710,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     const int64_t ui = (p / (TILE / PATCH)) * w.n_ranges + q;
     const uint32_t *items = w.wl_items + w.wl_off[ui];
     const int n_items = (int)(w.wl_off[ui + 1] - w.wl_off[ui]);
-    int cur = 0;
+    int cur = 0, nch = 0;
     uint32_t e = lane < n_items ? items[lane] : 0u;  // entries of the next chunk
     while (cur < n_items) {
         const int nbn = min(CB, n_items - cur);
@@ -1075,13 +1078,15 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             }
             }
         }
-        // flush fp32 partial sums into the fp64 accumulators
+        // flush fp32 partial sums into the fp64 accumulators (several frequencies: the
+        // global fp64 partials every BF_FLUSHN-th chunk and after the last one)
+        const bool flush64 = !MF || (++nch & (BF_FLUSHN - 1)) == 0 || cur >= n_items;
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             if (!MF) {
                 S.acc[R * lane + j][0][0] += (double)pre[j][0];
                 S.acc[R * lane + j][0][1] += (double)pim[j][0];
-            } else {
+            } else if (flush64) {
                 if (j < nvalid) {
                     double2 *pp = w.part + (q * w.n_pad + sb + j) * NF;
 #pragma unroll
