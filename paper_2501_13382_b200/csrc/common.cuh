@@ -119,8 +119,6 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 // the counts, the entries (pass 2).
 // wstats (4 x n_tiles, zeroed): per tile a9 candidate beams, their segments, tight
 // candidate beams, their segments.
-int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
-                         unsigned long long *wstats, cudaStream_t st);
 // Queue order: keys (longest-first bucket << 32 | range) and unit values, radix-sorted.
 int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
                           const int64_t *counts, uint64_t *keys, int32_t *vals, cudaStream_t st);
@@ -141,7 +139,9 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                  double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
                  int64_t row_base, cudaStream_t st);
 int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox, int64_t n_tiles,
-                    double omega_min, uint32_t *bits, uint32_t *tbits, cudaStream_t st);
+                    double omega_min, uint32_t *bits, uint32_t *tbits, int64_t range_beams,
+                    int64_t n_ranges, unsigned long long *counts, unsigned long long *wstats,
+                    cudaStream_t st);
 int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
                     double *spl, cudaStream_t st);
 

@@ -408,14 +408,20 @@ int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_
 }
 
 // Tile-level work list (exact fp64 candidate test, exact_fp64.cu) for tiling t.
-int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st) {
+// counts (n_tiles x n_ranges, zeroed) and wstats (4 x n_tiles, zeroed) may be null; else
+// the work-list kernel also adds the tight candidates per (tile, beam range) and the
+// per-tile statistics there.
+int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st,
+                   int64_t range_beams = 0, int64_t n_ranges = 0,
+                   unsigned long long *counts = nullptr, unsigned long long *wstats = nullptr) {
     const int64_t n_words = (a.n_beams + 31) / 32;
     uint32_t *bits, *tbits;
     BF_TRY(c->get(B_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
     BF_TRY(c->get(B_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
     double wmin = INFINITY;
     for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
-    BF_TRY(launch_worklist(a, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, st));
+    BF_TRY(launch_worklist(a, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, range_beams,
+                           n_ranges, counts, wstats, st));
     t.wl_bits = bits;
     t.wl_tight = tbits;
     t.wl_words = n_words;
@@ -431,10 +437,6 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     if (precision == BF_PRECISION_FP64) return launch_gbs_fp64(a, st);
     Tiling t;
     BF_TRY(build_tiling(c, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
-    BF_TRY(build_worklist(c, a, t, st));
-    unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
-    BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &d_cand));
-    BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
     Fp32Work w{};
     const int64_t rows = a.n_beams * a.max_seg;
     const int P = gbs_fp32_patch();
@@ -468,13 +470,18 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
         w.wide_k = (float)(wmax / (2.0 * 3.141592653589793 * a.c) / lk);
         w.wide_q = (float)(wmax / (2.0 * a.c * a.width_b) / lq);
     }
-    {   // compacted tight work list: counts -> exclusive scan -> entries
+    unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
+    BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &d_cand));
+    BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
+    {   // compacted tight work list: counts (from the work-list kernel) -> exclusive scan
+        // -> entries
         const int64_t nu = t.n_tiles * w.n_ranges;
         int64_t *cnt;
         BF_TRY(c->get(B_WLTMP, (size_t)(nu + 1), &cnt));
         BF_TRY(c->get(B_WLOFF, (size_t)(nu + 1), &w.wl_off));
-        BF_TRY_CUDA(cudaMemsetAsync(cnt + nu, 0, sizeof(int64_t), st));
-        BF_TRY(launch_fp32_wl_count(a, t, w, cnt, d_cand, st));
+        BF_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nu + 1), st));
+        BF_TRY(build_worklist(c, a, t, st, w.range_beams, w.n_ranges,
+                              reinterpret_cast<unsigned long long *>(cnt), d_cand));
         size_t tmp_bytes = 0;
         BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, w.wl_off, (int)(nu + 1), st));
         void *tmp;

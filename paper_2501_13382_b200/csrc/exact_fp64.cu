@@ -513,9 +513,14 @@ __device__ __forceinline__ unsigned beam_dead_for_tile(const WordRows &w, int jb
 // One block per 32-beam word: the word's rows are read once into shared memory and
 // every warp sweeps a share of the tiles; bit j of (tile, word) = beam 32*word + j is a
 // candidate (bits: a9 bound, tbits: tight bound, tbits subset of bits).
+// With counts != null it also adds popc(tight word) to counts[tile * n_ranges + range]
+// (compaction offsets of the fp32 kernel's work list) and the per-tile statistics
+// wstats[{0,1,2,3} * n_tiles + tile] = a9 beams, a9 beam segments, tight beams, tight
+// beam segments (the FLOP model of bench.py).
 __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, const double4 *tbox,
                                 int64_t n_tiles, int64_t n_words, double rscale, uint32_t *bits,
-                                uint32_t *tbits) {
+                                uint32_t *tbits, int64_t range_beams, int64_t n_ranges,
+                                unsigned long long *counts, unsigned long long *wstats) {
     extern __shared__ double wsm[];
     __shared__ int ns_s[32];
     const int S = (int)a.max_seg;
@@ -553,6 +558,20 @@ __global__ void worklist_kernel(const GbsArgs a, const double4 *centre, const do
         if (lane == 0) {
             bits[t * n_words + word] = m;
             tbits[t * n_words + word] = mt;
+        }
+        if (counts && m) {
+            const unsigned sg = __reduce_add_sync(0xffffffffu, (dead & 1u) ? 0u : (unsigned)ns);
+            const unsigned sgt = __reduce_add_sync(0xffffffffu, (dead & 2u) ? 0u : (unsigned)ns);
+            if (lane == 0) {
+                atomicAdd(&wstats[t], (unsigned long long)__popc(m));
+                atomicAdd(&wstats[n_tiles + t], (unsigned long long)sg);
+                if (mt) {
+                    const int64_t q = 32 * word / range_beams;
+                    atomicAdd(&counts[t * n_ranges + q], (unsigned long long)__popc(mt));
+                    atomicAdd(&wstats[2 * n_tiles + t], (unsigned long long)__popc(mt));
+                    atomicAdd(&wstats[3 * n_tiles + t], (unsigned long long)sgt);
+                }
+            }
         }
     }
 }
@@ -629,7 +648,9 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
 }
 
 int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox, int64_t n_tiles,
-                    double omega_min, uint32_t *bits, uint32_t *tbits, cudaStream_t st) {
+                    double omega_min, uint32_t *bits, uint32_t *tbits, int64_t range_beams,
+                    int64_t n_ranges, unsigned long long *counts, unsigned long long *wstats,
+                    cudaStream_t st) {
     if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
     const int64_t n_words = (a.n_beams + 31) / 32;
     // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
@@ -638,7 +659,8 @@ int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox
     BF_TRY_CUDA(cudaFuncSetAttribute(worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     worklist_kernel<<<(unsigned)n_words, 256, smem, st>>>(a, centre, tbox, n_tiles, n_words,
-                                                          rscale, bits, tbits);
+                                                          rscale, bits, tbits, range_beams,
+                                                          n_ranges, counts, wstats);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

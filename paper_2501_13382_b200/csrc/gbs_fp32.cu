@@ -16,8 +16,9 @@
 //    (patch, beam range) units from an atomic queue (range-major, so all warps
 //    share one L2-resident slice of the bundle).  No CTA barriers at all.
 //  * Per unit the warp reads its tile's slice of the compacted tight work list
-//    (entries (n_segs - 1) << 27 | beam, built by wl_count / scan / wl_compact from
-//    the exact fp64 bitmask of exact_fp64.cu), <= 32 beams / ROWCAP rows per chunk:
+//    (entries (n_segs - 1) << 27 | beam: counted by the work-list kernel of
+//    exact_fp64.cu, scanned, written by wl_compact from its exact fp64 bitmask),
+//    <= 32 beams / ROWCAP rows per chunk:
 //    stages the rows into warp-private shared memory in patch-local fp32 (fp64
 //    conversion), classifies each (patch, beam) with one lane per beam (cut / behind /
 //    dominated segments from the patch's bounding box, first- and second-order
@@ -1274,47 +1275,6 @@ __global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, double *a
     evals[oi] += ev;
 }
 
-// One warp per (tile, beam range): candidate count of the tight work list (compaction
-// offsets) and the per-tile statistics of both lists (FLOP model).
-__global__ void wl_count_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w,
-                                int64_t *counts, unsigned long long *wstats) {
-    const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (u >= tl.n_tiles * w.n_ranges) return;
-    const int64_t tile = u / w.n_ranges, q = u - tile * w.n_ranges;
-    const int64_t w0 = q * w.range_beams / 32;
-    const int64_t w1 = min(tl.wl_words, (q + 1) * w.range_beams / 32);
-    const uint32_t *bits = tl.wl_bits + tile * tl.wl_words;
-    const uint32_t *tbits = tl.wl_tight + tile * tl.wl_words;
-    unsigned c = 0, ct = 0, sg = 0, sgt = 0;
-    for (int64_t i = w0 + lane; i < w1; i += 32) {
-        const unsigned m = bits[i], mt = tbits[i];
-        c += __popc(m);
-        ct += __popc(mt);
-        for (unsigned x = m; x; x &= x - 1) {
-            const int j = __ffs(x) - 1;
-            const unsigned ns = (unsigned)a.n_segs[32 * i + j];
-            sg += ns;
-            if ((mt >> j) & 1u) sgt += ns;
-        }
-    }
-    c = __reduce_add_sync(0xffffffffu, c);
-    ct = __reduce_add_sync(0xffffffffu, ct);
-    sg = __reduce_add_sync(0xffffffffu, sg);
-    sgt = __reduce_add_sync(0xffffffffu, sgt);
-    if (lane == 0) {
-        counts[u] = ct;
-        if (c) {
-            atomicAdd(&wstats[tile], (unsigned long long)c);
-            atomicAdd(&wstats[tl.n_tiles + tile], (unsigned long long)sg);
-        }
-        if (ct) {
-            atomicAdd(&wstats[2 * tl.n_tiles + tile], (unsigned long long)ct);
-            atomicAdd(&wstats[3 * tl.n_tiles + tile], (unsigned long long)sgt);
-        }
-    }
-}
-
 // Sort keys of the unit queue: longest-first in half-octave buckets of the unit's
 // candidate count, range-major inside a bucket (concurrent units share a beam range, so
 // its rows stay L2-resident).  A unit near the source can run for ~10 ms; started late
@@ -1484,18 +1444,6 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
     if (w.n_patches > 0) {
         patch_kernel<<<(unsigned)((w.n_patches * 32 + 127) / 128), 128, 0, st>>>(
             a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen, w.pbox);
-        note_launch();
-    }
-    BF_TRY_CUDA(cudaGetLastError());
-    return BF_OK;
-}
-
-int launch_fp32_wl_count(const GbsArgs &a, const Tiling &t, const Fp32Work &w, int64_t *counts,
-                         unsigned long long *wstats, cudaStream_t st) {
-    const int64_t nu = t.n_tiles * w.n_ranges;
-    if (nu > 0) {
-        wl_count_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(a, t, w, counts,
-                                                                           wstats);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
