@@ -92,7 +92,8 @@ struct Fp32Work {
     double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum
     int *part_ev;             // per (beam range, sorted receiver): unit evaluation count
     unsigned *unit_ctr;       // persistent-kernel work queue head
-    unsigned *n_wide;         // statistics: units of wide patches
+    unsigned *n_wide;         // units of wide patches (device)
+    int64_t n_wide_host;      // the same, read back before the launch (0: no wide kernel)
     float wide_k, wide_q;     // patch radius RW is wide iff RW wide_k > 1 or RW^2 wide_q > 1
     uint32_t *wl_items;       // compacted tight work list: per (tile, beam range), ascending
                               // beams, entry = (n_segs - 1) << 27 | beam

@@ -473,39 +473,27 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
     unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
     BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &d_cand));
     BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
-    {   // compacted tight work list: counts (from the work-list kernel) -> exclusive scan
-        // -> entries
-        const int64_t nu = t.n_tiles * w.n_ranges;
-        int64_t *cnt;
-        BF_TRY(c->get(B_WLTMP, (size_t)(nu + 1), &cnt));
-        BF_TRY(c->get(B_WLOFF, (size_t)(nu + 1), &w.wl_off));
-        BF_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nu + 1), st));
+    const int64_t nu_wl = t.n_tiles * w.n_ranges;
+    int64_t *cnt;
+    {   // tight work list counts (from the work-list kernel) -> exclusive scan
+        BF_TRY(c->get(B_WLTMP, (size_t)(nu_wl + 1), &cnt));
+        BF_TRY(c->get(B_WLOFF, (size_t)(nu_wl + 1), &w.wl_off));
+        BF_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nu_wl + 1), st));
         BF_TRY(build_worklist(c, a, t, st, w.range_beams, w.n_ranges,
                               reinterpret_cast<unsigned long long *>(cnt), d_cand));
         size_t tmp_bytes = 0;
-        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, w.wl_off, (int)(nu + 1), st));
+        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, w.wl_off,
+                                                  (int)(nu_wl + 1), st));
         void *tmp;
         BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
-        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, w.wl_off, (int)(nu + 1), st));
+        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, w.wl_off,
+                                                  (int)(nu_wl + 1), st));
         note_launch();
-        int64_t total = 0;  // entries: bounded by the tight candidate count (stats)
-        BF_TRY_CUDA(cudaMemcpyAsync(&total, w.wl_off + nu, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        BF_TRY_CUDA(cudaStreamSynchronize(st));
-        BF_TRY(c->get(B_WLITEMS, (size_t)(total + 1), &w.wl_items));
-        BF_TRY(launch_fp32_wl_compact(a, t, w, st));
     }
     BF_TRY(launch_fp32_prepare(a, t, w, st));
     {   // unit queue order (wide patches last; longest-first buckets, range-major inside
-        // a bucket);
-        // the counts (B_WLTMP) are still intact after the scan; the patch radii come
-        // from launch_fp32_prepare
+        // a bucket) from the counts and the patch radii of launch_fp32_prepare
         const int64_t nu = w.n_patches * w.n_ranges;
-        const int64_t *cnt;
-        {
-            int64_t *cm;
-            BF_TRY(c->get(B_WLTMP, (size_t)(t.n_tiles * w.n_ranges + 1), &cm));
-            cnt = cm;
-        }
         uint64_t *k0, *k1;
         int32_t *v0, *v1;
         BF_TRY(c->get(B_UKEYS, (size_t)nu, &k0));
@@ -525,6 +513,18 @@ int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st)
                                                     end_bit, st));
         note_launch();
         w.unit_order = dv.Current();
+    }
+    {   // one host sync: work-list length (buffer size) and wide-unit count (launches)
+        int64_t total = 0;
+        unsigned n_wide = 0;
+        BF_TRY_CUDA(cudaMemcpyAsync(&total, w.wl_off + nu_wl, sizeof(int64_t),
+                                    cudaMemcpyDeviceToHost, st));
+        BF_TRY_CUDA(cudaMemcpyAsync(&n_wide, w.n_wide, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                    st));
+        BF_TRY_CUDA(cudaStreamSynchronize(st));
+        w.n_wide_host = n_wide;
+        BF_TRY(c->get(B_WLITEMS, (size_t)(total + 1), &w.wl_items));
+        BF_TRY(launch_fp32_wl_compact(a, t, w, st));
     }
     GbsStats *d_stats;
     BF_TRY(c->get(B_STATS, 1, &d_stats));

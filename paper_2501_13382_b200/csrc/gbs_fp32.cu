@@ -1371,12 +1371,16 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
     // the wide kernel is submitted first on the launch stream, the common one right
     // after on the auxiliary stream (forked before the wide launch), so the wide CTAs
     // are dispatched first and the common kernel fills the remaining SM slots
-    BF_TRY_CUDA(cudaEventRecord(sp.fork, sp.st));
-    BF_TRY_CUDA(cudaStreamWaitEvent(sp.aux, sp.fork, 0));
-    BF_TRY((launch_class<NF, true>(a, t, w, K, stats, sp.st)));
-    BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.aux)));
-    BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
-    BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
+    if (w.n_wide_host != 0) {
+        BF_TRY_CUDA(cudaEventRecord(sp.fork, sp.st));
+        BF_TRY_CUDA(cudaStreamWaitEvent(sp.aux, sp.fork, 0));
+        BF_TRY((launch_class<NF, true>(a, t, w, K, stats, sp.st)));
+        BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.aux)));
+        BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
+        BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
+    } else {  // no wide patches: the common kernel alone
+        BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.st)));
+    }
 #if BF_HIST
     {
         unsigned long long h[4];
