@@ -103,6 +103,7 @@ struct Fp32Consts {
     float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
     float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
     float b, b2;             // width_b, width_b^2
+    int ascending;           // omegas nondecreasing (cutk nondecreasing)
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
     double rcut_scale;       // 72 c / (omega_min b): R_cut^2 = rcut_scale * (s_end^2 + b^2)
     float rscale;            // (float) rcut_scale
@@ -1068,7 +1069,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 for (int j = 0; j < R; ++j)
                     if (((lvm >> j) & 1u) && !(q2j[j] * K.cutk[f] > m2j[j]))
                         lf |= 1u << j;  // ex_re < -36 (kernels.py:384)
-                if (__any_sync(0xffffffffu, lf != 0)) {
+                if (!__any_sync(0xffffffffu, lf != 0)) {
+                    // ascending frequencies: the cut radius shrinks with omega, so every
+                    // later frequency is cut for the whole warp as well
+                    if (K.ascending) break;
+                    continue;
+                }
+                {
 #pragma unroll
                     for (int j = 0; j < R; ++j)
                         eval_freq(K, f, sj[j], gq[j], ainv[j],
@@ -1410,6 +1417,9 @@ Fp32Consts make_consts(const GbsArgs &a) {
         K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
         K.nhkbl2e[f] = (float)(-(w * 0.5 / a.c) * a.width_b * 1.4426950408889634);
     }
+    K.ascending = 1;
+    for (int f = 1; f < a.nf; ++f)
+        if (!(K.cutk[f] >= K.cutk[f - 1])) K.ascending = 0;
     K.b = (float)a.width_b;
     K.b2 = (float)(a.width_b * a.width_b);
     K.b2_64 = a.width_b * a.width_b;

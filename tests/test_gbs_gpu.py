@@ -369,7 +369,9 @@ def test_worklist_bitexact_vs_oracle(name, dense):
     ((50.0, 63.0, 80.0, 100.0, 125.0, 160.0, 200.0, 250.0), (20.0, 0.0, 2.0), (10.0, -5.0),
      -10.0),
     # the paper's beam parameter: the cutoff never fires, every non-behind pair evaluated
-    ((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0), -45874.0)])
+    ((125.0,), (20.0, 0.0, 2.0), (-10.0, -20.0), -45874.0),
+    # frequencies not in ascending order (no early exit of the frequency loop)
+    ((500.0, 63.0, 250.0, 125.0), (0.0, 20.0, 2.0), (-30.0, 5.0), -10.0)])
 def test_fp32_dense_city_vs_oracle(freqs, src, corner, im_b, threads):
     """Config-3 receiver density (0.25 m) around street corners of the city scene: every
     fp32 path (single survivor, corner wedge, several candidates with junction and
