@@ -13,8 +13,11 @@
 //    a row SoA: origin/len and direction/s0 in fp64, the amplitude factor and
 //    cutoff radius in fp32, and fp64-exact phase anchors (turns) at both ends.
 //  * The kernel is PERSISTENT: every warp is an independent worker that pulls
-//    (patch, beam range) units from an atomic queue (range-major, so all warps
-//    share one L2-resident slice of the bundle).  No CTA barriers at all.
+//    (patch, beam range) units from an atomic queue, longest units first in
+//    half-octave buckets and range-major inside a bucket (concurrent warps share
+//    an L2-resident slice of the bundle).  No CTA barriers at all.  Units of WIDE
+//    patches (sparse receiver sets) go to a second instantiation with an fp64 tail,
+//    launched concurrently (gbs_fp32_kernel<NF, true>).
 //  * Per unit the warp reads its tile's slice of the compacted tight work list
 //    (entries (n_segs - 1) << 27 | beam: counted by the work-list kernel of
 //    exact_fp64.cu, scanned, written by wl_compact from its exact fp64 bitmask),
@@ -25,7 +28,8 @@
 //    bounds), then sums the live beams in ascending order through the
 //    single-survivor path, the junction block (corner wedges and junction ties) and the
 //    several-candidate scan with fp64 re-decision of near ties (exact_pending).
-//  * fp32 partial sums are flushed per chunk into fp64 accumulators; a unit
+//  * fp32 partial sums are flushed into fp64 accumulators per chunk (every
+//    BF_FLUSHN chunks with several frequencies); a unit
 //    stores its fp64 partial per (beam range, receiver) and fold_kernel adds the
 //    ranges in ascending order to the caller's acc (in-place continuation,
 //    kernels.py:358-359) -- the result is deterministic and independent of
@@ -39,8 +43,9 @@
 // Compile-time switches (tuning and diagnostics; the defaults are the product):
 //   BF_ROWCAP rows per staged chunk, BF_MINB CTAs/SM for NF = 1, BF_RANGES beam ranges per
 //   call, BF_EVG receivers per evaluation branch, BF_WARPS warps per CTA, BF_NORED (no
-//   explicit turn reduction before MUFU sin/cos); BF_ABL skips work for ablation timings
-//   (results invalid), BF_HIST prints debug counters.
+//   explicit turn reduction before MUFU sin/cos), BF_FLUSHN (chunks per fp64 flush with
+//   several frequencies), BF_NOPF (no junction-row prefetch); BF_ABL skips work for
+//   ablation timings (results invalid), BF_HIST prints debug counters.
 namespace bf {
 namespace {
 
