@@ -355,7 +355,8 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak, "traffic": traffic,
-                         "work_list": "tight (tile, beam) list walked by the kernel",
+                         "work_list": "tight (tile, beam) list walked by the kernel, "
+                                      f"tiles of {shard.tile_size()} receivers",
                          "frac_a9_list": flop_a9 / kernel_s / 1e12 / peak,
                          "frac_evaluated_items": flop_live / kernel_s / 1e12 / peak,
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, committed "

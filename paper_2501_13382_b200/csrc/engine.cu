@@ -190,7 +190,7 @@ __device__ __forceinline__ uint64_t spread3(uint64_t x) {
 }
 
 // Hilbert index of a receiver (the tiling order: consecutive receivers are spatial
-// neighbours with no jumps, so 128-receiver patches and 512-receiver tiles are compact).
+// neighbours with no jumps, so 128-receiver patches and 1024-receiver tiles are compact).
 // A planar set (third extent < 1/64 of the largest) is cut along its longest axis into
 // square blocks of the second extent, each traversed by the 2-D curve (which enters a
 // block at its lower-left and leaves at its lower-right corner, so consecutive blocks
@@ -381,6 +381,8 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
         tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm, rloc, cen, box);
     else if (T == 256)
         tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm, rloc, cen, box);
+    else if (T == 1024)
+        tile_kernel<1024><<<(unsigned)out->n_tiles, 1024, 0, st>>>(obs, n, perm, rloc, cen, box);
     else
         return fail(BF_EINVAL, "unsupported tile size %d", T);
     note_launch();

@@ -75,7 +75,10 @@ namespace {
 #endif
 constexpr int R = 4;                    // receivers per lane
 constexpr int PATCH = 32 * R;           // receivers per warp patch
-constexpr int TILE = 4 * PATCH;         // receivers per work-list tile
+#ifndef BF_TILEP
+#define BF_TILEP 8
+#endif
+constexpr int TILE = BF_TILEP * PATCH;  // receivers per work-list tile
 #ifndef BF_WARPS
 #define BF_WARPS 4
 #endif
