@@ -3,11 +3,12 @@
  *
  * Plain pointers and sizes only (no torch / C++ types).  Every entry point
  * returns a bf_status; on failure bf_last_error() returns a thread-local
- * message.  All functions are thread-safe.  Calls on one device serialise on
- * that device's engine stream; a *_dev call given a caller stream returns once its
- * work is enqueued, and the next call that uses the device's workspaces (on any
- * stream) is ordered after it by an event, so concurrent callers on different
- * streams never see each other's scratch buffers.
+ * message.  All functions are thread-safe.  A *_dev call given a caller stream
+ * returns once its work is enqueued -- it never waits on the device (work-list
+ * buffers are sized from a bound, statistics are copied back asynchronously) --
+ * and the next call that uses the device's workspaces (on any stream) is ordered
+ * after it by an event, so concurrent callers on different streams never see
+ * each other's scratch buffers.  Results never depend on environment variables.
  *
  * Reference interface each entry point replaces (paths relative to
  * /root/reference/pkg/src/beamfield/):
@@ -61,6 +62,11 @@ enum {
     BF_PRECISION_FP64 = 1  /* oracle mode: reference operation order, no FMA */
 };
 
+/* Flags of bf_trace_range_dev. */
+enum {
+    BF_TRACE_EXHAUSTIVE = 1 /* test every triangle (self-check of the cluster culling) */
+};
+
 /* Library identification and diagnostics. */
 const char *bf_version(void);
 const char *bf_last_error(void);
@@ -68,12 +74,23 @@ int bf_device_count(void);
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t bf_launch_count(void);
 
+/* Device-memory budget (bytes) of the summation's beam-group workspaces and
+ * staging on `device`; 0 = automatic (1/8 of device memory, at most 24 GiB).
+ * Changes the grouping only, never the results. */
+int bf_set_memory_budget(int device, int64_t bytes);
+
 /*
- * Drop-in for kernels.gbs_accumulate (kernels.py:352-355) on HOST buffers.
- * Argument order follows the reference; array sizes (n_beams = rows/max_seg,
- * n_obs, nf) are passed right after the array they size.  Host->device copies
- * of the beam range / observer range, the kernels and the device->host copy
- * of acc/evals[obs_lo:obs_hi] all happen inside the call.
+ * Drop-in for kernels.gbs_accumulate (kernels.py:352-355) on HOST buffers
+ * (pageable or pinned).  Argument order follows the reference; array sizes
+ * (n_beams = rows/max_seg, n_obs, nf) are passed right after the array they size.
+ * The call streams the beam range through the device in groups: host threads
+ * pack each group's valid rows (no padding) into pinned staging, 68 B per segment
+ * in fp32 mode (origin, direction, len, s0 in fp64 -- the exact re-decisions
+ * need them bit for bit -- and the fp32 amplitude refl*w_b*phi sqrt(c)/(2 pi c)),
+ * and the copy of group g+1 overlaps the summation of group g; device memory
+ * stays within the budget however large the bundle.  fp64 mode streams padded
+ * beam chunks the same way.  acc/evals[obs_lo:obs_hi] are copied back at the end.
+ * Result bits equal bf_gbs_accumulate_dev's on the same inputs.
  */
 int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir,
                       const double *seg_e1, const double *seg_e2,
@@ -97,7 +114,18 @@ enum {
 /*
  * Same operator on DEVICE buffers (all pointers are device pointers on
  * `device`).  Asynchronous on `stream` (cudaStream_t, NULL = the engine's own
- * stream, which the call synchronises before returning).
+ * stream, which the call synchronises before returning).  `omegas` is a HOST
+ * array.  Any nf: frequencies are summed in groups of 8 (acc columns are
+ * independent).  fp32 mode needs max_seg <= 30 (BF_EINVAL otherwise, before any
+ * work) and fewer than 2^27 beams per call.
+ *
+ * The beams are summed in groups of whole beam ranges (the range size depends
+ * only on the beam and frequency counts) whose workspaces fit the memory budget
+ * (bf_set_memory_budget); the fp32 result bits do not depend on the budget, on
+ * device vs host inputs, or on how receivers are sharded (BF_FLAG_OBS_PRESORTED).
+ * They do depend on the call's beam and observer sets (patch-local fp32
+ * geometry): splitting a call changes fp32 results within the fp32 tolerance,
+ * while fp64 mode is bit-identical under any split of beams or observers.
  */
 int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
                           const double *seg_e1, const double *seg_e2,
@@ -189,7 +217,7 @@ int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
                        int64_t r_max, int64_t max_seg, double *seg_origin, double *seg_dir,
                        double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
                        double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo,
-                       int64_t hi, int64_t row_base, int device, void *stream);
+                       int64_t hi, int64_t row_base, int flags, int device, void *stream);
 
 /*
  * pressure = calibration * acc (parallel.py:343) and spl = 20 log10(|p|/2e-5),
@@ -206,8 +234,11 @@ int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_by
 /* Statistics of the last fp32 bf_gbs_accumulate* call on this thread:
  * candidate (beam, receiver) pairs of the tile work list, total pairs, fp64
  * tie re-decisions, receiver tiles, non-behind pairs (P_nb), the CUDA-event
- * duration of the summation kernel on its launch stream, and the sum of n_segs
- * over candidate pairs (the scan term of the FLOP model). Any pointer may be NULL. */
+ * duration of the summation (first summation kernel start to last kernel end),
+ * and the sum of n_segs over candidate pairs (the scan term of the FLOP model).
+ * Any pointer may be NULL.  The counters are copied back asynchronously by the
+ * call; this function waits for that copy (the only place the engine waits on
+ * the device for statistics). */
 int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
                   int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms,
                   int64_t *candidate_pair_segs);

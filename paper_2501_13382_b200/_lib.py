@@ -25,9 +25,10 @@ EXPORTS = (
     "bf_gbs_accumulate", "bf_gbs_accumulate_dev", "bf_nearest_on_segments",
     "bf_trace_range_dev", "bf_field_finalize_dev", "bf_plan_chunks", "bf_last_stats",
     "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats", "bf_worklist",
-    "bf_last_pair_stats", "bf_write_field_csv",
+    "bf_last_pair_stats", "bf_write_field_csv", "bf_set_memory_budget",
 )
 FLAG_OBS_PRESORTED = 1
+TRACE_EXHAUSTIVE = 1
 
 _lock = threading.Lock()
 _lib = None
@@ -58,7 +59,8 @@ def _declare(lib):
     lib.bf_nearest_on_segments.argtypes = [VP] * 7 + [VP, I64, I64, VP, I64, VP, VP, I64, VP,
                                                       INT]
     lib.bf_trace_range_dev.argtypes = ([VP, VP, VP, VP, I64, VP, F64, VP, VP, VP, VP, F64, I64,
-                                        I64] + [VP] * 9 + [I64, I64, I64, INT, VP])
+                                        I64] + [VP] * 9 + [I64, I64, I64, INT, INT, VP])
+    lib.bf_set_memory_budget.argtypes = [INT, I64]
     lib.bf_field_finalize_dev.argtypes = [VP, I64, F64, VP, VP, INT, VP]
     lib.bf_plan_chunks.argtypes = [I64, I64, I64, I64P, I64, I64P]
     lib.bf_last_stats.argtypes = [I64P, I64P, I64P, I64P, I64P, D, I64P]
@@ -102,6 +104,13 @@ def check(status: int) -> None:
     if status == BF_EIO:
         raise OSError(msg)
     raise EngineError(f"[bf_status {status}] {msg}")
+
+
+def set_memory_budget(device: int, nbytes: int) -> None:
+    """Beam-group workspace budget of the summation on `device` (0 = automatic).
+
+    Changes how a call is grouped, never its results (bf_set_memory_budget)."""
+    check(load().bf_set_memory_budget(int(device), int(nbytes)))
 
 
 def launch_count() -> int:

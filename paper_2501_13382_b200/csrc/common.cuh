@@ -6,7 +6,8 @@
 
 #include "../../include/bf_gbs.h"
 
-#define BF_MAXF 8            // frequencies per call supported by the kernels
+#define BF_MAXF 8            // frequencies per kernel launch (calls loop over groups of <= 8)
+#define BF_FP32_MAX_SEG 30   // fp32 path: survivor masks share a word with two flag bits
 #define BF_CUTOFF_EXPONENT (-36.0)  // kernels.py:18
 #define BF_EPS_HIT 1e-6              // kernels.py:14
 
@@ -46,8 +47,25 @@ struct GbsArgs {
     double omegas[BF_MAXF];
     double c, width_b, phi_amp;
     int use_cutoff;
-    double *acc;      // (n_obs, nf) complex, interleaved
+    double *acc;      // (n_obs, acc_stride) complex, interleaved; columns [0, nf) are ours
+    int64_t acc_stride;  // complex values per observer row of acc (>= nf)
     int64_t *evals;   // (n_obs,)
+};
+
+// Compact segment rows on the device (the fp32 path's input layout): beam b owns rows
+// [start[b], start[b] + n_segs[b]) of p0/p1/amp, no padding (the reference's padded
+// PathBundle rows beyond n_segs, beamtrace.py:274-288, are dropped when packing).
+// start has n_beams + 1 entries; start[n_beams] = end of the last beam's rows.
+// p0/p1 are exact copies of the reference's fp64 values (the exact re-decisions and the
+// work-list bound use them bit for bit); amp is the fp32 amplitude factor
+// A = phi sqrt(c)/(2 pi c) * refl * w_b (kernels.py:388,397 without omega).
+struct Rows {
+    const int64_t *start;
+    const double4 *p0;  // per row: origin xyz, len
+    const double4 *p1;  // per row: direction xyz, s0
+    const float *amp;   // per row: A
+    int64_t n_beams;
+    int64_t max_seg;    // bound on segments per beam (the padded row count)
 };
 
 // Work-list statistics of the fp32 path (device counters, copied back).
@@ -82,18 +100,18 @@ struct Tiling {
 // Workspace of the fp32 path (engine.cu allocates, gbs_fp32.cu fills and uses).
 // Row arrays use the padded row index b*max_seg + k of the reference bundle.
 struct Fp32Work {
-    double4 *p0;              // per row: origin xyz, len
-    double4 *p1;              // per row: direction xyz, s0
-    float2 *p2;               // per row: amplitude factor A, cutoff radius R_cut
-    float *pa;                // per row and frequency: phase anchors at s0, s0+len (turns)
+    const int64_t *start;     // compact rows (Rows): beam -> first row
+    const double4 *p0;        // per row: origin xyz, len
+    const double4 *p1;        // per row: direction xyz, s0
+    const float *amp;         // per row: amplitude factor A
+    const float *pa;          // per row and frequency: phase anchors at s0, s0+len (turns)
     float4 *prl;              // sorted receiver -> patch-local fp32 coordinates, |r|^2
     double4 *pcen;            // per patch: centre xyz, radius
     float4 *pbox;             // per patch: bounding-box half extents xyz, radius (patch-local)
     double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum
     int *part_ev;             // per (beam range, sorted receiver): unit evaluation count
     unsigned *unit_ctr;       // persistent-kernel work queue head
-    unsigned *n_wide;         // units of wide patches (device)
-    int64_t n_wide_host;      // the same, read back before the launch (0: no wide kernel)
+    unsigned *n_wide;         // units of wide patches (device; the wide kernel takes them)
     float wide_k, wide_q;     // patch radius RW is wide iff RW wide_k > 1 or RW^2 wide_q > 1
     uint32_t *wl_items;       // compacted tight work list: per (tile, beam range), ascending
                               // beams, entry = (n_segs - 1) << 27 | beam
@@ -114,7 +132,20 @@ int launch_gbs_fp64(const GbsArgs &a, cudaStream_t st);
 int gbs_fp32_tile();
 int gbs_fp32_patch();
 int64_t gbs_fp32_range_beams(int64_t n_beams, int nf);
-int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st);
+// Padded reference bundle (GbsArgs, local beams) -> compact rows.  start must already
+// hold the exclusive scan of n_segs (n_beams + 1 entries); amp_scale = phi sqrt(c)/(2 pi c).
+int launch_rows_pack(const GbsArgs &a, const int64_t *start, double4 *p0, double4 *p1,
+                     float *amp, cudaStream_t st);
+// cnt[0] = 0, cnt[b + 1] = n_segs[b] clamped to [0, max_seg]; an inclusive scan of cnt
+// (engine.cu, cub) then gives the compact row starts.
+int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t *cnt,
+                      cudaStream_t st);
+// fp64-exact phase anchors of the compact rows [0, rows_bound) (rows past
+// start[n_beams] are skipped): pa[row * nf + f] = frac(kappa_f s0), frac(kappa_f (s0+len)).
+int launch_fp32_anchors(const GbsArgs &a, const Rows &r, int64_t rows_bound, float *pa,
+                        cudaStream_t st);
+// Patch-local receivers of the tiling (w.prl, w.pcen, w.pbox).
+int launch_fp32_patches(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st);
 // Work-list compaction (north star: prefix-sum compaction into (beam, tile) lists):
 // counts per (tile, range) into w.wl_off (pass 1), then, after an exclusive scan of
 // the counts, the entries (pass 2).
@@ -123,10 +154,13 @@ int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 // Queue order: keys (longest-first bucket << 32 | range) and unit values, radix-sorted.
 int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
                           const int64_t *counts, uint64_t *keys, int32_t *vals, cudaStream_t st);
-int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
-                           cudaStream_t st);
+int launch_fp32_wl_compact(const Tiling &t, const Fp32Work &w, cudaStream_t st);
+// The summation of one group of beam ranges (wide-patch kernel on st.aux first, the
+// common kernel on st.st), without the fold.
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
                     const StreamPair &st);
+// acc[:, :nf] += the group's unit partials over its ranges (ascending), evals alike.
+int launch_fp32_fold(const GbsArgs &a, const Tiling &t, const Fp32Work &w, cudaStream_t st);
 int launch_nearest(const GbsArgs &a, const int64_t *q_obs, const int64_t *q_beam,
                    int64_t n_query, double *out, cudaStream_t st);
 // cbox: scratch for ceil(n_tri/16) cluster boxes (6 doubles each), or null for the
@@ -139,10 +173,11 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
                  double *seg_e1, double *seg_e2, double *seg_len, double *seg_s0,
                  double *seg_refl, int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
                  int64_t row_base, cudaStream_t st);
-int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox, int64_t n_tiles,
-                    double omega_min, uint32_t *bits, uint32_t *tbits, int64_t range_beams,
-                    int64_t n_ranges, unsigned long long *counts, unsigned long long *wstats,
-                    cudaStream_t st);
+// Work lists of tiling (centre, tbox) against the compact rows r (beams [0, r.n_beams)).
+int launch_worklist(const GbsArgs &a, const Rows &r, const double4 *centre, const double4 *tbox,
+                    int64_t n_tiles, double omega_min, uint32_t *bits, uint32_t *tbits,
+                    int64_t range_beams, int64_t n_ranges, unsigned long long *counts,
+                    unsigned long long *wstats, cudaStream_t st);
 int launch_finalize(const double *acc, int64_t n, double calibration, double *pressure,
                     double *spl, cudaStream_t st);
 

@@ -1,11 +1,25 @@
-// engine.cu -- device contexts, receiver tiling and the extern "C" ABI.
+// engine.cu -- device contexts, receiver tiling, the beam-group pipeline and the
+// extern "C" ABI.
 //
 // The ABI (include/bf_gbs.h) is the drop-in boundary for the reference's
 // kernels.gbs_accumulate (kernels.py:352-399) and its neighbours; this file
 // owns everything between that boundary and the kernels: argument checks that
 // mirror the reference's contracts, per-device streams and grow-only
-// workspaces, host<->device staging of the caller's ranges, the Hilbert
-// receiver tiling used by the fp32 kernel, and the beam segment prefix sums.
+// workspaces, the Hilbert receiver tiling used by the fp32 kernel, and the
+// pipeline that sums a call's beams in GROUPS of whole beam ranges:
+//
+//   per group (a slot of device buffers, its own stream):  compact rows (packed on the
+//   device from the padded bundle, or packed on host threads into pinned staging and
+//   copied) -> phase anchors -> tile work list -> scan -> unit queue order ->
+//   compaction -> summation kernels;  then, on the call's stream, in group order:
+//   fold of the group's range partials into acc.
+//
+// The range size depends only on the call's beam count and frequency count, groups are
+// whole ranges and the folds add the ranges in ascending order, so the result bits do
+// not depend on the grouping (memory budget), on host vs device inputs, or on the number
+// of ranks.  Nothing in a call waits on the host: work-list buffers are sized from an
+// upper bound, the wide-patch kernel is always launched, and statistics are copied back
+// asynchronously and only waited for when bf_last_stats asks.
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
@@ -14,18 +28,19 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
+#include "hostpool.h"
 
 namespace bf {
 
 namespace {
 thread_local char g_err[512] = "";
-thread_local GbsStats g_last_stats = {};
-thread_local int64_t g_last_total_pairs = 0, g_last_tiles = 0;
 std::atomic<uint64_t> g_launches{0};
 }  // namespace
 
@@ -68,30 +83,93 @@ struct Buf {
     }
 };
 
+// Grow-only pinned host buffer.
+struct PinBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int get(size_t bytes, void **out) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            size_t want = bytes + bytes / 4 + 256;
+            BF_TRY_CUDA(cudaHostAlloc(&p, want, cudaHostAllocPortable));
+            cap = want;
+        }
+        *out = p;
+        return BF_OK;
+    }
+};
+
+// Call-level device workspaces.
 enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
-    B_SEGSTART, B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_STATS,
-    B_QOBS, B_QBEAM, B_QOUT, B_WLBITS, B_WLCNT, B_P0, B_P1, B_P2, B_PA, B_PRL, B_PCEN,
-    B_DONE, B_UCTR, B_WLTIGHT, B_PARTEV, B_WLITEMS, B_WLOFF, B_WLTMP, B_PBOX, B_TBOX, B_UKEYS, B_UKEYS2, B_UVALS, B_UVALS2, B_CBOX, B_COUNT
+    B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_TBOX, B_STATS, B_CAND,
+    B_QOBS, B_QBEAM, B_QOUT, B_PRL, B_PCEN, B_PBOX, B_CBOX, B_WLBITS, B_WLTIGHT, B_COUNT
+};
+
+// Per-slot device workspaces of one beam group.
+enum SlotBufId {
+    S_START, S_P0, S_P1, S_AMP, S_PA, S_WLBITS, S_WLTIGHT, S_WLCNT, S_WLOFF, S_WLITEMS,
+    S_UKEYS, S_UKEYS2, S_UVALS, S_UVALS2, S_PART, S_PARTEV, S_UCTR, S_CUB, S_F64, S_COUNT
+};
+// Per-slot pinned staging (host-buffer ABI).
+enum SlotPinId { P_START, P_P0, P_P1, P_AMP, P_F64, P_COUNT };
+// Call-level pinned staging (host-buffer ABI).
+enum CallPinId { H_OBS, H_ACC, H_EV, H_COUNT };
+
+constexpr int NSLOT = 3;  // beam groups in flight
+
+struct Slot {
+    cudaStream_t ss = nullptr, sw = nullptr;  // the group's stream, its wide-kernel stream
+    cudaEvent_t fork = nullptr, join = nullptr, kdone = nullptr, freed = nullptr,
+                h2d = nullptr;
+    bool freed_valid = false, h2d_valid = false;
+    Buf buf[S_COUNT];
+    PinBuf pin[P_COUNT];
+    template <typename T>
+    int get(SlotBufId id, size_t n, T **out) {
+        void *p;
+        BF_TRY(buf[id].get(n * sizeof(T) + 16, &p));
+        *out = (T *)p;
+        return BF_OK;
+    }
+    template <typename T>
+    int pinned(SlotPinId id, size_t n, T **out) {
+        void *p;
+        BF_TRY(pin[id].get(n * sizeof(T) + 16, &p));
+        *out = (T *)p;
+        return BF_OK;
+    }
 };
 
 struct DeviceCtx {
     int dev = -1;
+    int sms = 0;
+    size_t total_mem = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // Completion of the last call that used this context's workspaces.  Calls may come
     // on different caller streams and return before their kernels finish; each call
     // orders itself after the previous one (StreamOrder) so no workspace is reused early.
     cudaEvent_t done = nullptr;
     bool done_valid = false;
-    cudaStream_t aux = nullptr;              // second stream for the wide-patch kernel
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaEvent_t pro = nullptr;  // end of a call's prologue (tiling) on its stream
+    int64_t budget = 0;         // group-workspace budget in bytes (0: automatic)
     std::mutex mu;
     Buf buf[B_COUNT];
+    PinBuf hpin[H_COUNT];
+    Slot slot[NSLOT];
     template <typename T>
     int get(BufId id, size_t n, T **out) {
         void *p;
         BF_TRY(buf[id].get(n * sizeof(T) + 16, &p));
+        *out = (T *)p;
+        return BF_OK;
+    }
+    template <typename T>
+    int pinned(CallPinId id, size_t n, T **out) {
+        void *p;
+        BF_TRY(hpin[id].get(n * sizeof(T) + 16, &p));
         *out = (T *)p;
         return BF_OK;
     }
@@ -133,14 +211,123 @@ int get_ctx(int device, DeviceCtx **out) {
                         device, prop.major, prop.minor);
         DeviceCtx *c = new DeviceCtx();
         c->dev = device;
+        c->sms = prop.multiProcessorCount;
+        c->total_mem = prop.totalGlobalMem;
+        const unsigned fl = cudaEventDisableTiming;
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming));
-        BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, fl));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->pro, fl));
+        for (Slot &s : c->slot) {
+            BF_TRY_CUDA(cudaStreamCreateWithFlags(&s.ss, cudaStreamNonBlocking));
+            BF_TRY_CUDA(cudaStreamCreateWithFlags(&s.sw, cudaStreamNonBlocking));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.fork, fl));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.join, fl));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.kdone, fl));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.freed, fl));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.h2d, fl));
+        }
         g_ctx[device] = c;
     }
     *out = g_ctx[device];
+    return BF_OK;
+}
+
+// ---------------------------------------------------- deferred statistics ----
+
+// Statistics of the last fp32 call on this thread: the device counters are copied into
+// pinned memory at the end of the call (stream-ordered) and reduced only when asked.
+// Two buffers alternate, so a call never waits for the one right before it.
+struct StatsBuf {
+    cudaEvent_t ready = nullptr, t0 = nullptr, t1 = nullptr;
+    bool inflight = false;
+    GbsStats *h_stats = nullptr;
+    unsigned long long *h_cand = nullptr;
+    size_t cand_cap = 0;
+    int64_t n_tiles = 0, tile = 0, n_obs = 0;
+};
+struct PendingStats {
+    int dev = -1;
+    StatsBuf buf[2];
+    int cur = 0;           // buffer of the last call
+    bool pending = false;  // buf[cur] holds an unread call
+    GbsStats last = {};
+    int64_t last_total_pairs = 0, last_tiles = 0;
+};
+thread_local PendingStats g_ps;
+
+int stats_events(int dev) {
+    if (g_ps.dev == dev && g_ps.buf[0].ready) return BF_OK;
+    for (StatsBuf &b : g_ps.buf) {
+        if (b.ready) {
+            cudaEventSynchronize(b.ready);
+            cudaEventDestroy(b.ready);
+            cudaEventDestroy(b.t0);
+            cudaEventDestroy(b.t1);
+        }
+        b.inflight = false;
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming));
+        BF_TRY_CUDA(cudaEventCreate(&b.t0));
+        BF_TRY_CUDA(cudaEventCreate(&b.t1));
+    }
+    g_ps.pending = false;
+    g_ps.dev = dev;
+    return BF_OK;
+}
+
+void materialize_stats() {
+    if (!g_ps.pending) return;
+    g_ps.pending = false;
+    StatsBuf &b = g_ps.buf[g_ps.cur];
+    b.inflight = false;
+    if (cudaEventSynchronize(b.ready) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    GbsStats h = *b.h_stats;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, b.t0, b.t1) != cudaSuccess) {
+        cudaGetLastError();
+        ms = 0.f;
+    }
+    h.kernel_ms = ms;
+    unsigned long long cp = 0, cs = 0, tp = 0, ts = 0;
+    const int64_t nt = b.n_tiles;
+    for (int64_t i = 0; i < nt; ++i) {
+        const unsigned long long in_tile =
+            (unsigned long long)((i + 1 < nt) ? b.tile : b.n_obs - i * b.tile);
+        cp += b.h_cand[(size_t)i] * in_tile;
+        cs += b.h_cand[(size_t)(nt + i)] * in_tile;
+        tp += b.h_cand[(size_t)(2 * nt + i)] * in_tile;
+        ts += b.h_cand[(size_t)(3 * nt + i)] * in_tile;
+    }
+    h.candidate_pairs = cp;
+    h.cand_pair_segs = cs;
+    h.tight_pairs = tp;
+    h.tight_pair_segs = ts;
+    g_ps.last = h;
+    g_ps.last_tiles = nt;
+    if (getenv("BF_DEBUG_STATS"))
+        fprintf(stderr, "bf stats: items culled %llu single %llu wedge %llu multi %llu ties %llu\n",
+                h.paths[0], h.paths[1], h.paths[2], h.paths[3], h.tie_pairs);
+}
+
+// Starts a call's statistics (forgets the previous call's).
+void stats_begin(int64_t total_pairs) {
+    g_ps.pending = false;
+    g_ps.last = GbsStats{};
+    g_ps.last_tiles = 0;
+    g_ps.last_total_pairs = total_pairs;
+}
+
+// The buffer the current fp32 call writes: the one not used by the previous call, after
+// its copy from two calls back has landed.
+int stats_next(StatsBuf **out) {
+    const int i = g_ps.cur ^ 1;
+    StatsBuf &b = g_ps.buf[i];
+    if (b.inflight) BF_TRY_CUDA(cudaEventSynchronize(b.ready));
+    b.inflight = false;
+    g_ps.cur = i;
+    *out = &b;
     return BF_OK;
 }
 
@@ -394,10 +581,11 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
     return BF_OK;
 }
 
+
 int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_t obs_lo,
              int64_t obs_hi, int64_t beam_lo, int64_t beam_hi, int precision) {
     if (max_seg < 1) return fail(BF_EINVAL, "max_seg must be >= 1");
-    if (nf < 0 || nf > BF_MAXF) return fail(BF_EINVAL, "nf=%lld outside 0..%d", (long long)nf, BF_MAXF);
+    if (nf < 0) return fail(BF_EINVAL, "negative frequency count %lld", (long long)nf);
     if (obs_lo < 0 || obs_hi < obs_lo || obs_hi > n_obs)
         return fail(BF_EINVAL, "observer range [%lld,%lld) outside [0,%lld)", (long long)obs_lo,
                     (long long)obs_hi, (long long)n_obs);
@@ -406,171 +594,428 @@ int validate(int64_t n_beams, int64_t max_seg, int64_t n_obs, int64_t nf, int64_
                     (long long)beam_hi, (long long)n_beams);
     if (precision != BF_PRECISION_FP32 && precision != BF_PRECISION_FP64)
         return fail(BF_EINVAL, "unknown precision %d", precision);
+    if (precision == BF_PRECISION_FP32 && max_seg > BF_FP32_MAX_SEG)
+        return fail(BF_EINVAL,
+                    "fp32 mode supports max_seg <= %d (r_max <= %d), got %lld; use fp64 mode",
+                    BF_FP32_MAX_SEG, BF_FP32_MAX_SEG - 1, (long long)max_seg);
+    if (obs_hi - obs_lo > INT32_MAX)
+        return fail(BF_EINVAL, "observer range too large (%lld); split the call",
+                    (long long)(obs_hi - obs_lo));
+    if (precision == BF_PRECISION_FP32 && beam_hi - beam_lo >= ((int64_t)1 << 27))
+        return fail(BF_EINVAL, "more than 2^27 beams in one fp32 call; split the beam range");
     return BF_OK;
 }
 
-// Tile-level work list (exact fp64 candidate test, exact_fp64.cu) for tiling t.
-// counts (n_tiles x n_ranges, zeroed) and wstats (4 x n_tiles, zeroed) may be null; else
-// the work-list kernel also adds the tight candidates per (tile, beam range) and the
-// per-tile statistics there.
-int build_worklist(DeviceCtx *c, const GbsArgs &a, Tiling &t, cudaStream_t st,
-                   int64_t range_beams = 0, int64_t n_ranges = 0,
-                   unsigned long long *counts = nullptr, unsigned long long *wstats = nullptr) {
-    const int64_t n_words = (a.n_beams + 31) / 32;
-    uint32_t *bits, *tbits;
-    BF_TRY(c->get(B_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
-    BF_TRY(c->get(B_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
-    double wmin = INFINITY;
-    for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
-    BF_TRY(launch_worklist(a, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, range_beams,
-                           n_ranges, counts, wstats, st));
-    t.wl_bits = bits;
-    t.wl_tight = tbits;
-    t.wl_words = n_words;
+// Group-workspace budget: the caller's (bf_set_memory_budget) or 1/8 of device memory,
+// at most 24 GiB.  Only the grouping depends on it, never the result bits.
+int64_t group_budget(DeviceCtx *c) {
+    if (c->budget > 0) return c->budget;
+    return std::min<int64_t>((int64_t)(c->total_mem / 8), (int64_t)24 << 30);
+}
+
+struct GroupPlan {
+    int64_t range_beams = 0, n_ranges = 0;
+    std::vector<std::pair<int64_t, int64_t>> groups;  // [q0, q1) in ranges
+};
+
+// Beam groups of whole ranges sized so that NSLOT groups' workspaces fit the budget.
+// The host-buffer path ramps the group size up from one range (1, 2, 4, ...) so the
+// first group's copy is short and the later copies hide behind the summation.
+void plan_groups(DeviceCtx *c, int64_t nb, int64_t max_seg, int nf, int64_t n_tiles,
+                 int64_t n_patches, int64_t n_pad, bool host, GroupPlan *g) {
+    g->range_beams = gbs_fp32_range_beams(nb, nf);
+    const int64_t rb = g->range_beams;
+    g->n_ranges = (nb + rb - 1) / rb;
+    const int64_t per_range = n_pad * (16 * nf + 4) + n_patches * 24 + n_tiles * 16;
+    const int64_t per_beam = n_tiles / 4 + 1 + n_tiles * 4 + max_seg * (68 + 8 * nf) + 8;
+    const int64_t per_r = per_range + rb * per_beam;
+    const int64_t budget = group_budget(c);
+    int64_t max_r;
+    if (!host && per_r * g->n_ranges <= budget)
+        max_r = g->n_ranges;  // everything in one group
+    else
+        max_r = std::max<int64_t>(1, budget / NSLOT / std::max<int64_t>(per_r, 1));
+    max_r = std::min(max_r, std::max<int64_t>(1, (((int64_t)1 << 27) - 1) / (rb * max_seg)));
+    max_r = std::min(max_r, std::max<int64_t>(1, (((int64_t)1 << 31) - 1) / std::max<int64_t>(n_patches, 1)));
+    max_r = std::min(max_r, g->n_ranges);
+    g->groups.clear();
+    int64_t q = 0, step = host ? 1 : max_r;
+    while (q < g->n_ranges) {
+        const int64_t n = std::min(step, g->n_ranges - q);
+        g->groups.emplace_back(q, q + n);
+        q += n;
+        step = std::min(max_r, step * 2);
+    }
+}
+
+// Host -> device of `bytes` from host memory that may be pageable: pinned sources are
+// copied directly, pageable ones through pinned staging filled on the host threads.
+int h2d(void *dst, const void *src, size_t bytes, PinBuf &stage, cudaStream_t st) {
+    if (bytes == 0) return BF_OK;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        BF_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return BF_OK;
+    }
+    cudaGetLastError();
+    void *p;
+    BF_TRY(stage.get(bytes, &p));
+    parallel_copy(p, src, bytes);
+    BF_TRY_CUDA(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st));
     return BF_OK;
 }
 
-// Runs the operator on device-resident LOCAL ranges (a.obs etc. already offset).
-int run_gbs(DeviceCtx *c, GbsArgs &a, int precision, int flags, cudaStream_t st) {
-    g_last_stats = GbsStats{};
-    g_last_total_pairs = a.n_obs * a.n_beams;
-    g_last_tiles = 0;
-    if (a.n_obs <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
-    if (precision == BF_PRECISION_FP64) return launch_gbs_fp64(a, st);
-    Tiling t;
-    BF_TRY(build_tiling(c, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
-    Fp32Work w{};
-    const int64_t rows = a.n_beams * a.max_seg;
-    const int P = gbs_fp32_patch();
-    w.n_patches = (a.n_obs + P - 1) / P;
-    w.range_beams = gbs_fp32_range_beams(a.n_beams, a.nf);
-    w.n_ranges = (a.n_beams + w.range_beams - 1) / w.range_beams;
-    if (w.n_patches * w.n_ranges >= (int64_t)1 << 31)
-        return fail(BF_EINVAL, "too many (patch, beam range) units; split the call");
-    if (a.n_beams >= ((int64_t)1 << 27))
-        return fail(BF_EINVAL, "more than 2^27 beams in one call; split the beam range");
-    BF_TRY(c->get(B_P0, rows, &w.p0));
-    BF_TRY(c->get(B_P1, rows, &w.p1));
-    BF_TRY(c->get(B_P2, rows, &w.p2));
-    BF_TRY(c->get(B_PA, 2 * rows * a.nf, &w.pa));
-    BF_TRY(c->get(B_PRL, a.n_obs, &w.prl));
-    BF_TRY(c->get(B_PCEN, w.n_patches, &w.pcen));
-    BF_TRY(c->get(B_PBOX, w.n_patches, &w.pbox));
-    w.n_pad = w.n_patches * P;
-    BF_TRY(c->get(B_DONE, (size_t)(w.n_ranges * w.n_pad * a.nf), &w.part));
-    BF_TRY(c->get(B_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
-    BF_TRY(c->get(B_UCTR, 3, &w.unit_ctr));
-    w.n_wide = w.unit_ctr + 2;
-    BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), st));
-    {   // wide patches (fp64 tail, see unit_keys_kernel): kappa_max RW > 16 turns or
-        // omega_max RW^2 / (2 c b) > 200 (the fp32 error of r.d and q^2 grows with RW;
-        // at these bounds it stays ~5x below the 0.01 dB gate at 50 dB below the maximum)
-        double wmax = 0.0;
-        for (int f = 0; f < a.nf; ++f) wmax = a.omegas[f] > wmax ? a.omegas[f] : wmax;
-        const char *ek = getenv("BF_WIDE_TURNS"), *eq = getenv("BF_WIDE_Q");  // tuning
-        const double lk = ek ? atof(ek) : 16.0, lq = eq ? atof(eq) : 200.0;
-        w.wide_k = (float)(wmax / (2.0 * 3.141592653589793 * a.c) / lk);
-        w.wide_q = (float)(wmax / (2.0 * a.c * a.width_b) / lq);
-    }
-    unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
-    BF_TRY(c->get(B_WLCNT, (size_t)(4 * t.n_tiles), &d_cand));
-    BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
-    const int64_t nu_wl = t.n_tiles * w.n_ranges;
-    int64_t *cnt;
-    {   // tight work list counts (from the work-list kernel) -> exclusive scan
-        BF_TRY(c->get(B_WLTMP, (size_t)(nu_wl + 1), &cnt));
-        BF_TRY(c->get(B_WLOFF, (size_t)(nu_wl + 1), &w.wl_off));
-        BF_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nu_wl + 1), st));
-        BF_TRY(build_worklist(c, a, t, st, w.range_beams, w.n_ranges,
-                              reinterpret_cast<unsigned long long *>(cnt), d_cand));
-        size_t tmp_bytes = 0;
-        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, w.wl_off,
-                                                  (int)(nu_wl + 1), st));
-        void *tmp;
-        BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
-        BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, w.wl_off,
-                                                  (int)(nu_wl + 1), st));
-        note_launch();
-    }
-    BF_TRY(launch_fp32_prepare(a, t, w, st));
-    {   // unit queue order (wide patches last; longest-first buckets, range-major inside
-        // a bucket) from the counts and the patch radii of launch_fp32_prepare
-        const int64_t nu = w.n_patches * w.n_ranges;
-        uint64_t *k0, *k1;
-        int32_t *v0, *v1;
-        BF_TRY(c->get(B_UKEYS, (size_t)nu, &k0));
-        BF_TRY(c->get(B_UKEYS2, (size_t)nu, &k1));
-        BF_TRY(c->get(B_UVALS, (size_t)nu, &v0));
-        BF_TRY(c->get(B_UVALS2, (size_t)nu, &v1));
-        BF_TRY(launch_fp32_unit_keys(t, w, cnt, k0, v0, st));
-        const int end_bit = 40;  // wide << 39 | bucket (7 bits) << 32 | range
-        cub::DoubleBuffer<uint64_t> dk(k0, k1);
-        cub::DoubleBuffer<int32_t> dv(v0, v1);
-        size_t tmp_bytes = 0;
-        BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int)nu, 0,
-                                                    end_bit, st));
-        void *tmp;
-        BF_TRY(c->buf[B_CUB].get(tmp_bytes + 16, &tmp));
-        BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, dv, (int)nu, 0,
-                                                    end_bit, st));
-        note_launch();
-        w.unit_order = dv.Current();
-    }
-    {   // one host sync: work-list length (buffer size) and wide-unit count (launches)
-        int64_t total = 0;
-        unsigned n_wide = 0;
-        BF_TRY_CUDA(cudaMemcpyAsync(&total, w.wl_off + nu_wl, sizeof(int64_t),
-                                    cudaMemcpyDeviceToHost, st));
-        BF_TRY_CUDA(cudaMemcpyAsync(&n_wide, w.n_wide, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                    st));
+// Device -> host of `bytes` into host memory that may be pageable (synchronises st).
+int d2h_sync(void *dst, const void *src, size_t bytes, PinBuf &stage, cudaStream_t st) {
+    cudaPointerAttributes at;
+    if (bytes == 0) return check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        BF_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
         BF_TRY_CUDA(cudaStreamSynchronize(st));
-        w.n_wide_host = n_wide;
-        BF_TRY(c->get(B_WLITEMS, (size_t)(total + 1), &w.wl_items));
-        BF_TRY(launch_fp32_wl_compact(a, t, w, st));
+        return BF_OK;
     }
-    GbsStats *d_stats;
-    BF_TRY(c->get(B_STATS, 1, &d_stats));
-    BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
-    if (!c->ev0) {
-        BF_TRY_CUDA(cudaEventCreate(&c->ev0));
-        BF_TRY_CUDA(cudaEventCreate(&c->ev1));
-    }
-    BF_TRY_CUDA(cudaEventRecord(c->ev0, st));
-    BF_TRY(launch_gbs_fp32(a, t, w, d_stats, StreamPair{st, c->aux, c->fork, c->join}));
-    BF_TRY_CUDA(cudaEventRecord(c->ev1, st));
-    GbsStats h;
-    BF_TRY_CUDA(cudaMemcpyAsync(&h, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost, st));
+    cudaGetLastError();
+    void *p;
+    BF_TRY(stage.get(bytes, &p));
+    BF_TRY_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyDeviceToHost, st));
     BF_TRY_CUDA(cudaStreamSynchronize(st));
-    BF_TRY_CUDA(cudaEventElapsedTime(&h.kernel_ms, c->ev0, c->ev1));
-    std::vector<unsigned long long> cand((size_t)(4 * t.n_tiles));
-    BF_TRY_CUDA(cudaMemcpy(cand.data(), d_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
-                           cudaMemcpyDeviceToHost));
-    unsigned long long cp = 0, cs = 0, tp = 0, ts = 0;
-    for (int64_t i = 0; i < t.n_tiles; ++i) {
-        const unsigned long long in_tile =
-            (unsigned long long)((i + 1 < t.n_tiles) ? t.tile : a.n_obs - i * t.tile);
-        cp += cand[(size_t)i] * in_tile;
-        cs += cand[(size_t)(t.n_tiles + i)] * in_tile;
-        tp += cand[(size_t)(2 * t.n_tiles + i)] * in_tile;
-        ts += cand[(size_t)(3 * t.n_tiles + i)] * in_tile;
+    parallel_copy(dst, p, bytes);
+    return BF_OK;
+}
+
+// Compact rows of host beams [b0, b0 + nb) (local indices of h) packed on the host
+// threads into the slot's pinned staging and copied to its device buffers on s.ss.
+int rows_from_host(const GbsArgs &h, int64_t b0, int64_t nb, Slot &s, Rows *out,
+                   int64_t *n_rows) {
+    if (s.h2d_valid) BF_TRY_CUDA(cudaEventSynchronize(s.h2d));  // staging reused
+    int64_t *hs;
+    BF_TRY(s.pinned(P_START, (size_t)(nb + 1), &hs));
+    const int64_t S = h.max_seg;
+    hs[0] = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        int64_t n = h.n_segs[b0 + i];
+        n = n < 0 ? 0 : (n > S ? S : n);
+        hs[i + 1] = hs[i] + n;
     }
-    h.candidate_pairs = cp;
-    h.cand_pair_segs = cs;
-    h.tight_pairs = tp;
-    h.tight_pair_segs = ts;
-    g_last_stats = h;
-    if (getenv("BF_DEBUG_STATS")) {
-        unsigned nw = 0;
-        cudaMemcpy(&nw, w.n_wide, sizeof(unsigned), cudaMemcpyDeviceToHost);
-        fprintf(stderr, "bf units: %lld, of wide patches %u\n",
-                (long long)(w.n_patches * w.n_ranges), nw);
+    const int64_t rows = hs[nb];
+    double4 *hp0, *hp1;
+    float *ha;
+    BF_TRY(s.pinned(P_P0, (size_t)rows, &hp0));
+    BF_TRY(s.pinned(P_P1, (size_t)rows, &hp1));
+    BF_TRY(s.pinned(P_AMP, (size_t)rows, &ha));
+    const double amp_scale = h.phi_amp * sqrt(h.c) / (2.0 * 3.141592653589793 * h.c);
+    parallel_for(nb, 4096, [&](int64_t lo, int64_t hi) {
+        for (int64_t i = lo; i < hi; ++i) {
+            const int64_t b = b0 + i, dst0 = hs[i], n = hs[i + 1] - hs[i];
+            const double wb = h.weights[b];
+            for (int64_t k = 0; k < n; ++k) {
+                const int64_t row = b * S + k, d = dst0 + k;
+                const double *o = h.seg_origin + 3 * row, *dd = h.seg_dir + 3 * row;
+                hp0[d] = make_double4(o[0], o[1], o[2], h.seg_len[row]);
+                hp1[d] = make_double4(dd[0], dd[1], dd[2], h.seg_s0[row]);
+                // same operations as rows_pack_kernel: (amp_scale * refl) * w_b, one rounding
+                ha[d] = (float)(amp_scale * h.seg_refl[row] * wb);
+            }
+        }
+    });
+    int64_t *ds;
+    double4 *dp0, *dp1;
+    float *da;
+    BF_TRY(s.get(S_START, (size_t)(nb + 1), &ds));
+    BF_TRY(s.get(S_P0, (size_t)std::max<int64_t>(rows, 1), &dp0));
+    BF_TRY(s.get(S_P1, (size_t)std::max<int64_t>(rows, 1), &dp1));
+    BF_TRY(s.get(S_AMP, (size_t)std::max<int64_t>(rows, 1), &da));
+    const auto H2D = cudaMemcpyHostToDevice;
+    BF_TRY_CUDA(cudaMemcpyAsync(ds, hs, 8 * (size_t)(nb + 1), H2D, s.ss));
+    BF_TRY_CUDA(cudaMemcpyAsync(dp0, hp0, 32 * (size_t)rows, H2D, s.ss));
+    BF_TRY_CUDA(cudaMemcpyAsync(dp1, hp1, 32 * (size_t)rows, H2D, s.ss));
+    BF_TRY_CUDA(cudaMemcpyAsync(da, ha, 4 * (size_t)rows, H2D, s.ss));
+    BF_TRY_CUDA(cudaEventRecord(s.h2d, s.ss));
+    s.h2d_valid = true;
+    *out = Rows{ds, dp0, dp1, da, nb, S};
+    *n_rows = rows;
+    return BF_OK;
+}
+
+// Compact rows of device beams [b0, b0 + nb) of the padded bundle in g (local indices),
+// packed on s.ss.  The row count stays on the device; rows_bound = nb * max_seg.
+int rows_from_device(const GbsArgs &g, Slot &s, Rows *out) {
+    const int64_t nb = g.n_beams, S = g.max_seg;
+    int64_t *ds;
+    double4 *dp0, *dp1;
+    float *da;
+    BF_TRY(s.get(S_START, (size_t)(nb + 1), &ds));
+    BF_TRY(s.get(S_P0, (size_t)std::max<int64_t>(nb * S, 1), &dp0));
+    BF_TRY(s.get(S_P1, (size_t)std::max<int64_t>(nb * S, 1), &dp1));
+    BF_TRY(s.get(S_AMP, (size_t)std::max<int64_t>(nb * S, 1), &da));
+    BF_TRY(launch_rows_count(g.n_segs, nb, S, ds, s.ss));
+    size_t tb = 0;
+    BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, ds, ds, (int)(nb + 1), s.ss));
+    void *tmp;
+    BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
+    BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, ds, ds, (int)(nb + 1), s.ss));
+    note_launch();
+    BF_TRY(launch_rows_pack(g, ds, dp0, dp1, da, s.ss));
+    *out = Rows{ds, dp0, dp1, da, nb, S};
+    return BF_OK;
+}
+
+// The fp32 operator on LOCAL ranges: base.obs/acc/evals are device pointers (offset to
+// obs_lo, acc rows of base.acc_stride complex values); base.seg_*/n_segs/weights are the
+// padded bundle from beam_lo, on the device or (host_rows) in host memory.
+int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf,
+             bool host_rows, int flags, cudaStream_t st) {
+    stats_begin(base.n_obs * base.n_beams);
+    if (base.n_obs <= 0 || base.n_beams <= 0 || nf <= 0) return BF_OK;
+    // ---- prologue on the call's stream: receiver tiling, patches, zeroed counters
+    Tiling t;
+    BF_TRY(build_tiling(c, base.obs, base.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
+    Fp32Work w0{};
+    const int P = gbs_fp32_patch();
+    w0.n_patches = (base.n_obs + P - 1) / P;
+    w0.n_pad = w0.n_patches * P;
+    BF_TRY(c->get(B_PRL, (size_t)base.n_obs, &w0.prl));
+    BF_TRY(c->get(B_PCEN, (size_t)w0.n_patches, &w0.pcen));
+    BF_TRY(c->get(B_PBOX, (size_t)w0.n_patches, &w0.pbox));
+    BF_TRY(launch_fp32_patches(base, t, w0, st));
+    GbsStats *d_stats;
+    unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
+    BF_TRY(c->get(B_STATS, 1, &d_stats));
+    BF_TRY(c->get(B_CAND, (size_t)(4 * t.n_tiles), &d_cand));
+    BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
+    BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
+    BF_TRY_CUDA(cudaEventRecord(c->pro, st));
+    for (Slot &s : c->slot) BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->pro, 0));
+    BF_TRY(stats_events(c->dev));
+    StatsBuf *sb;
+    BF_TRY(stats_next(&sb));
+    bool timed = false;
+    int64_t gi = 0;
+    // ---- frequency groups of <= BF_MAXF (acc columns are independent)
+    for (int64_t f0 = 0; f0 < nf; f0 += BF_MAXF) {
+        GbsArgs ag = base;
+        ag.nf = (int)std::min<int64_t>(BF_MAXF, nf - f0);
+        for (int f = 0; f < BF_MAXF; ++f) ag.omegas[f] = f < ag.nf ? omegas[f0 + f] : 0.0;
+        ag.acc = base.acc + 2 * f0;
+        Fp32Work wf = w0;
+        {   // wide patches (fp64 tail, see unit_keys_kernel): kappa_max RW > 16 turns or
+            // omega_max RW^2 / (2 c b) > 200 (the fp32 error of r.d and q^2 grows with RW;
+            // at these bounds it stays ~5x below the 0.01 dB gate at 50 dB below the maximum)
+            double wmax = 0.0;
+            for (int f = 0; f < ag.nf; ++f) wmax = ag.omegas[f] > wmax ? ag.omegas[f] : wmax;
+            wf.wide_k = (float)(wmax / (2.0 * 3.141592653589793 * ag.c) / 16.0);
+            wf.wide_q = (float)(wmax / (2.0 * ag.c * ag.width_b) / 200.0);
+        }
+        double wmin = INFINITY;
+        for (int f = 0; f < ag.nf; ++f) wmin = ag.omegas[f] < wmin ? ag.omegas[f] : wmin;
+        GroupPlan plan;
+        plan_groups(c, ag.n_beams, ag.max_seg, ag.nf, t.n_tiles, w0.n_patches, w0.n_pad,
+                    host_rows, &plan);
+        const int64_t rb = plan.range_beams;
+        for (const auto &grp : plan.groups) {
+            Slot &s = c->slot[gi++ % NSLOT];
+            if (s.freed_valid) BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, s.freed, 0));
+            const int64_t b0 = grp.first * rb, b1 = std::min(grp.second * rb, ag.n_beams);
+            GbsArgs gg = ag;
+            gg.n_beams = b1 - b0;
+            const int64_t r0 = b0 * ag.max_seg;
+            gg.seg_origin = ag.seg_origin + 3 * r0;
+            gg.seg_dir = ag.seg_dir + 3 * r0;
+            gg.seg_e1 = gg.seg_e2 = nullptr;
+            gg.seg_len = ag.seg_len + r0;
+            gg.seg_s0 = ag.seg_s0 + r0;
+            gg.seg_refl = ag.seg_refl + r0;
+            gg.n_segs = ag.n_segs + b0;
+            gg.weights = ag.weights + b0;
+            // ---- compact rows of the group
+            Rows rv;
+            int64_t rows_bound;
+            if (host_rows) {
+                BF_TRY(rows_from_host(ag, b0, gg.n_beams, s, &rv, &rows_bound));
+            } else {
+                BF_TRY(rows_from_device(gg, s, &rv));
+                rows_bound = gg.n_beams * gg.max_seg;
+            }
+            Fp32Work w = wf;
+            w.start = rv.start;
+            w.p0 = rv.p0;
+            w.p1 = rv.p1;
+            w.amp = rv.amp;
+            float *pa;
+            BF_TRY(s.get(S_PA, (size_t)(2 * std::max<int64_t>(rows_bound, 1) * ag.nf), &pa));
+            BF_TRY(launch_fp32_anchors(gg, rv, rows_bound, pa, s.ss));
+            w.pa = pa;
+            w.range_beams = rb;
+            w.n_ranges = grp.second - grp.first;
+            // ---- tight work list of the group: bitmasks + counts per (tile, range)
+            const int64_t n_words = (gg.n_beams + 31) / 32;
+            uint32_t *bits, *tbits;
+            BF_TRY(s.get(S_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
+            BF_TRY(s.get(S_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
+            const int64_t nu_wl = t.n_tiles * w.n_ranges;
+            int64_t *cnt;
+            BF_TRY(s.get(S_WLCNT, (size_t)(nu_wl + 1), &cnt));
+            BF_TRY(s.get(S_WLOFF, (size_t)(nu_wl + 1), &w.wl_off));
+            BF_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nu_wl + 1), s.ss));
+            BF_TRY(launch_worklist(gg, rv, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, rb,
+                                   w.n_ranges, reinterpret_cast<unsigned long long *>(cnt),
+                                   d_cand, s.ss));
+            Tiling tg = t;
+            tg.wl_bits = bits;
+            tg.wl_tight = tbits;
+            tg.wl_words = n_words;
+            {
+                size_t tb = 0;
+                BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, w.wl_off,
+                                                          (int)(nu_wl + 1), s.ss));
+                void *tmp;
+                BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
+                BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, w.wl_off,
+                                                          (int)(nu_wl + 1), s.ss));
+                note_launch();
+            }
+            // ---- unit queue order (wide patches last; longest-first buckets, range-major
+            //      inside a bucket) from the counts and the patch radii
+            BF_TRY(s.get(S_UCTR, 3, &w.unit_ctr));
+            w.n_wide = w.unit_ctr + 2;
+            BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), s.ss));
+            {
+                const int64_t nu = w.n_patches * w.n_ranges;
+                uint64_t *k0, *k1;
+                int32_t *v0, *v1;
+                BF_TRY(s.get(S_UKEYS, (size_t)nu, &k0));
+                BF_TRY(s.get(S_UKEYS2, (size_t)nu, &k1));
+                BF_TRY(s.get(S_UVALS, (size_t)nu, &v0));
+                BF_TRY(s.get(S_UVALS2, (size_t)nu, &v1));
+                BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
+                const int end_bit = 40;  // wide << 39 | bucket (7 bits) << 32 | range
+                cub::DoubleBuffer<uint64_t> dk(k0, k1);
+                cub::DoubleBuffer<int32_t> dv(v0, v1);
+                size_t tb = 0;
+                BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nu, 0,
+                                                            end_bit, s.ss));
+                void *tmp;
+                BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
+                BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nu, 0,
+                                                            end_bit, s.ss));
+                note_launch();
+                w.unit_order = dv.Current();
+            }
+            // ---- compacted work list: sized by its bound (tiles x beams), no host sync
+            BF_TRY(s.get(S_WLITEMS, (size_t)(t.n_tiles * gg.n_beams + 1), &w.wl_items));
+            BF_TRY(launch_fp32_wl_compact(tg, w, s.ss));
+            BF_TRY(s.get(S_PART, (size_t)(w.n_ranges * w.n_pad * ag.nf), &w.part));
+            BF_TRY(s.get(S_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
+            if (!timed) {
+                BF_TRY_CUDA(cudaEventRecord(sb->t0, s.ss));
+                timed = true;
+            }
+            BF_TRY(launch_gbs_fp32(gg, tg, w, d_stats, StreamPair{s.ss, s.sw, s.fork, s.join}));
+            BF_TRY_CUDA(cudaEventRecord(s.kdone, s.ss));
+            // ---- fold on the call's stream, groups in order
+            BF_TRY_CUDA(cudaStreamWaitEvent(st, s.kdone, 0));
+            BF_TRY(launch_fp32_fold(gg, tg, w, st));
+            BF_TRY_CUDA(cudaEventRecord(s.freed, st));
+            s.freed_valid = true;
+        }
     }
-    if (getenv("BF_DEBUG_STATS"))
-        fprintf(stderr, "bf stats: items culled %llu single %llu wedge %llu multi %llu "
-                "(surv 2:%llu 3:%llu 4:%llu 5+:%llu) ties %llu\n", h.paths[0], h.paths[1],
-                h.paths[2], h.paths[3], h.multi_surv[0], h.multi_surv[1], h.multi_surv[2],
-                h.multi_surv[3], h.tie_pairs);
-    g_last_tiles = t.n_tiles;
+    BF_TRY_CUDA(cudaEventRecord(sb->t1, st));
+    // ---- statistics: copied back asynchronously, reduced on request (bf_last_stats)
+    if (!sb->h_stats)
+        BF_TRY_CUDA(cudaHostAlloc(&sb->h_stats, sizeof(GbsStats), cudaHostAllocPortable));
+    if (sb->cand_cap < (size_t)(4 * t.n_tiles)) {
+        if (sb->h_cand) cudaFreeHost(sb->h_cand);
+        sb->h_cand = nullptr;
+        sb->cand_cap = 0;
+        BF_TRY_CUDA(cudaHostAlloc(&sb->h_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
+                                  cudaHostAllocPortable));
+        sb->cand_cap = (size_t)(4 * t.n_tiles);
+    }
+    BF_TRY_CUDA(cudaMemcpyAsync(sb->h_stats, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost,
+                                st));
+    BF_TRY_CUDA(cudaMemcpyAsync(sb->h_cand, d_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
+                                cudaMemcpyDeviceToHost, st));
+    BF_TRY_CUDA(cudaEventRecord(sb->ready, st));
+    sb->inflight = true;
+    sb->n_tiles = t.n_tiles;
+    sb->tile = t.tile;
+    sb->n_obs = base.n_obs;
+    g_ps.pending = true;
+    return BF_OK;
+}
+
+// The fp64 (oracle-mode) operator on device-resident LOCAL ranges, frequency groups of
+// <= BF_MAXF (one thread per observer continues acc in ascending beam order).
+int run_fp64(const GbsArgs &base, const double *omegas, int64_t nf, cudaStream_t st) {
+    if (base.n_obs <= 0 || base.n_beams <= 0 || nf <= 0) return BF_OK;
+    for (int64_t f0 = 0; f0 < nf; f0 += BF_MAXF) {
+        GbsArgs ag = base;
+        ag.nf = (int)std::min<int64_t>(BF_MAXF, nf - f0);
+        for (int f = 0; f < BF_MAXF; ++f) ag.omegas[f] = f < ag.nf ? omegas[f0 + f] : 0.0;
+        ag.acc = base.acc + 2 * f0;
+        BF_TRY(launch_gbs_fp64(ag, st));
+    }
+    return BF_OK;
+}
+
+// fp64 operator on HOST padded rows: beam chunks (budgeted) copied through two pinned
+// staging slots while the previous chunk sums; per observer the beams still run in
+// ascending order, so the result equals one device call bit for bit.
+int run_fp64_host(DeviceCtx *c, const GbsArgs &h, const double *omegas, int64_t nf,
+                  cudaStream_t st) {
+    if (h.n_obs <= 0 || h.n_beams <= 0 || nf <= 0) return BF_OK;
+    const int64_t S = h.max_seg;
+    const int64_t per_beam = S * (4 * 24 + 3 * 8) + 4 + 8;
+    const int64_t chunk = std::max<int64_t>(
+        1, std::min<int64_t>(h.n_beams, group_budget(c) / 2 / per_beam));
+    BF_TRY_CUDA(cudaEventRecord(c->pro, st));
+    int64_t gi = 0;
+    for (int64_t b0 = 0; b0 < h.n_beams; b0 += chunk, ++gi) {
+        Slot &s = c->slot[gi % 2];
+        const int64_t nb = std::min(chunk, h.n_beams - b0), rows = nb * S;
+        BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->pro, 0));
+        if (s.freed_valid) BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, s.freed, 0));
+        if (s.h2d_valid) BF_TRY_CUDA(cudaEventSynchronize(s.h2d));
+        const size_t bytes = (size_t)(rows * (4 * 24 + 3 * 8) + nb * 12);
+        char *hp, *dp;
+        BF_TRY(s.pinned(P_F64, bytes, &hp));
+        BF_TRY(s.get(S_F64, bytes, &dp));
+        // carve: origin, dir, e1, e2 (24 B/row), len, s0, refl (8 B/row), weights, n_segs
+        const size_t off[10] = {0,
+                                (size_t)rows * 24,
+                                (size_t)rows * 48,
+                                (size_t)rows * 72,
+                                (size_t)rows * 96,
+                                (size_t)rows * 104,
+                                (size_t)rows * 112,
+                                (size_t)rows * 120,
+                                (size_t)rows * 120 + (size_t)nb * 8,
+                                bytes};
+        const void *src[9] = {h.seg_origin + 3 * b0 * S, h.seg_dir + 3 * b0 * S,
+                              h.seg_e1 + 3 * b0 * S,     h.seg_e2 + 3 * b0 * S,
+                              h.seg_len + b0 * S,        h.seg_s0 + b0 * S,
+                              h.seg_refl + b0 * S,       h.weights + b0,
+                              h.n_segs + b0};
+        for (int i = 0; i < 9; ++i) parallel_copy(hp + off[i], src[i], off[i + 1] - off[i]);
+        BF_TRY_CUDA(cudaMemcpyAsync(dp, hp, bytes, cudaMemcpyHostToDevice, s.ss));
+        BF_TRY_CUDA(cudaEventRecord(s.h2d, s.ss));
+        s.h2d_valid = true;
+        BF_TRY_CUDA(cudaStreamWaitEvent(st, s.h2d, 0));
+        GbsArgs g = h;
+        g.seg_origin = (const double *)(dp + off[0]);
+        g.seg_dir = (const double *)(dp + off[1]);
+        g.seg_e1 = (const double *)(dp + off[2]);
+        g.seg_e2 = (const double *)(dp + off[3]);
+        g.seg_len = (const double *)(dp + off[4]);
+        g.seg_s0 = (const double *)(dp + off[5]);
+        g.seg_refl = (const double *)(dp + off[6]);
+        g.weights = (const double *)(dp + off[7]);
+        g.n_segs = (const int32_t *)(dp + off[8]);
+        g.n_beams = nb;
+        BF_TRY(run_fp64(g, omegas, nf, st));
+        BF_TRY_CUDA(cudaEventRecord(s.freed, st));
+        s.freed_valid = true;
+    }
     return BF_OK;
 }
 
@@ -581,7 +1026,7 @@ using namespace bf;
 
 extern "C" {
 
-const char *bf_version(void) { return "paper_2501_13382_b200 0.1.0 (sm_100a)"; }
+const char *bf_version(void) { return "paper_2501_13382_b200 0.2.0 (sm_100a)"; }
 
 const char *bf_last_error(void) { return g_err; }
 
@@ -596,35 +1041,50 @@ int bf_device_count(void) {
 
 uint64_t bf_launch_count(void) { return g_launches.load(); }
 
+int bf_set_memory_budget(int device, int64_t bytes) {
+    if (bytes < 0) return fail(BF_EINVAL, "negative memory budget");
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->budget = bytes;
+    return BF_OK;
+}
+
 int bf_last_stats(int64_t *candidate_pairs, int64_t *total_pairs, int64_t *tie_pairs,
                   int64_t *n_tiles, int64_t *nonbehind_pairs, double *kernel_ms,
                   int64_t *candidate_pair_segs) {
-    if (candidate_pair_segs) *candidate_pair_segs = (int64_t)g_last_stats.cand_pair_segs;
-    if (nonbehind_pairs) *nonbehind_pairs = (int64_t)g_last_stats.nb_pairs;
-    if (kernel_ms) *kernel_ms = (double)g_last_stats.kernel_ms;
-    if (candidate_pairs) *candidate_pairs = (int64_t)g_last_stats.candidate_pairs;
-    if (total_pairs) *total_pairs = g_last_total_pairs;
-    if (tie_pairs) *tie_pairs = (int64_t)g_last_stats.tie_pairs;
-    if (n_tiles) *n_tiles = g_last_tiles;
+    materialize_stats();
+    const GbsStats &s = g_ps.last;
+    if (candidate_pair_segs) *candidate_pair_segs = (int64_t)s.cand_pair_segs;
+    if (nonbehind_pairs) *nonbehind_pairs = (int64_t)s.nb_pairs;
+    if (kernel_ms) *kernel_ms = (double)s.kernel_ms;
+    if (candidate_pairs) *candidate_pairs = (int64_t)s.candidate_pairs;
+    if (total_pairs) *total_pairs = g_ps.last_total_pairs;
+    if (tie_pairs) *tie_pairs = (int64_t)s.tie_pairs;
+    if (n_tiles) *n_tiles = g_ps.last_tiles;
     return BF_OK;
 }
 
 int bf_last_pair_stats(int64_t *a9_pairs, int64_t *a9_pair_segs, int64_t *tight_pairs,
                        int64_t *tight_pair_segs, int64_t *live_pairs, int64_t *live_pair_segs) {
-    if (a9_pairs) *a9_pairs = (int64_t)g_last_stats.candidate_pairs;
-    if (a9_pair_segs) *a9_pair_segs = (int64_t)g_last_stats.cand_pair_segs;
-    if (tight_pairs) *tight_pairs = (int64_t)g_last_stats.tight_pairs;
-    if (tight_pair_segs) *tight_pair_segs = (int64_t)g_last_stats.tight_pair_segs;
-    if (live_pairs) *live_pairs = (int64_t)g_last_stats.live_pairs;
-    if (live_pair_segs) *live_pair_segs = (int64_t)g_last_stats.live_pair_segs;
+    materialize_stats();
+    const GbsStats &s = g_ps.last;
+    if (a9_pairs) *a9_pairs = (int64_t)s.candidate_pairs;
+    if (a9_pair_segs) *a9_pair_segs = (int64_t)s.cand_pair_segs;
+    if (tight_pairs) *tight_pairs = (int64_t)s.tight_pairs;
+    if (tight_pair_segs) *tight_pair_segs = (int64_t)s.tight_pair_segs;
+    if (live_pairs) *live_pairs = (int64_t)s.live_pairs;
+    if (live_pair_segs) *live_pair_segs = (int64_t)s.live_pair_segs;
     return BF_OK;
 }
 
 int bf_last_path_stats(int64_t *culled, int64_t *single, int64_t *wedge, int64_t *multi) {
-    if (culled) *culled = (int64_t)g_last_stats.paths[0];
-    if (single) *single = (int64_t)g_last_stats.paths[1];
-    if (wedge) *wedge = (int64_t)g_last_stats.paths[2];
-    if (multi) *multi = (int64_t)g_last_stats.paths[3];
+    materialize_stats();
+    const GbsStats &s = g_ps.last;
+    if (culled) *culled = (int64_t)s.paths[0];
+    if (single) *single = (int64_t)s.paths[1];
+    if (wedge) *wedge = (int64_t)s.paths[2];
+    if (multi) *multi = (int64_t)s.paths[3];
     return BF_OK;
 }
 
@@ -639,13 +1099,15 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
                           int64_t beam_hi, int precision, int flags, int device,
                           void *stream) {
     BF_TRY(validate(n_beams, max_seg, n_obs, nf, obs_lo, obs_hi, beam_lo, beam_hi, precision));
+    if (precision == BF_PRECISION_FP64 && (!seg_e1 || !seg_e2))
+        return fail(BF_EINVAL, "fp64 mode needs seg_e1/seg_e2");
     DeviceCtx *ctx;
     BF_TRY(get_ctx(device, &ctx));
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
     StreamOrder order(ctx, st);
-    GbsArgs a;
+    GbsArgs a{};
     const int64_t r0 = beam_lo * max_seg;
     a.seg_origin = seg_origin + 3 * r0;
     a.seg_dir = seg_dir + 3 * r0;
@@ -660,17 +1122,20 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
     a.max_seg = max_seg;
     a.n_beams = beam_hi - beam_lo;
     a.n_obs = obs_hi - obs_lo;
-    a.nf = (int)nf;
-    for (int f = 0; f < BF_MAXF; ++f) a.omegas[f] = f < nf ? omegas[f] : 0.0;
+    a.nf = (int)std::min<int64_t>(nf, BF_MAXF);
     a.c = c;
     a.width_b = width_b;
     a.phi_amp = phi_amp;
     a.use_cutoff = use_cutoff ? 1 : 0;
     a.acc = acc + 2 * obs_lo * nf;
+    a.acc_stride = nf;
     a.evals = evals + obs_lo;
-    if (precision == BF_PRECISION_FP64 && (!seg_e1 || !seg_e2))
-        return fail(BF_EINVAL, "fp64 mode needs seg_e1/seg_e2");
-    BF_TRY(run_gbs(ctx, a, precision, flags, st));
+    if (precision == BF_PRECISION_FP64) {
+        stats_begin(a.n_obs * a.n_beams);
+        BF_TRY(run_fp64(a, omegas, nf, st));
+    } else {
+        BF_TRY(run_fp32(ctx, a, omegas, nf, false, flags, st));
+    }
     if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
     return BF_OK;
 }
@@ -684,7 +1149,10 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
                       int64_t obs_lo, int64_t obs_hi, int64_t beam_lo, int64_t beam_hi,
                       int precision, int device) {
     BF_TRY(validate(n_beams, max_seg, n_obs, nf, obs_lo, obs_hi, beam_lo, beam_hi, precision));
+    if (precision == BF_PRECISION_FP64 && (!seg_e1 || !seg_e2))
+        return fail(BF_EINVAL, "fp64 mode needs seg_e1/seg_e2");
     const int64_t nb = beam_hi - beam_lo, no = obs_hi - obs_lo;
+    stats_begin(no * nb);
     if (nb == 0 || no == 0 || nf == 0) return BF_OK;
     DeviceCtx *ctx;
     BF_TRY(get_ctx(device, &ctx));
@@ -692,68 +1160,45 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = ctx->stream;
     StreamOrder order(ctx, st);
-    const bool need_frame = precision == BF_PRECISION_FP64;
-    const int64_t rows = nb * max_seg, r0 = beam_lo * max_seg;
-    double *d_or, *d_dir, *d_e1 = nullptr, *d_e2 = nullptr, *d_len, *d_s0, *d_refl, *d_w, *d_obs,
-                                *d_acc;
-    int32_t *d_ns;
+    // observers and the caller's acc/evals rows go to the device first (the tiling needs
+    // the observers; acc/evals are only read by the first fold)
+    double *d_obs, *d_acc;
     int64_t *d_ev;
-    BF_TRY(ctx->get(B_ORIGIN, 3 * rows, &d_or));
-    BF_TRY(ctx->get(B_DIR, 3 * rows, &d_dir));
-    if (need_frame) {
-        BF_TRY(ctx->get(B_E1, 3 * rows, &d_e1));
-        BF_TRY(ctx->get(B_E2, 3 * rows, &d_e2));
-    }
-    BF_TRY(ctx->get(B_LEN, rows, &d_len));
-    BF_TRY(ctx->get(B_S0, rows, &d_s0));
-    BF_TRY(ctx->get(B_REFL, rows, &d_refl));
-    BF_TRY(ctx->get(B_NSEGS, nb, &d_ns));
-    BF_TRY(ctx->get(B_W, nb, &d_w));
-    BF_TRY(ctx->get(B_OBS, 3 * no, &d_obs));
-    BF_TRY(ctx->get(B_ACC, 2 * no * nf, &d_acc));
-    BF_TRY(ctx->get(B_EVALS, no, &d_ev));
-    const auto H2D = cudaMemcpyHostToDevice;
-    BF_TRY_CUDA(cudaMemcpyAsync(d_or, seg_origin + 3 * r0, 24 * rows, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_dir, seg_dir + 3 * r0, 24 * rows, H2D, st));
-    if (need_frame) {
-        BF_TRY_CUDA(cudaMemcpyAsync(d_e1, seg_e1 + 3 * r0, 24 * rows, H2D, st));
-        BF_TRY_CUDA(cudaMemcpyAsync(d_e2, seg_e2 + 3 * r0, 24 * rows, H2D, st));
-    }
-    BF_TRY_CUDA(cudaMemcpyAsync(d_len, seg_len + r0, 8 * rows, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_s0, seg_s0 + r0, 8 * rows, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_refl, seg_refl + r0, 8 * rows, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_ns, n_segs + beam_lo, 4 * nb, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_w, weights + beam_lo, 8 * nb, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_obs, obs + 3 * obs_lo, 24 * no, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_acc, acc + 2 * obs_lo * nf, 16 * no * nf, H2D, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(d_ev, evals + obs_lo, 8 * no, H2D, st));
-    GbsArgs a;
-    a.seg_origin = d_or;
-    a.seg_dir = d_dir;
-    a.seg_e1 = d_e1;
-    a.seg_e2 = d_e2;
-    a.seg_len = d_len;
-    a.seg_s0 = d_s0;
-    a.seg_refl = d_refl;
-    a.n_segs = d_ns;
-    a.weights = d_w;
+    BF_TRY(ctx->get(B_OBS, (size_t)(3 * no), &d_obs));
+    BF_TRY(ctx->get(B_ACC, (size_t)(2 * no * nf), &d_acc));
+    BF_TRY(ctx->get(B_EVALS, (size_t)no, &d_ev));
+    BF_TRY(h2d(d_obs, obs + 3 * obs_lo, 24 * (size_t)no, ctx->hpin[H_OBS], st));
+    BF_TRY(h2d(d_acc, acc + 2 * obs_lo * nf, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
+    BF_TRY(h2d(d_ev, evals + obs_lo, 8 * (size_t)no, ctx->hpin[H_EV], st));
+    GbsArgs a{};
+    const int64_t r0 = beam_lo * max_seg;
+    a.seg_origin = seg_origin + 3 * r0;
+    a.seg_dir = seg_dir + 3 * r0;
+    a.seg_e1 = seg_e1 ? seg_e1 + 3 * r0 : nullptr;
+    a.seg_e2 = seg_e2 ? seg_e2 + 3 * r0 : nullptr;
+    a.seg_len = seg_len + r0;
+    a.seg_s0 = seg_s0 + r0;
+    a.seg_refl = seg_refl + r0;
+    a.n_segs = n_segs + beam_lo;
+    a.weights = weights + beam_lo;
     a.obs = d_obs;
     a.max_seg = max_seg;
     a.n_beams = nb;
     a.n_obs = no;
-    a.nf = (int)nf;
-    for (int f = 0; f < BF_MAXF; ++f) a.omegas[f] = f < nf ? omegas[f] : 0.0;
+    a.nf = (int)std::min<int64_t>(nf, BF_MAXF);
     a.c = c;
     a.width_b = width_b;
     a.phi_amp = phi_amp;
     a.use_cutoff = use_cutoff ? 1 : 0;
     a.acc = d_acc;
+    a.acc_stride = nf;
     a.evals = d_ev;
-    BF_TRY(run_gbs(ctx, a, precision, 0, st));
-    const auto D2H = cudaMemcpyDeviceToHost;
-    BF_TRY_CUDA(cudaMemcpyAsync(acc + 2 * obs_lo * nf, d_acc, 16 * no * nf, D2H, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(evals + obs_lo, d_ev, 8 * no, D2H, st));
-    BF_TRY_CUDA(cudaStreamSynchronize(st));
+    if (precision == BF_PRECISION_FP64)
+        BF_TRY(run_fp64_host(ctx, a, omegas, nf, st));
+    else
+        BF_TRY(run_fp32(ctx, a, omegas, nf, true, 0, st));
+    BF_TRY(d2h_sync(acc + 2 * obs_lo * nf, d_acc, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
+    BF_TRY(d2h_sync(evals + obs_lo, d_ev, 8 * (size_t)no, ctx->hpin[H_EV], st));
     return BF_OK;
 }
 
@@ -828,7 +1273,7 @@ int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
                        int64_t max_seg, double *seg_origin, double *seg_dir, double *seg_e1,
                        double *seg_e2, double *seg_len, double *seg_s0, double *seg_refl,
                        int32_t *n_segs, int32_t *n_refls, int64_t lo, int64_t hi,
-                       int64_t row_base, int device, void *stream) {
+                       int64_t row_base, int flags, int device, void *stream) {
     if (r_max < 0 || max_seg < r_max + 1) return fail(BF_EINVAL, "max_seg must be >= r_max+1");
     if (hi < lo || lo < row_base) return fail(BF_EINVAL, "bad ray range");
     if (n_tri < 0) return fail(BF_EINVAL, "negative triangle count");
@@ -838,11 +1283,10 @@ int bf_trace_range_dev(const double *v0, const double *v1, const double *v2,
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
     StreamOrder order(ctx, st);
-    // triangle-cluster boxes for the hit search; BF_TRACE_EXHAUSTIVE=1 tests every
+    // triangle-cluster boxes for the hit search; BF_TRACE_EXHAUSTIVE tests every
     // triangle (the self-check of the culling, same bits)
     double *cbox = nullptr;
-    const char *ex = getenv("BF_TRACE_EXHAUSTIVE");
-    if (n_tri > 0 && !(ex && ex[0] == '1'))
+    if (n_tri > 0 && !(flags & BF_TRACE_EXHAUSTIVE))
         BF_TRY(ctx->get(B_CBOX, (size_t)(6 * trace_cluster_count(n_tri)), &cbox));
     BF_TRY(launch_trace(v0, v1, v2, refl_coef, n_tri, cbox, bounds, diameter, origin, dirs, e1s, e2s,
                         length_cap, r_max, max_seg, seg_origin, seg_dir, seg_e1, seg_e2, seg_len,
@@ -856,7 +1300,6 @@ int bf_field_finalize_dev(const double *acc, int64_t n, double calibration, doub
     if (n < 0) return fail(BF_EINVAL, "negative size");
     DeviceCtx *ctx;
     BF_TRY(get_ctx(device, &ctx));
-    std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
     BF_TRY(launch_finalize(acc, n, calibration, pressure, spl, st));
@@ -884,12 +1327,14 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     cudaStream_t st = ctx->stream;
     StreamOrder order(ctx, st);
     const int64_t rows = n_beams * max_seg;
-    double *d_or, *d_dir, *d_len, *d_s0, *d_obs;
+    double *d_or, *d_dir, *d_len, *d_s0, *d_obs, *d_refl, *d_w;
     int32_t *d_ns;
     BF_TRY(ctx->get(B_ORIGIN, 3 * rows, &d_or));
     BF_TRY(ctx->get(B_DIR, 3 * rows, &d_dir));
     BF_TRY(ctx->get(B_LEN, rows, &d_len));
     BF_TRY(ctx->get(B_S0, rows, &d_s0));
+    BF_TRY(ctx->get(B_REFL, rows, &d_refl));
+    BF_TRY(ctx->get(B_W, n_beams, &d_w));
     BF_TRY(ctx->get(B_NSEGS, n_beams, &d_ns));
     BF_TRY(ctx->get(B_OBS, 3 * n_obs, &d_obs));
     const auto H2D = cudaMemcpyHostToDevice;
@@ -897,6 +1342,8 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     BF_TRY_CUDA(cudaMemcpyAsync(d_dir, seg_dir, 24 * rows, H2D, st));
     BF_TRY_CUDA(cudaMemcpyAsync(d_len, seg_len, 8 * rows, H2D, st));
     BF_TRY_CUDA(cudaMemcpyAsync(d_s0, seg_s0, 8 * rows, H2D, st));
+    BF_TRY_CUDA(cudaMemsetAsync(d_refl, 0, 8 * rows, st));  // amplitudes are not used here
+    BF_TRY_CUDA(cudaMemsetAsync(d_w, 0, 8 * n_beams, st));
     BF_TRY_CUDA(cudaMemcpyAsync(d_ns, n_segs, 4 * n_beams, H2D, st));
     BF_TRY_CUDA(cudaMemcpyAsync(d_obs, obs, 24 * n_obs, H2D, st));
     GbsArgs a{};
@@ -904,6 +1351,8 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     a.seg_dir = d_dir;
     a.seg_len = d_len;
     a.seg_s0 = d_s0;
+    a.seg_refl = d_refl;
+    a.weights = d_w;
     a.n_segs = d_ns;
     a.obs = d_obs;
     a.max_seg = max_seg;
@@ -913,18 +1362,32 @@ int bf_worklist(const double *seg_origin, const double *seg_dir, const double *s
     for (int f = 0; f < BF_MAXF; ++f) a.omegas[f] = f < nf ? omegas[f] : 0.0;
     a.c = c;
     a.width_b = width_b;
+    a.phi_amp = 1.0;
     a.use_cutoff = use_cutoff ? 1 : 0;
     Tiling t;
     BF_TRY(build_tiling(ctx, d_obs, n_obs, false, st, &t));
-    BF_TRY(build_worklist(ctx, a, t, st));
+    Slot &s = ctx->slot[0];
+    BF_TRY_CUDA(cudaEventRecord(ctx->pro, st));
+    BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, ctx->pro, 0));
+    Rows rv;
+    BF_TRY(rows_from_device(a, s, &rv));
     const int64_t n_words = (n_beams + 31) / 32;
+    uint32_t *d_bits, *d_tbits;
+    BF_TRY(ctx->get(B_WLBITS, (size_t)(n_tiles * n_words), &d_bits));
+    BF_TRY(ctx->get(B_WLTIGHT, (size_t)(n_tiles * n_words), &d_tbits));
+    double wmin = INFINITY;
+    for (int f = 0; f < a.nf; ++f) wmin = a.omegas[f] < wmin ? a.omegas[f] : wmin;
+    BF_TRY(launch_worklist(a, rv, t.centre, t.tbox, n_tiles, wmin, d_bits, d_tbits, 0, 0, nullptr,
+                           nullptr, s.ss));
+    BF_TRY_CUDA(cudaEventRecord(s.kdone, s.ss));
+    BF_TRY_CUDA(cudaStreamWaitEvent(st, s.kdone, 0));
     const auto D2H = cudaMemcpyDeviceToHost;
     BF_TRY_CUDA(cudaMemcpyAsync(perm, t.perm, 4 * n_obs, D2H, st));
     BF_TRY_CUDA(cudaMemcpyAsync(centre, t.centre, 32 * n_tiles, D2H, st));
     if (tile_box) BF_TRY_CUDA(cudaMemcpyAsync(tile_box, t.tbox, 32 * n_tiles, D2H, st));
-    BF_TRY_CUDA(cudaMemcpyAsync(bits, t.wl_bits, 4 * n_tiles * n_words, D2H, st));
+    BF_TRY_CUDA(cudaMemcpyAsync(bits, d_bits, 4 * n_tiles * n_words, D2H, st));
     if (tight_bits)
-        BF_TRY_CUDA(cudaMemcpyAsync(tight_bits, t.wl_tight, 4 * n_tiles * n_words, D2H, st));
+        BF_TRY_CUDA(cudaMemcpyAsync(tight_bits, d_tbits, 4 * n_tiles * n_words, D2H, st));
     BF_TRY_CUDA(cudaStreamSynchronize(st));
     return BF_OK;
 }

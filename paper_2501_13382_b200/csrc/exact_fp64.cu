@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(128) gbs_fp64_kernel(const GbsArgs a) {
 #pragma unroll
     for (int f = 0; f < (NF > 0 ? NF : BF_MAXF); ++f) {
         if (f < nf) {
-            acc_re[f] = a.acc[2 * (oi * nf + f) + 0];
-            acc_im[f] = a.acc[2 * (oi * nf + f) + 1];
+            acc_re[f] = a.acc[2 * (oi * a.acc_stride + f) + 0];
+            acc_im[f] = a.acc[2 * (oi * a.acc_stride + f) + 1];
         }
     }
     int64_t ev = 0;
@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(128) gbs_fp64_kernel(const GbsArgs a) {
 #pragma unroll
     for (int f = 0; f < (NF > 0 ? NF : BF_MAXF); ++f) {
         if (f < nf) {
-            a.acc[2 * (oi * nf + f) + 0] = acc_re[f];
-            a.acc[2 * (oi * nf + f) + 1] = acc_im[f];
+            a.acc[2 * (oi * a.acc_stride + f) + 0] = acc_re[f];
+            a.acc[2 * (oi * a.acc_stride + f) + 1] = acc_im[f];
         }
     }
     a.evals[oi] += ev;
@@ -517,40 +517,47 @@ __device__ __forceinline__ unsigned beam_dead_for_tile(const WordRows &w, int jb
 // (compaction offsets of the fp32 kernel's work list) and the per-tile statistics
 // wstats[{0,1,2,3} * n_tiles + tile] = a9 beams, a9 beam segments, tight beams, tight
 // beam segments (the FLOP model of bench.py).
-__global__ void worklist_kernel(const GbsArgs a, const double4 *centre, const double4 *tbox,
-                                int64_t n_tiles, int64_t n_words, double rscale, uint32_t *bits,
-                                uint32_t *tbits, int64_t range_beams, int64_t n_ranges,
+__global__ void worklist_kernel(const GbsArgs a, const Rows r, const double4 *centre,
+                                const double4 *tbox, int64_t n_tiles, int64_t n_words,
+                                double rscale, uint32_t *bits, uint32_t *tbits,
+                                int64_t range_beams, int64_t n_ranges,
                                 unsigned long long *counts, unsigned long long *wstats) {
     extern __shared__ double wsm[];
     __shared__ int ns_s[32];
-    const int S = (int)a.max_seg;
+    __shared__ int64_t st_s[33];
+    const int S = (int)r.max_seg;
     const int64_t word = blockIdx.x;
     WordRows w{wsm, wsm + 32 * S, wsm + 64 * S, wsm + 96 * S, wsm + 128 * S, wsm + 160 * S,
                wsm + 192 * S, wsm + 224 * S};
+    if (threadIdx.x < 33) {
+        const int64_t b = min(32 * word + threadIdx.x, r.n_beams);
+        st_s[threadIdx.x] = r.start[b];
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < 32 * S; i += blockDim.x) {
-        const int jb = i / S, k = i - jb * S;  // padded rows are beam-major
-        const int64_t b = 32 * word + jb;
-        if (b >= a.n_beams || k >= a.n_segs[b]) continue;
-        const int64_t row = b * S + k;
+        const int jb = i / S, k = i - jb * S;  // beam-major
+        const int64_t row = st_s[jb] + k;
+        if (row >= st_s[jb + 1]) continue;
         const int o = 32 * k + jb;
-        const_cast<double *>(w.ox)[o] = a.seg_origin[3 * row];
-        const_cast<double *>(w.oy)[o] = a.seg_origin[3 * row + 1];
-        const_cast<double *>(w.oz)[o] = a.seg_origin[3 * row + 2];
-        const_cast<double *>(w.dx)[o] = a.seg_dir[3 * row];
-        const_cast<double *>(w.dy)[o] = a.seg_dir[3 * row + 1];
-        const_cast<double *>(w.dz)[o] = a.seg_dir[3 * row + 2];
-        const_cast<double *>(w.s0)[o] = a.seg_s0[row];
-        const_cast<double *>(w.len)[o] = a.seg_len[row];
+        const double4 q0 = r.p0[row], q1 = r.p1[row];  // exact copies of the bundle's fp64
+        const_cast<double *>(w.ox)[o] = q0.x;
+        const_cast<double *>(w.oy)[o] = q0.y;
+        const_cast<double *>(w.oz)[o] = q0.z;
+        const_cast<double *>(w.dx)[o] = q1.x;
+        const_cast<double *>(w.dy)[o] = q1.y;
+        const_cast<double *>(w.dz)[o] = q1.z;
+        const_cast<double *>(w.s0)[o] = q1.w;
+        const_cast<double *>(w.len)[o] = q0.w;
     }
     const int lane = threadIdx.x & 31;
     const int64_t b = 32 * word + lane;
-    if (threadIdx.x < 32) ns_s[lane] = b < a.n_beams ? a.n_segs[b] : 0;
+    if (threadIdx.x < 32) ns_s[lane] = (int)(st_s[lane + 1] - st_s[lane]);
     __syncthreads();
     const int ns = ns_s[lane];
     for (int64_t t = threadIdx.x >> 5; t < n_tiles; t += blockDim.x >> 5) {
         const double4 c = centre[t], h = tbox[t];
         unsigned dead = 3u;
-        if (b < a.n_beams)
+        if (b < r.n_beams)
             dead = beam_dead_for_tile(w, lane, ns, a.width_b, c.x, c.y, c.z, c.w, h.x, h.y, h.z,
                                       rscale);
         const unsigned m = __ballot_sync(0xffffffffu, !(dead & 1u));
@@ -647,18 +654,18 @@ int launch_trace(const double *v0, const double *v1, const double *v2, const dou
     return BF_OK;
 }
 
-int launch_worklist(const GbsArgs &a, const double4 *centre, const double4 *tbox, int64_t n_tiles,
-                    double omega_min, uint32_t *bits, uint32_t *tbits, int64_t range_beams,
-                    int64_t n_ranges, unsigned long long *counts, unsigned long long *wstats,
-                    cudaStream_t st) {
-    if (n_tiles <= 0 || a.n_beams <= 0) return BF_OK;
-    const int64_t n_words = (a.n_beams + 31) / 32;
+int launch_worklist(const GbsArgs &a, const Rows &r, const double4 *centre, const double4 *tbox,
+                    int64_t n_tiles, double omega_min, uint32_t *bits, uint32_t *tbits,
+                    int64_t range_beams, int64_t n_ranges, unsigned long long *counts,
+                    unsigned long long *wstats, cudaStream_t st) {
+    if (n_tiles <= 0 || r.n_beams <= 0) return BF_OK;
+    const int64_t n_words = (r.n_beams + 31) / 32;
     // no cutoff -> nothing is ever cut (only the behind test of segment 0 remains)
     const double rscale = a.use_cutoff ? 72.0 * a.c / (omega_min * a.width_b) : INFINITY;
-    const size_t smem = 8 * 32 * sizeof(double) * (size_t)a.max_seg;
+    const size_t smem = 8 * 32 * sizeof(double) * (size_t)r.max_seg;
     BF_TRY_CUDA(cudaFuncSetAttribute(worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    worklist_kernel<<<(unsigned)n_words, 256, smem, st>>>(a, centre, tbox, n_tiles, n_words,
+    worklist_kernel<<<(unsigned)n_words, 256, smem, st>>>(a, r, centre, tbox, n_tiles, n_words,
                                                           rscale, bits, tbits, range_beams,
                                                           n_ranges, counts, wstats);
     note_launch();

@@ -164,10 +164,10 @@ struct WarpSmem {
     float4 geo2[ROWS<MF>];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
     float2 aux[ROWS<MF>];      // s0, A (amplitude factor x omega_0)
     float4 anc[NF][ROWS<MF>];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
-    unsigned rowinfo[ROWS<MF>];  // chunk row -> beam << 5 | segment
+    unsigned rowinfo[ROWS<MF>];  // chunk row -> compact row (Rows) of the group
     short brow[CB + 1];      // chunk beam -> first chunk row
-    int gbeam[CB];           // chunk beam -> local beam index
-    int4 desc[CB];           // chunk beam -> (beam, survivor word, first row, D bits)
+    unsigned grow0[CB];      // chunk beam -> compact row of its segment 0
+    int4 desc[CB];           // chunk beam -> (segment-0 row, survivor word, first row, D bits)
     // fp64 accumulators of the unit (NF == 1); with several frequencies they live in
     // the unit's slice of the global partial buffer instead (shared memory is the
     // occupancy limit there)
@@ -395,10 +395,9 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
 // Live mask of the R receivers of a single-segment-0 beam whose patch reaches the
 // launch plane: behind = proj < 0 (kernels.py:348,375); |proj| within the fp32
 // error bound is re-decided with the reference's exact fp64 projection.
-__device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Work &w,
-                                             const float (&pj)[R], const double (*p64)[3],
-                                             int nvalid, float D, int64_t beam, int k,
-                                             unsigned &ties) {
+__device__ __forceinline__ unsigned behind_mask(const Fp32Work &w, const float (&pj)[R],
+                                             const double (*p64)[3], int nvalid, float D,
+                                             int64_t row, unsigned &ties) {
     const float tolp = PROJ_ERR * D;
     unsigned m = 0, amb = 0;
 #pragma unroll
@@ -409,8 +408,7 @@ __device__ __forceinline__ unsigned behind_mask(const GbsArgs &a, const Fp32Work
             amb |= 1u << j;
     }
     if (amb) {  // rare: one copy of the fp64 code
-        const int64_t row = beam * a.max_seg + k;
-        const double4 o4 = w.p0[row], d4 = w.p1[row];  // packed fp64 rows (exact copies)
+        const double4 o4 = w.p0[row], d4 = w.p1[row];  // compact fp64 rows (exact copies)
         const double ox = o4.x, oy = o4.y, oz = o4.z;
         const double dx = d4.x, dy = d4.y, dz = d4.z;
         ties += __popc(amb);
@@ -551,7 +549,7 @@ __device__ __forceinline__ ExactPick exact_pick(const double4 *__restrict__ p0,
 template <int NF, bool MF>
 __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts &K,
                                               const WarpSmem<NF, MF> &S,
-                                              int64_t beam, int r0, unsigned surv, unsigned pend,
+                                              int64_t row0, int r0, unsigned surv, unsigned pend,
                                               const float (&rx)[R], const float (&ry)[R],
                                               const float (&rz)[R], const float (&rr)[R],
                                               const float (&best)[R], const int (&kb)[R],
@@ -571,7 +569,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         const int j = __ffs(pend) - 1;
         pend &= pend - 1;
         const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
-        const ExactPick e = exact_pick(w.p0, w.p1, beam * a.max_seg,
+        const ExactPick e = exact_pick(w.p0, w.p1, row0,
                                        S.geo0 + r0, S.geo1 + r0, surv, pick4(kb, j), x, y, z,
                                        pick4(best, j), Db, S.p64[R * lane + j]);
         if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
@@ -582,7 +580,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         const float q2 =
             fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
                   0.f);
-        const float s = (float)(w.p1[beam * a.max_seg + k].w + e.bt);  // kernels.py:344
+        const float s = (float)(w.p1[row0 + k].w + e.bt);  // kernels.py:344
         // anchor choice follows the exact clamp
         const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
         const float A = S.aux[r0 + k].y;
@@ -609,24 +607,22 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
 
 // Stage chunk rows [0, nrows) into warp-private shared memory, patch-local.
 template <int NF, bool MF>
-__device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &w, int64_t max_seg,
-                                           int nrows, double cx, double cy, double cz, float RW,
+__device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &w, int nrows,
+                                           double cx, double cy, double cz, float RW,
                                            const Fp32Consts &K, int lane) {
     // software-pipelined: the next row's loads are in flight while this row converts
-    auto grow = [&](int r) {
-        const unsigned info = S.rowinfo[r];  // beam << 5 | k
-        return (int64_t)(info >> 5) * max_seg + (info & 31);
-    };
+    auto grow = [&](int r) { return (int64_t)S.rowinfo[r]; };
     const float2 *pa2 = reinterpret_cast<const float2 *>(w.pa);
     int r = lane;
     int64_t g = 0;
     double4 p0 = make_double4(0, 0, 0, 0), p1 = p0;
-    float2 p2 = make_float2(0.f, 0.f), ae0 = p2;
+    float p2 = 0.f;
+    float2 ae0 = make_float2(0.f, 0.f);
     if (r < nrows) {
         g = grow(r);
         p0 = w.p0[g];  // o.xyz, len
         p1 = w.p1[g];  // d.xyz, s0
-        p2 = w.p2[g];  // A, R_cut
+        p2 = w.amp[g];  // A
         ae0 = pa2[g * NF];
     }
 #pragma unroll 1
@@ -634,12 +630,13 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
         const int rn = r + 32;
         int64_t gn = 0;
         double4 p0n = p0, p1n = p1;
-        float2 p2n = p2, aen = ae0;
+        float p2n = p2;
+        float2 aen = ae0;
         if (rn < nrows) {
             gn = grow(rn);
             p0n = w.p0[gn];
             p1n = w.p1[gn];
-            p2n = w.p2[gn];
+            p2n = w.amp[gn];
             aen = pa2[gn * NF];
         }
         const double wcx = cx - p0.x, wcy = cy - p0.y, wcz = cz - p0.z;
@@ -650,7 +647,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
         S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
                                 (float)(ucx * ucx + ucy * ucy + ucz * ucz));
         const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + p0.w) + RW + 1.f;
-        S.aux[r] = make_float2((float)p1.w, p2.x * K.omega[0]);
+        S.aux[r] = make_float2((float)p1.w, p2 * K.omega[0]);
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             const float2 ae = f ? pa2[g * NF + f] : ae0;
@@ -725,7 +722,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     while (cur < n_items) {
         const int nbn = min(CB, n_items - cur);
         const int ns = lane < nbn ? (int)(e >> 27) + 1 : 0;
-        const int beam_l = (int)(e & 0x7ffffffu);
+        const unsigned row_l = e & 0x7ffffffu;  // compact row of the beam's segment 0
         // ---- row capacity: keep the prefix of beams whose rows fit ROWS<MF>
         int incl = ns;
 #pragma unroll
@@ -737,10 +734,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         const int nbc = __popc(fit);
         const int nrows = __shfl_sync(0xffffffffu, incl, nbc - 1);
         if (lane < nbc) {
-            S.gbeam[lane] = beam_l;
+            S.grow0[lane] = row_l;
             S.brow[lane] = incl - ns;
 #pragma unroll 1
-            for (int k = 0; k < ns; ++k) S.rowinfo[incl - ns + k] = ((unsigned)beam_l << 5) | k;
+            for (int k = 0; k < ns; ++k) S.rowinfo[incl - ns + k] = row_l + k;
         }
         cur += nbc;
         // the next chunk's entries: in flight during this chunk
@@ -750,7 +747,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         {
             const double4 c = w.pcen[p];  // re-read (L1) rather than held in registers
 #if !(BF_ABL & 64)
-            stage_rows<NF, MF>(S, w, a.max_seg, nrows, c.x, c.y, c.z, RW, K, lane);
+            stage_rows<NF, MF>(S, w, nrows, c.x, c.y, c.z, RW, K, lane);
 #endif
         }
         __syncwarp();
@@ -771,7 +768,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 const unsigned m = word & ~(BEHIND_CHECK | WEDGE);
                 const int ka = __ffs(m) - 1;
                 if ((word & WEDGE) || (m != 0 && m == (3u << ka))) {
-                    const int64_t g = (int64_t)S.gbeam[lane] * a.max_seg + ka;
+                    const int64_t g = (int64_t)S.grow0[lane] + ka;
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g));
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p1 + g));
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(w.p0 + g + 1));
@@ -779,7 +776,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
             }
 #endif
-            S.desc[lane] = make_int4(S.gbeam[lane], (int)word, r0, __float_as_int(D));
+            S.desc[lane] = make_int4((int)S.grow0[lane], (int)word, r0, __float_as_int(D));
         }
         const unsigned live = __ballot_sync(0xffffffffu, word != 0);
         {
@@ -829,7 +826,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #endif
             const int4 dsc = S.desc[__ffs(lm) - 1];
             lm &= lm - 1;
-            const int64_t beam = dsc.x;
+            const int64_t row0 = (unsigned)dsc.x;  // compact row of segment 0
             const unsigned bword = (unsigned)dsc.y;
             const unsigned surv = bword & ~(BEHIND_CHECK | WEDGE);
             const int r0 = dsc.z;
@@ -877,7 +874,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 lvm = (1u << R) - 1;
                 if (bword & BEHIND_CHECK)
-                    lvm = behind_mask(a, w, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, beam, k, ties);
+                    lvm = behind_mask(w, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, row0 + k, ties);
             } else {
                 // receivers decided at the junction of segments ka, ka+1 (corner wedge):
                 // both clamped distances are distances to the reflection point, an exact
@@ -975,7 +972,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
-                    const Junction J = load_junction(w.p0, w.p1, beam * a.max_seg + ka);
+                    const Junction J = load_junction(w.p0, w.p1, row0 + ka);
                     const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
                     const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
@@ -1007,7 +1004,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     }
                 }
                 if (__any_sync(0xffffffffu, pend != 0))
-                    exact_pending<NF, MF>(a, K, S, beam, r0, surv, pend, rx, ry, rz, rr, best, kb,
+                    exact_pending<NF, MF>(a, K, S, row0, r0, surv, pend, rx, ry, rz, rr, best, kb,
                                       Db, lane, sj, q2j, Aj, bj, pref, lvm, ties, w);
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
@@ -1024,8 +1021,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 for (int j = 0; j < R; ++j) {
                     s64[j] = 0.0;
                     if ((lvm >> j) & 1u) {
-                        const unsigned info = S.rowinfo[pref[j] & (ROWS<MF> - 1)];
-                        const int64_t g = (int64_t)(info >> 5) * a.max_seg + (info & 31);
+                        const int64_t g = S.rowinfo[pref[j] & (ROWS<MF> - 1)];
                         const double4 o = w.p0[g], d = w.p1[g];
                         const double *P = S.p64[R * lane + j];
                         const double wx = __dsub_rn(P[0], o.x), wy = __dsub_rn(P[1], o.y),
@@ -1185,28 +1181,48 @@ __global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5
 
 // ------------------------------------------------------------ preparation ----
 
-// Row SoA of the padded reference bundle (beamtrace.py:274-288), tile-independent
-// parts of the staging computed once: p0 = (o, len), p1 = (d, s0) in fp64,
-// p2 = (A = phi sqrt(c)/(2 pi c) refl w_b, R_cut), pa = fp64-exact anchors
-// frac(omega/(2 pi c) s) at s0 and s0 + len, per frequency.
-__global__ void pack_kernel(const GbsArgs a, const Fp32Consts K, double4 *p0, double4 *p1,
-                            float2 *p2, float2 *pa) {
+// Padded reference bundle (beamtrace.py:274-288) -> compact rows: thread per padded row,
+// rows k < n_segs[b] go to start[b] + k.  p0 = (o, len), p1 = (d, s0) are exact fp64
+// copies; amp = (float)(phi sqrt(c)/(2 pi c) * refl * w_b) (kernels.py:388,397).
+__global__ void rows_pack_kernel(const GbsArgs a, double amp_scale, const int64_t *start,
+                                 double4 *p0, double4 *p1, float *amp) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= a.n_beams * a.max_seg) return;
     const int64_t b = row / a.max_seg;
-    const int k = (int)(row - b * a.max_seg);
-    if (k >= a.n_segs[b]) return;
-    const double len = a.seg_len[row], s0 = a.seg_s0[row];
-    p0[row] = make_double4(a.seg_origin[3 * row], a.seg_origin[3 * row + 1],
-                           a.seg_origin[3 * row + 2], len);
-    p1[row] = make_double4(a.seg_dir[3 * row], a.seg_dir[3 * row + 1], a.seg_dir[3 * row + 2], s0);
-    const double se = s0 + len;
-    const double rcut = sqrt(K.rcut_scale * (se * se + K.b2_64)) * (1.0 + 1e-5) + 1e-3;
-    const double A = K.amp_scale * a.seg_refl[row] * a.weights[b];
-    p2[row] = make_float2((float)A, (float)rcut);
-    for (int f = 0; f < a.nf; ++f)
-        pa[row * a.nf + f] = make_float2((float)frac_turns(K.kappa64[f] * s0),
-                                         (float)frac_turns(K.kappa64[f] * se));
+    const int64_t k = row - b * a.max_seg;
+    const int64_t dst = start[b] + k;
+    if (dst >= start[b + 1]) return;
+    p0[dst] = make_double4(a.seg_origin[3 * row], a.seg_origin[3 * row + 1],
+                           a.seg_origin[3 * row + 2], a.seg_len[row]);
+    p1[dst] = make_double4(a.seg_dir[3 * row], a.seg_dir[3 * row + 1], a.seg_dir[3 * row + 2],
+                           a.seg_s0[row]);
+    amp[dst] = (float)(amp_scale * a.seg_refl[row] * a.weights[b]);
+}
+
+// start[b + 1] = n_segs[b] clamped to [0, max_seg] (the scan input; start[0] = 0).
+__global__ void rows_count_kernel(const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
+                                  int64_t *cnt) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > n_beams) return;
+    if (b == n_beams) {
+        cnt[0] = 0;
+        return;
+    }
+    int64_t n = n_segs[b];
+    n = n < 0 ? 0 : (n > max_seg ? max_seg : n);
+    cnt[b + 1] = n;
+}
+
+// Phase anchors of every compact row, per frequency: frac(omega/(2 pi c) s) at s0 and
+// s0 + len in fp64 (turns), rounded to fp32 once.
+__global__ void anchors_kernel(const Rows r, int64_t rows_bound, int nf, Fp32Consts K,
+                               float2 *pa) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= rows_bound || row >= r.start[r.n_beams]) return;
+    const double s0 = r.p1[row].w, se = s0 + r.p0[row].w;
+    for (int f = 0; f < nf; ++f)
+        pa[row * nf + f] = make_float2((float)frac_turns(K.kappa64[f] * s0),
+                                       (float)frac_turns(K.kappa64[f] * se));
 }
 
 // One warp per patch: fp64 bounding-box centre c_P, patch-local r = p - c_P in
@@ -1270,20 +1286,20 @@ __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
 }
 
 // acc[oi] += sum over beam ranges q (ascending) of the units' partials; evals alike.
-__global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, double *acc,
-                            int64_t *evals) {
+__global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, int64_t stride,
+                            double *acc, int64_t *evals) {
     const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (si >= tl.n) return;
     const int64_t oi = tl.perm[si];
     for (int f = 0; f < nf; ++f) {
-        double re = acc[2 * (oi * nf + f)], im = acc[2 * (oi * nf + f) + 1];
+        double re = acc[2 * (oi * stride + f)], im = acc[2 * (oi * stride + f) + 1];
         for (int64_t q = 0; q < w.n_ranges; ++q) {
             const double2 v = w.part[(q * w.n_pad + si) * nf + f];
             re += v.x;
             im += v.y;
         }
-        acc[2 * (oi * nf + f)] = re;
-        acc[2 * (oi * nf + f) + 1] = im;
+        acc[2 * (oi * stride + f)] = re;
+        acc[2 * (oi * stride + f) + 1] = im;
     }
     int64_t ev = 0;
     for (int64_t q = 0; q < w.n_ranges; ++q) ev += w.part_ev[q * w.n_pad + si];
@@ -1315,8 +1331,8 @@ __global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_
 }
 
 // One warp per (tile, beam range): ascending candidate beams with their segment
-// counts, (n_segs - 1) << 27 | beam, at the scanned offset.
-__global__ void wl_compact_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w) {
+// counts, (n_segs - 1) << 27 | compact row of segment 0, at the scanned offset.
+__global__ void wl_compact_kernel(const Tiling tl, const Fp32Work w) {
     const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (u >= tl.n_tiles * w.n_ranges) return;
@@ -1339,8 +1355,9 @@ __global__ void wl_compact_kernel(const GbsArgs a, const Tiling tl, const Fp32Wo
         int64_t pos = base + incl - c;
         for (; m; m &= m - 1) {
             const int64_t beam = 32 * i + __ffs(m) - 1;
-            const uint32_t ns = (uint32_t)a.n_segs[beam];
-            out[pos++] = ((ns - 1u) << 27) | (uint32_t)beam;
+            const int64_t r0 = w.start[beam];
+            const uint32_t ns = (uint32_t)(w.start[beam + 1] - r0);
+            out[pos++] = ((ns - 1u) << 27) | (uint32_t)r0;
         }
         base += __shfl_sync(0xffffffffu, incl, 31);
     }
@@ -1351,19 +1368,29 @@ int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp3
                  GbsStats *stats, cudaStream_t st) {
     constexpr bool MF = NF > 1 || WIDE;
     const size_t smem = WARPS * sizeof(WarpSmem<NF, MF>);
-    BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF, WIDE>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, sms = 0, per_sm = 0;
+    // per-device launch geometry, computed once (attribute + occupancy queries cost host time
+    // on every call otherwise); a benign race writes the same values
+    constexpr int MAXDEV = 64;
+    static int grid_cache[MAXDEV] = {};
+    int dev = 0;
     BF_TRY_CUDA(cudaGetDevice(&dev));
-    BF_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gbs_fp32_kernel<NF, WIDE>,
-                                                              THREADS, smem));
-    if (per_sm < 1) return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
-    if (getenv("BF_DEBUG_STATS"))
-        fprintf(stderr, "bf fp32 kernel%s: %zu B shared per CTA (%zu per warp), %d CTAs/SM\n",
-                WIDE ? " (wide patches)" : "", smem, sizeof(WarpSmem<NF, MF>), per_sm);
+    if (dev >= MAXDEV) return fail(BF_ENODEV, "device index %d >= %d", dev, MAXDEV);
+    if (grid_cache[dev] == 0) {
+        BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF, WIDE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int sms = 0, per_sm = 0;
+        BF_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, gbs_fp32_kernel<NF, WIDE>, THREADS, smem));
+        if (per_sm < 1)
+            return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
+        if (getenv("BF_DEBUG_STATS"))
+            fprintf(stderr, "bf fp32 kernel%s: %zu B shared per CTA (%zu per warp), %d CTAs/SM\n",
+                    WIDE ? " (wide patches)" : "", smem, sizeof(WarpSmem<NF, MF>), per_sm);
+        grid_cache[dev] = sms * per_sm;
+    }
     const int64_t units = w.n_patches * w.n_ranges;
-    int64_t grid = (int64_t)sms * per_sm;
+    int64_t grid = grid_cache[dev];
     const int64_t need = (units + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
     gbs_fp32_kernel<NF, WIDE><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
@@ -1374,6 +1401,8 @@ int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp3
 
 // The wide-patch kernel goes first on the auxiliary stream; the common kernel's CTAs
 // take the SM slots as the wide ones retire (no tail of a second sequential launch).
+// Both are always launched: the wide-unit count is on the device (unit_keys_kernel), and
+// with none every warp of the wide kernel exits after one atomic (no host round trip).
 template <int NF>
 int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
               GbsStats *stats, const StreamPair &sp) {
@@ -1383,19 +1412,12 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
         cudaMemcpyToSymbolAsync(g_hist, z, sizeof(z), 0, cudaMemcpyHostToDevice, sp.st);
     }
 #endif
-    // the wide kernel is submitted first on the launch stream, the common one right
-    // after on the auxiliary stream (forked before the wide launch), so the wide CTAs
-    // are dispatched first and the common kernel fills the remaining SM slots
-    if (w.n_wide_host != 0) {
-        BF_TRY_CUDA(cudaEventRecord(sp.fork, sp.st));
-        BF_TRY_CUDA(cudaStreamWaitEvent(sp.aux, sp.fork, 0));
-        BF_TRY((launch_class<NF, true>(a, t, w, K, stats, sp.st)));
-        BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.aux)));
-        BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
-        BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
-    } else {  // no wide patches: the common kernel alone
-        BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.st)));
-    }
+    BF_TRY_CUDA(cudaEventRecord(sp.fork, sp.st));
+    BF_TRY_CUDA(cudaStreamWaitEvent(sp.aux, sp.fork, 0));
+    BF_TRY((launch_class<NF, true>(a, t, w, K, stats, sp.aux)));
+    BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.st)));
+    BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
+    BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
 #if BF_HIST
     {
         unsigned long long h[4];
@@ -1404,9 +1426,6 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
         fprintf(stderr, "bf hist: exact re-decision rounds %llu\n", h[2]);
     }
 #endif
-    fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, sp.st>>>(t, w, a.nf, a.acc, a.evals);
-    note_launch();
-    BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
 }
 
@@ -1449,20 +1468,46 @@ int gbs_fp32_patch() { return PATCH; }
 int64_t gbs_fp32_range_beams(int64_t n_beams, int nf) {
     // BF_RANGES ranges for one frequency, fewer with several (the partial buffer holds
     // ranges x receivers x frequencies complex values)
+    // (small calls get 32-beam ranges: more (patch, range) units to spread over the SMs)
     const int64_t ranges = BF_RANGES / nf > 8 ? BF_RANGES / nf : 8;
     int64_t rb = (n_beams + ranges - 1) / ranges;
     rb = (rb + 31) / 32 * 32;
-    return rb < 256 ? 256 : rb;
+    return rb < 32 ? 32 : rb;
 }
 
-int launch_fp32_prepare(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st) {
-    const Fp32Consts K = make_consts(a);
+int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t *cnt,
+                      cudaStream_t st) {
+    rows_count_kernel<<<(unsigned)((n_beams + 1 + 255) / 256), 256, 0, st>>>(n_segs, n_beams,
+                                                                             max_seg, cnt);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_rows_pack(const GbsArgs &a, const int64_t *start, double4 *p0, double4 *p1,
+                     float *amp, cudaStream_t st) {
     const int64_t rows = a.n_beams * a.max_seg;
-    if (rows > 0) {
-        pack_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(a, K, w.p0, w.p1, w.p2,
-                                                                    reinterpret_cast<float2 *>(w.pa));
-        note_launch();
-    }
+    if (rows <= 0) return BF_OK;
+    const double amp_scale = a.phi_amp * sqrt(a.c) / (2.0 * 3.141592653589793 * a.c);
+    rows_pack_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(a, amp_scale, start, p0, p1,
+                                                                     amp);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_fp32_anchors(const GbsArgs &a, const Rows &r, int64_t rows_bound, float *pa,
+                        cudaStream_t st) {
+    if (rows_bound <= 0 || r.n_beams <= 0) return BF_OK;
+    const Fp32Consts K = make_consts(a);
+    anchors_kernel<<<(unsigned)((rows_bound + 255) / 256), 256, 0, st>>>(
+        r, rows_bound, a.nf, K, reinterpret_cast<float2 *>(pa));
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_fp32_patches(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st) {
     if (w.n_patches > 0) {
         patch_kernel<<<(unsigned)((w.n_patches * 32 + 127) / 128), 128, 0, st>>>(
             a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen, w.pbox);
@@ -1483,11 +1528,10 @@ int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
     return BF_OK;
 }
 
-int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
-                           cudaStream_t st) {
+int launch_fp32_wl_compact(const Tiling &t, const Fp32Work &w, cudaStream_t st) {
     const int64_t nu = t.n_tiles * w.n_ranges;
     if (nu > 0) {
-        wl_compact_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(a, t, w);
+        wl_compact_kernel<<<(unsigned)((nu * 32 + 127) / 128), 128, 0, st>>>(t, w);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
@@ -1496,9 +1540,7 @@ int launch_fp32_wl_compact(const GbsArgs &a, const Tiling &t, const Fp32Work &w,
 
 int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsStats *d_stats,
                     const StreamPair &st) {
-    if (t.n <= 0 || a.n_beams <= 0 || a.nf <= 0) return BF_OK;
-    if (a.max_seg > 30)  // survivor masks share the word with two flag bits
-        return fail(BF_EINVAL, "max_seg %lld exceeds 30 (r_max <= 29)", (long long)a.max_seg);
+    if (t.n <= 0 || a.nf <= 0 || w.n_ranges <= 0) return BF_OK;
     const Fp32Consts K = make_consts(a);
     switch (a.nf) {
         case 1: return launch_nf<1>(a, t, w, K, d_stats, st);
@@ -1511,6 +1553,15 @@ int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsSta
         case 8: return launch_nf<8>(a, t, w, K, d_stats, st);
         default: return fail(BF_EINVAL, "nf=%d outside 1..%d", a.nf, BF_MAXF);
     }
+}
+
+int launch_fp32_fold(const GbsArgs &a, const Tiling &t, const Fp32Work &w, cudaStream_t st) {
+    if (t.n <= 0 || w.n_ranges <= 0) return BF_OK;
+    fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, st>>>(t, w, a.nf, a.acc_stride, a.acc,
+                                                               a.evals);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
 }
 
 }  // namespace bf

@@ -8,10 +8,11 @@ trace -> sum loop, parallel.py:297-338, moved onto the B200):
   (the reference PathBundle layout, beamtrace.py:274-288);
 * :class:`DeviceBundle` -- a device PathBundle (torch tensors) + upload from a
   host PathBundle (pinned, async);
-* :func:`accumulate` -- ``bf_gbs_accumulate_dev`` on device buffers;
-* :class:`ChunkStreamer` -- double-buffered pinned host -> HBM streaming of
-  beam chunks for ray sets larger than one device pass (plan_chunks semantics,
-  parallel.py:91-105), copy of chunk i+1 overlapping the summation of chunk i.
+* :func:`accumulate` -- ``bf_gbs_accumulate_dev`` on device buffers.
+
+Host-resident bundles larger than the device budget need no Python streaming:
+the host-buffer ABI (``bf_gbs_accumulate``) streams beam groups through pinned
+staging itself, copy of group g+1 overlapping the summation of group g.
 
 PyTorch is used for allocation, streams and events only.
 """
@@ -36,9 +37,12 @@ def _vp(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
+    """The cudaStream_t of `stream`; None -> torch's current stream on `device`, so the
+    engine's work is ordered after the torch kernels that produced its inputs."""
     if stream is None:
-        return None
+        torch = _torch()
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
 
 
@@ -138,7 +142,8 @@ class DeviceBundle:
 
 
 def trace_device_rows(dscene: DeviceScene, source, launch, cfg, c, lo, hi, device,
-                      row_base=None, out: DeviceBundle | None = None, stream=None):
+                      row_base=None, out: DeviceBundle | None = None, stream=None,
+                      exhaustive=False):
     """Trace launch rays [lo, hi) on the GPU (kernels.trace_range, kernels.py:282-301).
 
     Fills ``out`` (allocated when None) rows [(lo-row_base)*S, (hi-row_base)*S).
@@ -165,7 +170,8 @@ def trace_device_rows(dscene: DeviceScene, source, launch, cfg, c, lo, hi, devic
         float(cfg.length_cap(c)), int(cfg.r_max), S, _vp(out.seg_origin), _vp(out.seg_dir),
         _vp(out.seg_e1), _vp(out.seg_e2), _vp(out.seg_len), _vp(out.seg_s0),
         _vp(out.seg_refl), _vp(out.n_segs), _vp(out.n_refls), lo - row_base, hi - row_base, 0,
-        device.index or 0, _stream_ptr(stream)))
+        _lib.TRACE_EXHAUSTIVE if exhaustive else 0, device.index or 0,
+        _stream_ptr(stream, device)))
     d = {k: getattr(out, k) for k in SEG_FIELDS + ("n_segs", "n_refls", "weights")}
     d["max_seg"] = S
     d["bundle"] = out
@@ -192,7 +198,7 @@ def accumulate(bundle: DeviceBundle, obs, omegas, width_b, use_cutoff, acc, eval
         float(bundle.amplitude_phi), int(bool(use_cutoff)), _vp(acc), _vp(evals), int(obs_lo),
         int(obs_hi), int(beam_lo), int(beam_hi), prec,
         _lib.FLAG_OBS_PRESORTED if presorted else 0, obs.device.index or 0,
-        _stream_ptr(stream)))
+        _stream_ptr(stream, obs.device)))
 
 
 def finalize(acc, calibration, stream=None):
@@ -203,79 +209,5 @@ def finalize(acc, calibration, stream=None):
     spl = torch.empty(acc.shape, dtype=torch.float64, device=acc.device)
     _lib.check(lib.bf_field_finalize_dev(_vp(acc), acc.numel(), float(calibration),
                                          _vp(pressure), _vp(spl), acc.device.index or 0,
-                                         _stream_ptr(stream)))
+                                         _stream_ptr(stream, acc.device)))
     return pressure, spl
-
-
-class ChunkStreamer:
-    """Double-buffered pinned-host -> HBM streaming of beam chunks.
-
-    The reference sizes chunks with plan_chunks (parallel.py:91-105) and runs
-    trace+sum per chunk.  Here a host-resident PathBundle larger than one device
-    pass is cut into beam chunks; chunk i+1 is copied on a copy stream (pinned
-    source, cudaMemcpyAsync) while chunk i is summed on the compute stream, with
-    event ping-pong between two device buffers.  Beam order is preserved, so the
-    per-observer sums continue exactly as a single call would.
-    """
-
-    def __init__(self, bundle, chunk_sizes, device, with_frame=False):
-        torch = _torch()
-        self.b = bundle
-        self.sizes = [int(s) for s in chunk_sizes]
-        self.device = device
-        self.with_frame = with_frame
-        self.copy_stream = torch.cuda.Stream(device)
-        S = int(bundle.max_seg)
-        cap = max(self.sizes)
-        fields = ["seg_origin", "seg_dir", "seg_len", "seg_s0", "seg_refl"]
-        if with_frame:
-            fields += ["seg_e1", "seg_e2"]
-        self.fields = fields
-        # Pinned host staging of the whole bundle (one registration).
-        self.host = {}
-        for f in fields:
-            a = np.ascontiguousarray(getattr(bundle, f), dtype=np.float64)
-            self.host[f] = torch.from_numpy(a).pin_memory()
-        self.host["n_segs"] = torch.from_numpy(
-            np.ascontiguousarray(bundle.n_segs, dtype=np.int32)).pin_memory()
-        self.host["weights"] = torch.from_numpy(
-            np.ascontiguousarray(bundle.weights, dtype=np.float64)).pin_memory()
-        self.bufs = [DeviceBundle.empty(cap, S, device, float(bundle.c),
-                                        float(bundle.beam_param_im),
-                                        float(bundle.amplitude_phi)) for _ in range(2)]
-        if not with_frame:
-            for db in self.bufs:
-                db.seg_e1 = None
-                db.seg_e2 = None
-        self.ready = [torch.cuda.Event() for _ in range(2)]
-        self.free = [torch.cuda.Event() for _ in range(2)]
-
-    def _copy(self, i, lo, n):
-        torch = _torch()
-        S = int(self.b.max_seg)
-        db = self.bufs[i % 2]
-        with torch.cuda.stream(self.copy_stream):
-            self.copy_stream.wait_event(self.free[i % 2])
-            for f in self.fields:
-                src = self.host[f]
-                rows = slice(lo * S, (lo + n) * S)
-                getattr(db, f)[: n * S].copy_(src[rows], non_blocking=True)
-            db.n_segs[:n].copy_(self.host["n_segs"][lo:lo + n], non_blocking=True)
-            db.weights[:n].copy_(self.host["weights"][lo:lo + n], non_blocking=True)
-            self.ready[i % 2].record(self.copy_stream)
-
-    def run(self, consume, compute_stream):
-        """consume(device_bundle, n_beams, global_lo) is called per chunk on compute_stream."""
-        torch = _torch()
-        for e in self.free:
-            e.record(compute_stream)
-        starts = np.concatenate([[0], np.cumsum(self.sizes)])
-        if self.sizes:
-            self._copy(0, 0, self.sizes[0])
-        for i, n in enumerate(self.sizes):
-            if i + 1 < len(self.sizes):
-                self._copy(i + 1, int(starts[i + 1]), self.sizes[i + 1])
-            compute_stream.wait_event(self.ready[i % 2])
-            with torch.cuda.stream(compute_stream):
-                consume(self.bufs[i % 2], n, int(starts[i]))
-            self.free[i % 2].record(compute_stream)

@@ -25,7 +25,7 @@ from .beamtrace import (Atmosphere, LaunchGrid, SourceSpec, TraceConfig, allocat
                         launch_directions)
 from .errors import BudgetError
 from .gbs import FieldResult, ObserverSet, calibrate_phi
-from .kernels import DEFAULT_PRECISION
+from .kernels import PIPELINE_PRECISION
 
 MODES = ("sequential", "flat", "dynamic")
 DEFAULT_SPLIT_THRESHOLD = 4096
@@ -170,7 +170,7 @@ def run_pipeline(scene, source: SourceSpec, grid: LaunchGrid, cfg: TraceConfig,
     import torch
 
     from . import engine, shard
-    precision = DEFAULT_PRECISION if precision is None else precision
+    precision = PIPELINE_PRECISION if precision is None else precision
     t_start = time.perf_counter()
     dev = _device(device)
     torch.cuda.set_device(dev)
@@ -259,7 +259,9 @@ def pipeline_calibration(source: SourceSpec, grid: LaunchGrid, cfg: TraceConfig,
                                    launch, cfg, c, 0, len(launch), dev)
     torch.cuda.synchronize(dev)
     bundle = out["bundle"].to_host()
-    return calibrate_phi(bundle, atmosphere, source, device=dev.index)
+    # 26 x F single-receiver sums: always in fp64 (oracle) mode, so the scale is the
+    # reference's to ~1e-12 whichever precision the field itself is summed in
+    return calibrate_phi(bundle, atmosphere, source, precision="fp64", device=dev.index)
 
 
 def run_snapshots(scene, sources, grid: LaunchGrid, cfg: TraceConfig, observers: ObserverSet,

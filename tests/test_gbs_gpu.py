@@ -95,12 +95,14 @@ def test_tracer_bitexact_vs_reference(name):
         assert np.array_equal(got.view(np.uint64), b[f].view(np.uint64)), f
 
 
-def test_device_path_equals_host_path():
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_device_path_equals_host_path(precision):
+    """Host-buffer ABI (pageable numpy, streamed beam groups) == device ABI, bit for bit."""
     import torch
 
     from paper_2501_13382_b200 import kernels
     b = load_case("city_street")
-    acc_h, ev_h = run(b, "fp32")
+    acc_h, ev_h = run(b, precision)
     dev = torch.device("cuda", 0)
     t = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa
     obs = b["obs"]
@@ -110,10 +112,99 @@ def test_device_path_equals_host_path():
                            t(b["seg_len"]), t(b["seg_s0"]), t(b["seg_refl"]),
                            t(b["n_segs"], torch.int32), b["max_seg"], t(b["weights"]), t(obs),
                            b["omegas"], float(b["c"]), -float(b["beam_param_im"]), 1.0, True,
-                           acc, ev, 0, obs.shape[0], 0, b["n_segs"].shape[0])
+                           acc, ev, 0, obs.shape[0], 0, b["n_segs"].shape[0],
+                           precision=precision)
     torch.cuda.synchronize()
     assert np.array_equal(acc.cpu().numpy(), acc_h)
     assert np.array_equal(ev.cpu().numpy(), ev_h)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_memory_budget_grouping_bitexact(precision):
+    """A device budget far below the bundle: the host ABI streams many beam groups
+    (fp32: groups of whole beam ranges, fp64: padded chunks) through pinned staging and
+    the device ABI sums in many groups; the bits equal the one-group call's."""
+    import torch
+
+    from paper_2501_13382_b200 import _lib, engine, kernels
+    b = load_case("city_corner_f5")
+    obs = np.ascontiguousarray(b["obs"][:3000])
+    nb = b["n_segs"].shape[0]
+    ref, rev = run(b, precision, obs, [(0, obs.shape[0], 0, nb)])
+    dev = torch.device("cuda", 0)
+    db = engine.DeviceBundle.from_host(_pb(b), dev)
+    od = torch.from_numpy(obs).to(dev)
+    try:
+        _lib.set_memory_budget(0, 1 << 20)  # 1 MiB: dozens of groups
+        got, gev = run(b, precision, obs, [(0, obs.shape[0], 0, nb)])
+        acc = torch.zeros((obs.shape[0], 5), dtype=torch.complex128, device=dev)
+        ev = torch.zeros(obs.shape[0], dtype=torch.int64, device=dev)
+        engine.accumulate(db, od, b["omegas"], -float(b["beam_param_im"]), True, acc, ev,
+                          precision=precision)
+        torch.cuda.synchronize()
+    finally:
+        _lib.set_memory_budget(0, 0)
+    assert np.array_equal(got, ref) and np.array_equal(gev, rev)
+    assert np.array_equal(acc.cpu().numpy(), ref) and np.array_equal(ev.cpu().numpy(), rev)
+    assert rel_l2(ref, b["acc"][:3000]) <= (FP64_TOL if precision == "fp64" else FP32_L2)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_many_frequencies(precision, threads):
+    """F = 21 (1/3-octave bands 100 Hz - 10 kHz): summed in groups of <= 8 frequencies,
+    against the oracle (kernels.py:362,380 loop over any nf)."""
+    from paper_2501_13382_b200 import kernels
+    b = load_case("city_street")
+    obs = np.ascontiguousarray(b["obs"][::3])
+    om = 2 * np.pi * 100.0 * 10 ** (np.arange(21) / 10.0)
+    args = gbs_args(b, obs)
+    args[11] = om
+    nb = b["n_segs"].shape[0]
+    ref = np.zeros((obs.shape[0], 21), np.complex128)
+    rev = np.zeros(obs.shape[0], np.int64)
+    oracle.gbs_accumulate(*args, ref, rev, 0, obs.shape[0], 0, nb, threads=threads)
+    acc = np.zeros_like(ref)
+    ev = np.zeros_like(rev)
+    kernels.gbs_accumulate(*args, acc, ev, 0, obs.shape[0], 0, nb, precision=precision)
+    if precision == "fp64":
+        assert rel_l2(acc, ref) <= FP64_TOL and np.array_equal(ev, rev)
+    else:
+        for f in range(21):
+            assert rel_l2(acc[:, f], ref[:, f]) <= FP32_L2, f
+        assert tl_db(acc, ref, floor_db=-60.0) <= FP32_TL_DB
+        assert abs(int(ev.sum()) - int(rev.sum())) <= 1e-4 * int(rev.sum()) + 10
+
+
+def test_device_call_returns_before_the_kernels_end():
+    """The device ABI never waits on the GPU: a config-3-sized call returns while its
+    work is still queued on the caller's stream (no host syncs inside the call)."""
+    import time
+
+    import torch
+
+    from paper_2501_13382_b200 import engine
+    b = load_case("city_street")
+    dev = torch.device("cuda", 0)
+    db = engine.DeviceBundle.from_host(_pb(b), dev, with_frame=False)
+    x = np.arange(600) * 0.25 - 75.0
+    X, Y = np.meshgrid(x, x, indexing="xy")
+    obs = torch.from_numpy(np.stack([X.ravel(), Y.ravel(), np.full(X.size, 1.8)], 1)).to(dev)
+    acc = torch.zeros((obs.shape[0], 1), dtype=torch.complex128, device=dev)
+    ev = torch.zeros(obs.shape[0], dtype=torch.int64, device=dev)
+    s = torch.cuda.Stream(dev)
+    for _ in range(3):  # warm-up: grow-only workspaces and both statistics buffers
+        engine.accumulate(db, obs, b["omegas"], 10.0, True, acc, ev, stream=s)
+    torch.cuda.synchronize()
+    blocker = torch.cuda.Event()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(200_000_000)  # keep the stream busy (~0.1 s)
+        t0 = time.perf_counter()
+        engine.accumulate(db, obs, b["omegas"], 10.0, True, acc, ev, stream=s)
+        host_s = time.perf_counter() - t0
+        blocker.record(s)
+    assert not blocker.query()  # the call's kernels have not run yet
+    torch.cuda.synchronize()
+    assert host_s < 0.05
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
@@ -207,34 +298,6 @@ def _pb(b):
                       gamma2=b["gamma2"], c=float(b["c"]),
                       beam_param_im=float(b["beam_param_im"]),
                       amplitude_phi=float(b["amplitude_phi"]))
-
-
-def test_chunk_streamer_equals_single_call():
-    """Host-streamed beam chunks (double-buffered pinned copies) == one device call."""
-    import torch
-
-    from paper_2501_13382_b200 import engine
-    b = load_case("city_street")
-    dev = torch.device("cuda", 0)
-    pb = _pb(b)
-    obs = torch.from_numpy(b["obs"]).to(dev)
-    n = obs.shape[0]
-    ref = torch.zeros((n, 1), dtype=torch.complex128, device=dev)
-    rev = torch.zeros(n, dtype=torch.int64, device=dev)
-    engine.accumulate(engine.DeviceBundle.from_host(pb, dev, with_frame=False), obs,
-                      b["omegas"], 10.0, True, ref, rev, precision="fp32")
-    acc = torch.zeros_like(ref)
-    ev = torch.zeros_like(rev)
-    streamer = engine.ChunkStreamer(pb, [700, 700, 648], dev)
-    st = torch.cuda.current_stream(dev)
-
-    def consume(db, nb, lo):
-        engine.accumulate(db, obs, b["omegas"], 10.0, True, acc, ev, beam_hi=nb, stream=st)
-
-    streamer.run(consume, st)
-    torch.cuda.synchronize()
-    assert rel_l2(acc.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
-    assert torch.equal(ev, rev)
 
 
 def test_async_calls_on_two_streams():
@@ -562,7 +625,7 @@ def test_tile_order_compact_patches(n1, n2):
 
 
 @pytest.mark.parametrize("src", [(0.0, 20.0, 2.0), (-37.0, 3.0, 25.0), (150.0, -260.0, 1.0)])
-def test_tracer_cluster_culling_equals_exhaustive(src, monkeypatch):
+def test_tracer_cluster_culling_equals_exhaustive(src):
     """The tracer's triangle-cluster culling returns the same bits as testing every
     triangle (config-4 city: 500 buildings, 5002 triangles, up to 8 reflections)."""
     import torch
@@ -579,11 +642,11 @@ def test_tracer_cluster_culling_equals_exhaustive(src, monkeypatch):
     c = Atmosphere(20.0).sound_speed
     ds = engine.DeviceScene.from_scene(sc, dev)
     out = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("BF_TRACE_EXHAUSTIVE", mode)
-        out[mode] = engine.trace_device_rows(ds, source, launch, cfg, c, 0, len(launch), dev)
+    for mode in (False, True):
+        out[mode] = engine.trace_device_rows(ds, source, launch, cfg, c, 0, len(launch), dev,
+                                             exhaustive=mode)
         torch.cuda.synchronize()
-    a, b = out["0"]["bundle"], out["1"]["bundle"]
+    a, b = out[False]["bundle"], out[True]["bundle"]
     for name in ("seg_origin", "seg_dir", "seg_e1", "seg_e2", "seg_len", "seg_s0", "seg_refl",
                  "n_segs", "n_refls"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
