@@ -6,12 +6,19 @@
 A step is one pass of the hot path -- kernels.gbs_accumulate over ALL beams x
 ALL receivers of the workload -- on synthetic inputs traced
 on the device from the named scene.  Default workload: config 3 (city block,
-50 buildings, 500k rays, 1000x1000 receivers, 125 Hz), the north-star city
-shape.  `value` = N_beams x N_receivers / device time per step (max over
-ranks), inputs resident in HBM; `e2e` = the same metric through the
-reference-facing host-buffer call (H2D + kernels + D2H inside the timed
-region).  Under torchrun each rank sums its receiver tiles (shard.py) and the
-field is gathered to rank 0 inside the timed region (strong scaling).
+50 buildings, 500k rays, 1000x1000 receivers, 125 Hz).  `value` = N_beams x
+N_receivers / device time per step (max over ranks), inputs resident in HBM;
+`e2e` = the same metric through the reference-facing host-buffer call
+(kernels.gbs_accumulate on pageable numpy arrays -> bf_gbs_accumulate: host
+packing, H2D, kernels and D2H inside the timed region).  With N > 1 each rank
+sums its receiver tiles (shard.py) and the field is gathered to rank 0 inside
+the timed region (strong scaling: the problem is fixed).  `--gpus N` without
+torchrun re-launches itself under torch.distributed.run with N ranks.
+
+The same JSON line carries two more measurements of the same metric:
+`north_star_shape` (config 4: dense city, 4M rays x 4M receivers, the
+north-star shape, with its own roofline / e2e / CPU baseline / parity sample)
+and `fp64_oracle_mode` (the headline workload in the fp64 oracle mode).
 
 `--impl reference` times the reference algorithm's CPU implementation (the C
 oracle restatement in oracle/, bit-exact with the reference) on all host
@@ -23,6 +30,7 @@ import argparse
 import glob
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -34,6 +42,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "beam-receiver evals/sec and GBS wall time at 1/2/4/8 B200 vs CPU ref (cores stated)"
 
+CITY3 = (5, 10, 40.0, 20.0, 300.0)
+CITY4 = (20, 25, 40.0, 20.0, 600.0)
 CONFIGS = {
     "cfg1": dict(desc="open plane, 2k rays, 128x128 receivers (config 1)", scene="plane",
                  scene_args=(1000.0,), src=(0.0, 0.0, 5.0), freqs=(500.0,), im_b=-12.0,
@@ -44,12 +54,16 @@ CONFIGS = {
                  n_theta=250, n_phi=400, n_steps=8000, r_max=4,
                  grid=((-256.0, -256.0, 1.5), 0.5, 1024, 1024)),
     "cfg3": dict(desc="city block, 50 buildings, 500k rays, 1000x1000 receivers (config 3)",
-                 scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0), src=(20.0, 0.0, 2.0),
+                 scene="city", scene_args=CITY3, src=(20.0, 0.0, 2.0),
                  freqs=(125.0,), im_b=-10.0, n_theta=500, n_phi=1000, n_steps=5000, r_max=8,
                  grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
+    "cfg4": dict(desc="dense city, 500 buildings, 4M rays, 2000x2000 receivers (config 4)",
+                 scene="city", scene_args=CITY4, src=(0.0, 20.0, 2.0), freqs=(125.0,),
+                 im_b=-10.0, n_theta=2000, n_phi=2000, n_steps=5000, r_max=8,
+                 grid=((-400.0, -400.0, 1.8), 0.4, 2000, 2000)),
     # config-3 variant with the five-frequency set of the survey (63-1000 Hz)
     "cfg3s_f5": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers, F=5 "
-                          "(63-1000 Hz variant)", scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0),
+                          "(63-1000 Hz variant)", scene="city", scene_args=CITY3,
                      src=(20.0, 0.0, 2.0), freqs=(63.0, 125.0, 250.0, 500.0, 1000.0), im_b=-10.0,
                      n_theta=100, n_phi=200, n_steps=5000, r_max=8,
                      grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
@@ -57,12 +71,12 @@ CONFIGS = {
     # fires, so every non-behind pair is evaluated (no work-list culling)
     "cfg3s_pb": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers, "
                           "im_b=-45874 (paper beam parameter variant)", scene="city",
-                     scene_args=(5, 10, 40.0, 20.0, 300.0), src=(20.0, 0.0, 2.0),
+                     scene_args=CITY3, src=(20.0, 0.0, 2.0),
                      freqs=(125.0,), im_b=-45874.0, n_theta=100, n_phi=200, n_steps=5000,
                      r_max=8, grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
     # profiling variant of config 3: same scene/receivers, 20k rays (ncu replays stay short)
     "cfg3s": dict(desc="city block, 50 buildings, 20k rays, 1000x1000 receivers (cfg3 profile "
-                       "variant)", scene="city", scene_args=(5, 10, 40.0, 20.0, 300.0),
+                       "variant)", scene="city", scene_args=CITY3,
                   src=(20.0, 0.0, 2.0), freqs=(125.0,), im_b=-10.0, n_theta=100, n_phi=200,
                   n_steps=5000, r_max=8, grid=((-125.0, -125.0, 1.8), 0.25, 1000, 1000)),
 }
@@ -172,10 +186,6 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def flush_l2(buf):
-    buf.add_(1.0)  # 256 MiB write > 126 MB L2
-
-
 def flop_model(total_pairs_segs, p_nb, evals, nf):
     """Algorithmic FLOP / MUFU of SURVEY.md 8(d) for the pairs evaluated."""
     flop = 19.0 * total_pairs_segs + (16.0 + 5.0 * nf) * p_nb + 22.0 * evals
@@ -183,34 +193,64 @@ def flop_model(total_pairs_segs, p_nb, evals, nf):
     return flop, mufu
 
 
-def run_ours(args):
+class Dist:
+    """World of the run: NCCL ranks (one GPU each), or gloo ranks sharing cuda:0
+    (BF_BENCH_SHARE_DEVICE=1, a functional check of the multi-rank path)."""
+
+    def __init__(self, gpus):
+        import torch
+        import torch.distributed as dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != gpus:
+            raise SystemExit(f"bench.py: --gpus {gpus} but WORLD_SIZE={self.world}")
+        self.share = os.environ.get("BF_BENCH_SHARE_DEVICE") == "1"
+        if self.share:
+            self.local = 0
+        if self.world > 1:
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines in the log
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.dev = torch.device("cuda", self.local)
+        self.red_dev = torch.device("cpu") if self.share else self.dev
+        torch.cuda.set_device(self.dev)
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+
+    def max(self, *vals):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=self.red_dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
+
+    def close(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+def measure(D, name, precision, steps, warmup, peaks, cpu_budget, e2e_steps, cpu_sample=None):
+    """One workload at one precision on all ranks; the result dict on rank 0."""
     import torch
-    import torch.distributed as dist
 
     from paper_2501_13382_b200 import _lib, engine, kernels, shard
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # BF_BENCH_SHARE_DEVICE=1: every rank on cuda:0 with gloo (functional check of the
-    # multi-rank path on a one-GPU box; its timings are not a scaling measurement)
-    share = os.environ.get("BF_BENCH_SHARE_DEVICE") == "1"
-    if share:
-        local = 0
-    if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    red_dev = torch.device("cpu") if share else dev  # where the max-over-ranks reduce runs
-    torch.cuda.set_device(dev)
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS[name]
     sc, src, launch, tcfg, c, obs_np = make_inputs(cfg)
     omegas = src.omegas
     nf = omegas.shape[0]
     width_b = -src.beam_param_im
+    dev = D.dev
 
-    # ---- inputs: trace on the device (sm_100a tracer), resident in HBM
+    # ---- inputs: traced on the device by the sm_100a tracer (every rank), in HBM
     dscene = engine.DeviceScene.from_scene(sc, dev)
     tr = engine.trace_device_rows(dscene, src, launch, tcfg, c, 0, len(launch), dev)
     bundle = tr["bundle"]
@@ -220,40 +260,36 @@ def run_ours(args):
     obs_all = torch.from_numpy(obs_np).to(dev)
     n_total = obs_all.shape[0]
     order = shard.tile_order(obs_all)
-    mine = shard.rank_indices(order, rank, world)
+    mine = shard.rank_indices(order, D.rank, D.world)
     obs = obs_all.index_select(0, mine).contiguous()
     n_loc = obs.shape[0]
     acc = torch.zeros((n_loc, nf), dtype=torch.complex128, device=dev)
     evals = torch.zeros(n_loc, dtype=torch.int64, device=dev)
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    prec = args.precision
-
     # the gather's index plan is part of the partition, built once (not per step)
-    plan = shard.GatherPlan(order, world, n_total) if world > 1 else None
+    plan = shard.GatherPlan(order, D.world, n_total) if D.world > 1 else None
 
     def step():
         acc.zero_()
         evals.zero_()
-        engine.accumulate(bundle, obs, omegas, width_b, True, acc, evals, precision=prec,
+        engine.accumulate(bundle, obs, omegas, width_b, True, acc, evals, precision=precision,
                           stream=stream, presorted=True)
-        if world > 1:
-            shard.gather_field(acc, evals, order, rank, world, n_total, plan=plan)
+        if D.world > 1:
+            shard.gather_field(acc, evals, order, D.rank, D.world, n_total, plan=plan)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    peaks = _lib.probe_peaks(local) if rank == 0 else None
 
     # ---- timed region (device events per step; L2 flushed between steps)
-    if world > 1:
-        dist.barrier()
+    D.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     ms_steps, kern_ms, stats = [], [], []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush_l2(flush)
+    with ClockSampler(D.local) as clk:
+        for _ in range(steps):
+            flush.add_(1.0)  # 256 MiB write > 126 MB L2
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -266,52 +302,45 @@ def run_ours(args):
             stats.append(st)
         torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
-    if world > 1:
-        dist.barrier()
-    ms = float(np.mean(ms_steps))
-    t = torch.tensor([ms, float(np.mean(kern_ms))], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_max = float(t[0]), float(t[1])
+    D.barrier()
+    ms_max, kern_max = D.max(np.mean(ms_steps), np.mean(kern_ms))
     pairs = float(nb) * float(n_total)
     value = pairs / (ms_max / 1e3)
 
-    # ---- e2e: reference-facing host-buffer call (C ABI bf_gbs_accumulate)
-    host = {k: torch.empty(tuple(getattr(bundle, k).shape), dtype=getattr(bundle, k).dtype,
-                           pin_memory=True) for k in engine.SEG_FIELDS + ("n_segs", "weights")}
-    for k, v in host.items():
-        v.copy_(getattr(bundle, k))
-    hb = {k: v.numpy() for k, v in host.items()}
-    obs_h = torch.empty((n_loc, 3), dtype=torch.float64, pin_memory=True)
-    obs_h.copy_(obs)
-    obs_h = obs_h.numpy()
-    acc_h = torch.zeros((n_loc, nf), dtype=torch.complex128, pin_memory=True).numpy()
-    ev_h = torch.zeros(n_loc, dtype=torch.int64, pin_memory=True).numpy()
+    # ---- e2e: reference-facing host-buffer call on PAGEABLE numpy arrays
+    hb = {k: getattr(bundle, k).cpu().numpy().copy() for k in engine.SEG_FIELDS + (
+        "n_segs", "weights")}
+    obs_h = obs.cpu().numpy().copy()
+    acc_h = np.zeros((n_loc, nf), np.complex128)
+    ev_h = np.zeros(n_loc, np.int64)
 
     def e2e_step():
-        kernels.gbs_accumulate(hb["seg_origin"], hb["seg_dir"], hb["seg_e1"], hb["seg_e2"],
-                               hb["seg_len"], hb["seg_s0"], hb["seg_refl"], hb["n_segs"],
-                               bundle.max_seg, hb["weights"], obs_h, omegas, c, width_b,
-                               src.amplitude_phi, True, acc_h, ev_h, 0, n_loc, 0, nb,
-                               precision=prec, device=local)
+        acc_h[...] = 0
+        ev_h[...] = 0
+        kernels.gbs_accumulate(hb["seg_origin"], hb["seg_dir"], hb["seg_e1"],
+                               hb["seg_e2"], hb["seg_len"], hb["seg_s0"], hb["seg_refl"],
+                               hb["n_segs"], bundle.max_seg, hb["weights"], obs_h, omegas, c,
+                               width_b, src.amplitude_phi, True, acc_h, ev_h, 0, n_loc, 0, nb,
+                               precision=precision, device=D.local)
 
     e2e_step()
+    e2e_same = bool(np.array_equal(acc_h, acc.cpu().numpy()))
     e2e_t = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(e2e_steps):
+        D.barrier()
         t0 = time.perf_counter()
         e2e_step()
         e2e_t.append(time.perf_counter() - t0)
-    tt = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    e2e_s = float(tt[0])
-    rows = nb * bundle.max_seg
-    per_row = 24 * 2 + 8 * 3 + (48 if prec == "fp64" else 0)
-    h2d = rows * per_row + nb * 12 + n_loc * (24 + 16 * nf + 8)
+    (e2e_s,) = D.max(np.mean(e2e_t))
+    rows = int(bundle.n_segs.sum().item())
+    if precision == "fp32":  # compact rows: o, d, len, s0 (fp64) + amplitude (fp32)
+        h2d = rows * 68 + nb * 8 + n_loc * (24 + 16 * nf + 8)
+    else:  # padded fp64 rows incl. the frames
+        h2d = nb * bundle.max_seg * 120 + nb * 12 + n_loc * (24 + 16 * nf + 8)
     d2h = n_loc * (16 * nf + 8)
 
     out = None
-    if rank == 0:
+    if D.rank == 0:
         st = stats[-1]
         ev_sum = int(evals.sum().item())
         p_nb = st["nonbehind_pairs"]
@@ -321,37 +350,42 @@ def run_ours(args):
         flop_a9, _ = flop_model(float(st["candidate_pair_segs"]), p_nb, ev_sum, nf)
         flop_live, _ = flop_model(float(st["live_pair_segs"]), p_nb, ev_sum, nf)
         kernel_s = kern_max / 1e3
-        if prec == "fp64":
+        if precision == "fp64":
             # oracle mode: dense kernel, no work list or kernel statistics -> FLOP model
             # over all pairs (segment scan + evaluations), timed by the step
-            flop = flop_a9 = flop_live = 19.0 * n_total * sum_segs + 22.0 * ev_sum
+            flop = flop_a9 = flop_live = 19.0 * n_loc * sum_segs + 22.0 * ev_sum
             mufu = 3.0 * ev_sum
             kernel_s = ms_max / 1e3
         traffic = None  # DRAM bytes of the summation kernel from the committed ncu capture
         for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "round*", "ncu_*_traffic.json"))):
             with open(tf) as fh:
                 tj = json.load(fh)
-            if tj.get("config") == args.config and world == 1:
+            if tj.get("config") == name and D.world == 1 and precision == "fp32":
                 traffic = tj["dram_read_bytes"] + tj["dram_write_bytes"]
         ach = flop / kernel_s / 1e12
-        clocks = clk.summary()
         peak = peaks["fp32_tflops"]
         out = {
             "metric": METRIC, "value": value, "unit": "beam-receiver evals/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "n_gpus": D.world, "steps": steps, "warmup": warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg['desc']}", "beams": nb,
+            "dtype": "f32" if precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"{name}: {cfg['desc']}", "beams": nb,
                        "receivers": n_total, "segments": sum_segs, "max_seg": bundle.max_seg,
                        "freqs_hz": list(cfg["freqs"]), "im_b": cfg["im_b"],
-                       "precision": prec, "parallelism": f"receiver-tiles x{world}",
+                       "precision": precision,
+                       "parallelism": f"receiver-tiles x{D.world}" + (
+                           " (ranks share cuda:0, gloo)" if D.share else ""),
                        "l2": "flushed (256 MiB write) between timed steps",
-                       "inputs": "traced on device by the sm_100a tracer (bit-exact vs reference)"},
+                       "inputs": "traced on device by the sm_100a tracer (bit-exact vs "
+                                 "reference), on every rank, before the timed region"},
             "gbs_wall_s": ms_max / 1e3,
             "e2e": {"value": pairs / e2e_s, "unit": "beam-receiver evals/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "seconds_per_step": e2e_s,
-                    "path": "kernels.gbs_accumulate(host numpy, pinned) -> bf_gbs_accumulate"},
+                    "seconds_per_step": e2e_s, "steps": e2e_steps,
+                    "equals_device_result_bitwise": e2e_same,
+                    "path": "kernels.gbs_accumulate(pageable numpy) -> bf_gbs_accumulate "
+                            "(host threads pack compact rows into pinned staging, beam groups "
+                            "streamed); per rank, max over ranks, no field gather"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": ach / peak, "traffic": traffic,
@@ -361,8 +395,8 @@ def run_ours(args):
                          "frac_evaluated_items": flop_live / kernel_s / 1e12 / peak,
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, committed "
                                          "profile of this config)" if traffic else None,
-                         "peak_source": "measured FFMA stream (bf_probe_peaks), this GPU",
-                         "kernel": "gbs_fp32_kernel" if prec == "fp32" else
+                         "peak_source": peaks["source"],
+                         "kernel": "gbs_fp32_kernel" if precision == "fp32" else
                                    "gbs_fp64_kernel (oracle mode, dense; FP32 peak as a "
                                    "common yardstick)",
                          "kernel_ms": kernel_s * 1e3,
@@ -379,16 +413,18 @@ def run_ours(args):
                          "candidate_pairs_tight": st["tight_pairs"],
                          "evaluated_item_pairs": st["live_pairs"],
                          "dense_pairs": int(nb) * int(n_loc)},
-            "clocks": clocks,
+            "clocks": clk.summary(),
         }
-    if world == 1 and not args.no_cpu_baseline:
+    if D.world == 1 and cpu_budget > 0:
         acc_gpu = acc.cpu().numpy()
         ev_gpu = evals.cpu().numpy()
         order_np = order.cpu().numpy()
-        hb_full = dict(hb, max_seg=bundle.max_seg)
-        th = cpu_threads()
-        rate, sample, idx, acc_cpu, ev_cpu, dt = time_oracle_sample(
-            hb_full, obs_np, omegas, c, width_b, src.amplitude_phi, args.cpu_budget, th)
+        if cpu_sample is None:
+            hbf = dict(hb, max_seg=bundle.max_seg)
+            th = cpu_threads()
+            cpu_sample = time_oracle_sample(hbf, obs_np, omegas, c, width_b, src.amplitude_phi,
+                                            cpu_budget, th) + (th,)
+        rate, sample, idx, acc_cpu, ev_cpu, dt, th = cpu_sample
         pos = np.empty(n_total, np.int64)
         pos[order_np] = np.arange(n_total)
         mine_acc = acc_gpu[pos[idx]]
@@ -406,13 +442,39 @@ def run_ours(args):
                 np.abs(mine_acc[strong]) / np.abs(ref[strong]))))) if strong.any() else 0.0,
             "max_dtl_db_all": float(np.max(np.abs(20 * np.log10(
                 np.abs(mine_acc[m]) / np.abs(ref[m]))))) if m.any() else 0.0,
+            "zero_where_reference_nonzero": int(np.sum(m & (np.abs(mine_acc) == 0))),
             "evals_diff": int(np.abs(ev_gpu[pos[idx]] - ev_cpu).sum()),
         }
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    del bundle, tr, acc, evals, flush, obs, obs_all, hb
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out, cpu_sample
+
+
+def run_ours(args):
+    from paper_2501_13382_b200 import _lib
+    D = Dist(args.gpus)
+    peaks = None
+    if D.rank == 0:
+        p = _lib.probe_peaks(D.local)
+        peaks = {"fp32_tflops": p["fp32_tflops"], "mufu_tops": p["mufu_tops"],
+                 "source": "measured FFMA / FFMA2 stream (bf_probe_peaks, the faster of the "
+                           "two), this GPU"}
+    cpu = 0.0 if args.no_cpu_baseline else args.cpu_budget
+    line, sample = measure(D, args.config, args.precision, args.steps, args.warmup, peaks, cpu,
+                           e2e_steps=max(1, min(args.steps, 3)))
+    if not args.headline_only:
+        ns, _ = measure(D, "cfg4", "fp32", min(args.steps, 2), 3, peaks, cpu, e2e_steps=1)
+        if D.rank == 0:
+            line["north_star_shape"] = ns
+        if args.precision == "fp32":
+            o64, _ = measure(D, args.config, "fp64", min(args.steps, 2), 3, peaks, cpu,
+                             e2e_steps=1, cpu_sample=sample)
+            if D.rank == 0:
+                line["fp64_oracle_mode"] = o64
+    if D.rank == 0:
+        print(json.dumps(line), flush=True)
+    D.close()
 
 
 def run_reference(args):
@@ -458,6 +520,14 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -471,9 +541,17 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=60.0,
                     help="total seconds of CPU work for the --impl reference arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="skip the config-4 and fp64 measurements of the same line")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -139,6 +139,33 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
                           void *stream);
 
 /*
+ * Compact segment rows resident on one device -- the traced-ray output repacked into
+ * the fp32 path's SoA (beam b owns rows [start[b], start[b+1]); per row origin/len and
+ * direction/s0 in fp64, the fp32 amplitude A = phi sqrt(c)/(2 pi c) refl w_b: 68 B per
+ * segment, no padding).  run_pipeline appends each traced chunk
+ * (parallel.py:297-338) and sums ALL rays in one call, so the field does not depend on
+ * the chunk plan.  Handles are not thread-safe; calls on them serialise on the device.
+ */
+typedef struct bf_rows bf_rows;
+int bf_rows_create(int device, bf_rows **out);
+int bf_rows_destroy(bf_rows *rows);
+/* Beams and (exact) rows appended so far. */
+int bf_rows_info(const bf_rows *rows, int64_t *n_beams, int64_t *n_rows);
+/* Appends the valid rows of padded DEVICE bundle beams [0, n_beams) (reference PathBundle
+ * layout, beamtrace.py:218-288; max_seg <= 30).  Ordered on `stream` (NULL = engine
+ * stream); returns after the append (one sync for the exact row count). */
+int bf_rows_append_dev(bf_rows *rows, const double *seg_origin, const double *seg_dir,
+                       const double *seg_len, const double *seg_s0, const double *seg_refl,
+                       const int32_t *n_segs, const double *weights, int64_t n_beams,
+                       int64_t max_seg, double c, double phi_amp, void *stream);
+/* bf_gbs_accumulate_dev (fp32 mode) over beams [beam_lo, beam_hi) of the resident rows:
+ * same result bits as bf_gbs_accumulate_dev on the concatenated padded bundle. */
+int bf_gbs_accumulate_rows_dev(const bf_rows *rows, const double *obs, int64_t n_obs,
+                               const double *omegas, int64_t nf, double width_b, int use_cutoff,
+                               double *acc, int64_t *evals, int64_t obs_lo, int64_t obs_hi,
+                               int64_t beam_lo, int64_t beam_hi, int flags, void *stream);
+
+/*
  * Work list of the fp32 path, exposed for verification: the
  * Hilbert receiver order perm (n_obs), tile centres/radii centre (n_tiles x 4:
  * x, y, z, R_T) and the candidate bitmask bits (n_tiles x ceil(n_beams/32)

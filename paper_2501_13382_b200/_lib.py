@@ -25,7 +25,8 @@ EXPORTS = (
     "bf_gbs_accumulate", "bf_gbs_accumulate_dev", "bf_nearest_on_segments",
     "bf_trace_range_dev", "bf_field_finalize_dev", "bf_plan_chunks", "bf_last_stats",
     "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats", "bf_worklist",
-    "bf_last_pair_stats", "bf_write_field_csv", "bf_set_memory_budget",
+    "bf_last_pair_stats", "bf_write_field_csv", "bf_set_memory_budget", "bf_rows_create",
+    "bf_rows_destroy", "bf_rows_info", "bf_rows_append_dev", "bf_gbs_accumulate_rows_dev",
 )
 FLAG_OBS_PRESORTED = 1
 TRACE_EXHAUSTIVE = 1
@@ -61,6 +62,12 @@ def _declare(lib):
     lib.bf_trace_range_dev.argtypes = ([VP, VP, VP, VP, I64, VP, F64, VP, VP, VP, VP, F64, I64,
                                         I64] + [VP] * 9 + [I64, I64, I64, INT, INT, VP])
     lib.bf_set_memory_budget.argtypes = [INT, I64]
+    lib.bf_rows_create.argtypes = [INT, ctypes.POINTER(VP)]
+    lib.bf_rows_destroy.argtypes = [VP]
+    lib.bf_rows_info.argtypes = [VP, I64P, I64P]
+    lib.bf_rows_append_dev.argtypes = [VP] * 8 + [I64, I64, F64, F64, VP]
+    lib.bf_gbs_accumulate_rows_dev.argtypes = [VP, VP, I64, VP, I64, F64, INT, VP, VP, I64, I64,
+                                               I64, I64, INT, VP]
     lib.bf_field_finalize_dev.argtypes = [VP, I64, F64, VP, VP, INT, VP]
     lib.bf_plan_chunks.argtypes = [I64, I64, I64, I64P, I64, I64P]
     lib.bf_last_stats.argtypes = [I64P, I64P, I64P, I64P, I64P, D, I64P]

@@ -136,10 +136,13 @@ int64_t gbs_fp32_range_beams(int64_t n_beams, int nf);
 // hold the exclusive scan of n_segs (n_beams + 1 entries); amp_scale = phi sqrt(c)/(2 pi c).
 int launch_rows_pack(const GbsArgs &a, const int64_t *start, double4 *p0, double4 *p1,
                      float *amp, cudaStream_t st);
-// cnt[0] = 0, cnt[b + 1] = n_segs[b] clamped to [0, max_seg]; an inclusive scan of cnt
-// (engine.cu, cub) then gives the compact row starts.
-int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t *cnt,
-                      cudaStream_t st);
+// cnt[0] = base, cnt[b + 1] = n_segs[b] clamped to [0, max_seg]; an inclusive scan of cnt
+// (engine.cu, cub) then gives the compact row starts (rows from `base` on).
+int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t base,
+                      int64_t *cnt, cudaStream_t st);
+// Beams [b0, b0 + nb) of resident rows src -> rows of their own (start rebased to 0).
+int launch_rows_slice(const Rows &src, int64_t b0, int64_t nb, int64_t *start, double4 *p0,
+                      double4 *p1, float *amp, cudaStream_t st);
 // fp64-exact phase anchors of the compact rows [0, rows_bound) (rows past
 // start[n_beams] are skipped): pa[row * nf + f] = frac(kappa_f s0), frac(kappa_f (s0+len)).
 int launch_fp32_anchors(const GbsArgs &a, const Rows &r, int64_t rows_bound, float *pa,

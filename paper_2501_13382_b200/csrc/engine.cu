@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <functional>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -619,8 +620,9 @@ struct GroupPlan {
 };
 
 // Beam groups of whole ranges sized so that NSLOT groups' workspaces fit the budget.
-// The host-buffer path ramps the group size up from one range (1, 2, 4, ...) so the
-// first group's copy is short and the later copies hide behind the summation.
+// The host-buffer path ramps the group size up from one range (1, 8, 64, ...) so the
+// first group's packing and copy are short and the later ones hide behind the summation
+// (few groups: each group's kernel ends in a tail of long units near the source).
 void plan_groups(DeviceCtx *c, int64_t nb, int64_t max_seg, int nf, int64_t n_tiles,
                  int64_t n_patches, int64_t n_pad, bool host, GroupPlan *g) {
     g->range_beams = gbs_fp32_range_beams(nb, nf);
@@ -644,7 +646,7 @@ void plan_groups(DeviceCtx *c, int64_t nb, int64_t max_seg, int nf, int64_t n_ti
         const int64_t n = std::min(step, g->n_ranges - q);
         g->groups.emplace_back(q, q + n);
         q += n;
-        step = std::min(max_r, step * 2);
+        step = std::min(max_r, step * 8);
     }
 }
 
@@ -748,7 +750,7 @@ int rows_from_device(const GbsArgs &g, Slot &s, Rows *out) {
     BF_TRY(s.get(S_P0, (size_t)std::max<int64_t>(nb * S, 1), &dp0));
     BF_TRY(s.get(S_P1, (size_t)std::max<int64_t>(nb * S, 1), &dp1));
     BF_TRY(s.get(S_AMP, (size_t)std::max<int64_t>(nb * S, 1), &da));
-    BF_TRY(launch_rows_count(g.n_segs, nb, S, ds, s.ss));
+    BF_TRY(launch_rows_count(g.n_segs, nb, S, 0, ds, s.ss));
     size_t tb = 0;
     BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, ds, ds, (int)(nb + 1), s.ss));
     void *tmp;
@@ -760,11 +762,53 @@ int rows_from_device(const GbsArgs &g, Slot &s, Rows *out) {
     return BF_OK;
 }
 
+}  // namespace
+}  // namespace bf
+
+// Compact segment rows resident on one device (bf_rows_*): appended chunk by chunk,
+// summed in one call.
+struct bf_rows {
+    int device = 0;
+    int64_t n_beams = 0, n_rows = 0;     // exact totals
+    int64_t cap_beams = 0, cap_rows = 0;  // allocated
+    int64_t max_seg = 0;                  // largest padded row count appended
+    double c = 0.0, phi_amp = 0.0;
+    int64_t *start = nullptr;             // n_beams + 1
+    double4 *p0 = nullptr, *p1 = nullptr;
+    float *amp = nullptr;
+    bf::Rows view() const { return bf::Rows{start, p0, p1, amp, n_beams, max_seg}; }
+};
+
+namespace bf {
+namespace {
+
+// Beams [b0, b0 + nb) of resident rows copied into the slot's own rows (start at 0).
+int rows_from_resident(const bf_rows &R, int64_t b0, int64_t nb, Slot &s, Rows *out) {
+    const int64_t S = R.max_seg;
+    int64_t *ds;
+    double4 *dp0, *dp1;
+    float *da;
+    BF_TRY(s.get(S_START, (size_t)(nb + 1), &ds));
+    BF_TRY(s.get(S_P0, (size_t)std::max<int64_t>(nb * S, 1), &dp0));
+    BF_TRY(s.get(S_P1, (size_t)std::max<int64_t>(nb * S, 1), &dp1));
+    BF_TRY(s.get(S_AMP, (size_t)std::max<int64_t>(nb * S, 1), &da));
+    BF_TRY(launch_rows_slice(R.view(), b0, nb, ds, dp0, dp1, da, s.ss));
+    *out = Rows{ds, dp0, dp1, da, nb, S};
+    return BF_OK;
+}
+
 // The fp32 operator on LOCAL ranges: base.obs/acc/evals are device pointers (offset to
 // obs_lo, acc rows of base.acc_stride complex values); base.seg_*/n_segs/weights are the
 // padded bundle from beam_lo, on the device or (host_rows) in host memory.
+// first_fold (may be null) runs on the host right before the first fold is enqueued on st
+// (the host-buffer path stages and uploads the caller's acc/evals there, overlapping the
+// first group's kernels).
+// resident (may be null): the beams are rows [beam_off, beam_off + base.n_beams) of these
+// resident compact rows instead of base.seg_*.
 int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf,
-             bool host_rows, int flags, cudaStream_t st) {
+             bool host_rows, int flags, cudaStream_t st,
+             const std::function<int()> *first_fold = nullptr,
+             const bf_rows *resident = nullptr, int64_t beam_off = 0) {
     stats_begin(base.n_obs * base.n_beams);
     if (base.n_obs <= 0 || base.n_beams <= 0 || nf <= 0) return BF_OK;
     // ---- prologue on the call's stream: receiver tiling, patches, zeroed counters
@@ -830,7 +874,11 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             // ---- compact rows of the group
             Rows rv;
             int64_t rows_bound;
-            if (host_rows) {
+            if (resident) {
+                BF_TRY(rows_from_resident(*resident, beam_off + b0, gg.n_beams, s, &rv));
+                rows_bound = gg.n_beams * resident->max_seg;
+                gg.max_seg = resident->max_seg;
+            } else if (host_rows) {
                 BF_TRY(rows_from_host(ag, b0, gg.n_beams, s, &rv, &rows_bound));
             } else {
                 BF_TRY(rows_from_device(gg, s, &rv));
@@ -913,6 +961,10 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             BF_TRY(launch_gbs_fp32(gg, tg, w, d_stats, StreamPair{s.ss, s.sw, s.fork, s.join}));
             BF_TRY_CUDA(cudaEventRecord(s.kdone, s.ss));
             // ---- fold on the call's stream, groups in order
+            if (first_fold) {
+                BF_TRY((*first_fold)());
+                first_fold = nullptr;
+            }
             BF_TRY_CUDA(cudaStreamWaitEvent(st, s.kdone, 0));
             BF_TRY(launch_fp32_fold(gg, tg, w, st));
             BF_TRY_CUDA(cudaEventRecord(s.freed, st));
@@ -1160,16 +1212,22 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
     BF_TRY_CUDA(cudaSetDevice(device));
     cudaStream_t st = ctx->stream;
     StreamOrder order(ctx, st);
-    // observers and the caller's acc/evals rows go to the device first (the tiling needs
-    // the observers; acc/evals are only read by the first fold)
+    // observers go to the device first (the tiling needs them); the caller's acc/evals
+    // rows are only read by the first fold, so they are staged and uploaded while the
+    // first beam group sums (fp32) -- or right away (fp64)
     double *d_obs, *d_acc;
     int64_t *d_ev;
     BF_TRY(ctx->get(B_OBS, (size_t)(3 * no), &d_obs));
     BF_TRY(ctx->get(B_ACC, (size_t)(2 * no * nf), &d_acc));
     BF_TRY(ctx->get(B_EVALS, (size_t)no, &d_ev));
     BF_TRY(h2d(d_obs, obs + 3 * obs_lo, 24 * (size_t)no, ctx->hpin[H_OBS], st));
-    BF_TRY(h2d(d_acc, acc + 2 * obs_lo * nf, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
-    BF_TRY(h2d(d_ev, evals + obs_lo, 8 * (size_t)no, ctx->hpin[H_EV], st));
+    bool uploaded = false;
+    const std::function<int()> upload_fields = [&]() -> int {
+        BF_TRY(h2d(d_acc, acc + 2 * obs_lo * nf, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
+        BF_TRY(h2d(d_ev, evals + obs_lo, 8 * (size_t)no, ctx->hpin[H_EV], st));
+        uploaded = true;
+        return BF_OK;
+    };
     GbsArgs a{};
     const int64_t r0 = beam_lo * max_seg;
     a.seg_origin = seg_origin + 3 * r0;
@@ -1193,12 +1251,159 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
     a.acc = d_acc;
     a.acc_stride = nf;
     a.evals = d_ev;
-    if (precision == BF_PRECISION_FP64)
+    if (precision == BF_PRECISION_FP64) {
+        BF_TRY(upload_fields());
         BF_TRY(run_fp64_host(ctx, a, omegas, nf, st));
-    else
-        BF_TRY(run_fp32(ctx, a, omegas, nf, true, 0, st));
+    } else {
+        BF_TRY(run_fp32(ctx, a, omegas, nf, true, 0, st, &upload_fields));
+    }
+    if (!uploaded) BF_TRY(upload_fields());  // (no group ran: acc/evals come back unchanged)
     BF_TRY(d2h_sync(acc + 2 * obs_lo * nf, d_acc, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
     BF_TRY(d2h_sync(evals + obs_lo, d_ev, 8 * (size_t)no, ctx->hpin[H_EV], st));
+    return BF_OK;
+}
+
+int bf_rows_create(int device, bf_rows **out) {
+    if (!out) return fail(BF_EINVAL, "null output");
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(device, &ctx));
+    bf_rows *r = new bf_rows();
+    r->device = device;
+    *out = r;
+    return BF_OK;
+}
+
+int bf_rows_destroy(bf_rows *rows) {
+    if (!rows) return BF_OK;
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(rows->device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(rows->device));
+    if (ctx->done_valid) cudaEventSynchronize(ctx->done);  // no call still reads them
+    cudaFree(rows->start);
+    cudaFree(rows->p0);
+    cudaFree(rows->p1);
+    cudaFree(rows->amp);
+    delete rows;
+    return BF_OK;
+}
+
+int bf_rows_info(const bf_rows *rows, int64_t *n_beams, int64_t *n_rows) {
+    if (!rows) return fail(BF_EINVAL, "null rows");
+    if (n_beams) *n_beams = rows->n_beams;
+    if (n_rows) *n_rows = rows->n_rows;
+    return BF_OK;
+}
+
+int bf_rows_append_dev(bf_rows *rows, const double *seg_origin, const double *seg_dir,
+                       const double *seg_len, const double *seg_s0, const double *seg_refl,
+                       const int32_t *n_segs, const double *weights, int64_t n_beams,
+                       int64_t max_seg, double c, double phi_amp, void *stream) {
+    if (!rows) return fail(BF_EINVAL, "null rows");
+    if (n_beams < 0 || max_seg < 1) return fail(BF_EINVAL, "bad sizes");
+    if (max_seg > BF_FP32_MAX_SEG)
+        return fail(BF_EINVAL, "compact rows serve the fp32 path: max_seg <= %d",
+                    BF_FP32_MAX_SEG);
+    if (rows->n_beams > 0 && (c != rows->c || phi_amp != rows->phi_amp))
+        return fail(BF_EINVAL, "appended bundles must share c and amplitude_phi");
+    if (n_beams == 0) return BF_OK;
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(rows->device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(rows->device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    StreamOrder order(ctx, st);
+    // capacity: exact rows so far + the padded bound of this chunk (grow-only, copied)
+    const int64_t need_b = rows->n_beams + n_beams + 1, need_r = rows->n_rows + n_beams * max_seg;
+    if (need_b > rows->cap_beams || need_r > rows->cap_rows) {
+        const int64_t cb = std::max(need_b, rows->cap_beams + rows->cap_beams / 2);
+        const int64_t cr = std::max(need_r, rows->cap_rows + rows->cap_rows / 2);
+        int64_t *ns;
+        double4 *n0, *n1;
+        float *na;
+        BF_TRY_CUDA(cudaMalloc(&ns, 8 * (size_t)cb));
+        BF_TRY_CUDA(cudaMalloc(&n0, 32 * (size_t)cr));
+        BF_TRY_CUDA(cudaMalloc(&n1, 32 * (size_t)cr));
+        BF_TRY_CUDA(cudaMalloc(&na, 4 * (size_t)cr));
+        if (rows->start) {
+            const auto D2D = cudaMemcpyDeviceToDevice;
+            BF_TRY_CUDA(cudaMemcpyAsync(ns, rows->start, 8 * (size_t)(rows->n_beams + 1), D2D, st));
+            BF_TRY_CUDA(cudaMemcpyAsync(n0, rows->p0, 32 * (size_t)rows->n_rows, D2D, st));
+            BF_TRY_CUDA(cudaMemcpyAsync(n1, rows->p1, 32 * (size_t)rows->n_rows, D2D, st));
+            BF_TRY_CUDA(cudaMemcpyAsync(na, rows->amp, 4 * (size_t)rows->n_rows, D2D, st));
+            BF_TRY_CUDA(cudaStreamSynchronize(st));
+            cudaFree(rows->start);
+            cudaFree(rows->p0);
+            cudaFree(rows->p1);
+            cudaFree(rows->amp);
+        }
+        rows->start = ns;
+        rows->p0 = n0;
+        rows->p1 = n1;
+        rows->amp = na;
+        rows->cap_beams = cb;
+        rows->cap_rows = cr;
+    }
+    GbsArgs a{};
+    a.seg_origin = seg_origin;
+    a.seg_dir = seg_dir;
+    a.seg_len = seg_len;
+    a.seg_s0 = seg_s0;
+    a.seg_refl = seg_refl;
+    a.n_segs = n_segs;
+    a.weights = weights;
+    a.n_beams = n_beams;
+    a.max_seg = max_seg;
+    a.c = c;
+    a.phi_amp = phi_amp;
+    int64_t *st0 = rows->start + rows->n_beams;  // entry 0 = rows so far
+    BF_TRY(launch_rows_count(n_segs, n_beams, max_seg, rows->n_rows, st0, st));
+    size_t tb = 0;
+    BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, st0, st0, (int)(n_beams + 1), st));
+    void *tmp;
+    BF_TRY(ctx->buf[B_CUB].get(tb + 16, &tmp));
+    BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, st0, st0, (int)(n_beams + 1), st));
+    note_launch();
+    BF_TRY(launch_rows_pack(a, st0, rows->p0, rows->p1, rows->amp, st));
+    int64_t total = 0;  // the exact row count (the next append's offset): one sync
+    BF_TRY_CUDA(cudaMemcpyAsync(&total, st0 + n_beams, 8, cudaMemcpyDeviceToHost, st));
+    BF_TRY_CUDA(cudaStreamSynchronize(st));
+    rows->n_beams += n_beams;
+    rows->n_rows = total;
+    rows->max_seg = std::max(rows->max_seg, max_seg);
+    rows->c = c;
+    rows->phi_amp = phi_amp;
+    return BF_OK;
+}
+
+int bf_gbs_accumulate_rows_dev(const bf_rows *rows, const double *obs, int64_t n_obs,
+                               const double *omegas, int64_t nf, double width_b, int use_cutoff,
+                               double *acc, int64_t *evals, int64_t obs_lo, int64_t obs_hi,
+                               int64_t beam_lo, int64_t beam_hi, int flags, void *stream) {
+    if (!rows) return fail(BF_EINVAL, "null rows");
+    BF_TRY(validate(rows->n_beams, std::max<int64_t>(rows->max_seg, 1), n_obs, nf, obs_lo,
+                    obs_hi, beam_lo, beam_hi, BF_PRECISION_FP32));
+    DeviceCtx *ctx;
+    BF_TRY(get_ctx(rows->device, &ctx));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    BF_TRY_CUDA(cudaSetDevice(rows->device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    StreamOrder order(ctx, st);
+    GbsArgs a{};
+    a.obs = obs + 3 * obs_lo;
+    a.max_seg = std::max<int64_t>(rows->max_seg, 1);
+    a.n_beams = beam_hi - beam_lo;
+    a.n_obs = obs_hi - obs_lo;
+    a.nf = (int)std::min<int64_t>(nf, BF_MAXF);
+    a.c = rows->c;
+    a.width_b = width_b;
+    a.phi_amp = rows->phi_amp;
+    a.use_cutoff = use_cutoff ? 1 : 0;
+    a.acc = acc + 2 * obs_lo * nf;
+    a.acc_stride = nf;
+    a.evals = evals + obs_lo;
+    BF_TRY(run_fp32(ctx, a, omegas, nf, false, flags, st, nullptr, rows, beam_lo));
+    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
     return BF_OK;
 }
 

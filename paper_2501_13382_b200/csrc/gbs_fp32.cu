@@ -38,6 +38,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 // Compile-time switches (tuning and diagnostics; the defaults are the product):
@@ -110,6 +112,8 @@ struct Fp32Consts {
     float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36); 0 without cutoff
     float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
     float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
+    double nhkbl2e64[BF_MAXF];
+    float tiny;              // amplitudes below this are redone in fp64 (0 with the cutoff)
     float b, b2;             // width_b, width_b^2
     int ascending;           // omegas nondecreasing (cutk nondecreasing)
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
@@ -182,17 +186,34 @@ struct WarpSmem {
 // sqrt(c) (s + i b)/m2 exp(-g b) exp(i(omega s/c + g s)), contribution
 // i omega/(2 pi c) w_b field.  `base[f]` is the fp64-anchored axial phase
 // omega s/(2 pi c) reduced to turns.
+//
+// Without the cutoff exp(-g b) can fall below the fp32 range (a receiver far off every
+// beam axis: the reference's fp64 sum is ~1e-40..1e-300 of the field maximum).  An
+// amplitude below K.tiny (2^-100; 0 with the cutoff, where exp(-g b) >= e^-36) is
+// recomputed in fp64 from the same fp32 s, q^2, m2 and phase and added straight into
+// the fp64 accumulator, so such receivers keep the reference's magnitude.
+__device__ __noinline__ void tiny_contribution(const Fp32Consts &K, int f, float s, float gq,
+                                               float ainv, float sn, float cs, double *acc64) {
+    const double e = exp2((double)gq * K.nhkbl2e64[f]);
+    const double amp = (double)ainv * e * (double)(f > 0 ? K.omrel[f] : 1.f);
+    const double as = amp * (double)s, ab = amp * (double)K.b;
+    acc64[0] += -as * (double)sn - ab * (double)cs;
+    acc64[1] += as * (double)cs - ab * (double)sn;
+}
 // One frequency of a pair's contribution (the several-frequency tail): gq = q^2/m2,
 // ainv = A/m2 shared across frequencies.
 __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float s, float gq,
                                           float ainv, float base, float2 &acc, unsigned &ev,
-                                          int shift, bool live) {
+                                          int shift, bool live, double *acc64) {
     const float turns = fmaf(gq * s, K.hk2pi[f], base);
     const float ph = turns * 6.283185307179586f;
     const float sn = sin_approx(ph), cs = cos_approx(ph);
     const float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]) * K.omrel[f];
     const float as = amp * s, ab = amp * K.b;
-    if (live) {  // i * amp * (s + i b) * (cos + i sin)
+    if (live && amp < K.tiny) {
+        tiny_contribution(K, f, s, gq, ainv, sn, cs, acc64);
+        ev += 1u << shift;
+    } else if (live) {  // i * amp * (s + i b) * (cos + i sin)
         float2 v = acc;
         v.x = fmaf(-as, sn, fmaf(-ab, cs, v.x));
         v.y = fmaf(as, cs, fmaf(-ab, sn, v.y));
@@ -205,7 +226,7 @@ template <int NF>
 __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
                                           float m2, float A, const float *base,
                                           float (&pre)[NF], float (&pim)[NF], unsigned &ev,
-                                          int shift, bool live) {
+                                          int shift, bool live, double *acc64) {
     const float inv = rcp_approx(m2);
     const float gq = q2 * inv;
     const float ainv = A * inv;
@@ -223,7 +244,10 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
         float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]);
         if (f > 0) amp *= K.omrel[f];
         const float as = amp * s, ab = amp * K.b;
-        if (lf) {  // i * amp * (s + i b) * (cos + i sin)
+        if (lf && amp < K.tiny) {
+            tiny_contribution(K, f, s, gq, ainv, sn, cs, acc64);
+            ev += 1u << shift;
+        } else if (lf) {  // i * amp * (s + i b) * (cos + i sin)
             pre[f] = fmaf(-as, sn, fmaf(-ab, cs, pre[f]));
             pim[f] = fmaf(as, cs, fmaf(-ab, sn, pim[f]));
             ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
@@ -1052,7 +1076,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     for (int j = g; j < g + EVG; ++j)
                         eval_pair<1>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], Aj[j], bj[j],
                                      pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
-                                     EVG == 1 || ((lvm >> j) & 1u));
+                                     EVG == 1 || ((lvm >> j) & 1u), S.acc[R * lane + j][0]);
                 }
             } else {
             // several frequencies: the cutoff grows with omega, so each frequency is
@@ -1085,7 +1109,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         eval_freq(K, f, sj[j], gq[j], ainv[j],
                                   WIDE ? (float)frac_turns(K.kappa64[f] * s64[j])
                                        : phase_of<NF, MF>(S, K, f, pref[j], bj[j][0]),
-                                  S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                                  S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u,
+                                  reinterpret_cast<double *>(
+                                      w.part + (q * w.n_pad + sb + j) * NF + f));
                 }
             }
             }
@@ -1199,18 +1225,35 @@ __global__ void rows_pack_kernel(const GbsArgs a, double amp_scale, const int64_
     amp[dst] = (float)(amp_scale * a.seg_refl[row] * a.weights[b]);
 }
 
-// start[b + 1] = n_segs[b] clamped to [0, max_seg] (the scan input; start[0] = 0).
+// start[b + 1] = n_segs[b] clamped to [0, max_seg] (the scan input; start[0] = base).
 __global__ void rows_count_kernel(const int32_t *n_segs, int64_t n_beams, int64_t max_seg,
-                                  int64_t *cnt) {
+                                  int64_t base, int64_t *cnt) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b > n_beams) return;
     if (b == n_beams) {
-        cnt[0] = 0;
+        cnt[0] = base;
         return;
     }
     int64_t n = n_segs[b];
     n = n < 0 ? 0 : (n > max_seg ? max_seg : n);
     cnt[b + 1] = n;
+}
+
+// Beams [b0, b0 + nb) of resident compact rows -> a group's own rows starting at 0:
+// start rebased, rows copied (thread i: start entry i <= nb and row i < nb * max_seg).
+__global__ void rows_slice_kernel(const Rows src, int64_t b0, int64_t nb, int64_t *start,
+                                  double4 *p0, double4 *p1, float *amp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t base = src.start[b0];
+    if (i <= nb) start[i] = src.start[b0 + i] - base;
+    if (i < nb * src.max_seg) {
+        const int64_t row = base + i;
+        if (row < src.start[b0 + nb]) {
+            p0[i] = src.p0[row];
+            p1[i] = src.p1[row];
+            amp[i] = src.amp[row];
+        }
+    }
 }
 
 // Phase anchors of every compact row, per frequency: frac(omega/(2 pi c) s) at s0 and
@@ -1442,8 +1485,10 @@ Fp32Consts make_consts(const GbsArgs &a) {
         K.omrel[f] = f < a.nf ? (float)(w / a.omegas[0]) : 0.f;
         K.cutk[f] = a.use_cutoff ? (float)(w * a.width_b / (72.0 * a.c)) : 0.f;  // 0: never cut
         K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
-        K.nhkbl2e[f] = (float)(-(w * 0.5 / a.c) * a.width_b * 1.4426950408889634);
+        K.nhkbl2e64[f] = -(w * 0.5 / a.c) * a.width_b * 1.4426950408889634;
+        K.nhkbl2e[f] = (float)K.nhkbl2e64[f];
     }
+    K.tiny = a.use_cutoff ? 0.f : 0x1p-100f;
     K.ascending = 1;
     for (int f = 1; f < a.nf; ++f)
         if (!(K.cutk[f] >= K.cutk[f - 1])) K.ascending = 0;
@@ -1475,10 +1520,20 @@ int64_t gbs_fp32_range_beams(int64_t n_beams, int nf) {
     return rb < 32 ? 32 : rb;
 }
 
-int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t *cnt,
-                      cudaStream_t st) {
+int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t base,
+                      int64_t *cnt, cudaStream_t st) {
     rows_count_kernel<<<(unsigned)((n_beams + 1 + 255) / 256), 256, 0, st>>>(n_segs, n_beams,
-                                                                             max_seg, cnt);
+                                                                             max_seg, base, cnt);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
+int launch_rows_slice(const Rows &src, int64_t b0, int64_t nb, int64_t *start, double4 *p0,
+                      double4 *p1, float *amp, cudaStream_t st) {
+    const int64_t n = std::max<int64_t>(nb + 1, nb * src.max_seg);
+    rows_slice_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, b0, nb, start, p0, p1,
+                                                                   amp);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

@@ -1,5 +1,7 @@
 // probe.cu -- pipe-throughput microbenchmarks for the roofline denominators.
-// FP32: 8 independent FFMA chains per thread; MUFU: 8 independent ex2 chains.
+// FP32: 8 independent FFMA chains per thread, and 8 independent packed FFMA2 (f32x2)
+// chains (sm_100: same FLOP rate, half the issue slots; the faster is the peak);
+// MUFU: 8 independent ex2 chains.
 #include "common.cuh"
 
 namespace bf {
@@ -18,6 +20,32 @@ __global__ void __launch_bounds__(256) ffma_probe(float *out, int iters, float a
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678f) out[0] = s;
+}
+
+__global__ void __launch_bounds__(256) ffma2_probe(float *out, int iters, float a0, float b0) {
+    unsigned long long x[8], a, b;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(a) : "f"(a0));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(b0));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float u = threadIdx.x * 1e-3f + i, v = u + 0.5f;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(x[i]) : "f"(u), "f"(v));
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[i]) : "l"(a), "l"(b));
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        float u, v;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(u), "=f"(v) : "l"(x[i]));
+        s += u + v;
+    }
     if (s == 12345.678f) out[0] = s;
 }
 
@@ -52,7 +80,7 @@ extern "C" int bf_probe_peaks(int device, double *fp32_tflops, double *mufu_tops
     cudaEventCreate(&e1);
     const int blocks = p.multiProcessorCount * 8, threads = 256;
     const int fi = 4096, mi = 512;
-    float best_f = 1e30f, best_m = 1e30f;
+    float best_f = 1e30f, best_m = 1e30f, best_f2 = 1e30f;
     for (int rep = 0; rep < 4; ++rep) {
         float ms;
         cudaEventRecord(e0);
@@ -67,15 +95,23 @@ extern "C" int bf_probe_peaks(int device, double *fp32_tflops, double *mufu_tops
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         if (rep) best_m = ms < best_m ? ms : best_m;
+        cudaEventRecord(e0);
+        ffma2_probe<<<blocks, threads>>>(out, fi, 0.999f, 1e-3f);  // 2 x 8 x 8 FMA per iteration
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep) best_f2 = ms < best_f2 ? ms : best_f2;
     }
-    note_launch(8);
+    note_launch(12);
     cudaError_t err = cudaGetLastError();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(out);
     BF_TRY_CUDA(err);
     const double n = (double)blocks * threads * 16 * 8;
-    *fp32_tflops = 2.0 * n * fi / (best_f * 1e-3) / 1e12;
+    const double ffma = 2.0 * n * fi / (best_f * 1e-3) / 1e12;
+    const double ffma2 = 2.0 * (double)blocks * threads * 128 * fi / (best_f2 * 1e-3) / 1e12;
+    *fp32_tflops = ffma > ffma2 ? ffma : ffma2;
     *mufu_tops = n * mi / (best_m * 1e-3) / 1e12;
     return BF_OK;
 }

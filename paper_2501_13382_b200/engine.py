@@ -8,7 +8,10 @@ trace -> sum loop, parallel.py:297-338, moved onto the B200):
   (the reference PathBundle layout, beamtrace.py:274-288);
 * :class:`DeviceBundle` -- a device PathBundle (torch tensors) + upload from a
   host PathBundle (pinned, async);
-* :func:`accumulate` -- ``bf_gbs_accumulate_dev`` on device buffers.
+* :func:`accumulate` -- ``bf_gbs_accumulate_dev`` on device buffers;
+* :class:`SegmentRows` -- compact segment rows resident in HBM (``bf_rows_*``):
+  traced chunks are appended (68 B per segment, no padding) and every ray is
+  summed in one call, independent of the chunk plan.
 
 Host-resident bundles larger than the device budget need no Python streaming:
 the host-buffer ABI (``bf_gbs_accumulate``) streams beam groups through pinned
@@ -211,3 +214,64 @@ def finalize(acc, calibration, stream=None):
                                          _vp(pressure), _vp(spl), acc.device.index or 0,
                                          _stream_ptr(stream, acc.device)))
     return pressure, spl
+
+
+class SegmentRows:
+    """Compact segment rows resident on one device (bf_rows_*, include/bf_gbs.h).
+
+    ``append`` packs the valid rows of a padded DeviceBundle (the reference PathBundle
+    layout) behind the rows appended so far; ``accumulate`` runs the fp32 summation over
+    all (or a range of) the appended beams -- the same bits as one
+    ``bf_gbs_accumulate_dev`` call over the concatenated bundle.
+    """
+
+    def __init__(self, device):
+        torch = _torch()
+        self.device = torch.device(device)
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.bf_rows_create(self.device.index or 0, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.check(self._lib.bf_rows_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+    @property
+    def n_beams(self) -> int:
+        nb, nr = ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check(self._lib.bf_rows_info(self._h, ctypes.byref(nb), ctypes.byref(nr)))
+        return nb.value
+
+    @property
+    def n_rows(self) -> int:
+        nb, nr = ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check(self._lib.bf_rows_info(self._h, ctypes.byref(nb), ctypes.byref(nr)))
+        return nr.value
+
+    def append(self, bundle: DeviceBundle, n_beams=None, stream=None):
+        n = bundle.n_paths if n_beams is None else int(n_beams)
+        _lib.check(self._lib.bf_rows_append_dev(
+            self._h, _vp(bundle.seg_origin), _vp(bundle.seg_dir), _vp(bundle.seg_len),
+            _vp(bundle.seg_s0), _vp(bundle.seg_refl), _vp(bundle.n_segs), _vp(bundle.weights),
+            n, int(bundle.max_seg), float(bundle.c), float(bundle.amplitude_phi),
+            _stream_ptr(stream, self.device)))
+
+    def accumulate(self, obs, omegas, width_b, use_cutoff, acc, evals, obs_lo=0, obs_hi=None,
+                   beam_lo=0, beam_hi=None, stream=None, presorted=False):
+        n_obs = obs.numel() // 3
+        obs_hi = n_obs if obs_hi is None else obs_hi
+        beam_hi = self.n_beams if beam_hi is None else beam_hi
+        om = np.ascontiguousarray(np.atleast_1d(omegas), dtype=np.float64)
+        _lib.check(self._lib.bf_gbs_accumulate_rows_dev(
+            self._h, _vp(obs), n_obs, ctypes.c_void_p(om.ctypes.data), om.shape[0],
+            float(width_b), int(bool(use_cutoff)), _vp(acc), _vp(evals), int(obs_lo),
+            int(obs_hi), int(beam_lo), int(beam_hi),
+            _lib.FLAG_OBS_PRESORTED if presorted else 0, _stream_ptr(stream, obs.device)))

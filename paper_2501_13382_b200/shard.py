@@ -95,7 +95,7 @@ def gather_field(acc, evals, order, rank: int, world_size: int, n_total: int, gr
 
     acc is (n_local, F) complex128, evals (n_local,) int64, both in the rank's
     tile order.  Returns (acc_full, evals_full) on rank 0, (None, None) elsewhere.
-    Works for NCCL (CUDA tensors, one all_gather_into_tensor) and gloo (CPU tensors).
+    Works for NCCL (CUDA tensors, one dist.gather to rank 0) and gloo (CPU tensors).
     `plan` (GatherPlan of the same order/world) is built on the fly if not given.
     """
     import torch
@@ -109,15 +109,15 @@ def gather_field(acc, evals, order, rank: int, world_size: int, n_total: int, gr
     n_loc = acc.shape[0]
     pay[:n_loc, :2 * F] = torch.view_as_real(acc).reshape(n_loc, 2 * F)
     pay[:n_loc, 2 * F] = evals.view(torch.float64)
-    if dist.get_backend(group) == "gloo":  # gloo gathers host tensors, as a list
-        bufs = [torch.empty_like(pay.cpu()) for _ in range(world_size)]
-        dist.all_gather(bufs, pay.cpu(), group=group)
-        allp = torch.cat(bufs).to(acc.device)
-    else:
-        allp = torch.empty((world_size * cap, 2 * F + 1), dtype=torch.float64, device=acc.device)
-        dist.all_gather_into_tensor(allp, pay, group=group)
+    # one gather to rank 0 (only rank 0 receives the field: W x fewer bytes than an
+    # all-gather); gloo gathers host tensors
+    host = dist.get_backend(group) == "gloo"
+    src = pay.cpu() if host else pay
+    bufs = [torch.empty_like(src) for _ in range(world_size)] if rank == 0 else None
+    dist.gather(src, gather_list=bufs, dst=0, group=group)
     if rank != 0:
         return None, None
+    allp = torch.cat(bufs).to(acc.device)
     dest = plan.dest.to(acc.device)
     out = torch.zeros((n_total + 1, 2 * F + 1), dtype=torch.float64, device=acc.device)
     out[dest] = allp  # padding rows land in the extra row n_total

@@ -3,8 +3,8 @@ C oracle (all calls go through the C ABI in libbf_gbs.so).
 
 Tolerances (BASELINE.json north_star):
   fp64 mode: relL2(acc) <= 1e-12, evals bit-exact, nearest-segment k/behind bit-exact;
-  fp32 mode: relL2(acc) <= 1e-4, max dTL <= 0.01 dB over receivers within 60 dB of the
-  field maximum (the all-receiver max is asserted <= 0.05 dB).
+  fp32 mode: relL2(acc) <= 1e-4, max dTL <= 0.01 dB over EVERY receiver whose reference
+  value is non-zero (and, reported beside it, over receivers within 60 dB of the maximum).
 """
 import numpy as np
 import pytest
@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 FP64_TOL = 1e-12
 FP32_L2 = 1e-4
 FP32_TL_DB = 0.01
-FP32_TL_ALL_DB = 0.05
+FP32_TL_ALL_DB = 0.01
 
 
 def run(b, precision, obs=None, calls=None):
