@@ -109,11 +109,10 @@ struct Fp32Consts {
     double kappa64[BF_MAXF];
     float omega[BF_MAXF];
     float omrel[BF_MAXF];    // omega_f / omega_0 (the staged amplitude carries omega_0)
-    float cutk[BF_MAXF];     // omega*b/(72 c): pair cut iff q^2*cutk > m2 (ex_re < -36); 0 without cutoff
+    float cutk[BF_MAXF];     // omega*b/(72 c): q^2*cutk > m2 iff ex_re < -36 (kernels.py:384)
     float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
     float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
     double nhkbl2e64[BF_MAXF];
-    float tiny;              // amplitudes below this are redone in fp64 (0 with the cutoff)
     float b, b2;             // width_b, width_b^2
     int ascending;           // omegas nondecreasing (cutk nondecreasing)
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
@@ -187,13 +186,23 @@ struct WarpSmem {
 // i omega/(2 pi c) w_b field.  `base[f]` is the fp64-anchored axial phase
 // omega s/(2 pi c) reduced to turns.
 //
-// Without the cutoff exp(-g b) can fall below the fp32 range (a receiver far off every
-// beam axis: the reference's fp64 sum is ~1e-40..1e-300 of the field maximum).  An
-// amplitude below K.tiny (2^-100; 0 with the cutoff, where exp(-g b) >= e^-36) is
-// recomputed in fp64 from the same fp32 s, q^2, m2 and phase and added straight into
-// the fp64 accumulator, so such receivers keep the reference's magnitude.
-__device__ __noinline__ void tiny_contribution(const Fp32Consts &K, int f, float s, float gq,
-                                               float ainv, float sn, float cs, double *acc64) {
+// Without the cutoff (kernels.py:384-385 skipped) exp(-g b) falls below the fp32 range
+// for pairs far off a beam's axis: a receiver with only such pairs has a reference value
+// ~1e-40..1e-300 of the field maximum.  The kernels for calls without the cutoff
+// (TINY = true) therefore sum every pair beyond the cutoff exponent (ex_re < -36) in
+// fp64 instead: tiny_contribution redoes the evaluation from the same fp32 s, q^2, m2,
+// amplitude factor and phase with the exponential and products in fp64, added straight
+// into the fp64 accumulator.  Pairs within the exponent range stay fp32 (their amplitude
+// is >= e^-36 times the amplitude factor).  Calls with the cutoff never reach this code
+// (TINY = false kernels do not contain it).
+__device__ __forceinline__ void tiny_contribution(const Fp32Consts &K, int f, float s, float q2,
+                                                  float m2, float A, float base, double *acc64) {
+    const float inv = rcp_approx(m2);
+    const float gq = q2 * inv;
+    const float ainv = A * inv;
+    const float turns = fmaf(gq * s, K.hk2pi[f], base);
+    const float ph = turns * 6.283185307179586f;
+    const float sn = sin_approx(ph), cs = cos_approx(ph);
     const double e = exp2((double)gq * K.nhkbl2e64[f]);
     const double amp = (double)ainv * e * (double)(f > 0 ? K.omrel[f] : 1.f);
     const double as = amp * (double)s, ab = amp * (double)K.b;
@@ -204,16 +213,13 @@ __device__ __noinline__ void tiny_contribution(const Fp32Consts &K, int f, float
 // ainv = A/m2 shared across frequencies.
 __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float s, float gq,
                                           float ainv, float base, float2 &acc, unsigned &ev,
-                                          int shift, bool live, double *acc64) {
+                                          int shift, bool live) {
     const float turns = fmaf(gq * s, K.hk2pi[f], base);
     const float ph = turns * 6.283185307179586f;
     const float sn = sin_approx(ph), cs = cos_approx(ph);
     const float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]) * K.omrel[f];
     const float as = amp * s, ab = amp * K.b;
-    if (live && amp < K.tiny) {
-        tiny_contribution(K, f, s, gq, ainv, sn, cs, acc64);
-        ev += 1u << shift;
-    } else if (live) {  // i * amp * (s + i b) * (cos + i sin)
+    if (live) {  // i * amp * (s + i b) * (cos + i sin)
         float2 v = acc;
         v.x = fmaf(-as, sn, fmaf(-ab, cs, v.x));
         v.y = fmaf(as, cs, fmaf(-ab, sn, v.y));
@@ -226,7 +232,7 @@ template <int NF>
 __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
                                           float m2, float A, const float *base,
                                           float (&pre)[NF], float (&pim)[NF], unsigned &ev,
-                                          int shift, bool live, double *acc64) {
+                                          int shift, bool live) {
     const float inv = rcp_approx(m2);
     const float gq = q2 * inv;
     const float ainv = A * inv;
@@ -244,10 +250,7 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
         float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]);
         if (f > 0) amp *= K.omrel[f];
         const float as = amp * s, ab = amp * K.b;
-        if (lf && amp < K.tiny) {
-            tiny_contribution(K, f, s, gq, ainv, sn, cs, acc64);
-            ev += 1u << shift;
-        } else if (lf) {  // i * amp * (s + i b) * (cos + i sin)
+        if (lf) {  // i * amp * (s + i b) * (cos + i sin)
             pre[f] = fmaf(-as, sn, fmaf(-ab, cs, pre[f]));
             pim[f] = fmaf(as, cs, fmaf(-ab, sn, pim[f]));
             ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
@@ -688,7 +691,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
 
 
 // One (patch, beam range) unit.
-template <int NF, bool WIDE, bool MF = (NF > 1 || WIDE)>
+template <int NF, bool WIDE, bool TINY, bool MF = (NF > 1 || WIDE)>
 __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, const Fp32Work &w,
                                          const Fp32Consts &K, WarpSmem<NF, MF> &S, int64_t p,
                                          int64_t q, int lane, GbsStats *stats) {
@@ -1062,10 +1065,14 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
             }
             float m2j[R];
+            unsigned tiny = 0;  // (TINY) receivers beyond the cutoff exponent: fp64
 #pragma unroll
             for (int j = 0; j < R; ++j) {
                 m2j[j] = fmaf(sj[j], sj[j], K.b2);
-                if (!MF && q2j[j] * K.cutk[0] > m2j[j]) lvm &= ~(1u << j);  // cutk 0: no cutoff
+                if (!MF && q2j[j] * K.cutk[0] > m2j[j]) {  // ex_re < -36 (kernels.py:384)
+                    if (TINY && ((lvm >> j) & 1u)) tiny |= 1u << j;  // no cutoff: fp64 below
+                    lvm &= ~(1u << j);
+                }
             }
             if constexpr (!MF) {
             // receivers evaluated in groups of EVG (one branch, EVG independent chains)
@@ -1076,8 +1083,21 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     for (int j = g; j < g + EVG; ++j)
                         eval_pair<1>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], Aj[j], bj[j],
                                      pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
-                                     EVG == 1 || ((lvm >> j) & 1u), S.acc[R * lane + j][0]);
+                                     EVG == 1 || ((lvm >> j) & 1u));
                 }
+            if constexpr (TINY) {
+                if (tiny) {
+#pragma unroll 1
+                    for (int j = 0; j < R; ++j)
+                        if ((tiny >> j) & 1u) {
+                            tiny_contribution(K, 0, pick4(sj, j), pick4(q2j, j), pick4(m2j, j),
+                                              pick4(Aj, j), j == 0 ? bj[0][0] : j == 1 ? bj[1][0]
+                                                            : j == 2 ? bj[2][0] : bj[3][0],
+                                              S.acc[R * lane + j][0]);
+                            evp[j >> 1] += 1u << (16 * (j & 1));
+                        }
+                }
+            }
             } else {
             // several frequencies: the cutoff grows with omega, so each frequency is
             // evaluated only if some receiver of the warp is live for it
@@ -1092,26 +1112,44 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             // in shared memory (no per-frequency registers)
 #pragma unroll 1
             for (int f = 0; f < NF; ++f) {
-                unsigned lf = 0;
+                unsigned lf = 0, tf = 0;  // fp32 / (TINY) fp64 receivers of frequency f
 #pragma unroll
                 for (int j = 0; j < R; ++j)
-                    if (((lvm >> j) & 1u) && !(q2j[j] * K.cutk[f] > m2j[j]))
-                        lf |= 1u << j;  // ex_re < -36 (kernels.py:384)
-                if (!__any_sync(0xffffffffu, lf != 0)) {
+                    if ((lvm >> j) & 1u) {
+                        if (!(q2j[j] * K.cutk[f] > m2j[j]))
+                            lf |= 1u << j;  // ex_re >= -36 (kernels.py:384)
+                        else if (TINY)
+                            tf |= 1u << j;
+                    }
+                if (!__any_sync(0xffffffffu, (lf | tf) != 0)) {
                     // ascending frequencies: the cut radius shrinks with omega, so every
                     // later frequency is cut for the whole warp as well
                     if (K.ascending) break;
                     continue;
                 }
                 {
+                    unsigned tiny = 0;
 #pragma unroll
                     for (int j = 0; j < R; ++j)
                         eval_freq(K, f, sj[j], gq[j], ainv[j],
                                   WIDE ? (float)frac_turns(K.kappa64[f] * s64[j])
                                        : phase_of<NF, MF>(S, K, f, pref[j], bj[j][0]),
-                                  S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u,
-                                  reinterpret_cast<double *>(
-                                      w.part + (q * w.n_pad + sb + j) * NF + f));
+                                  S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                    if (TINY && tf) {
+#pragma unroll 1
+                        for (int j = 0; j < R; ++j)
+                            if ((tf >> j) & 1u) {
+                                evp[j >> 1] += 1u << (16 * (j & 1));
+                                tiny_contribution(
+                                    K, f, pick4(sj, j), pick4(q2j, j), pick4(m2j, j), pick4(Aj, j),
+                                    WIDE ? (float)frac_turns(K.kappa64[f] * s64[j])
+                                         : phase_of<NF, MF>(S, K, f, pick4(pref, j),
+                                                            j == 0 ? bj[0][0] : j == 1 ? bj[1][0]
+                                                            : j == 2 ? bj[2][0] : bj[3][0]),
+                                    reinterpret_cast<double *>(
+                                        w.part + (q * w.n_pad + sb + j) * NF + f));
+                            }
+                    }
                 }
             }
             }
@@ -1169,7 +1207,7 @@ __device__ __forceinline__ bool wide_patch(const Fp32Work &w, int64_t p) {
 
 // One launch per patch class, on two streams: WIDE = false takes queue positions
 // [0, n_units - n_wide), WIDE = true the rest (unit_keys_kernel sorts wide patches last).
-template <int NF, bool WIDE>
+template <int NF, bool WIDE, bool TINY>
 __global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5 ? 3 : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w, const Fp32Consts K,
                     GbsStats *stats) {
@@ -1191,7 +1229,7 @@ __global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5
         const unsigned id = (unsigned)w.unit_order[u];  // longest-first, see unit_keys_kernel
         const unsigned q = id / n_patches;
         const unsigned p = id - q * n_patches;
-        run_unit<NF, WIDE>(a, tl, w, K, S, p, q, lane, stats);
+        run_unit<NF, WIDE, TINY>(a, tl, w, K, S, p, q, lane, stats);
     }
     // per-lane counters straight into the device statistics
     __syncwarp();
@@ -1406,7 +1444,7 @@ __global__ void wl_compact_kernel(const Tiling tl, const Fp32Work w) {
     }
 }
 
-template <int NF, bool WIDE>
+template <int NF, bool WIDE, bool TINY>
 int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
                  GbsStats *stats, cudaStream_t st) {
     constexpr bool MF = NF > 1 || WIDE;
@@ -1419,12 +1457,12 @@ int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp3
     BF_TRY_CUDA(cudaGetDevice(&dev));
     if (dev >= MAXDEV) return fail(BF_ENODEV, "device index %d >= %d", dev, MAXDEV);
     if (grid_cache[dev] == 0) {
-        BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF, WIDE>,
+        BF_TRY_CUDA(cudaFuncSetAttribute(gbs_fp32_kernel<NF, WIDE, TINY>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int sms = 0, per_sm = 0;
         BF_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, gbs_fp32_kernel<NF, WIDE>, THREADS, smem));
+            &per_sm, gbs_fp32_kernel<NF, WIDE, TINY>, THREADS, smem));
         if (per_sm < 1)
             return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
         if (getenv("BF_DEBUG_STATS"))
@@ -1436,7 +1474,7 @@ int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp3
     int64_t grid = grid_cache[dev];
     const int64_t need = (units + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
-    gbs_fp32_kernel<NF, WIDE><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
+    gbs_fp32_kernel<NF, WIDE, TINY><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
@@ -1457,8 +1495,13 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
 #endif
     BF_TRY_CUDA(cudaEventRecord(sp.fork, sp.st));
     BF_TRY_CUDA(cudaStreamWaitEvent(sp.aux, sp.fork, 0));
-    BF_TRY((launch_class<NF, true>(a, t, w, K, stats, sp.aux)));
-    BF_TRY((launch_class<NF, false>(a, t, w, K, stats, sp.st)));
+    if (a.use_cutoff) {
+        BF_TRY((launch_class<NF, true, false>(a, t, w, K, stats, sp.aux)));
+        BF_TRY((launch_class<NF, false, false>(a, t, w, K, stats, sp.st)));
+    } else {  // kernels with the fp64 path for pairs beyond the cutoff exponent
+        BF_TRY((launch_class<NF, true, true>(a, t, w, K, stats, sp.aux)));
+        BF_TRY((launch_class<NF, false, true>(a, t, w, K, stats, sp.st)));
+    }
     BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
     BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
 #if BF_HIST
@@ -1483,12 +1526,11 @@ Fp32Consts make_consts(const GbsArgs &a) {
         K.kappa[f] = (float)K.kappa64[f];
         K.omega[f] = (float)w;
         K.omrel[f] = f < a.nf ? (float)(w / a.omegas[0]) : 0.f;
-        K.cutk[f] = a.use_cutoff ? (float)(w * a.width_b / (72.0 * a.c)) : 0.f;  // 0: never cut
+        K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
         K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
         K.nhkbl2e64[f] = -(w * 0.5 / a.c) * a.width_b * 1.4426950408889634;
         K.nhkbl2e[f] = (float)K.nhkbl2e64[f];
     }
-    K.tiny = a.use_cutoff ? 0.f : 0x1p-100f;
     K.ascending = 1;
     for (int f = 1; f < a.nf; ++f)
         if (!(K.cutk[f] >= K.cutk[f - 1])) K.ascending = 0;

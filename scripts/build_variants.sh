@@ -10,6 +10,6 @@ for v in "$@"; do
   name=$(echo "$v" | tr ' =' '_-' | tr -d 'D')
   mkdir -p build/var_$name
   /usr/local/cuda/bin/nvcc $FL $v -c gbs_fp32.cu -o build/var_$name/gbs_fp32.o -Xptxas -v 2> build/var_$name/ptxas.txt
-  /usr/local/cuda/bin/nvcc $ARCH -shared -o ../_lib/variants/libbf_gbs_$name.so build/engine.o build/var_$name/gbs_fp32.o build/exact_fp64.o build/probe.o build/writers.o -Xlinker -lpthread
+  /usr/local/cuda/bin/nvcc $ARCH -shared -o ../_lib/variants/libbf_gbs_$name.so build/engine.o build/var_$name/gbs_fp32.o build/exact_fp64.o build/probe.o build/writers.o build/hostpool.o -Xlinker -lpthread
   echo "$name $(grep -A2 ILi1E build/var_$name/ptxas.txt | grep -oE 'Used [0-9]+ registers|[0-9]+ bytes spill stores' | tr '\n' ' ')"
 done
