@@ -148,6 +148,35 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 }
 __device__ __forceinline__ double frac_turns(double x) { return x - rint(x); }
 
+// Packed fp32 pairs (receivers 2h, 2h+1 of a lane): FFMA2 / FMUL2 / FADD2 do the two
+// receivers' operations in one issue slot (sm_100), each with the rounding of the scalar
+// instruction; a scalar operand is broadcast (.F32 operand, no extra moves).
+#ifndef BF_PACKED_EVAL
+#define BF_PACKED_EVAL 0  // packed pairs in the evaluation tail (measured: no gain)
+#endif
+#ifndef BF_PACKED_GEOM
+#define BF_PACKED_GEOM 0  // packed pairs in the nearest-point geometry (no gain)
+#endif
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+template <bool P>
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    if constexpr (P) return __ffma2_rn(a, b, c);
+    return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+template <bool P>
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    if constexpr (P) return __fmul2_rn(a, b);
+    return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+template <bool P>
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    if constexpr (P) return __fadd2_rn(a, b);
+    return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+constexpr bool PE = BF_PACKED_EVAL, PG = BF_PACKED_GEOM;
+__device__ __forceinline__ float2 pair(const float (&v)[4], int h) { return make_float2(v[h], v[h + 1]); }
+
 
 constexpr unsigned BEHIND_CHECK = 0x80000000u;
 constexpr unsigned WEDGE = 0x40000000u;
@@ -256,6 +285,32 @@ __device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, f
             ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
         }
     }
+}
+
+// eval_pair<1> for receivers 2h, 2h+1 as packed pairs (same operations and rounding);
+// a receiver that is not live keeps its sums (selected, so its inputs may be anything).
+__device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2 q2, float2 m2,
+                                           float2 A, float2 base, float2 &pre, float2 &pim,
+                                           unsigned &ev, bool l0, bool l1) {
+    const float2 inv = make_float2(rcp_approx(m2.x), rcp_approx(m2.y));
+    const float2 gq = mul2<PE>(q2, inv);
+    const float2 ainv = mul2<PE>(A, inv);
+    const float2 gqs = mul2<PE>(gq, s);
+    const float2 turns = fma2<PE>(gqs, bc2(K.hk2pi[0]), base);
+    const float2 ph = mul2<PE>(turns, bc2(6.283185307179586f));
+    const float2 sn = make_float2(sin_approx(ph.x), sin_approx(ph.y));
+    const float2 cs = make_float2(cos_approx(ph.x), cos_approx(ph.y));
+    const float2 ex = mul2<PE>(gq, bc2(K.nhkbl2e[0]));
+    const float2 amp = mul2<PE>(ainv, make_float2(ex2_approx(ex.x), ex2_approx(ex.y)));
+    const float2 as = mul2<PE>(amp, s), ab = mul2<PE>(amp, bc2(K.b));
+    // i * amp * (s + i b) * (cos + i sin)
+    const float2 npre = fma2<PE>(neg2(as), sn, fma2<PE>(neg2(ab), cs, pre));
+    const float2 npim = fma2<PE>(as, cs, fma2<PE>(neg2(ab), sn, pim));
+    pre.x = l0 ? npre.x : pre.x;
+    pim.x = l0 ? npim.x : pim.x;
+    pre.y = l1 ? npre.y : pre.y;
+    pim.y = l1 ? npim.y : pim.y;
+    ev += (l0 ? 1u : 0u) + (l1 ? 0x10000u : 0u);  // evaluation counts (kernels.py:399)
 }
 
 // Phase anchor of the nearest point: interior -> centre anchor + kappa (r.d);
@@ -728,12 +783,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     }
     // fp32 partial sums of the chunk: registers with one frequency, shared memory
     // (S.facc) with several
-    float pre[R][1], pim[R][1];
+    float2 pre2[R / 2], pim2[R / 2];  // (one frequency) receivers 2h, 2h+1
     unsigned evp[R / 2] = {};  // evaluation counts of receivers 2i, 2i+1 (16-bit fields)
     unsigned ties = 0, nbp = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-        pre[j][0] = pim[j][0] = 0.f;
+        if (!(j & 1)) pre2[j >> 1] = pim2[j >> 1] = make_float2(0.f, 0.f);
         if constexpr (MF) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
@@ -883,21 +938,36 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if constexpr (!MF) an[0] = S.anc[0][row];
                 float pj[R];
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                    const float proj = dl + g1.w;
-                    pj[j] = proj;
-                    Aj[j] = ax.y;
-                    if constexpr (!MF) {
-                        bj[j][0] = anchor_phase(K.kappa[0], proj, dl, g0.w, an[0]);
-                    } else {
-                        bj[j][0] = dl;
-                        pref[j] = phase_ref(row, proj, g0.w);
+                for (int h = 0; h < R; h += 2) {  // receivers h, h+1 as packed pairs
+                    const float2 X = pair(rx, h), Y = pair(ry, h), Z = pair(rz, h);
+                    const float2 dl = fma2<PG>(X, bc2(g1.x), fma2<PG>(Y, bc2(g1.y), mul2<PG>(Z, bc2(g1.z))));
+                    const float2 proj = add2<PG>(dl, bc2(g1.w));
+                    const float2 qq = fma2<PG>(neg2(dl), dl,
+                                           fma2<PG>(bc2(g2.x), X, fma2<PG>(bc2(g2.y), Y,
+                                                fma2<PG>(bc2(g2.z), Z, add2<PG>(bc2(g2.w), pair(rr, h))))));
+                    const float2 t = make_float2(fminf(fmaxf(proj.x, 0.f), g0.w),
+                                                 fminf(fmaxf(proj.y, 0.f), g0.w));
+                    const float2 sv = add2<PG>(bc2(ax.x), t);
+                    float2 bf;
+                    if constexpr (!MF) bf = fma2<PG>(bc2(K.kappa[0]), dl, bc2(an[0].x));
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int j = h + u;
+                        const float pr = u ? proj.y : proj.x;
+                        pj[j] = pr;
+                        Aj[j] = ax.y;
+                        if constexpr (!MF) {  // anchor_phase with the packed centre term
+                            float b = u ? bf.y : bf.x;
+                            b = pr >= g0.w ? an[0].z : b;
+                            b = pr <= 0.f ? an[0].y : b;
+                            bj[j][0] = b;
+                        } else {
+                            bj[j][0] = u ? dl.y : dl.x;
+                            pref[j] = phase_ref(row, pr, g0.w);
+                        }
+                        sj[j] = u ? sv.y : sv.x;
+                        q2j[j] = fmaxf(u ? qq.y : qq.x, 0.f);
                     }
-                    sj[j] = ax.x + fminf(fmaxf(proj, 0.f), g0.w);
-                    q2j[j] = fmaxf(
-                        fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
-                        0.f);
                 }
                 lvm = (1u << R) - 1;
                 if (bword & BEHIND_CHECK)
@@ -935,15 +1005,25 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g0 = S.geo0[r0 + k];
                     const float4 g1 = S.geo1[r0 + k];
 #pragma unroll
-                    for (int j = 0; j < R; ++j) {
-                        const float wx = rx[j] + g0.x, wy = ry[j] + g0.y, wz = rz[j] + g0.z;
-                        const float proj = wx * g1.x + wy * g1.y + wz * g1.z;
-                        const float t = fminf(fmaxf(proj, 0.f), g0.w);
-                        const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
-                        const float d2 = vx * vx + vy * vy + vz * vz;
-                        second[j] = fminf(second[j], fmaxf(best[j], d2));
-                        kb[j] = d2 < best[j] ? k : kb[j];
-                        best[j] = fminf(best[j], d2);
+                    for (int h = 0; h < R; h += 2) {  // receivers h, h+1 as packed pairs
+                        const float2 wx = add2<PG>(pair(rx, h), bc2(g0.x));
+                        const float2 wy = add2<PG>(pair(ry, h), bc2(g0.y));
+                        const float2 wz = add2<PG>(pair(rz, h), bc2(g0.z));
+                        const float2 proj =
+                            fma2<PG>(wz, bc2(g1.z), fma2<PG>(wy, bc2(g1.y), mul2<PG>(wx, bc2(g1.x))));
+                        const float2 nt = make_float2(-fminf(fmaxf(proj.x, 0.f), g0.w),
+                                                      -fminf(fmaxf(proj.y, 0.f), g0.w));
+                        const float2 vx = fma2<PG>(nt, bc2(g1.x), wx), vy = fma2<PG>(nt, bc2(g1.y), wy),
+                                     vz = fma2<PG>(nt, bc2(g1.z), wz);
+                        const float2 d2p = fma2<PG>(vz, vz, fma2<PG>(vy, vy, mul2<PG>(vx, vx)));
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int j = h + u;
+                            const float d2 = u ? d2p.y : d2p.x;
+                            second[j] = fminf(second[j], fmaxf(best[j], d2));
+                            kb[j] = d2 < best[j] ? k : kb[j];
+                            best[j] = fminf(best[j], d2);
+                        }
                     }
                 }
                 // two adjacent candidates: ties at the junction go to the wedge decision
@@ -1067,23 +1147,30 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             float m2j[R];
             unsigned tiny = 0;  // (TINY) receivers beyond the cutoff exponent: fp64
 #pragma unroll
+            for (int h = 0; h < R; h += 2) {
+                const float2 m2p = fma2<PG>(pair(sj, h), pair(sj, h), bc2(K.b2));
+                m2j[h] = m2p.x;
+                m2j[h + 1] = m2p.y;
+            }
+#pragma unroll
             for (int j = 0; j < R; ++j) {
-                m2j[j] = fmaf(sj[j], sj[j], K.b2);
                 if (!MF && q2j[j] * K.cutk[0] > m2j[j]) {  // ex_re < -36 (kernels.py:384)
                     if (TINY && ((lvm >> j) & 1u)) tiny |= 1u << j;  // no cutoff: fp64 below
                     lvm &= ~(1u << j);
                 }
             }
             if constexpr (!MF) {
-            // receivers evaluated in groups of EVG (one branch, EVG independent chains)
+            // receivers evaluated in groups of EVG (one branch, EVG independent chains),
+            // as packed pairs
 #pragma unroll
             for (int g = 0; g < R; g += EVG)
                 if (lvm & (((1u << EVG) - 1u) << g)) {
 #pragma unroll
-                    for (int j = g; j < g + EVG; ++j)
-                        eval_pair<1>(K, a.use_cutoff, sj[j], q2j[j], m2j[j], Aj[j], bj[j],
-                                     pre[j], pim[j], evp[j >> 1], 16 * (j & 1),
-                                     EVG == 1 || ((lvm >> j) & 1u));
+                    for (int h = g; h < g + EVG; h += 2)
+                        eval_pair2(K, pair(sj, h), pair(q2j, h), pair(m2j, h), pair(Aj, h),
+                                   make_float2(bj[h][0], bj[h + 1][0]), pre2[h >> 1],
+                                   pim2[h >> 1], evp[h >> 1], (lvm >> h) & 1u,
+                                   (lvm >> (h + 1)) & 1u);
                 }
             if constexpr (TINY) {
                 if (tiny) {
@@ -1160,8 +1247,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             if (!MF) {
-                S.acc[R * lane + j][0][0] += (double)pre[j][0];
-                S.acc[R * lane + j][0][1] += (double)pim[j][0];
+                S.acc[R * lane + j][0][0] += (double)((j & 1) ? pre2[j >> 1].y : pre2[j >> 1].x);
+                S.acc[R * lane + j][0][1] += (double)((j & 1) ? pim2[j >> 1].y : pim2[j >> 1].x);
             } else if (flush64) {
                 if (j < nvalid) {
                     double2 *pp = w.part + (q * w.n_pad + sb + j) * NF;
@@ -1175,7 +1262,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
                 for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
             }
-            pre[j][0] = pim[j][0] = 0.f;
+            if (j & 1) pre2[j >> 1] = pim2[j >> 1] = make_float2(0.f, 0.f);  // pair flushed
         }
 #pragma unroll
         for (int j = 0; j < R; ++j) S.evc[R * lane + j] += (evp[j >> 1] >> (16 * (j & 1))) & 0xffffu;
