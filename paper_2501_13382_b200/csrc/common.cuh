@@ -104,7 +104,6 @@ struct Fp32Work {
     const double4 *p0;        // per row: origin xyz, len
     const double4 *p1;        // per row: direction xyz, s0
     const float *amp;         // per row: amplitude factor A
-    const float *pa;          // per row and frequency: phase anchors at s0, s0+len (turns)
     float4 *prl;              // sorted receiver -> patch-local fp32 coordinates, |r|^2
     double4 *pcen;            // per patch: centre xyz, radius
     float4 *pbox;             // per patch: bounding-box half extents xyz, radius (patch-local)
@@ -143,10 +142,6 @@ int launch_rows_count(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, i
 // Beams [b0, b0 + nb) of resident rows src -> rows of their own (start rebased to 0).
 int launch_rows_slice(const Rows &src, int64_t b0, int64_t nb, int64_t *start, double4 *p0,
                       double4 *p1, float *amp, cudaStream_t st);
-// fp64-exact phase anchors of the compact rows [0, rows_bound) (rows past
-// start[n_beams] are skipped): pa[row * nf + f] = frac(kappa_f s0), frac(kappa_f (s0+len)).
-int launch_fp32_anchors(const GbsArgs &a, const Rows &r, int64_t rows_bound, float *pa,
-                        cudaStream_t st);
 // Patch-local receivers of the tiling (w.prl, w.pcen, w.pbox).
 int launch_fp32_patches(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st);
 // Work-list compaction (north star: prefix-sum compaction into (beam, tile) lists):

@@ -10,7 +10,7 @@
 //
 //   per group (a slot of device buffers, its own stream):  compact rows (packed on the
 //   device from the padded bundle, or packed on host threads into pinned staging and
-//   copied) -> phase anchors -> tile work list -> scan -> unit queue order ->
+//   copied) -> tile work list -> scan -> unit queue order ->
 //   compaction -> summation kernels;  then, on the call's stream, in group order:
 //   fold of the group's range partials into acc.
 //
@@ -111,7 +111,7 @@ enum BufId {
 
 // Per-slot device workspaces of one beam group.
 enum SlotBufId {
-    S_START, S_P0, S_P1, S_AMP, S_PA, S_WLBITS, S_WLTIGHT, S_WLCNT, S_WLOFF, S_WLITEMS,
+    S_START, S_P0, S_P1, S_AMP, S_WLBITS, S_WLTIGHT, S_WLCNT, S_WLOFF, S_WLITEMS,
     S_UKEYS, S_UKEYS2, S_UVALS, S_UVALS2, S_PART, S_PARTEV, S_UCTR, S_CUB, S_F64, S_COUNT
 };
 // Per-slot pinned staging (host-buffer ABI).
@@ -884,15 +884,12 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
                 BF_TRY(rows_from_device(gg, s, &rv));
                 rows_bound = gg.n_beams * gg.max_seg;
             }
+            (void)rows_bound;
             Fp32Work w = wf;
             w.start = rv.start;
             w.p0 = rv.p0;
             w.p1 = rv.p1;
             w.amp = rv.amp;
-            float *pa;
-            BF_TRY(s.get(S_PA, (size_t)(2 * std::max<int64_t>(rows_bound, 1) * ag.nf), &pa));
-            BF_TRY(launch_fp32_anchors(gg, rv, rows_bound, pa, s.ss));
-            w.pa = pa;
             w.range_beams = rb;
             w.n_ranges = grp.second - grp.first;
             // ---- tight work list of the group: bitmasks + counts per (tile, range)

@@ -11,7 +11,8 @@
 //    represents ~100 m absolute coordinates.
 //  * pack_kernel converts the reference's padded fp64 bundle once per call into
 //    a row SoA: origin/len and direction/s0 in fp64, the amplitude factor and
-//    cutoff radius in fp32, and fp64-exact phase anchors (turns) at both ends.
+//    cutoff radius in fp32, and fp64-exact phase anchors (radians, reduced in fp64) at
+//    both ends.
 //  * The kernel is PERSISTENT: every warp is an independent worker that pulls
 //    (patch, beam range) units from an atomic queue, longest units first in
 //    half-octave buckets and range-major inside a bucket (concurrent warps share
@@ -44,8 +45,7 @@
 
 // Compile-time switches (tuning and diagnostics; the defaults are the product):
 //   BF_ROWCAP rows per staged chunk, BF_MINB CTAs/SM for NF = 1, BF_RANGES beam ranges per
-//   call, BF_EVG receivers per evaluation branch, BF_WARPS warps per CTA, BF_NORED (no
-//   explicit turn reduction before MUFU sin/cos), BF_FLUSHN (chunks per fp64 flush with
+//   call, BF_EVG receivers per evaluation branch, BF_WARPS warps per CTA, BF_FLUSHN (chunks per fp64 flush with
 //   several frequencies), BF_NOPF (no junction-row prefetch); BF_ABL skips work for
 //   ablation timings (results invalid), BF_HIST prints debug counters.
 namespace bf {
@@ -62,9 +62,6 @@ namespace {
 #endif
 #ifndef BF_HIST
 #define BF_HIST 0
-#endif
-#ifndef BF_NORED
-#define BF_NORED 1
 #endif
 #ifndef BF_EVG
 #define BF_EVG 4
@@ -105,16 +102,16 @@ __device__ __forceinline__ T pick4(const T (&v)[4], int j) {
 }
 
 struct Fp32Consts {
-    float kappa[BF_MAXF];    // omega/(2 pi c), turns per metre
-    double kappa64[BF_MAXF];
+    double kappa64[BF_MAXF]; // omega/(2 pi c), turns per metre (fp64 anchors)
     float omega[BF_MAXF];
     float omrel[BF_MAXF];    // omega_f / omega_0 (the staged amplitude carries omega_0)
-    float cutk[BF_MAXF];     // omega*b/(72 c): q^2*cutk > m2 iff ex_re < -36 (kernels.py:384)
-    float hk2pi[BF_MAXF];    // hk/(2 pi): g*s in turns = (q^2/m2)*s*hk2pi
-    float nhkbl2e[BF_MAXF];  // -hk*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
+    float lomrel[BF_MAXF];   // log2(omrel)
+    float gcut[BF_MAXF];     // 72 c/(omega b): q^2/m2 > gcut iff ex_re < -36 (kernels.py:384)
+    float kh[BF_MAXF];       // omega/(2 c): phase = an' + kh (c2 + (q^2/m2) s) radians
+    float nhkbl2e[BF_MAXF];  // -kh*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
     double nhkbl2e64[BF_MAXF];
     float b, b2;             // width_b, width_b^2
-    int ascending;           // omegas nondecreasing (cutk nondecreasing)
+    int ascending;           // omegas nondecreasing (gcut nonincreasing)
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
     double rcut_scale;       // 72 c / (omega_min b): R_cut^2 = rcut_scale * (s_end^2 + b^2)
     float rscale;            // (float) rcut_scale
@@ -147,6 +144,10 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return y;
 }
 __device__ __forceinline__ double frac_turns(double x) { return x - rint(x); }
+// x turns reduced to [-1/2, 1/2] and expressed in radians (fp64), rounded once
+__device__ __forceinline__ float frac_rad(double x) {
+    return (float)(6.283185307179586 * (x - rint(x)));
+}
 
 // Packed fp32 pairs (receivers 2h, 2h+1 of a lane): FFMA2 / FMUL2 / FADD2 do the two
 // receivers' operations in one issue slot (sm_100), each with the rounding of the scalar
@@ -194,8 +195,9 @@ struct WarpSmem {
     float4 geo0[ROWS<MF>];     // wc.xyz (c_P - o), len
     float4 geo1[ROWS<MF>];     // d.xyz, Pc (projection of c_P)
     float4 geo2[ROWS<MF>];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
-    float2 aux[ROWS<MF>];      // s0, A (amplitude factor x omega_0)
-    float4 anc[NF][ROWS<MF>];  // phase anchors (turns): centre proj, start, end; anc[0].w = D
+    float2 aux[ROWS<MF>];      // s0 + Pc', A (amplitude factor x omega_0); Pc' = clamp(Pc, 0, len)
+    float4 anc[ROWS<MF>];      // an' (exact phase at s0 + Pc', radians), lo2, hi2, d2 (clamp2)
+    float ancf[MF ? NF : 1][MF ? ROWS<MF> : 1];  // several frequencies: an' per frequency
     unsigned rowinfo[ROWS<MF>];  // chunk row -> compact row (Rows) of the group
     short brow[CB + 1];      // chunk beam -> first chunk row
     unsigned grow0[CB];      // chunk beam -> compact row of its segment 0
@@ -212,42 +214,46 @@ struct WarpSmem {
 
 // Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
 // sqrt(c) (s + i b)/m2 exp(-g b) exp(i(omega s/c + g s)), contribution
-// i omega/(2 pi c) w_b field.  `base[f]` is the fp64-anchored axial phase
-// omega s/(2 pi c) reduced to turns.
+// i omega/(2 pi c) w_b field.
+//
+// Axial phase.  Staging clamps the patch centre's projection to the segment, Pc' =
+// clamp(Pc, 0, len), and stores the exact phase there (an' = omega (s0 + Pc')/c reduced
+// modulo 2 pi in fp64), lo2 = -2 Pc', hi2 = 2 (len - Pc') and d2 = 2 (Pc - Pc').  A
+// receiver's clamped arc length is then s = s0 + Pc' + c2/2 with c2 = clamp(2 r.d + d2,
+// lo2, hi2) = 2 (clamp(proj, 0, len) - Pc'), and its phase is an' + kh (c2 + g s) with
+// kh = omega/(2c) (g s = q^2 s/m2 is the off-axis term).  |c2| stays within a few patch
+// radii (a receiver clamped at an end has its patch centre projecting near that end, or
+// beyond it where Pc' is the end itself and c2 = 0), so the fp32 phase carries the same
+// ~eps kh RW error as an interior point.
 //
 // Without the cutoff (kernels.py:384-385 skipped) exp(-g b) falls below the fp32 range
 // for pairs far off a beam's axis: a receiver with only such pairs has a reference value
 // ~1e-40..1e-300 of the field maximum.  The kernels for calls without the cutoff
 // (TINY = true) therefore sum every pair beyond the cutoff exponent (ex_re < -36) in
-// fp64 instead: tiny_contribution redoes the evaluation from the same fp32 s, q^2, m2,
-// amplitude factor and phase with the exponential and products in fp64, added straight
-// into the fp64 accumulator.  Pairs within the exponent range stay fp32 (their amplitude
-// is >= e^-36 times the amplitude factor).  Calls with the cutoff never reach this code
-// (TINY = false kernels do not contain it).
-__device__ __forceinline__ void tiny_contribution(const Fp32Consts &K, int f, float s, float q2,
-                                                  float m2, float A, float base, double *acc64) {
-    const float inv = rcp_approx(m2);
-    const float gq = q2 * inv;
-    const float ainv = A * inv;
-    const float turns = fmaf(gq * s, K.hk2pi[f], base);
-    const float ph = turns * 6.283185307179586f;
+// fp64 instead: tiny_contribution redoes the evaluation from the same fp32 s, g = q^2/m2,
+// 1/m2, amplitude factor and phase with the exponential and products in fp64, added
+// straight into the fp64 accumulator.  Pairs within the exponent range stay fp32 (their
+// amplitude is >= e^-36 times the amplitude factor).  Calls with the cutoff never reach
+// this code (TINY = false kernels do not contain it).
+__device__ __forceinline__ void tiny_contribution(const Fp32Consts &K, int f, float s, float gq,
+                                                  float inv, float A, float ph, double *acc64) {
     const float sn = sin_approx(ph), cs = cos_approx(ph);
     const double e = exp2((double)gq * K.nhkbl2e64[f]);
-    const double amp = (double)ainv * e * (double)(f > 0 ? K.omrel[f] : 1.f);
+    const double amp = (double)(A * inv) * e * (double)(f > 0 ? K.omrel[f] : 1.f);
     const double as = amp * (double)s, ab = amp * (double)K.b;
     acc64[0] += -as * (double)sn - ab * (double)cs;
     acc64[1] += as * (double)cs - ab * (double)sn;
 }
-// One frequency of a pair's contribution (the several-frequency tail): gq = q^2/m2,
-// ainv = A/m2 shared across frequencies.
-__device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float s, float gq,
-                                          float ainv, float base, float2 &acc, unsigned &ev,
+
+// One frequency of a pair's contribution (the several-frequency tail): ph the phase,
+// gq = q^2/m2, ais = A s/m2 and aib = A b/m2 shared across frequencies; omrel[f] folded
+// into the exponent (lomrel[f] = log2(omega_f/omega_0)).
+__device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float ph, float gq,
+                                          float ais, float aib, float2 &acc, unsigned &ev,
                                           int shift, bool live) {
-    const float turns = fmaf(gq * s, K.hk2pi[f], base);
-    const float ph = turns * 6.283185307179586f;
     const float sn = sin_approx(ph), cs = cos_approx(ph);
-    const float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]) * K.omrel[f];
-    const float as = amp * s, ab = amp * K.b;
+    const float e = ex2_approx(fmaf(gq, K.nhkbl2e[f], K.lomrel[f]));
+    const float as = e * ais, ab = e * aib;
     if (live) {  // i * amp * (s + i b) * (cos + i sin)
         float2 v = acc;
         v.x = fmaf(-as, sn, fmaf(-ab, cs, v.x));
@@ -257,47 +263,15 @@ __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float s, f
     }
 }
 
-template <int NF>
-__device__ __forceinline__ void eval_pair(const Fp32Consts &K, int use_cutoff, float s, float q2,
-                                          float m2, float A, const float *base,
-                                          float (&pre)[NF], float (&pim)[NF], unsigned &ev,
-                                          int shift, bool live) {
-    const float inv = rcp_approx(m2);
-    const float gq = q2 * inv;
-    const float ainv = A * inv;
-    const float gqs = gq * s;
-#pragma unroll
-    for (int f = 0; f < NF; ++f) {
-        const bool lf = live && !(NF > 1 && q2 * K.cutk[f] > m2);  // ex_re < -36
-        float turns = fmaf(gqs, K.hk2pi[f], base[f]);
-#if !BF_NORED
-        turns -= rintf(turns);
-#endif
-        const float ph = turns * 6.283185307179586f;
-        const float sn = sin_approx(ph), cs = cos_approx(ph);
-        // A carries omega_0 (staging); omrel[f] = omega_f / omega_0
-        float amp = ainv * ex2_approx(gq * K.nhkbl2e[f]);
-        if (f > 0) amp *= K.omrel[f];
-        const float as = amp * s, ab = amp * K.b;
-        if (lf) {  // i * amp * (s + i b) * (cos + i sin)
-            pre[f] = fmaf(-as, sn, fmaf(-ab, cs, pre[f]));
-            pim[f] = fmaf(as, cs, fmaf(-ab, sn, pim[f]));
-            ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
-        }
-    }
-}
-
-// eval_pair<1> for receivers 2h, 2h+1 as packed pairs (same operations and rounding);
-// a receiver that is not live keeps its sums (selected, so its inputs may be anything).
-__device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2 q2, float2 m2,
+// One frequency, receivers 2h, 2h+1 as packed pairs: gq = q^2/m2, inv = 1/m2, b = an' +
+// kh c2 (the axial phase); a receiver that is not live keeps its sums (selected, so its
+// inputs may be anything).
+__device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2 gq, float2 inv,
                                            float2 A, float2 base, float2 &pre, float2 &pim,
                                            unsigned &ev, bool l0, bool l1) {
-    const float2 inv = make_float2(rcp_approx(m2.x), rcp_approx(m2.y));
-    const float2 gq = mul2<PE>(q2, inv);
     const float2 ainv = mul2<PE>(A, inv);
-    const float2 gqs = mul2<PE>(gq, s);
-    const float2 turns = fma2<PE>(gqs, bc2(K.hk2pi[0]), base);
-    const float2 ph = mul2<PE>(turns, bc2(6.283185307179586f));
+    const float2 gk = mul2<PE>(gq, bc2(K.kh[0]));
+    const float2 ph = fma2<PE>(gk, s, base);
     const float2 sn = make_float2(sin_approx(ph.x), sin_approx(ph.y));
     const float2 cs = make_float2(cos_approx(ph.x), cos_approx(ph.y));
     const float2 ex = mul2<PE>(gq, bc2(K.nhkbl2e[0]));
@@ -313,34 +287,9 @@ __device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2
     ev += (l0 ? 1u : 0u) + (l1 ? 0x10000u : 0u);  // evaluation counts (kernels.py:399)
 }
 
-// Phase anchor of the nearest point: interior -> centre anchor + kappa (r.d);
-// clamped -> exact start / end anchor (turns).
-// Axial phase (turns) of the nearest point from the row's anchor `an` (centre
-// projection / start / end): interior -> an.x + kappa (r.d); clamped -> exact end anchor.
-__device__ __forceinline__ float anchor_phase(float kappa, float proj, float dl, float len,
-                                              const float4 &an) {
-    float bf = fmaf(kappa, dl, an.x);
-    bf = proj >= len ? an.z : bf;
-    bf = proj <= 0.f ? an.y : bf;
-    return bf;
-}
-
-
-// Several frequencies: the nearest point's phase is kept as (row | clamp << 8, r.d) and
-// resolved per frequency in the tail; clamp 1 = start anchor, 2 = end anchor, 0 =
-// interior (anchor_phase's choice, same order of tests).
-__device__ __forceinline__ int phase_ref(int row, float proj, float len) {
-    int st = proj >= len ? 2 : 0;
-    st = proj <= 0.f ? 1 : st;
-    return row | (st << 8);
-}
-
-template <int NF, bool MF>
-__device__ __forceinline__ float phase_of(const WarpSmem<NF, MF> &S, const Fp32Consts &K, int f,
-                                          int ref, float dl) {
-    const float4 an = S.anc[f][ref & (ROWS<MF> - 1)];
-    const int st = ref >> 8;
-    return st == 1 ? an.y : st == 2 ? an.z : fmaf(K.kappa[f], dl, an.x);
+// c2 = 2 (clamp(proj, 0, len) - Pc') from r.d and the row's (lo2, hi2, d2) (see above).
+__device__ __forceinline__ float clamp2(float dl, const float4 &an) {
+    return fminf(fmaxf(fmaf(2.f, dl, an.w), an.y), an.z);
 }
 
 // Distance of the patch centre (the origin of patch-local coordinates) to
@@ -377,7 +326,8 @@ __device__ __forceinline__ float patch_dist(const WarpSmem<NF, MF> &S, const Fp3
     const float hn = uc > 1e-6f ? 0.5f * rcp_approx(uc) : 0.f;
     const float rn = uc > 1e-6f ? reach(B, g2.x * hn, g2.y * hn, g2.z * hn, 1.f) : B.w;
     const float rd = reach(B, g1.x, g1.y, g1.z, 1.f);
-    const float s_hi = S.aux[r].x + fminf(fmaxf(proj + rd * 1.00002f + 2e-3f, 0.f), g0.w);
+    const float s0 = fmaf(0.5f, S.anc[r].y, S.aux[r].x);  // s0 = (s0 + Pc') - Pc'
+    const float s_hi = s0 + fminf(fmaxf(proj + rd * 1.00002f + 2e-3f, 0.f), g0.w);
     const float rk = sqrt_approx(K.rscale * fmaf(s_hi, s_hi, K.b2)) * 1.00002f + 1e-3f;
     *cut = uc * 0.99999f > (rk + rn) * 1.00002f + 2e-3f;
     *proj_out = proj;
@@ -410,8 +360,8 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
     int kj = 0;
 #pragma unroll 1
     for (int k = 0; k < ns; ++k) {
-        D = fmaxf(D, S.anc[0][r0 + k].w);
         const float4 g0 = S.geo0[r0 + k];
+        D = fmaxf(D, fabsf(g0.x) + fabsf(g0.y) + fabsf(g0.z) + g0.w);
         const float4 g1 = S.geo1[r0 + k];
         const float t = fminf(fmaxf(g1.w, 0.f), g0.w);
         const float vx = g0.x - t * g1.x, vy = g0.y - t * g1.y, vz = g0.z - t * g1.z;
@@ -421,6 +371,7 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
             kj = k;
         }
     }
+    D = D * 1.000001f + RW + 1.f;  // error scale |c_P - o|_1 + len + R_W + 1 (DESIGN 5)
     const float p0 = S.geo1[r0].w;
     // pass 2: survivors (segments that can be the nearest for some receiver of the
     // patch) and whether every survivor is dead for the whole patch -- pruned
@@ -663,17 +614,12 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
             fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
                   0.f);
         const float s = (float)(w.p1[row0 + k].w + e.bt);  // kernels.py:344
-        // anchor choice follows the exact clamp
-        const float proj = e.bt == 0.0 ? -1.f : e.bt == e.len ? INFINITY : dl + g1.w;
+        // phase reference follows the exact clamp
+        const float4 an = S.anc[r0 + k];
+        const float c2 = e.bt == 0.0 ? an.y : e.bt == e.len ? an.z : clamp2(dl, an);
         const float A = S.aux[r0 + k].y;
-        float b;
-        int ref = 0;
-        if constexpr (!MF) {
-            b = anchor_phase(K.kappa[0], proj, dl, S.geo0[r0 + k].w, S.anc[0][r0 + k]);
-        } else {
-            b = dl;
-            ref = phase_ref(r0 + k, proj, S.geo0[r0 + k].w);
-        }
+        const float b = MF ? c2 : fmaf(K.kh[0], c2, an.x);
+        const int ref = r0 + k;
 #pragma unroll
         for (int jj = 0; jj < R; ++jj)
             if (jj == j) {
@@ -694,32 +640,25 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
                                            const Fp32Consts &K, int lane) {
     // software-pipelined: the next row's loads are in flight while this row converts
     auto grow = [&](int r) { return (int64_t)S.rowinfo[r]; };
-    const float2 *pa2 = reinterpret_cast<const float2 *>(w.pa);
     int r = lane;
-    int64_t g = 0;
     double4 p0 = make_double4(0, 0, 0, 0), p1 = p0;
     float p2 = 0.f;
-    float2 ae0 = make_float2(0.f, 0.f);
     if (r < nrows) {
-        g = grow(r);
+        const int64_t g = grow(r);
         p0 = w.p0[g];  // o.xyz, len
         p1 = w.p1[g];  // d.xyz, s0
         p2 = w.amp[g];  // A
-        ae0 = pa2[g * NF];
     }
 #pragma unroll 1
     for (; r < nrows; r += 32) {
         const int rn = r + 32;
-        int64_t gn = 0;
         double4 p0n = p0, p1n = p1;
         float p2n = p2;
-        float2 aen = ae0;
         if (rn < nrows) {
-            gn = grow(rn);
+            const int64_t gn = grow(rn);
             p0n = w.p0[gn];
             p1n = w.p1[gn];
             p2n = w.amp[gn];
-            aen = pa2[gn * NF];
         }
         const double wcx = cx - p0.x, wcy = cy - p0.y, wcz = cz - p0.z;
         const double pc = wcx * p1.x + wcy * p1.y + wcz * p1.z;
@@ -728,19 +667,19 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
         S.geo1[r] = make_float4((float)p1.x, (float)p1.y, (float)p1.z, (float)pc);
         S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
                                 (float)(ucx * ucx + ucy * ucy + ucz * ucz));
-        const float D = (float)(fabs(wcx) + fabs(wcy) + fabs(wcz) + p0.w) + RW + 1.f;
-        S.aux[r] = make_float2((float)p1.w, p2 * K.omega[0]);
+        // the centre's projection clamped to the segment; phase references (clamp2)
+        const double pcc = pc < 0.0 ? 0.0 : (pc > p0.w ? p0.w : pc);
+        const double sp = p1.w + pcc;
+        S.aux[r] = make_float2((float)sp, p2 * K.omega[0]);
+        S.anc[r] = make_float4(frac_rad(K.kappa64[0] * sp), (float)(-2.0 * pcc),
+                               (float)(2.0 * (p0.w - pcc)), (float)(2.0 * (pc - pcc)));
+        if constexpr (MF) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-            const float2 ae = f ? pa2[g * NF + f] : ae0;
-            S.anc[f][r] =
-                make_float4((float)frac_turns(K.kappa64[f] * (p1.w + pc)), ae.x, ae.y, f ? 0.f : D);
+            for (int f = 0; f < NF; ++f) S.ancf[f][r] = frac_rad(K.kappa64[f] * sp);
         }
-        g = gn;
         p0 = p0n;
         p1 = p1n;
         p2 = p2n;
-        ae0 = aen;
     }
 }
 
@@ -930,48 +869,45 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 // ---- single surviving segment: it is the nearest for every receiver
                 const int k = __ffs(surv) - 1;
                 const int row = r0 + k;
-                const float4 g0 = S.geo0[row];
                 const float4 g1 = S.geo1[row];
                 const float4 g2 = S.geo2[row];
                 const float2 ax = S.aux[row];
-                float4 an[1];
-                if constexpr (!MF) an[0] = S.anc[0][row];
-                float pj[R];
+                const float4 an = S.anc[row];
+                float dlj[R];
 #pragma unroll
                 for (int h = 0; h < R; h += 2) {  // receivers h, h+1 as packed pairs
                     const float2 X = pair(rx, h), Y = pair(ry, h), Z = pair(rz, h);
                     const float2 dl = fma2<PG>(X, bc2(g1.x), fma2<PG>(Y, bc2(g1.y), mul2<PG>(Z, bc2(g1.z))));
-                    const float2 proj = add2<PG>(dl, bc2(g1.w));
                     const float2 qq = fma2<PG>(neg2(dl), dl,
                                            fma2<PG>(bc2(g2.x), X, fma2<PG>(bc2(g2.y), Y,
                                                 fma2<PG>(bc2(g2.z), Z, add2<PG>(bc2(g2.w), pair(rr, h))))));
-                    const float2 t = make_float2(fminf(fmaxf(proj.x, 0.f), g0.w),
-                                                 fminf(fmaxf(proj.y, 0.f), g0.w));
-                    const float2 sv = add2<PG>(bc2(ax.x), t);
+                    const float2 c2 = make_float2(clamp2(dl.x, an), clamp2(dl.y, an));
+                    const float2 sv = fma2<PG>(bc2(0.5f), c2, bc2(ax.x));
                     float2 bf;
-                    if constexpr (!MF) bf = fma2<PG>(bc2(K.kappa[0]), dl, bc2(an[0].x));
+                    if constexpr (!MF) bf = fma2<PG>(bc2(K.kh[0]), c2, bc2(an.x));
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         const int j = h + u;
-                        const float pr = u ? proj.y : proj.x;
-                        pj[j] = pr;
+                        dlj[j] = u ? dl.y : dl.x;
                         Aj[j] = ax.y;
-                        if constexpr (!MF) {  // anchor_phase with the packed centre term
-                            float b = u ? bf.y : bf.x;
-                            b = pr >= g0.w ? an[0].z : b;
-                            b = pr <= 0.f ? an[0].y : b;
-                            bj[j][0] = b;
+                        if constexpr (!MF) {
+                            bj[j][0] = u ? bf.y : bf.x;
                         } else {
-                            bj[j][0] = u ? dl.y : dl.x;
-                            pref[j] = phase_ref(row, pr, g0.w);
+                            bj[j][0] = u ? c2.y : c2.x;
+                            pref[j] = row;
                         }
                         sj[j] = u ? sv.y : sv.x;
                         q2j[j] = fmaxf(u ? qq.y : qq.x, 0.f);
                     }
                 }
                 lvm = (1u << R) - 1;
-                if (bword & BEHIND_CHECK)
-                    lvm = behind_mask(w, pj, S.p64 + R * lane, nvalid, S.anc[0][row].w, row0 + k, ties);
+                if (bword & BEHIND_CHECK) {
+                    float pj[R];
+#pragma unroll
+                    for (int j = 0; j < R; ++j) pj[j] = dlj[j] + g1.w;
+                    lvm = behind_mask(w, pj, S.p64 + R * lane, nvalid, __int_as_float(dsc.w),
+                                      row0 + k, ties);
+                }
             } else {
                 // receivers decided at the junction of segments ka, ka+1 (corner wedge):
                 // both clamped distances are distances to the reflection point, an exact
@@ -1028,8 +964,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 // two adjacent candidates: ties at the junction go to the wedge decision
                 const bool pair = surv == (3u << ka);
-                const float jtol =
-                    pair ? PROJ_ERR * fmaxf(S.anc[0][r0 + ka].w, S.anc[0][r0 + ka + 1].w) : 0.f;
+                const float jtol = pair ? PROJ_ERR * Db : 0.f;  // Db >= either row's D
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const int k = kb[j];
@@ -1043,7 +978,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g1 = S.geo1[r0 + k];
                     const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
                     const float proj = dl + g1.w;
-                    if (k == 0 && fabsf(proj) <= PROJ_ERR * S.anc[0][r0].w) exact = true;
+                    if (k == 0 && fabsf(proj) <= PROJ_ERR * Db) exact = true;
                     if (exact) {
                         if (j >= nvalid) continue;
                         if (pair) {
@@ -1065,14 +1000,15 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     q2j[j] = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
                                    0.f);
                     const float2 ax = S.aux[r0 + k];
-                    const float len = S.geo0[r0 + k].w;
-                    sj[j] = ax.x + fminf(fmaxf(proj, 0.f), len);
+                    const float4 an = S.anc[r0 + k];
+                    const float c2 = clamp2(dl, an);
+                    sj[j] = fmaf(0.5f, c2, ax.x);
                     Aj[j] = ax.y;
                     if constexpr (!MF) {
-                        bj[j][0] = anchor_phase(K.kappa[0], proj, dl, len, S.anc[0][r0 + k]);
+                        bj[j][0] = fmaf(K.kh[0], c2, an.x);
                     } else {
-                        bj[j][0] = dl;
-                        pref[j] = phase_ref(r0 + k, proj, len);
+                        bj[j][0] = c2;
+                        pref[j] = r0 + k;
                     }
                     lvm |= 1u << j;
                 }
@@ -1083,11 +1019,11 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
                     const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
-                    float ea[1], sb_[1];  // end anchor of ka, start anchor of ka+1
-                    if constexpr (!MF) {
-                        ea[0] = S.anc[0][ra].z;
-                        sb_[0] = S.anc[0][rb].y;
-                    }
+                    // phase references at the end of ka (c2 = hi2) and the start of ka+1
+                    // (c2 = lo2)
+                    const float4 ana = S.anc[ra], anb = S.anc[rb];
+                    const float ea = MF ? ana.z : fmaf(K.kh[0], ana.z, ana.x);
+                    const float sb_ = MF ? anb.y : fmaf(K.kh[0], anb.y, anb.x);
                     ties += __popc(jp);
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
@@ -1101,12 +1037,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                             0.f);
                         sj[j] = wb ? J.sb : J.sa;
                         Aj[j] = wb ? Ab : Aa;
-                        if constexpr (!MF) {
-                            bj[j][0] = wb ? sb_[0] : ea[0];
-                        } else {
-                            bj[j][0] = 0.f;
-                            pref[j] = wb ? (rb | (1 << 8)) : (ra | (2 << 8));
-                        }
+                        bj[j][0] = wb ? sb_ : ea;
+                        if constexpr (MF) pref[j] = wb ? rb : ra;
                         lvm |= 1u << j;
                     }
                 }
@@ -1144,22 +1076,26 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     }
                 }
             }
-            float m2j[R];
+            // 1/m2 and g = q^2/m2 of every receiver (m2 = s^2 + b^2)
+            float invj[R], gqj[R];
             unsigned tiny = 0;  // (TINY) receivers beyond the cutoff exponent: fp64
 #pragma unroll
             for (int h = 0; h < R; h += 2) {
                 const float2 m2p = fma2<PG>(pair(sj, h), pair(sj, h), bc2(K.b2));
-                m2j[h] = m2p.x;
-                m2j[h + 1] = m2p.y;
+                invj[h] = rcp_approx(m2p.x);
+                invj[h + 1] = rcp_approx(m2p.y);
+                const float2 gp = mul2<PG>(pair(q2j, h), pair(invj, h));
+                gqj[h] = gp.x;
+                gqj[h + 1] = gp.y;
             }
+            if constexpr (!MF) {
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-                if (!MF && q2j[j] * K.cutk[0] > m2j[j]) {  // ex_re < -36 (kernels.py:384)
+                if (gqj[j] > K.gcut[0]) {  // ex_re < -36 (kernels.py:384)
                     if (TINY && ((lvm >> j) & 1u)) tiny |= 1u << j;  // no cutoff: fp64 below
                     lvm &= ~(1u << j);
                 }
             }
-            if constexpr (!MF) {
             // receivers evaluated in groups of EVG (one branch, EVG independent chains),
             // as packed pairs
 #pragma unroll
@@ -1167,7 +1103,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (lvm & (((1u << EVG) - 1u) << g)) {
 #pragma unroll
                     for (int h = g; h < g + EVG; h += 2)
-                        eval_pair2(K, pair(sj, h), pair(q2j, h), pair(m2j, h), pair(Aj, h),
+                        eval_pair2(K, pair(sj, h), pair(gqj, h), pair(invj, h), pair(Aj, h),
                                    make_float2(bj[h][0], bj[h + 1][0]), pre2[h >> 1],
                                    pim2[h >> 1], evp[h >> 1], (lvm >> h) & 1u,
                                    (lvm >> (h + 1)) & 1u);
@@ -1177,33 +1113,36 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll 1
                     for (int j = 0; j < R; ++j)
                         if ((tiny >> j) & 1u) {
-                            tiny_contribution(K, 0, pick4(sj, j), pick4(q2j, j), pick4(m2j, j),
-                                              pick4(Aj, j), j == 0 ? bj[0][0] : j == 1 ? bj[1][0]
-                                                            : j == 2 ? bj[2][0] : bj[3][0],
-                                              S.acc[R * lane + j][0]);
+                            const float sv = pick4(sj, j), gv = pick4(gqj, j);
+                            const float bv = j == 0 ? bj[0][0] : j == 1 ? bj[1][0]
+                                           : j == 2 ? bj[2][0] : bj[3][0];
+                            tiny_contribution(K, 0, sv, gv, pick4(invj, j), pick4(Aj, j),
+                                              fmaf(gv * K.kh[0], sv, bv), S.acc[R * lane + j][0]);
                             evp[j >> 1] += 1u << (16 * (j & 1));
                         }
                 }
             }
             } else {
-            // several frequencies: the cutoff grows with omega, so each frequency is
+            // several frequencies: phase an'_f + kh_f X with X = c2 + g s (frequency
+            // independent; WIDE: c2 = 0 and an'_f from the fp64 arc length), amplitude
+            // A/m2 (s + i b) shared; the cutoff grows with omega, so each frequency is
             // evaluated only if some receiver of the warp is live for it
-            float gq[R], ainv[R];
+            float X[R], ais[R], aib[R];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-                const float inv = rcp_approx(m2j[j]);
-                gq[j] = q2j[j] * inv;
-                ainv[j] = Aj[j] * inv;
+                X[j] = fmaf(gqj[j], sj[j], WIDE ? 0.f : bj[j][0]);
+                const float ainv = Aj[j] * invj[j];
+                ais[j] = ainv * sj[j];
+                aib[j] = ainv * K.b;
             }
-            // per frequency: the phase base from the (row, clamp) reference, partial sums
-            // in shared memory (no per-frequency registers)
+            // per frequency: partial sums in shared memory (no per-frequency registers)
 #pragma unroll 1
             for (int f = 0; f < NF; ++f) {
                 unsigned lf = 0, tf = 0;  // fp32 / (TINY) fp64 receivers of frequency f
 #pragma unroll
                 for (int j = 0; j < R; ++j)
                     if ((lvm >> j) & 1u) {
-                        if (!(q2j[j] * K.cutk[f] > m2j[j]))
+                        if (!(gqj[j] > K.gcut[f]))
                             lf |= 1u << j;  // ex_re >= -36 (kernels.py:384)
                         else if (TINY)
                             tf |= 1u << j;
@@ -1215,24 +1154,22 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     continue;
                 }
                 {
-                    unsigned tiny = 0;
+                    float ph[R];
 #pragma unroll
-                    for (int j = 0; j < R; ++j)
-                        eval_freq(K, f, sj[j], gq[j], ainv[j],
-                                  WIDE ? (float)frac_turns(K.kappa64[f] * s64[j])
-                                       : phase_of<NF, MF>(S, K, f, pref[j], bj[j][0]),
-                                  S.facc[f][j][lane], evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                    for (int j = 0; j < R; ++j) {
+                        const float an = WIDE ? frac_rad(K.kappa64[f] * s64[j]) : S.ancf[f][pref[j]];
+                        ph[j] = fmaf(K.kh[f], X[j], an);
+                        eval_freq(K, f, ph[j], gqj[j], ais[j], aib[j], S.facc[f][j][lane],
+                                  evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                    }
                     if (TINY && tf) {
 #pragma unroll 1
                         for (int j = 0; j < R; ++j)
                             if ((tf >> j) & 1u) {
                                 evp[j >> 1] += 1u << (16 * (j & 1));
                                 tiny_contribution(
-                                    K, f, pick4(sj, j), pick4(q2j, j), pick4(m2j, j), pick4(Aj, j),
-                                    WIDE ? (float)frac_turns(K.kappa64[f] * s64[j])
-                                         : phase_of<NF, MF>(S, K, f, pick4(pref, j),
-                                                            j == 0 ? bj[0][0] : j == 1 ? bj[1][0]
-                                                            : j == 2 ? bj[2][0] : bj[3][0]),
+                                    K, f, pick4(sj, j), pick4(gqj, j), pick4(invj, j), pick4(Aj, j),
+                                    pick4(ph, j),
                                     reinterpret_cast<double *>(
                                         w.part + (q * w.n_pad + sb + j) * NF + f));
                             }
@@ -1379,18 +1316,6 @@ __global__ void rows_slice_kernel(const Rows src, int64_t b0, int64_t nb, int64_
             amp[i] = src.amp[row];
         }
     }
-}
-
-// Phase anchors of every compact row, per frequency: frac(omega/(2 pi c) s) at s0 and
-// s0 + len in fp64 (turns), rounded to fp32 once.
-__global__ void anchors_kernel(const Rows r, int64_t rows_bound, int nf, Fp32Consts K,
-                               float2 *pa) {
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= rows_bound || row >= r.start[r.n_beams]) return;
-    const double s0 = r.p1[row].w, se = s0 + r.p0[row].w;
-    for (int f = 0; f < nf; ++f)
-        pa[row * nf + f] = make_float2((float)frac_turns(K.kappa64[f] * s0),
-                                       (float)frac_turns(K.kappa64[f] * se));
 }
 
 // One warp per patch: fp64 bounding-box centre c_P, patch-local r = p - c_P in
@@ -1610,17 +1535,17 @@ Fp32Consts make_consts(const GbsArgs &a) {
         const double w = f < a.nf ? a.omegas[f] : 0.0;
         if (f < a.nf && w < wmin) wmin = w;
         K.kappa64[f] = w / (two_pi * a.c);
-        K.kappa[f] = (float)K.kappa64[f];
         K.omega[f] = (float)w;
         K.omrel[f] = f < a.nf ? (float)(w / a.omegas[0]) : 0.f;
-        K.cutk[f] = (float)(w * a.width_b / (72.0 * a.c));
-        K.hk2pi[f] = (float)(w * 0.5 / a.c / two_pi);
+        K.lomrel[f] = f < a.nf && w > 0 ? (float)log2(w / a.omegas[0]) : 0.f;
+        K.gcut[f] = w > 0 ? (float)(72.0 * a.c / (w * a.width_b)) : INFINITY;
+        K.kh[f] = (float)(w * 0.5 / a.c);
         K.nhkbl2e64[f] = -(w * 0.5 / a.c) * a.width_b * 1.4426950408889634;
         K.nhkbl2e[f] = (float)K.nhkbl2e64[f];
     }
     K.ascending = 1;
     for (int f = 1; f < a.nf; ++f)
-        if (!(K.cutk[f] >= K.cutk[f - 1])) K.ascending = 0;
+        if (!(K.gcut[f] <= K.gcut[f - 1])) K.ascending = 0;
     K.b = (float)a.width_b;
     K.b2 = (float)(a.width_b * a.width_b);
     K.b2_64 = a.width_b * a.width_b;
@@ -1675,17 +1600,6 @@ int launch_rows_pack(const GbsArgs &a, const int64_t *start, double4 *p0, double
     const double amp_scale = a.phi_amp * sqrt(a.c) / (2.0 * 3.141592653589793 * a.c);
     rows_pack_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(a, amp_scale, start, p0, p1,
                                                                      amp);
-    note_launch();
-    BF_TRY_CUDA(cudaGetLastError());
-    return BF_OK;
-}
-
-int launch_fp32_anchors(const GbsArgs &a, const Rows &r, int64_t rows_bound, float *pa,
-                        cudaStream_t st) {
-    if (rows_bound <= 0 || r.n_beams <= 0) return BF_OK;
-    const Fp32Consts K = make_consts(a);
-    anchors_kernel<<<(unsigned)((rows_bound + 255) / 256), 256, 0, st>>>(
-        r, rows_bound, a.nf, K, reinterpret_cast<float2 *>(pa));
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;
