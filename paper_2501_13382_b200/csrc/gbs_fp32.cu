@@ -138,6 +138,23 @@ __device__ __forceinline__ float cos_approx(float x) {
     asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 1/x on the FMA pipe (x > 0 normal): bit-trick seed (|rel err| <= 5.1e-2) and three
+// Newton steps (6.6e-6, then rounding level ~6e-8).  The evaluation is bound by the
+// MUFU (XU) pipe -- rcp, ex2, sin, cos per pair at 16/clk/SM -- so the reciprocal moves
+// to the FMA pipe, which has the issue slots to spare.
+#ifndef BF_RCP_NR
+#define BF_RCP_NR 0  // measured: slower (the kernel is issue-bound, not XU-bound)
+#endif
+__device__ __forceinline__ float rcp_nr(float x) {
+#if BF_RCP_NR
+    float y = __int_as_float(0x7ef311c3 - __float_as_int(x));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) y = fmaf(y, fmaf(-x, y, 1.f), y);
+    return y;
+#else
+    return rcp_approx(x);
+#endif
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -249,8 +266,7 @@ __device__ __forceinline__ void tiny_contribution(const Fp32Consts &K, int f, fl
 // gq = q^2/m2, ais = A s/m2 and aib = A b/m2 shared across frequencies; omrel[f] folded
 // into the exponent (lomrel[f] = log2(omega_f/omega_0)).
 __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float ph, float gq,
-                                          float ais, float aib, float2 &acc, unsigned &ev,
-                                          int shift, bool live) {
+                                          float ais, float aib, float2 &acc, bool live) {
     const float sn = sin_approx(ph), cs = cos_approx(ph);
     const float e = ex2_approx(fmaf(gq, K.nhkbl2e[f], K.lomrel[f]));
     const float as = e * ais, ab = e * aib;
@@ -259,17 +275,18 @@ __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float ph, 
         v.x = fmaf(-as, sn, fmaf(-ab, cs, v.x));
         v.y = fmaf(as, cs, fmaf(-ab, sn, v.y));
         acc = v;
-        ev += 1u << shift;  // evaluation count (kernels.py:399), 16-bit field
     }
 }
 
 // One frequency, receivers 2h, 2h+1 as packed pairs: gq = q^2/m2, inv = 1/m2, b = an' +
-// kh c2 (the axial phase); a receiver that is not live keeps its sums (selected, so its
-// inputs may be anything).
+// kh c2 (the axial phase); a receiver that is not live adds zero (its amplitude factor is
+// selected to 0, so its inputs must be finite: every path leaves finite s, q^2, A, b).
 __device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2 gq, float2 inv,
                                            float2 A, float2 base, float2 &pre, float2 &pim,
-                                           unsigned &ev, bool l0, bool l1) {
-    const float2 ainv = mul2<PE>(A, inv);
+                                           bool l0, bool l1) {
+    float2 ainv = mul2<PE>(A, inv);
+    ainv.x = l0 ? ainv.x : 0.f;
+    ainv.y = l1 ? ainv.y : 0.f;
     const float2 gk = mul2<PE>(gq, bc2(K.kh[0]));
     const float2 ph = fma2<PE>(gk, s, base);
     const float2 sn = make_float2(sin_approx(ph.x), sin_approx(ph.y));
@@ -278,14 +295,14 @@ __device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2
     const float2 amp = mul2<PE>(ainv, make_float2(ex2_approx(ex.x), ex2_approx(ex.y)));
     const float2 as = mul2<PE>(amp, s), ab = mul2<PE>(amp, bc2(K.b));
     // i * amp * (s + i b) * (cos + i sin)
-    const float2 npre = fma2<PE>(neg2(as), sn, fma2<PE>(neg2(ab), cs, pre));
-    const float2 npim = fma2<PE>(as, cs, fma2<PE>(neg2(ab), sn, pim));
-    pre.x = l0 ? npre.x : pre.x;
-    pim.x = l0 ? npim.x : pim.x;
-    pre.y = l1 ? npre.y : pre.y;
-    pim.y = l1 ? npim.y : pim.y;
-    ev += (l0 ? 1u : 0u) + (l1 ? 0x10000u : 0u);  // evaluation counts (kernels.py:399)
+    pre = fma2<PE>(neg2(as), sn, fma2<PE>(neg2(ab), cs, pre));
+    pim = fma2<PE>(as, cs, fma2<PE>(neg2(ab), sn, pim));
 }
+
+// Evaluation counts (kernels.py:399) of a lane's R = 4 receivers as byte fields: bit j of a
+// receiver mask -> byte j (one multiply, no carries: the shifted copies never overlap).
+// A chunk adds at most CB * NF evaluations per receiver (checked where it is used).
+__device__ __forceinline__ unsigned spread4(unsigned m) { return (m * 0x00204081u) & 0x01010101u; }
 
 // c2 = 2 (clamp(proj, 0, len) - Pc') from r.d and the row's (lo2, hi2, d2) (see above).
 __device__ __forceinline__ float clamp2(float dl, const float4 &an) {
@@ -723,7 +740,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     // fp32 partial sums of the chunk: registers with one frequency, shared memory
     // (S.facc) with several
     float2 pre2[R / 2], pim2[R / 2];  // (one frequency) receivers 2h, 2h+1
-    unsigned evp[R / 2] = {};  // evaluation counts of receivers 2i, 2i+1 (16-bit fields)
+    // byte counters: a receiver gets <= CBN * NF <= 255 evaluations per chunk
+    constexpr int CBN = NF * CB <= 255 ? CB : 255 / NF;
+    static_assert(R == 4 && CBN * NF <= 255, "byte evaluation counters");
+    unsigned evb = 0;  // evaluation counts of the lane's receivers in the chunk (byte fields)
     unsigned ties = 0, nbp = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -741,7 +761,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     int cur = 0, nch = 0;
     uint32_t e = lane < n_items ? items[lane] : 0u;  // entries of the next chunk
     while (cur < n_items) {
-        const int nbn = min(CB, n_items - cur);
+        const int nbn = min(CBN, n_items - cur);
         const int ns = lane < nbn ? (int)(e >> 27) + 1 : 0;
         const unsigned row_l = e & 0x7ffffffu;  // compact row of the beam's segment 0
         // ---- row capacity: keep the prefix of beams whose rows fit ROWS<MF>
@@ -839,14 +859,18 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         //      the nearest point of every receiver (s, q^2, row, proj, r.d) and the
         //      mask of non-behind receivers; one shared tail applies the cutoff and
         //      evaluates the contributions.
+        // the next item's descriptor is loaded one item ahead (its shared-memory latency
+        // overlaps the current item)
+        int4 dnext = S.desc[live ? __ffs(live) - 1 : 0];
 #pragma unroll 1
 #if BF_ABL & 16
         for (unsigned lm = 0; lm;) {  // ablation: no summation at all
 #else
         for (unsigned lm = live; lm;) {
 #endif
-            const int4 dsc = S.desc[__ffs(lm) - 1];
+            const int4 dsc = dnext;
             lm &= lm - 1;
+            dnext = S.desc[lm ? __ffs(lm) - 1 : 0];
             const int64_t row0 = (unsigned)dsc.x;  // compact row of segment 0
             const unsigned bword = (unsigned)dsc.y;
             const unsigned surv = bword & ~(BEHIND_CHECK | WEDGE);
@@ -897,7 +921,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                             pref[j] = row;
                         }
                         sj[j] = u ? sv.y : sv.x;
-                        q2j[j] = fmaxf(u ? qq.y : qq.x, 0.f);
+                        q2j[j] = u ? qq.y : qq.x;  // may round below 0: harmless (g ~ -eps)
                     }
                 }
                 lvm = (1u << R) - 1;
@@ -915,6 +939,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 unsigned jp;
                 int ka = __ffs(surv) - 1;
                 unsigned pend = 0;  // receivers re-decided by the general fp64 search
+                // receivers no path decides (behind, padding) still go through the
+                // evaluation with a zero amplitude: finite inputs
+#pragma unroll
+                for (int j = 0; j < R; ++j) sj[j] = q2j[j] = Aj[j] = bj[j][0] = 0.f;
                 float best[R];
                 int kb[R];
                 float Db = 0.f;
@@ -997,8 +1025,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     }
                     if (k == 0 && proj < 0.f) continue;  // behind the source
                     const float4 g2 = S.geo2[r0 + k];
-                    q2j[j] = fmaxf(fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
-                                   0.f);
+                    q2j[j] = fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j]))));
                     const float2 ax = S.aux[r0 + k];
                     const float4 an = S.anc[r0 + k];
                     const float c2 = clamp2(dl, an);
@@ -1042,6 +1069,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         lvm |= 1u << j;
                     }
                 }
+#if BF_HIST
+                if (pend) atomicAdd(&g_hist[__popc(surv) <= 2 ? 0 : 1], (unsigned long long)__popc(pend));
+                if (jp) atomicAdd(&g_hist[3], (unsigned long long)__popc(jp));
+#endif
                 if (__any_sync(0xffffffffu, pend != 0))
                     exact_pending<NF, MF>(a, K, S, row0, r0, surv, pend, rx, ry, rz, rr, best, kb,
                                       Db, lane, sj, q2j, Aj, bj, pref, lvm, ties, w);
@@ -1082,8 +1113,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
             for (int h = 0; h < R; h += 2) {
                 const float2 m2p = fma2<PG>(pair(sj, h), pair(sj, h), bc2(K.b2));
-                invj[h] = rcp_approx(m2p.x);
-                invj[h + 1] = rcp_approx(m2p.y);
+                invj[h] = rcp_nr(m2p.x);
+                invj[h + 1] = rcp_nr(m2p.y);
                 const float2 gp = mul2<PG>(pair(q2j, h), pair(invj, h));
                 gqj[h] = gp.x;
                 gqj[h + 1] = gp.y;
@@ -1105,8 +1136,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     for (int h = g; h < g + EVG; h += 2)
                         eval_pair2(K, pair(sj, h), pair(gqj, h), pair(invj, h), pair(Aj, h),
                                    make_float2(bj[h][0], bj[h + 1][0]), pre2[h >> 1],
-                                   pim2[h >> 1], evp[h >> 1], (lvm >> h) & 1u,
-                                   (lvm >> (h + 1)) & 1u);
+                                   pim2[h >> 1], (lvm >> h) & 1u, (lvm >> (h + 1)) & 1u);
                 }
             if constexpr (TINY) {
                 if (tiny) {
@@ -1118,10 +1148,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                                            : j == 2 ? bj[2][0] : bj[3][0];
                             tiny_contribution(K, 0, sv, gv, pick4(invj, j), pick4(Aj, j),
                                               fmaf(gv * K.kh[0], sv, bv), S.acc[R * lane + j][0]);
-                            evp[j >> 1] += 1u << (16 * (j & 1));
                         }
                 }
             }
+            evb += spread4(lvm | tiny);
             } else {
             // several frequencies: phase an'_f + kh_f X with X = c2 + g s (frequency
             // independent; WIDE: c2 = 0 and an'_f from the fp64 arc length), amplitude
@@ -1160,13 +1190,13 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         const float an = WIDE ? frac_rad(K.kappa64[f] * s64[j]) : S.ancf[f][pref[j]];
                         ph[j] = fmaf(K.kh[f], X[j], an);
                         eval_freq(K, f, ph[j], gqj[j], ais[j], aib[j], S.facc[f][j][lane],
-                                  evp[j >> 1], 16 * (j & 1), (lf >> j) & 1u);
+                                  (lf >> j) & 1u);
                     }
+                    evb += spread4(lf | tf);
                     if (TINY && tf) {
 #pragma unroll 1
                         for (int j = 0; j < R; ++j)
                             if ((tf >> j) & 1u) {
-                                evp[j >> 1] += 1u << (16 * (j & 1));
                                 tiny_contribution(
                                     K, f, pick4(sj, j), pick4(gqj, j), pick4(invj, j), pick4(Aj, j),
                                     pick4(ph, j),
@@ -1202,9 +1232,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             if (j & 1) pre2[j >> 1] = pim2[j >> 1] = make_float2(0.f, 0.f);  // pair flushed
         }
 #pragma unroll
-        for (int j = 0; j < R; ++j) S.evc[R * lane + j] += (evp[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-#pragma unroll
-        for (int i = 0; i < R / 2; ++i) evp[i] = 0;
+        for (int j = 0; j < R; ++j) S.evc[R * lane + j] += (evb >> (8 * j)) & 0xffu;
+        evb = 0;
         __syncwarp();  // every lane is done with this chunk's shared rows
     }
     // ---- the unit's partial sums (fp64) for fold_kernel, which adds the beam
@@ -1521,7 +1550,7 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
         unsigned long long h[4];
         cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, sp.st);
         cudaStreamSynchronize(sp.st);
-        fprintf(stderr, "bf hist: exact re-decision rounds %llu\n", h[2]);
+        fprintf(stderr, "bf hist: pend(<=2 surv) %llu pend(>=3 surv) %llu exact rounds %llu junction %llu\n", h[0], h[1], h[2], h[3]);
     }
 #endif
     return BF_OK;
