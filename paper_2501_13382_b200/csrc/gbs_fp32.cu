@@ -224,7 +224,8 @@ struct WarpSmem {
     // occupancy limit there)
     double acc[MF ? 1 : PATCH][NF][2];
     // several frequencies: the chunk's fp32 partial sums, [f][receiver j][lane]
-    float2 facc[MF ? NF : 1][MF ? R : 1][32];
+    // (receivers 2h, 2h+1 of lane l in facc[f][h][l] as (re, im, re, im))
+    float4 facc[MF ? NF : 1][MF ? R / 2 : 1][32];
     int evc[PATCH];          // evaluation counts of the unit
     double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
 };
@@ -266,15 +267,14 @@ __device__ __forceinline__ void tiny_contribution(const Fp32Consts &K, int f, fl
 // gq = q^2/m2, ais = A s/m2 and aib = A b/m2 shared across frequencies; omrel[f] folded
 // into the exponent (lomrel[f] = log2(omega_f/omega_0)).
 __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float ph, float gq,
-                                          float ais, float aib, float2 &acc, bool live) {
+                                          float ais, float aib, float &are, float &aim,
+                                          bool live) {
     const float sn = sin_approx(ph), cs = cos_approx(ph);
     const float e = ex2_approx(fmaf(gq, K.nhkbl2e[f], K.lomrel[f]));
     const float as = e * ais, ab = e * aib;
     if (live) {  // i * amp * (s + i b) * (cos + i sin)
-        float2 v = acc;
-        v.x = fmaf(-as, sn, fmaf(-ab, cs, v.x));
-        v.y = fmaf(as, cs, fmaf(-ab, sn, v.y));
-        acc = v;
+        are = fmaf(-as, sn, fmaf(-ab, cs, are));
+        aim = fmaf(as, cs, fmaf(-ab, sn, aim));
     }
 }
 
@@ -749,8 +749,10 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     for (int j = 0; j < R; ++j) {
         if (!(j & 1)) pre2[j >> 1] = pim2[j >> 1] = make_float2(0.f, 0.f);
         if constexpr (MF) {
+            if (!(j & 1)) {
 #pragma unroll
-            for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
+                for (int f = 0; f < NF; ++f) S.facc[f][j >> 1][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
     }
 
@@ -1185,12 +1187,30 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 }
                 {
                     float ph[R];
+                    // phase references an'_f of the receivers' rows: one load when the
+                    // item is a single-segment one (the same row for every receiver)
+                    float an[R];
+                    if constexpr (WIDE) {
 #pragma unroll
-                    for (int j = 0; j < R; ++j) {
-                        const float an = WIDE ? frac_rad(K.kappa64[f] * s64[j]) : S.ancf[f][pref[j]];
-                        ph[j] = fmaf(K.kh[f], X[j], an);
-                        eval_freq(K, f, ph[j], gqj[j], ais[j], aib[j], S.facc[f][j][lane],
-                                  (lf >> j) & 1u);
+                        for (int j = 0; j < R; ++j) an[j] = frac_rad(K.kappa64[f] * s64[j]);
+                    } else {
+                        an[0] = S.ancf[f][pref[0]];
+                        if ((surv & (surv - 1)) == 0) {
+                            an[1] = an[2] = an[3] = an[0];
+                        } else {
+#pragma unroll
+                            for (int j = 1; j < R; ++j) an[j] = S.ancf[f][pref[j]];
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < R; h += 2) {
+                        float4 v = S.facc[f][h >> 1][lane];
+                        ph[h] = fmaf(K.kh[f], X[h], an[h]);
+                        ph[h + 1] = fmaf(K.kh[f], X[h + 1], an[h + 1]);
+                        eval_freq(K, f, ph[h], gqj[h], ais[h], aib[h], v.x, v.y, (lf >> h) & 1u);
+                        eval_freq(K, f, ph[h + 1], gqj[h + 1], ais[h + 1], aib[h + 1], v.z, v.w,
+                                  (lf >> (h + 1)) & 1u);
+                        S.facc[f][h >> 1][lane] = v;
                     }
                     evb += spread4(lf | tf);
                     if (TINY && tf) {
@@ -1222,12 +1242,15 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
                     for (int f = 0; f < NF; ++f) {
                         const double2 v = pp[f];
-                        const float2 c = S.facc[f][j][lane];
+                        const float4 c4 = S.facc[f][j >> 1][lane];
+                        const float2 c = (j & 1) ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
                         pp[f] = make_double2(v.x + (double)c.x, v.y + (double)c.y);
                     }
                 }
+                if (j & 1) {
 #pragma unroll
-                for (int f = 0; f < NF; ++f) S.facc[f][j][lane] = make_float2(0.f, 0.f);
+                    for (int f = 0; f < NF; ++f) S.facc[f][j >> 1][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
             if (j & 1) pre2[j >> 1] = pim2[j >> 1] = make_float2(0.f, 0.f);  // pair flushed
         }

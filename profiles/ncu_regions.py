@@ -11,8 +11,9 @@ import sys
 
 MARKERS = [  # (region name, first line containing this text starts the region)
     ("pick4", "T pick4("), ("consts/helpers", "struct Fp32Consts"),
-    ("eval_pair", "void eval_pair("), ("phase_base", "void phase_base("),
+    ("eval (tiny/freq/pair2)", "void tiny_contribution("), ("clamp2", "float clamp2("),
     ("classify", "float patch_dist("), ("behind_mask", "unsigned behind_mask("),
+    ("junction", "struct Junction {"),
     ("exact_pick", "struct ExactPick"), ("exact_pending", "void exact_pending("),
     ("stage", "void stage_rows("), ("unit_head", "void run_unit("),
     ("gather", "// ---- gather the next"), ("rows", "// ---- row capacity"),
