@@ -105,6 +105,7 @@ struct Fp32Work {
     const double4 *p1;        // per row: direction xyz, s0
     const float *amp;         // per row: amplitude factor A
     float4 *prl;              // sorted receiver -> patch-local fp32 coordinates, |r|^2
+    double4 *pos64;           // sorted receiver -> fp64 position (exact re-decisions)
     double4 *pcen;            // per patch: centre xyz, radius
     float4 *pbox;             // per patch: bounding-box half extents xyz, radius (patch-local)
     double2 *part;            // per (beam range, sorted receiver, frequency): unit partial sum

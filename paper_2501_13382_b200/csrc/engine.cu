@@ -106,7 +106,7 @@ struct PinBuf {
 enum BufId {
     B_ORIGIN, B_DIR, B_E1, B_E2, B_LEN, B_S0, B_REFL, B_NSEGS, B_W, B_OBS, B_ACC, B_EVALS,
     B_KEYS, B_KEYS2, B_VALS, B_VALS2, B_CUB, B_RLOC, B_CENTRE, B_BBOX, B_TBOX, B_STATS, B_CAND,
-    B_QOBS, B_QBEAM, B_QOUT, B_PRL, B_PCEN, B_PBOX, B_CBOX, B_WLBITS, B_WLTIGHT, B_COUNT
+    B_QOBS, B_QBEAM, B_QOUT, B_PRL, B_POS64, B_PCEN, B_PBOX, B_CBOX, B_WLBITS, B_WLTIGHT, B_COUNT
 };
 
 // Per-slot device workspaces of one beam group.
@@ -819,6 +819,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
     w0.n_patches = (base.n_obs + P - 1) / P;
     w0.n_pad = w0.n_patches * P;
     BF_TRY(c->get(B_PRL, (size_t)base.n_obs, &w0.prl));
+    BF_TRY(c->get(B_POS64, (size_t)base.n_obs, &w0.pos64));
     BF_TRY(c->get(B_PCEN, (size_t)w0.n_patches, &w0.pcen));
     BF_TRY(c->get(B_PBOX, (size_t)w0.n_patches, &w0.pbox));
     BF_TRY(launch_fp32_patches(base, t, w0, st));

@@ -227,7 +227,29 @@ struct WarpSmem {
     // (receivers 2h, 2h+1 of lane l in facc[f][h][l] as (re, im, re, im))
     float4 facc[MF ? NF : 1][MF ? R / 2 : 1][32];
     int evc[PATCH];          // evaluation counts of the unit
-    double p64[PATCH][3];    // fp64 receiver positions (exact re-decisions)
+    // fp64 receiver positions (exact re-decisions); the several-frequency kernels read
+    // them from the sorted global copy w.pos64 instead (shared memory is their occupancy
+    // limit)
+    double p64[MF ? 1 : PATCH][3];
+};
+
+// fp64 position of receiver j of the lane: the lane's slice of S.p64 (one frequency) or
+// the sorted global copy at sb + j (several frequencies)
+struct D3 {
+    double x, y, z;
+};
+template <bool G>
+struct Recv64 {
+    const double (*p64)[3];  // S.p64 + R * lane (G = false)
+    const double4 *pos;      // w.pos64 + sb (G = true)
+    __device__ __forceinline__ D3 operator()(int j) const {
+        if constexpr (G) {
+            const double4 v = pos[j];
+            return D3{v.x, v.y, v.z};
+        } else {
+            return D3{p64[j][0], p64[j][1], p64[j][2]};
+        }
+    }
 };
 
 // Gaussian-beam contribution of one pair (kernels.py:377-399): field = phi refl
@@ -445,8 +467,9 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
 // Live mask of the R receivers of a single-segment-0 beam whose patch reaches the
 // launch plane: behind = proj < 0 (kernels.py:348,375); |proj| within the fp32
 // error bound is re-decided with the reference's exact fp64 projection.
+template <bool G>
 __device__ __forceinline__ unsigned behind_mask(const Fp32Work &w, const float (&pj)[R],
-                                             const double (*p64)[3], int nvalid, float D,
+                                             const Recv64<G> &P64, int nvalid, float D,
                                              int64_t row, unsigned &ties) {
     const float tolp = PROJ_ERR * D;
     unsigned m = 0, amb = 0;
@@ -466,8 +489,8 @@ __device__ __forceinline__ unsigned behind_mask(const Fp32Work &w, const float (
         for (; amb; amb &= amb - 1) {
             const int j = __ffs(amb) - 1;
             // proj of kernels.py:328-331, reference operation order, no FMA
-            const double wx = __dsub_rn(p64[j][0], ox), wy = __dsub_rn(p64[j][1], oy),
-                         wz = __dsub_rn(p64[j][2], oz);
+            const D3 P = P64(j);
+            const double wx = __dsub_rn(P.x, ox), wy = __dsub_rn(P.y, oy), wz = __dsub_rn(P.z, oz);
             const double proj =
                 __dadd_rn(__dadd_rn(__dmul_rn(wx, dx), __dmul_rn(wy, dy)), __dmul_rn(wz, dz));
             if (!(proj < 0.0)) m |= 1u << j;
@@ -503,12 +526,12 @@ __device__ __forceinline__ Junction load_junction(const double4 *__restrict__ p0
 }
 
 // true -> segment k+1 is the reference's nearest segment (strict <: ties keep k)
-__device__ __forceinline__ bool junction_pick(const Junction &J, const double (&p)[3]) {
-    const double vx = __dsub_rn(__dsub_rn(p[0], J.ox), J.lx);
-    const double vy = __dsub_rn(__dsub_rn(p[1], J.oy), J.ly);
-    const double vz = __dsub_rn(__dsub_rn(p[2], J.oz), J.lz);
+__device__ __forceinline__ bool junction_pick(const Junction &J, const D3 &p) {
+    const double vx = __dsub_rn(__dsub_rn(p.x, J.ox), J.lx);
+    const double vy = __dsub_rn(__dsub_rn(p.y, J.oy), J.ly);
+    const double vz = __dsub_rn(__dsub_rn(p.z, J.oz), J.lz);
     const double da = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-    const double wx = __dsub_rn(p[0], J.bx), wy = __dsub_rn(p[1], J.by), wz = __dsub_rn(p[2], J.bz);
+    const double wx = __dsub_rn(p.x, J.bx), wy = __dsub_rn(p.y, J.by), wz = __dsub_rn(p.z, J.bz);
     const double db = __dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz));
     return db < da;
 }
@@ -526,8 +549,8 @@ __device__ __forceinline__ ExactPick exact_pick(const double4 *__restrict__ p0,
                                              const double4 *__restrict__ p1, int64_t row0,
                                              const float4 *geo0, const float4 *geo1,
                                              unsigned surv, int kf, float rx, float ry, float rz,
-                                             float best, float Db, const double (&p)[3]) {
-    const double px = p[0], py = p[1], pz = p[2];
+                                             float best, float Db, const D3 &p) {
+    const double px = p.x, py = p.y, pz = p.z;
     ExactPick e{0.0, 0.0, 0.0, -1};
     // pass 1 (fp32): contenders, the segments within the fp32 error of two distances of
     // the fp32 best (tight bound, DESIGN 5.8)
@@ -606,7 +629,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
                                               float Db, int lane, float (&sj)[R],
                                               float (&q2j)[R], float (&Aj)[R],
                                               float (&bj)[R][1], int (&pref)[R], unsigned &lvm,
-                                              unsigned &ties, const Fp32Work &w) {
+                                              unsigned &ties, const Fp32Work &w, const Recv64<MF> &P64) {
     ties += __popc(pend);
     // two adjacent candidates k, k+1 (most multi items): a receiver that projects
     // beyond the end of k and before the start of k+1 is decided like the corner wedge
@@ -621,7 +644,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
         const ExactPick e = exact_pick(w.p0, w.p1, row0,
                                        S.geo0 + r0, S.geo1 + r0, surv, pick4(kb, j), x, y, z,
-                                       pick4(best, j), Db, S.p64[R * lane + j]);
+                                       pick4(best, j), Db, P64(j));
         if (e.bk == 0 && e.bt == 0.0 && e.bp < 0.0) continue;  // behind
         const int k = e.bk;
         const float4 g1 = S.geo1[r0 + k];
@@ -714,6 +737,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     const int32_t *perm = tl.perm + sb;       // observer index of receiver j = perm[j]
     const int nvalid =  // receivers j < nvalid are real
         tl.n - sb < R ? (tl.n - sb > 0 ? (int)(tl.n - sb) : 0) : R;
+    const Recv64<MF> P64{S.p64 + (MF ? 0 : R * lane), w.pos64 + sb};
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         float4 rl = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -732,9 +756,11 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         S.evc[R * lane + j] = 0;
         if (j < nvalid) {
             const int64_t oi = perm[j];
-            S.p64[R * lane + j][0] = a.obs[3 * oi];
-            S.p64[R * lane + j][1] = a.obs[3 * oi + 1];
-            S.p64[R * lane + j][2] = a.obs[3 * oi + 2];
+            if constexpr (!MF) {
+                S.p64[R * lane + j][0] = a.obs[3 * oi];
+                S.p64[R * lane + j][1] = a.obs[3 * oi + 1];
+                S.p64[R * lane + j][2] = a.obs[3 * oi + 2];
+            }
         }
     }
     // fp32 partial sums of the chunk: registers with one frequency, shared memory
@@ -931,7 +957,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     float pj[R];
 #pragma unroll
                     for (int j = 0; j < R; ++j) pj[j] = dlj[j] + g1.w;
-                    lvm = behind_mask(w, pj, S.p64 + R * lane, nvalid, __int_as_float(dsc.w),
+                    lvm = behind_mask(w, pj, P64, nvalid, __int_as_float(dsc.w),
                                       row0 + k, ties);
                 }
             } else {
@@ -1057,7 +1083,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         if (!((jp >> j) & 1u)) continue;
-                        const bool wb = junction_pick(J, S.p64[R * lane + j]);
+                        const bool wb = junction_pick(J, P64(j));
                         const float4 g1 = wb ? g1b : g1a;
                         const float4 g2 = wb ? g2b : g2a;
                         const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
@@ -1077,7 +1103,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #endif
                 if (__any_sync(0xffffffffu, pend != 0))
                     exact_pending<NF, MF>(a, K, S, row0, r0, surv, pend, rx, ry, rz, rr, best, kb,
-                                      Db, lane, sj, q2j, Aj, bj, pref, lvm, ties, w);
+                                      Db, lane, sj, q2j, Aj, bj, pref, lvm, ties, w, P64);
             }
             // ---- shared tail: cutoff (kernels.py:384) and contributions (:386-399)
             nbp += __popc(lvm);
@@ -1095,9 +1121,9 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     if ((lvm >> j) & 1u) {
                         const int64_t g = S.rowinfo[pref[j] & (ROWS<MF> - 1)];
                         const double4 o = w.p0[g], d = w.p1[g];
-                        const double *P = S.p64[R * lane + j];
-                        const double wx = __dsub_rn(P[0], o.x), wy = __dsub_rn(P[1], o.y),
-                                     wz = __dsub_rn(P[2], o.z);
+                        const D3 P = P64(j);
+                        const double wx = __dsub_rn(P.x, o.x), wy = __dsub_rn(P.y, o.y),
+                                     wz = __dsub_rn(P.z, o.z);
                         const double proj = __dadd_rn(
                             __dadd_rn(__dmul_rn(wx, d.x), __dmul_rn(wy, d.y)), __dmul_rn(wz, d.z));
                         const double t = proj < 0.0 ? 0.0 : (proj > o.w ? o.w : proj);
@@ -1284,7 +1310,10 @@ __device__ __forceinline__ bool wide_patch(const Fp32Work &w, int64_t p) {
 // One launch per patch class, on two streams: WIDE = false takes queue positions
 // [0, n_units - n_wide), WIDE = true the rest (unit_keys_kernel sorts wide patches last).
 template <int NF, bool WIDE, bool TINY>
-__global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5 ? 3 : 2))
+#ifndef BF_MINB_MF
+#define BF_MINB_MF 4
+#endif
+__global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5 ? BF_MINB_MF : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w, const Fp32Consts K,
                     GbsStats *stats) {
     constexpr bool MF = NF > 1 || WIDE;
@@ -1373,7 +1402,8 @@ __global__ void rows_slice_kernel(const Rows src, int64_t b0, int64_t nb, int64_
 // One warp per patch: fp64 bounding-box centre c_P, patch-local r = p - c_P in
 // fp32 (w = |r|^2) and the patch radius (max |r|, padded).
 __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
-                             int64_t n_patches, float4 *prl, double4 *pcen, float4 *pbox) {
+                             int64_t n_patches, float4 *prl, double4 *pos64, double4 *pcen,
+                             float4 *pbox) {
     const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (p >= n_patches) return;
@@ -1390,6 +1420,7 @@ __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
             px[j] = obs[3 * oi];
             py[j] = obs[3 * oi + 1];
             pz[j] = obs[3 * oi + 2];
+            pos64[si] = make_double4(px[j], py[j], pz[j], 0.0);
             mn[0] = fmin(mn[0], px[j]); mx[0] = fmax(mx[0], px[j]);
             mn[1] = fmin(mn[1], py[j]); mx[1] = fmax(mx[1], py[j]);
             mn[2] = fmin(mn[2], pz[j]); mx[2] = fmax(mx[2], pz[j]);
@@ -1660,7 +1691,7 @@ int launch_rows_pack(const GbsArgs &a, const int64_t *start, double4 *p0, double
 int launch_fp32_patches(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStream_t st) {
     if (w.n_patches > 0) {
         patch_kernel<<<(unsigned)((w.n_patches * 32 + 127) / 128), 128, 0, st>>>(
-            a.obs, t.n, t.perm, w.n_patches, w.prl, w.pcen, w.pbox);
+            a.obs, t.n, t.perm, w.n_patches, w.prl, w.pos64, w.pcen, w.pbox);
         note_launch();
     }
     BF_TRY_CUDA(cudaGetLastError());
