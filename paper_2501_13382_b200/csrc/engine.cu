@@ -620,7 +620,7 @@ struct GroupPlan {
 };
 
 // Beam groups of whole ranges sized so that NSLOT groups' workspaces fit the budget.
-// The host-buffer path ramps the group size up from one range (1, 8, 64, ...) so the
+// The host-buffer path ramps the group size up from one range (1, 4, 16, ...) so the
 // first group's packing and copy are short and the later ones hide behind the summation
 // (few groups: each group's kernel ends in a tail of long units near the source).
 void plan_groups(DeviceCtx *c, int64_t nb, int64_t max_seg, int nf, int64_t n_tiles,
@@ -641,12 +641,18 @@ void plan_groups(DeviceCtx *c, int64_t nb, int64_t max_seg, int nf, int64_t n_ti
     max_r = std::min(max_r, std::max<int64_t>(1, (((int64_t)1 << 31) - 1) / std::max<int64_t>(n_patches, 1)));
     max_r = std::min(max_r, g->n_ranges);
     g->groups.clear();
-    int64_t q = 0, step = host ? 1 : max_r;
+#ifndef BF_HOST_FIRST
+#define BF_HOST_FIRST 1
+#endif
+#ifndef BF_HOST_RAMP
+#define BF_HOST_RAMP 4  // measured on config 3: 8 -> 447.6 ms, 4 -> 444.9, 3 -> 444.7, uniform groups worse
+#endif
+    int64_t q = 0, step = host ? std::min<int64_t>(BF_HOST_FIRST, max_r) : max_r;
     while (q < g->n_ranges) {
         const int64_t n = std::min(step, g->n_ranges - q);
         g->groups.emplace_back(q, q + n);
         q += n;
-        step = std::min(max_r, step * 8);
+        step = std::min(max_r, step * BF_HOST_RAMP);
     }
 }
 
