@@ -66,12 +66,17 @@ int check_cuda(cudaError_t e, const char *what) {
 
 namespace {
 
+// Bumped whenever a workspace (device or pinned) is reallocated or the statistics events
+// are recreated: a captured call graph (GraphCache) is only replayed while it is unchanged.
+std::atomic<uint64_t> g_pool_gen{0};
+
 // Grow-only device buffer.
 struct Buf {
     void *p = nullptr;
     size_t cap = 0;
     int get(size_t bytes, void **out) {
         if (bytes > cap) {
+            g_pool_gen.fetch_add(1);
             if (p) cudaFree(p);
             p = nullptr;
             cap = 0;
@@ -90,6 +95,7 @@ struct PinBuf {
     size_t cap = 0;
     int get(size_t bytes, void **out) {
         if (bytes > cap) {
+            g_pool_gen.fetch_add(1);
             if (p) cudaFreeHost(p);
             p = nullptr;
             cap = 0;
@@ -156,6 +162,18 @@ struct DeviceCtx {
     bool done_valid = false;
     cudaEvent_t pro = nullptr;  // end of a call's prologue (tiling) on its stream
     int64_t budget = 0;         // group-workspace budget in bytes (0: automatic)
+    // Small fp32 device calls repeated with identical arguments replay a captured graph
+    // of the whole call (tiling .. fold): one launch instead of ~30.  The first call with
+    // a key runs eagerly, the second is captured, later ones replay while no workspace has
+    // been reallocated since (g_pool_gen).
+    struct GraphCache {
+        std::vector<double> key;
+        bool seen = false;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t gen = 0;
+        int sb = -1;        // statistics buffer the graph writes
+        int launches = 0;   // library kernels in the graph
+    } gc;
     std::mutex mu;
     Buf buf[B_COUNT];
     PinBuf hpin[H_COUNT];
@@ -256,8 +274,17 @@ struct PendingStats {
 };
 thread_local PendingStats g_ps;
 
+// While a call is being captured into a graph (GraphCache) the statistics events are
+// recorded as external event nodes, so every replay records them for real.
+thread_local bool g_capturing = false;
+cudaError_t rec_ext(cudaEvent_t e, cudaStream_t s) {
+    return g_capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                       : cudaEventRecord(e, s);
+}
+
 int stats_events(int dev) {
     if (g_ps.dev == dev && g_ps.buf[0].ready) return BF_OK;
+    g_pool_gen.fetch_add(1);
     for (StatsBuf &b : g_ps.buf) {
         if (b.ready) {
             cudaEventSynchronize(b.ready);
@@ -330,6 +357,51 @@ int stats_next(StatsBuf **out) {
     g_ps.cur = i;
     *out = &b;
     return BF_OK;
+}
+
+// ------------------------------------------------------------ small sort ----
+
+// Stable key-value radix sort of n <= SMALL_SORT_N pairs in one CTA (the unit queue of a
+// small call: one launch instead of cub's multi-kernel device sort; the same order, both
+// sorts being stable).  Keys past n are padded with 2^end_bit - 1, above every real key.
+constexpr int SMALL_SORT_T = 512, SMALL_SORT_I = 16;
+constexpr int64_t SMALL_SORT_N = SMALL_SORT_T * SMALL_SORT_I;
+using SmallSort = cub::BlockRadixSort<uint64_t, SMALL_SORT_T, SMALL_SORT_I, int32_t>;
+
+__global__ void __launch_bounds__(SMALL_SORT_T)
+    small_sort_kernel(const uint64_t *keys, const int32_t *vals, int n, int end_bit,
+                      int32_t *out) {
+    extern __shared__ __align__(16) unsigned char smem_sort[];
+    auto &tmp = *reinterpret_cast<typename SmallSort::TempStorage *>(smem_sort);
+    uint64_t k[SMALL_SORT_I];
+    int32_t v[SMALL_SORT_I];
+    const uint64_t pad = (end_bit >= 64 ? ~0ull : ((1ull << end_bit) - 1ull));
+#pragma unroll
+    for (int i = 0; i < SMALL_SORT_I; ++i) {
+        const int idx = threadIdx.x * SMALL_SORT_I + i;  // blocked arrangement
+        k[i] = idx < n ? keys[idx] : pad;
+        v[i] = idx < n ? vals[idx] : 0;
+    }
+    SmallSort(tmp).Sort(k, v, 0, end_bit);
+#pragma unroll
+    for (int i = 0; i < SMALL_SORT_I; ++i) {
+        const int idx = threadIdx.x * SMALL_SORT_I + i;
+        if (idx < n) out[idx] = v[i];
+    }
+}
+
+int small_sort(const uint64_t *keys, const int32_t *vals, int n, int end_bit, int32_t *out,
+               cudaStream_t st) {
+    static bool attr = false;  // benign race: the same value
+    const int smem = (int)sizeof(typename SmallSort::TempStorage);
+    if (!attr) {
+        BF_TRY_CUDA(cudaFuncSetAttribute(small_sort_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    small_sort_kernel<<<1, SMALL_SORT_T, smem, st>>>(keys, vals, n, end_bit, out);
+    note_launch();
+    return check_cuda(cudaGetLastError(), "small_sort_kernel");
 }
 
 // ------------------------------------------------------------ tiling ----
@@ -941,17 +1013,22 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
                 BF_TRY(s.get(S_UVALS2, (size_t)nu, &v1));
                 BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
                 const int end_bit = 40;  // wide << 39 | bucket (7 bits) << 32 | range
-                cub::DoubleBuffer<uint64_t> dk(k0, k1);
-                cub::DoubleBuffer<int32_t> dv(v0, v1);
-                size_t tb = 0;
-                BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nu, 0,
-                                                            end_bit, s.ss));
-                void *tmp;
-                BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
-                BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nu, 0,
-                                                            end_bit, s.ss));
-                note_launch();
-                w.unit_order = dv.Current();
+                if (nu <= SMALL_SORT_N) {  // one CTA, one launch (small calls)
+                    BF_TRY(small_sort(k0, v0, (int)nu, end_bit, v1, s.ss));
+                    w.unit_order = v1;
+                } else {
+                    cub::DoubleBuffer<uint64_t> dk(k0, k1);
+                    cub::DoubleBuffer<int32_t> dv(v0, v1);
+                    size_t tb = 0;
+                    BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nu, 0,
+                                                                end_bit, s.ss));
+                    void *tmp;
+                    BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
+                    BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nu, 0,
+                                                                end_bit, s.ss));
+                    note_launch();
+                    w.unit_order = dv.Current();
+                }
             }
             // ---- compacted work list: sized by its bound (tiles x beams), no host sync
             BF_TRY(s.get(S_WLITEMS, (size_t)(t.n_tiles * gg.n_beams + 1), &w.wl_items));
@@ -959,7 +1036,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             BF_TRY(s.get(S_PART, (size_t)(w.n_ranges * w.n_pad * ag.nf), &w.part));
             BF_TRY(s.get(S_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
             if (!timed) {
-                BF_TRY_CUDA(cudaEventRecord(sb->t0, s.ss));
+                BF_TRY_CUDA(rec_ext(sb->t0, s.ss));
                 timed = true;
             }
             BF_TRY(launch_gbs_fp32(gg, tg, w, d_stats, StreamPair{s.ss, s.sw, s.fork, s.join}));
@@ -975,11 +1052,14 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             s.freed_valid = true;
         }
     }
-    BF_TRY_CUDA(cudaEventRecord(sb->t1, st));
+    BF_TRY_CUDA(rec_ext(sb->t1, st));
     // ---- statistics: copied back asynchronously, reduced on request (bf_last_stats)
-    if (!sb->h_stats)
+    if (!sb->h_stats) {
+        g_pool_gen.fetch_add(1);
         BF_TRY_CUDA(cudaHostAlloc(&sb->h_stats, sizeof(GbsStats), cudaHostAllocPortable));
+    }
     if (sb->cand_cap < (size_t)(4 * t.n_tiles)) {
+        g_pool_gen.fetch_add(1);
         if (sb->h_cand) cudaFreeHost(sb->h_cand);
         sb->h_cand = nullptr;
         sb->cand_cap = 0;
@@ -991,12 +1071,82 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
                                 st));
     BF_TRY_CUDA(cudaMemcpyAsync(sb->h_cand, d_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
                                 cudaMemcpyDeviceToHost, st));
-    BF_TRY_CUDA(cudaEventRecord(sb->ready, st));
+    BF_TRY_CUDA(rec_ext(sb->ready, st));
     sb->inflight = true;
     sb->n_tiles = t.n_tiles;
     sb->tile = t.tile;
     sb->n_obs = base.n_obs;
     g_ps.pending = true;
+    return BF_OK;
+}
+
+// Small device calls (see DeviceCtx::GraphCache): identical repeated calls replay a graph
+// captured from the second one.  The graph reads the caller's buffers at replay time, so
+// only the arguments (pointers, sizes, scalars, frequencies, flags, stream) form the key.
+#ifndef BF_GRAPHS
+#define BF_GRAPHS 1
+#endif
+#ifndef BF_GRAPH_MAX_PAIRS
+#define BF_GRAPH_MAX_PAIRS 268435456.0  // 2^28 beam-receiver pairs (calls of ~1 ms or less)
+#endif
+int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t nf, int flags,
+                   int device, cudaStream_t st) {
+    auto P = [](const void *p) { return (double)(uintptr_t)p; };
+    std::vector<double> key = {
+        (double)device, P(st), P(a.seg_origin), P(a.seg_dir), P(a.seg_len), P(a.seg_s0),
+        P(a.seg_refl), P(a.n_segs), P(a.weights), P(a.obs), P(a.acc), P(a.evals),
+        (double)a.n_beams, (double)a.max_seg, (double)a.n_obs, (double)nf, (double)a.acc_stride,
+        a.c, a.width_b, a.phi_amp, (double)a.use_cutoff, (double)flags, (double)c->budget};
+    for (int64_t f = 0; f < nf; ++f) key.push_back(omegas[f]);
+    DeviceCtx::GraphCache &g = c->gc;
+    const bool same = g.seen && g.key == key;
+    if (same && g.exec && g.gen == g_pool_gen.load()) {
+        // replay: the statistics land in the buffer the graph writes
+        stats_begin(a.n_obs * a.n_beams);
+        BF_TRY(stats_events(c->dev));
+        if (g.gen != g_pool_gen.load()) return run_fp32(c, a, omegas, nf, false, flags, st);
+        StatsBuf &b = g_ps.buf[g.sb];  // (a replay overwrites the previous one's statistics)
+        BF_TRY_CUDA(cudaGraphLaunch(g.exec, st));
+        note_launch(g.launches);
+        g_ps.cur = g.sb;
+        b.inflight = true;
+        g_ps.pending = true;
+        return BF_OK;
+    }
+    if (g.exec) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+    }
+    if (!same) {  // first call with this key: eager
+        g.key = key;
+        g.seen = true;
+        return run_fp32(c, a, omegas, nf, false, flags, st);
+    }
+    // second call: capture the whole call (the slot streams join the capture through the
+    // call's fork/join events; waits on events of earlier calls are dropped -- the graph
+    // launch itself is ordered after them on st)
+    for (Slot &sl : c->slot) sl.freed_valid = false;
+    BF_TRY_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    const uint64_t n0 = g_launches.load();
+    g_capturing = true;
+    const int rc = run_fp32(c, a, omegas, nf, false, flags, st);
+    g_capturing = false;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (rc != BF_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    BF_TRY_CUDA(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    BF_TRY_CUDA(ie);
+    g.launches = (int)(g_launches.load() - n0);
+    g.gen = g_pool_gen.load();
+    g.sb = g_ps.cur;
+    for (Slot &sl : c->slot) sl.freed_valid = false;  // their events were capture-internal
+    BF_TRY_CUDA(cudaGraphLaunch(g.exec, st));
+    g_ps.buf[g.sb].inflight = true;
     return BF_OK;
 }
 
@@ -1189,6 +1339,8 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
     if (precision == BF_PRECISION_FP64) {
         stats_begin(a.n_obs * a.n_beams);
         BF_TRY(run_fp64(a, omegas, nf, st));
+    } else if (BF_GRAPHS && (double)a.n_obs * (double)a.n_beams <= BF_GRAPH_MAX_PAIRS) {
+        BF_TRY(run_fp32_graph(ctx, a, omegas, nf, flags, device, st));
     } else {
         BF_TRY(run_fp32(ctx, a, omegas, nf, false, flags, st));
     }

@@ -651,3 +651,55 @@ def test_tracer_cluster_culling_equals_exhaustive(src):
                  "n_segs", "n_refls"):
         assert torch.equal(getattr(a, name), getattr(b, name)), name
     assert int(a.n_refls.max()) >= 2  # the rays do bounce between buildings
+
+
+def test_repeated_small_calls_replay_a_graph_bitexact():
+    """Identical small device calls: the first runs eagerly, the second is captured into a
+    CUDA graph, later ones replay it (engine.cu run_fp32_graph).  The sequence must equal,
+    bit for bit, the same calls made with a changing memory budget (a different key every
+    call, so always eager; the budget never changes a one-group call's bits), statistics
+    included; a call that reallocates the workspaces in between invalidates the graph."""
+    import torch
+
+    from paper_2501_13382_b200 import _lib, kernels
+    b = load_case("city_street")
+    dev = torch.device("cuda", 0)
+    t = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa
+    args = [t(b["seg_origin"]), t(b["seg_dir"]), t(b["seg_e1"]), t(b["seg_e2"]),
+            t(b["seg_len"]), t(b["seg_s0"]), t(b["seg_refl"]), t(b["n_segs"], torch.int32),
+            b["max_seg"], t(b["weights"]), t(b["obs"]), b["omegas"], float(b["c"]),
+            -float(b["beam_param_im"]), 1.0, True]
+    n_obs, nb = b["obs"].shape[0], b["n_segs"].shape[0]
+
+    def sequence(budgets, big_after=None):
+        acc = torch.zeros((n_obs, 1), dtype=torch.complex128, device=dev)
+        ev = torch.zeros(n_obs, dtype=torch.int64, device=dev)
+        out, evs = [], []
+        for i, bud in enumerate(budgets):
+            _lib.set_memory_budget(0, bud)
+            kernels.gbs_accumulate(*args, acc, ev, 0, n_obs, 0, nb, precision="fp32")
+            out.append(acc.cpu().numpy().copy())
+            st = _lib.last_stats()
+            evs.append((st["tie_pairs"], st["nonbehind_pairs"], st["tight_pairs"],
+                        tuple(st["patch_beams"].values())))
+            if big_after == i:  # a larger call grows the workspaces (new generation)
+                big = torch.cat([args[10]] * 4)
+                a2 = torch.zeros((big.shape[0], 1), dtype=torch.complex128, device=dev)
+                e2 = torch.zeros(big.shape[0], dtype=torch.int64, device=dev)
+                kernels.gbs_accumulate(*args[:10], big, *args[11:], a2, e2, 0, big.shape[0],
+                                       0, nb, precision="fp32")
+        _lib.set_memory_budget(0, 0)
+        return out, evs
+
+    n0 = _lib.launch_count()
+    ref, ref_st = sequence([(1 << 30) + i for i in range(5)])  # always eager
+    n_eager = _lib.launch_count() - n0
+    n0 = _lib.launch_count()
+    got, got_st = sequence([1 << 30] * 5)                      # eager, capture, 3 replays
+    assert _lib.launch_count() - n0 == n_eager  # replays count the graph's kernels
+    for r, g in zip(ref, got):
+        assert np.array_equal(r, g)
+    assert ref_st == got_st
+    got2, _ = sequence([1 << 30] * 5, big_after=2)             # graph invalidated midway
+    for r, g in zip(ref, got2):
+        assert np.array_equal(r, g)
