@@ -128,7 +128,10 @@ struct StreamPair {
 };
 
 // Launchers (return BF_OK or an error status).
-int launch_gbs_fp64(const GbsArgs &a, cudaStream_t st);
+// oracle-mode summation of the observers in tile order over each tile's tight work list
+// (a.obs / a.acc / a.evals indexed by perm[sorted position])
+int launch_gbs_fp64(const GbsArgs &a, const int32_t *perm, int tile, const uint32_t *tbits,
+                    int64_t n_words, cudaStream_t st);
 int gbs_fp32_tile();
 int gbs_fp32_patch();
 int64_t gbs_fp32_range_beams(int64_t n_beams, int nf);

@@ -1152,14 +1152,52 @@ int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t
 
 // The fp64 (oracle-mode) operator on device-resident LOCAL ranges, frequency groups of
 // <= BF_MAXF (one thread per observer continues acc in ascending beam order).
-int run_fp64(const GbsArgs &base, const double *omegas, int64_t nf, cudaStream_t st) {
+// base: device padded rows of the call's beams; t: the tiling of base.obs.  Beams go in
+// groups whose work-list bitmasks fit the budget: compact rows and the tight (tile, beam)
+// list of the group on the work slot's stream, then the oracle-mode kernel on st over
+// each tile's list (beams ascending within and across groups: the dense loop's bits).
+constexpr int FP64_SLOT = NSLOT - 1;  // (the host path stages its chunks in slots 0, 1)
+int run_fp64(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf,
+             const Tiling &t, cudaStream_t st) {
     if (base.n_obs <= 0 || base.n_beams <= 0 || nf <= 0) return BF_OK;
-    for (int64_t f0 = 0; f0 < nf; f0 += BF_MAXF) {
-        GbsArgs ag = base;
-        ag.nf = (int)std::min<int64_t>(BF_MAXF, nf - f0);
-        for (int f = 0; f < BF_MAXF; ++f) ag.omegas[f] = f < ag.nf ? omegas[f0 + f] : 0.0;
-        ag.acc = base.acc + 2 * f0;
-        BF_TRY(launch_gbs_fp64(ag, st));
+    double wmin = INFINITY;
+    for (int64_t f = 0; f < nf; ++f) wmin = omegas[f] < wmin ? omegas[f] : wmin;
+    const int64_t per_beam = t.n_tiles / 4 + 1 + base.max_seg * 68 + 16;
+    int64_t G = std::max<int64_t>(32, group_budget(c) / 2 / std::max<int64_t>(per_beam, 1));
+    G = std::min<int64_t>(G / 32 * 32, ((int64_t)1 << 27) / std::max<int64_t>(base.max_seg, 1));
+    Slot &s = c->slot[FP64_SLOT];
+    for (int64_t b0 = 0; b0 < base.n_beams; b0 += G) {
+        GbsArgs gg = base;
+        gg.n_beams = std::min(G, base.n_beams - b0);
+        const int64_t r0 = b0 * base.max_seg;
+        gg.seg_origin = base.seg_origin + 3 * r0;
+        gg.seg_dir = base.seg_dir + 3 * r0;
+        gg.seg_e1 = base.seg_e1 + 3 * r0;
+        gg.seg_e2 = base.seg_e2 + 3 * r0;
+        gg.seg_len = base.seg_len + r0;
+        gg.seg_s0 = base.seg_s0 + r0;
+        gg.seg_refl = base.seg_refl + r0;
+        gg.n_segs = base.n_segs + b0;
+        gg.weights = base.weights + b0;
+        BF_TRY_CUDA(cudaEventRecord(c->pro, st));  // the slot's buffers are free again
+        BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->pro, 0));
+        Rows rv;
+        BF_TRY(rows_from_device(gg, s, &rv));
+        const int64_t n_words = (gg.n_beams + 31) / 32;
+        uint32_t *bits, *tbits;
+        BF_TRY(s.get(S_WLBITS, (size_t)(t.n_tiles * n_words), &bits));
+        BF_TRY(s.get(S_WLTIGHT, (size_t)(t.n_tiles * n_words), &tbits));
+        BF_TRY(launch_worklist(gg, rv, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, 0, 0,
+                               nullptr, nullptr, s.ss));
+        BF_TRY_CUDA(cudaEventRecord(s.kdone, s.ss));
+        BF_TRY_CUDA(cudaStreamWaitEvent(st, s.kdone, 0));
+        for (int64_t f0 = 0; f0 < nf; f0 += BF_MAXF) {
+            GbsArgs ag = gg;
+            ag.nf = (int)std::min<int64_t>(BF_MAXF, nf - f0);
+            for (int f = 0; f < BF_MAXF; ++f) ag.omegas[f] = f < ag.nf ? omegas[f0 + f] : 0.0;
+            ag.acc = base.acc + 2 * f0;
+            BF_TRY(launch_gbs_fp64(ag, t.perm, t.tile, tbits, n_words, st));
+        }
     }
     return BF_OK;
 }
@@ -1170,6 +1208,8 @@ int run_fp64(const GbsArgs &base, const double *omegas, int64_t nf, cudaStream_t
 int run_fp64_host(DeviceCtx *c, const GbsArgs &h, const double *omegas, int64_t nf,
                   cudaStream_t st) {
     if (h.n_obs <= 0 || h.n_beams <= 0 || nf <= 0) return BF_OK;
+    Tiling t;
+    BF_TRY(build_tiling(c, h.obs, h.n_obs, false, st, &t));
     const int64_t S = h.max_seg;
     const int64_t per_beam = S * (4 * 24 + 3 * 8) + 4 + 8;
     const int64_t chunk = std::max<int64_t>(
@@ -1218,7 +1258,7 @@ int run_fp64_host(DeviceCtx *c, const GbsArgs &h, const double *omegas, int64_t 
         g.weights = (const double *)(dp + off[7]);
         g.n_segs = (const int32_t *)(dp + off[8]);
         g.n_beams = nb;
-        BF_TRY(run_fp64(g, omegas, nf, st));
+        BF_TRY(run_fp64(c, g, omegas, nf, t, st));
         BF_TRY_CUDA(cudaEventRecord(s.freed, st));
         s.freed_valid = true;
     }
@@ -1338,7 +1378,9 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
     a.evals = evals + obs_lo;
     if (precision == BF_PRECISION_FP64) {
         stats_begin(a.n_obs * a.n_beams);
-        BF_TRY(run_fp64(a, omegas, nf, st));
+        Tiling t;
+        BF_TRY(build_tiling(ctx, a.obs, a.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
+        BF_TRY(run_fp64(ctx, a, omegas, nf, t, st));
     } else if (BF_GRAPHS && (double)a.n_obs * (double)a.n_beams <= BF_GRAPH_MAX_PAIRS) {
         BF_TRY(run_fp32_graph(ctx, a, omegas, nf, flags, device, st));
     } else {

@@ -70,11 +70,21 @@ __device__ __forceinline__ Nearest nearest_exact(const GbsArgs &a, int64_t base,
     return r;
 }
 
-// One thread per observer, beams in ascending order (kernels.py:364-399).
+// One thread per observer, in tile order (sorted position si -> observer perm[si]);
+// the beams of the receiver's tile's TIGHT work list in ascending order
+// (kernels.py:364-399).  Every pair off the list is cut for every segment or behind
+// segment 0 (the list is sound: exact fp64 bounds with margins, oracle-pinned), so the
+// reference adds nothing for it: skipping it leaves acc and evals bit-identical to the
+// dense loop over all beams.  A warp's 32 receivers share a tile, so the beam loop is
+// warp-uniform.
 template <int NF>
-__global__ void __launch_bounds__(128) gbs_fp64_kernel(const GbsArgs a) {
-    const int64_t oi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (oi >= a.n_obs) return;
+__global__ void __launch_bounds__(128)
+    gbs_fp64_kernel(const GbsArgs a, const int32_t *perm, int tile, const uint32_t *tbits,
+                    int64_t n_words) {
+    const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (si >= a.n_obs) return;
+    const int64_t oi = perm[si];
+    const uint32_t *words = tbits + (si / tile) * n_words;
     const double pi = 3.141592653589793;  // np.pi
     const double c = a.c, width_b = a.width_b;
     const double sqrt_c = sqrt(c);
@@ -89,7 +99,9 @@ __global__ void __launch_bounds__(128) gbs_fp64_kernel(const GbsArgs a) {
         }
     }
     int64_t ev = 0;
-    for (int64_t b = 0; b < a.n_beams; ++b) {
+    for (int64_t wi = 0; wi < n_words; ++wi)
+    for (uint32_t m = __ldg(words + wi); m; m &= m - 1) {
+        const int64_t b = 32 * wi + __ffs(m) - 1;
         const int ns = __ldg(a.n_segs + b);
         if (ns == 0) continue;
         const Nearest r = nearest_exact(a, b * a.max_seg, ns, px, py, pz);
@@ -600,17 +612,18 @@ __global__ void finalize_kernel(const double *acc, int64_t n, double calibration
 
 }  // namespace
 
-int launch_gbs_fp64(const GbsArgs &a, cudaStream_t st) {
+int launch_gbs_fp64(const GbsArgs &a, const int32_t *perm, int tile, const uint32_t *tbits,
+                    int64_t n_words, cudaStream_t st) {
     if (a.n_obs <= 0) return BF_OK;
     const int threads = 128;
     const unsigned blocks = (unsigned)((a.n_obs + threads - 1) / threads);
     switch (a.nf) {
-        case 1: gbs_fp64_kernel<1><<<blocks, threads, 0, st>>>(a); break;
-        case 2: gbs_fp64_kernel<2><<<blocks, threads, 0, st>>>(a); break;
-        case 3: gbs_fp64_kernel<3><<<blocks, threads, 0, st>>>(a); break;
-        case 4: gbs_fp64_kernel<4><<<blocks, threads, 0, st>>>(a); break;
-        case 5: gbs_fp64_kernel<5><<<blocks, threads, 0, st>>>(a); break;
-        default: gbs_fp64_kernel<0><<<blocks, threads, 0, st>>>(a); break;
+        case 1: gbs_fp64_kernel<1><<<blocks, threads, 0, st>>>(a, perm, tile, tbits, n_words); break;
+        case 2: gbs_fp64_kernel<2><<<blocks, threads, 0, st>>>(a, perm, tile, tbits, n_words); break;
+        case 3: gbs_fp64_kernel<3><<<blocks, threads, 0, st>>>(a, perm, tile, tbits, n_words); break;
+        case 4: gbs_fp64_kernel<4><<<blocks, threads, 0, st>>>(a, perm, tile, tbits, n_words); break;
+        case 5: gbs_fp64_kernel<5><<<blocks, threads, 0, st>>>(a, perm, tile, tbits, n_words); break;
+        default: gbs_fp64_kernel<0><<<blocks, threads, 0, st>>>(a, perm, tile, tbits, n_words); break;
     }
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());

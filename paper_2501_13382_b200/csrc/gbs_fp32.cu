@@ -1071,8 +1071,6 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
                     const Junction J = load_junction(w.p0, w.p1, row0 + ka);
-                    const float4 g1a = S.geo1[ra], g2a = S.geo2[ra];
-                    const float4 g1b = S.geo1[rb], g2b = S.geo2[rb];
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
                     // phase references at the end of ka (c2 = hi2) and the start of ka+1
                     // (c2 = lo2)
@@ -1084,12 +1082,11 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     for (int j = 0; j < R; ++j) {
                         if (!((jp >> j) & 1u)) continue;
                         const bool wb = junction_pick(J, P64(j));
-                        const float4 g1 = wb ? g1b : g1a;
-                        const float4 g2 = wb ? g2b : g2a;
+                        const int rw = wb ? rb : ra;  // the winner's row (loads, not selects)
+                        const float4 g1 = S.geo1[rw];
+                        const float4 g2 = S.geo2[rw];
                         const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
-                        q2j[j] = fmaxf(
-                            fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j])))),
-                            0.f);
+                        q2j[j] = fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j]))));
                         sj[j] = wb ? J.sb : J.sa;
                         Aj[j] = wb ? Ab : Aa;
                         bj[j][0] = wb ? sb_ : ea;
@@ -1148,12 +1145,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 gqj[h + 1] = gp.y;
             }
             if constexpr (!MF) {
+            {   // ex_re < -36 (kernels.py:384) as one mask (no cutoff: fp64 below)
+                unsigned cutm = 0;
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                if (gqj[j] > K.gcut[0]) {  // ex_re < -36 (kernels.py:384)
-                    if (TINY && ((lvm >> j) & 1u)) tiny |= 1u << j;  // no cutoff: fp64 below
-                    lvm &= ~(1u << j);
-                }
+                for (int j = 0; j < R; ++j) cutm |= (gqj[j] > K.gcut[0] ? 1u : 0u) << j;
+                if (TINY) tiny = cutm & lvm;
+                lvm &= ~cutm;
             }
             // receivers evaluated in groups of EVG (one branch, EVG independent chains),
             // as packed pairs
