@@ -1193,15 +1193,12 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             // per frequency: partial sums in shared memory (no per-frequency registers)
 #pragma unroll 1
             for (int f = 0; f < NF; ++f) {
-                unsigned lf = 0, tf = 0;  // fp32 / (TINY) fp64 receivers of frequency f
+                // fp32 / (TINY) fp64 receivers of frequency f: ex_re < -36 (kernels.py:384)
+                const float gc = K.gcut[f];
+                unsigned cutm = 0;
 #pragma unroll
-                for (int j = 0; j < R; ++j)
-                    if ((lvm >> j) & 1u) {
-                        if (!(gqj[j] > K.gcut[f]))
-                            lf |= 1u << j;  // ex_re >= -36 (kernels.py:384)
-                        else if (TINY)
-                            tf |= 1u << j;
-                    }
+                for (int j = 0; j < R; ++j) cutm |= (gqj[j] > gc ? 1u : 0u) << j;
+                const unsigned lf = lvm & ~cutm, tf = TINY ? (lvm & cutm) : 0u;
                 if (!__any_sync(0xffffffffu, (lf | tf) != 0)) {
                     // ascending frequencies: the cut radius shrinks with omega, so every
                     // later frequency is cut for the whole warp as well
