@@ -96,6 +96,10 @@ constexpr float TIE_DD = 3.814697265625e-06f;       // 2^-18 (x d D)   tight tie
 constexpr float TIE_D2 = 4.76837158203125e-07f;     // 2^-21 (x d^2)
 constexpr float TIE_DSQ = 1.8189894035458565e-12f;  // 2^-39 (x D^2)
 
+#if BF_HIST
+__device__ unsigned long long g_hist[8];  // debug counters (BF_HIST builds only)
+#endif
+
 template <typename T>
 __device__ __forceinline__ T pick4(const T (&v)[4], int j) {
     return j == 0 ? v[0] : j == 1 ? v[1] : j == 2 ? v[2] : v[3];
@@ -425,6 +429,9 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
     const bool behind0 = p0 + r0d * 1.00002f + 2e-3f < 0.f;  // whole patch behind segment 0
     unsigned mask = 1u << kj;
     bool all_dead = cj || (kj == 0 && behind0);
+#if BF_HIST
+    bool all_cut = all_dead;  // debug: every segment cut (no pruning needed)
+#endif
 #pragma unroll 1
     for (int k = 0; k < ns; ++k) {
         if (k == kj) continue;
@@ -446,7 +453,14 @@ __device__ __forceinline__ unsigned classify(const WarpSmem<NF, MF> &S, const Fp
             mask |= 1u << k;
             all_dead = all_dead && (cut || (k == 0 && behind0));
         }
+#if BF_HIST
+        all_cut = all_cut && (cut || (k == 0 && behind0));
+#endif
     }
+#if BF_HIST
+    if (all_cut) atomicAdd(&g_hist[4], 1ull);
+    if (all_dead) atomicAdd(&g_hist[5], 1ull);
+#endif
     if (all_dead) return 0u;
     unsigned word = mask;
     // segment 0 survives and the patch reaches its launch plane
@@ -503,9 +517,6 @@ __device__ __forceinline__ unsigned behind_mask(const Fp32Work &w, const float (
 // receiver projects beyond the end of k and before the start of k+1, both clamped
 // distances (kernels.py:332-340) are distances to the reflection point and the
 // reference's choice is decided by fp64 rounding, reproduced here op for op.
-#if BF_HIST
-__device__ unsigned long long g_hist[4];  // debug: exact re-decision rounds (warp-level) in [2]
-#endif
 struct Junction {
     double ox, oy, oz;  // o_k
     double lx, ly, lz;  // len_k * d_k (t = len, kernels.py:337-339)
@@ -1315,7 +1326,9 @@ __global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5
     WarpSmem<NF, MF> &S = reinterpret_cast<WarpSmem<NF, MF> *>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const unsigned n_units = (unsigned)(w.n_patches * w.n_ranges);
-    const unsigned n_split = n_units - *w.n_wide;
+    const unsigned n_wide = *w.n_wide;
+    if (WIDE && n_wide == 0) return;  // (uniform over the grid) no atomics, no statistics
+    const unsigned n_split = n_units - n_wide;
     const unsigned u0 = WIDE ? n_split : 0u, u1 = WIDE ? n_units : n_split;
     const unsigned n_patches = (unsigned)w.n_patches;
     if (lane < 8) S.cnt[lane] = 0;
@@ -1330,15 +1343,20 @@ __global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5
         const unsigned p = id - q * n_patches;
         run_unit<NF, WIDE, TINY>(a, tl, w, K, S, p, q, lane, stats);
     }
-    // per-lane counters straight into the device statistics
-    __syncwarp();
-    if (lane == 0) {
-        atomicAdd(&stats->tie_pairs, S.cnt[0]);
-        atomicAdd(&stats->nb_pairs, S.cnt[1]);
+    // the CTA's warp counters summed in shared memory, then one set of atomics per CTA
+    // (per-warp atomics on the same eight addresses serialised into a tail of ~10 us)
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        unsigned long long v = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) atomicAdd(&stats->paths[i], S.cnt[2 + i]);
-        atomicAdd(&stats->live_pairs, S.cnt[6]);
-        atomicAdd(&stats->live_pair_segs, S.cnt[7]);
+        for (int wi = 0; wi < WARPS; ++wi)
+            v += reinterpret_cast<WarpSmem<NF, MF> *>(smem_raw)[wi].cnt[threadIdx.x];
+        unsigned long long *dst = threadIdx.x == 0 ? &stats->tie_pairs
+                                : threadIdx.x == 1 ? &stats->nb_pairs
+                                : threadIdx.x < 6  ? &stats->paths[threadIdx.x - 2]
+                                : threadIdx.x == 6 ? &stats->live_pairs
+                                                   : &stats->live_pair_segs;
+        if (v) atomicAdd(dst, v);
     }
 }
 
@@ -1578,7 +1596,7 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
               GbsStats *stats, const StreamPair &sp) {
 #if BF_HIST
     {
-        unsigned long long z[4] = {0, 0, 0, 0};
+        unsigned long long z[8] = {};
         cudaMemcpyToSymbolAsync(g_hist, z, sizeof(z), 0, cudaMemcpyHostToDevice, sp.st);
     }
 #endif
@@ -1595,9 +1613,10 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
     BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
 #if BF_HIST
     {
-        unsigned long long h[4];
+        unsigned long long h[8];
         cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, sp.st);
         cudaStreamSynchronize(sp.st);
+        fprintf(stderr, "bf hist: items all-cut %llu culled %llu\n", h[4], h[5]);
         fprintf(stderr, "bf hist: pend(<=2 surv) %llu pend(>=3 surv) %llu exact rounds %llu junction %llu\n", h[0], h[1], h[2], h[3]);
     }
 #endif
