@@ -25,7 +25,7 @@ from paper_2501_13382_b200.beamtrace import Atmosphere, LaunchGrid, SourceSpec, 
 from paper_2501_13382_b200.scene import make_city, make_ground_plane
 dev = torch.device("cuda", 0)
 PREC = os.environ.get("FUZZ_PREC", "fp32")
-fails = []; worst = 0.0
+fails = []; worst = 0.0; worst_all = 0.0; n_all_over = 0
 for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     rng = np.random.default_rng(5000 + seed)
     kind = rng.integers(0, 3)
@@ -77,11 +77,15 @@ for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     l2 = rel_l2(acc, ref); t60 = tl_db(acc, ref, floor_db=-60.0); tall = tl_db(acc, ref)
     evd = abs(int(ev.sum()) - int(rev.sum()))
     worst = max(worst, t60)
+    if np.isfinite(tall):
+        worst_all = max(worst_all, tall)
+        n_all_over += int(tall > 0.01)
     if PREC == "fp64":
         bad = l2 > 1e-12 or not np.array_equal(ev, rev)
     else:
         bad = l2 > 1e-4 or t60 > 0.01 or evd > 1e-4 * int(rev.sum()) + 10
     if bad:
         fails.append((seed, dict(kind=int(kind), nf=nf, im_b=round(im_b, 2), cut=use_cutoff, sp=round(sp, 3), R=round(R, 1), rmax=cfg.r_max if hasattr(cfg, 'r_max') else None, l2=l2, t60=t60, tall=tall, evd=evd, evsum=int(rev.sum()))))
-print("fuzz2", sys.argv[1:], "failures", len(fails), "worst t60 %.4f" % worst)
+print("fuzz2", sys.argv[1:], PREC, "failures", len(fails), "worst t60 %.4f" % worst,
+      "worst all-receiver dTL %.4f" % worst_all, "seeds with all-receiver dTL > 0.01:", n_all_over)
 for f in fails: print(f)
