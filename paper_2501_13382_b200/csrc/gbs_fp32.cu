@@ -83,6 +83,18 @@ constexpr int TILE = BF_TILEP * PATCH;  // receivers per work-list tile
 #endif
 constexpr int WARPS = BF_WARPS;         // independent warps per CTA
 constexpr int THREADS = 32 * WARPS;
+// several frequencies (and the wide-patch kernel): warps per CTA, CTAs per SM, and whether
+// the fp64 receiver positions stay in shared memory (else the sorted global copy)
+#ifndef BF_WARPS_MF
+#define BF_WARPS_MF 4
+#endif
+#ifndef BF_MF_P64_SMEM
+#define BF_MF_P64_SMEM 0
+#endif
+template <bool MF>
+constexpr int WARPS_OF = MF ? BF_WARPS_MF : WARPS;
+template <bool MF>
+constexpr bool P64G = MF && !BF_MF_P64_SMEM;  // fp64 receiver positions from global memory
 constexpr int CB = 32;                  // max beams per staged chunk
 constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk (one frequency)
 constexpr int ROWCAP_MF = 64;           // ... several frequencies (power of two, see ROWS)
@@ -234,7 +246,7 @@ struct WarpSmem {
     // fp64 receiver positions (exact re-decisions); the several-frequency kernels read
     // them from the sorted global copy w.pos64 instead (shared memory is their occupancy
     // limit)
-    double p64[MF ? 1 : PATCH][3];
+    double p64[P64G<MF> ? 1 : PATCH][3];
 };
 
 // fp64 position of receiver j of the lane: the lane's slice of S.p64 (one frequency) or
@@ -640,7 +652,8 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
                                               float Db, int lane, float (&sj)[R],
                                               float (&q2j)[R], float (&Aj)[R],
                                               float (&bj)[R][1], int (&pref)[R], unsigned &lvm,
-                                              unsigned &ties, const Fp32Work &w, const Recv64<MF> &P64) {
+                                              unsigned &ties, const Fp32Work &w,
+                                              const Recv64<P64G<MF>> &P64) {
     ties += __popc(pend);
     // two adjacent candidates k, k+1 (most multi items): a receiver that projects
     // beyond the end of k and before the start of k+1 is decided like the corner wedge
@@ -748,7 +761,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
     const int32_t *perm = tl.perm + sb;       // observer index of receiver j = perm[j]
     const int nvalid =  // receivers j < nvalid are real
         tl.n - sb < R ? (tl.n - sb > 0 ? (int)(tl.n - sb) : 0) : R;
-    const Recv64<MF> P64{S.p64 + (MF ? 0 : R * lane), w.pos64 + sb};
+    const Recv64<P64G<MF>> P64{S.p64 + (P64G<MF> ? 0 : R * lane), w.pos64 + sb};
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         float4 rl = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -767,7 +780,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
         S.evc[R * lane + j] = 0;
         if (j < nvalid) {
             const int64_t oi = perm[j];
-            if constexpr (!MF) {
+            if constexpr (!P64G<MF>) {
                 S.p64[R * lane + j][0] = a.obs[3 * oi];
                 S.p64[R * lane + j][1] = a.obs[3 * oi + 1];
                 S.p64[R * lane + j][2] = a.obs[3 * oi + 2];
@@ -1318,7 +1331,8 @@ template <int NF, bool WIDE, bool TINY>
 #ifndef BF_MINB_MF
 #define BF_MINB_MF 4
 #endif
-__global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5 ? BF_MINB_MF : 2))
+__global__ void __launch_bounds__(32 * WARPS_OF<(NF > 1 || WIDE)>,
+                                  (NF == 1 && !WIDE ? BF_MINB : NF <= 5 ? BF_MINB_MF : 2))
     gbs_fp32_kernel(const GbsArgs a, const Tiling tl, const Fp32Work w, const Fp32Consts K,
                     GbsStats *stats) {
     constexpr bool MF = NF > 1 || WIDE;
@@ -1349,7 +1363,7 @@ __global__ void __launch_bounds__(THREADS, (NF == 1 && !WIDE ? BF_MINB : NF <= 5
     if (threadIdx.x < 8) {
         unsigned long long v = 0;
 #pragma unroll
-        for (int wi = 0; wi < WARPS; ++wi)
+        for (int wi = 0; wi < WARPS_OF<MF>; ++wi)
             v += reinterpret_cast<WarpSmem<NF, MF> *>(smem_raw)[wi].cnt[threadIdx.x];
         unsigned long long *dst = threadIdx.x == 0 ? &stats->tie_pairs
                                 : threadIdx.x == 1 ? &stats->nb_pairs
@@ -1555,7 +1569,8 @@ template <int NF, bool WIDE, bool TINY>
 int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Consts &K,
                  GbsStats *stats, cudaStream_t st) {
     constexpr bool MF = NF > 1 || WIDE;
-    const size_t smem = WARPS * sizeof(WarpSmem<NF, MF>);
+    constexpr int NW = WARPS_OF<MF>;
+    const size_t smem = NW * sizeof(WarpSmem<NF, MF>);
     // per-device launch geometry, computed once (attribute + occupancy queries cost host time
     // on every call otherwise); a benign race writes the same values
     constexpr int MAXDEV = 64;
@@ -1569,7 +1584,7 @@ int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp3
         int sms = 0, per_sm = 0;
         BF_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         BF_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, gbs_fp32_kernel<NF, WIDE, TINY>, THREADS, smem));
+            &per_sm, gbs_fp32_kernel<NF, WIDE, TINY>, 32 * NW, smem));
         if (per_sm < 1)
             return fail(BF_ECUDA, "fp32 kernel does not fit on an SM (smem %zu)", smem);
         if (getenv("BF_DEBUG_STATS"))
@@ -1579,9 +1594,9 @@ int launch_class(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp3
     }
     const int64_t units = w.n_patches * w.n_ranges;
     int64_t grid = grid_cache[dev];
-    const int64_t need = (units + WARPS - 1) / WARPS;
+    const int64_t need = (units + NW - 1) / NW;
     if (grid > need) grid = need;
-    gbs_fp32_kernel<NF, WIDE, TINY><<<(unsigned)grid, THREADS, smem, st>>>(a, t, w, K, stats);
+    gbs_fp32_kernel<NF, WIDE, TINY><<<(unsigned)grid, 32 * NW, smem, st>>>(a, t, w, K, stats);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

@@ -80,6 +80,15 @@ for seed in range(int(sys.argv[1]), int(sys.argv[2])):
     if np.isfinite(tall):
         worst_all = max(worst_all, tall)
         n_all_over += int(tall > 0.01)
+        if tall > 0.01:  # where: the worst receiver's level below the field maximum
+            nz = np.abs(ref) > 0
+            d = np.full(ref.shape, 0.0)
+            d[nz] = np.abs(20 * np.log10(np.abs(acc[nz]) / np.abs(ref[nz])))
+            i = np.unravel_index(np.argmax(d), d.shape)
+            lvl = 20 * np.log10(np.abs(ref[i]) / np.abs(ref).max())
+            print("ALL", seed, "dTL %.4f at %.1f dB below max" % (tall, -lvl), "kind", int(kind),
+                  "nf", nf, "cut", use_cutoff, "imb", round(im_b, 2), "sp", round(sp, 3),
+                  "n>0.01", int((d > 0.01).sum()), "of", int(nz.sum()), flush=True)
     if PREC == "fp64":
         bad = l2 > 1e-12 or not np.array_equal(ev, rev)
     else:
