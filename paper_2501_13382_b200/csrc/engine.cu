@@ -1012,7 +1012,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
                 BF_TRY(s.get(S_UVALS, (size_t)nu, &v0));
                 BF_TRY(s.get(S_UVALS2, (size_t)nu, &v1));
                 BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
-                const int end_bit = 40;  // wide << 39 | bucket (7 bits) << 32 | range
+                const int end_bit = 14;  // wide << 13 | bucket (7 bits) << 6 | range (< 64)
                 if (nu <= SMALL_SORT_N) {  // one CTA, one launch (small calls)
                     BF_TRY(small_sort(k0, v0, (int)nu, end_bit, v1, s.ss));
                     w.unit_order = v1;

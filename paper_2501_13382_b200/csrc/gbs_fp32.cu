@@ -69,6 +69,7 @@ namespace {
 #ifndef BF_RANGES
 #define BF_RANGES 64
 #endif
+static_assert(BF_RANGES <= 64, "unit sort keys hold the beam range in 6 bits");
 #ifndef BF_FLUSHN
 #define BF_FLUSHN 4  // several frequencies: chunks per fp64 flush of the partials (power of 2)
 #endif
@@ -1528,7 +1529,9 @@ __global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_
     const int bucket = 2 * msb + (msb > 0 ? (int)((c >> (msb - 1)) & 1) : 0);  // < 128
     const bool wide = wide_patch(w, p);
     if (wide) atomicAdd(w.n_wide, 1u);
-    keys[u] = ((uint64_t)wide << 39) | ((uint64_t)(127 - bucket) << 32) | (uint64_t)q;
+    // 14 significant bits (wide, 7-bit bucket, range q < 64): the radix sorts need 2 (cub,
+    // 8-bit digits) or 4 (one CTA, 4-bit digits) passes instead of 5 / 10 over 40 bits
+    keys[u] = ((uint64_t)wide << 13) | ((uint64_t)(127 - bucket) << 6) | (uint64_t)q;
     vals[u] = (int32_t)u;
 }
 
