@@ -40,6 +40,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -111,6 +112,12 @@ constexpr float TIE_DSQ = 1.8189894035458565e-12f;  // 2^-39 (x D^2)
 
 #if BF_HIST
 __device__ unsigned long long g_hist[8];  // debug counters (BF_HIST builds only)
+#endif
+#ifndef BF_UNIT_TIMES
+#define BF_UNIT_TIMES 0  // debug: clock64 cycles of every unit to $BF_UNIT_TIMES_OUT
+#endif
+#if BF_UNIT_TIMES
+__device__ long long *g_unit_cycles;
 #endif
 
 template <typename T>
@@ -1356,7 +1363,13 @@ __global__ void __launch_bounds__(32 * WARPS_OF<(NF > 1 || WIDE)>,
         const unsigned id = (unsigned)w.unit_order[u];  // longest-first, see unit_keys_kernel
         const unsigned q = id / n_patches;
         const unsigned p = id - q * n_patches;
+#if BF_UNIT_TIMES
+        const long long c0 = clock64();
+#endif
         run_unit<NF, WIDE, TINY>(a, tl, w, K, S, p, q, lane, stats);
+#if BF_UNIT_TIMES
+        if (lane == 0 && g_unit_cycles) g_unit_cycles[id] = clock64() - c0;
+#endif
     }
     // the CTA's warp counters summed in shared memory, then one set of atomics per CTA
     // (per-warp atomics on the same eight addresses serialised into a tail of ~10 us)
@@ -1629,6 +1642,34 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
     }
     BF_TRY_CUDA(cudaEventRecord(sp.join, sp.aux));
     BF_TRY_CUDA(cudaStreamWaitEvent(sp.st, sp.join, 0));
+#if BF_UNIT_TIMES
+    {
+        const int64_t nu = w.n_patches * w.n_ranges;
+        long long *buf = nullptr;
+        cudaStreamSynchronize(sp.st);
+        cudaMalloc(&buf, 8 * nu);
+        cudaMemcpyToSymbol(g_unit_cycles, &buf, sizeof(buf));
+        cudaMemsetAsync(w.unit_ctr, 0, sizeof(unsigned), sp.st);
+        launch_class<NF, false, false>(a, t, w, K, stats, sp.st);  // re-run, timed per unit
+        cudaStreamSynchronize(sp.st);
+        std::vector<long long> h(nu);
+        cudaMemcpy(h.data(), buf, 8 * nu, cudaMemcpyDeviceToHost);
+        long long sum = 0;
+        for (long long v : h) sum += v;
+        fprintf(stderr, "bf unit times: %lld units, %lld cycles, err %s\n", (long long)nu, sum,
+                cudaGetErrorString(cudaGetLastError()));
+        long long *nul = nullptr;
+        cudaMemcpyToSymbol(g_unit_cycles, &nul, sizeof(nul));
+        cudaFree(buf);
+        if (const char *out = getenv("BF_UNIT_TIMES_OUT")) {
+            FILE *f = fopen(out, "wb");
+            const int64_t hdr[3] = {w.n_patches, w.n_ranges, TILE / PATCH};
+            fwrite(hdr, 8, 3, f);
+            fwrite(h.data(), 8, nu, f);
+            fclose(f);
+        }
+    }
+#endif
 #if BF_HIST
     {
         unsigned long long h[8];
