@@ -570,9 +570,15 @@ __global__ void tile_kernel(const double *obs, int64_t n, const int32_t *perm, f
         r.z = (float)(p[2] - s_c[2]);
         rloc[si] = r;
     }
-    const double rad = valid ? sqrt((double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z) : 0.0;
+    // the tile radius bounds |p - c| from above: fp64 offsets, rounded up to fp32 (the
+    // work-list cut tests use it as a conservative bound)
+    double rad = 0.0;
+    if (valid) {
+        const double dx = p[0] - s_c[0], dy = p[1] - s_c[1], dz = p[2] - s_c[2];
+        rad = sqrt(dx * dx + dy * dy + dz * dz) * (1.0 + 1e-15);
+    }
     const double rmax = BR(tmp).Reduce(rad, cub::Max());
-    if (threadIdx.x == 0) s_r = (float)rmax;
+    if (threadIdx.x == 0) s_r = __double2float_ru(rmax);
     __syncthreads();
     if (threadIdx.x == 0) {
         centre[blockIdx.x] = make_double4(s_c[0], s_c[1], s_c[2], (double)s_r);
