@@ -422,6 +422,12 @@ def test_worklist_bitexact_vs_oracle(name, dense):
     assert np.all(box[:, :3] >= 0) and np.all(box[:, :3] <= box[:, 3:4] * (1 + 1e-6) + 1e-9)
     assert np.array_equal(tbits, tref)
     assert not (tbits & ~bits).any()  # tight list is a subset of the a9 list
+    # the tile radius bounds every member's distance from the centre (fp64, no rounding
+    # below it: the cut tests rely on it)
+    so = obs[perm]
+    for t in range(nt):
+        d = np.sqrt(((so[t * T:(t + 1) * T] - centre[t, :3]) ** 2).sum(axis=1))
+        assert d.max() <= centre[t, 3], (t, d.max(), centre[t, 3])
     if dense:
         assert 0 < np.unpackbits(bits.view(np.uint8)).mean() < 1
 
