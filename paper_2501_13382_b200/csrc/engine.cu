@@ -29,6 +29,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <functional>
 #include <mutex>
@@ -1424,7 +1425,17 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
     BF_TRY(ctx->get(B_OBS, (size_t)(3 * no), &d_obs));
     BF_TRY(ctx->get(B_ACC, (size_t)(2 * no * nf), &d_acc));
     BF_TRY(ctx->get(B_EVALS, (size_t)no, &d_ev));
+    // BF_DEBUG_HOST=1: host-side phase times of this call on stderr (diagnostics only)
+    static const bool dbg = getenv("BF_DEBUG_HOST") != nullptr;
+    const auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t_a = now();
+    cudaEvent_t ev_dbg[3] = {};
+    if (dbg) {
+        for (auto &e : ev_dbg) cudaEventCreate(&e);
+        cudaEventRecord(ev_dbg[0], st);
+    }
     BF_TRY(h2d(d_obs, obs + 3 * obs_lo, 24 * (size_t)no, ctx->hpin[H_OBS], st));
+    const auto t_b = now();
     bool uploaded = false;
     const std::function<int()> upload_fields = [&]() -> int {
         BF_TRY(h2d(d_acc, acc + 2 * obs_lo * nf, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
@@ -1462,8 +1473,20 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
         BF_TRY(run_fp32(ctx, a, omegas, nf, true, 0, st, &upload_fields));
     }
     if (!uploaded) BF_TRY(upload_fields());  // (no group ran: acc/evals come back unchanged)
+    const auto t_c = now();
+    if (dbg) cudaEventRecord(ev_dbg[1], st);
     BF_TRY(d2h_sync(acc + 2 * obs_lo * nf, d_acc, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
     BF_TRY(d2h_sync(evals + obs_lo, d_ev, 8 * (size_t)no, ctx->hpin[H_EV], st));
+    if (dbg) {
+        const auto t_d = now();
+        float gpu_ms = 0.f;
+        cudaEventElapsedTime(&gpu_ms, ev_dbg[0], ev_dbg[1]);
+        const auto ms = [](auto x, auto y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+        fprintf(stderr, "bf host: obs upload %.2f ms, enqueue groups %.2f ms, wait+copy-out %.2f ms, "
+                "total %.2f ms; GPU obs..last fold %.2f ms\n", ms(t_a, t_b), ms(t_b, t_c), ms(t_c, t_d),
+                ms(t_a, t_d), gpu_ms);
+        for (auto &e : ev_dbg) cudaEventDestroy(e);
+    }
     return BF_OK;
 }
 
