@@ -162,6 +162,7 @@ struct DeviceCtx {
     cudaEvent_t done = nullptr;
     bool done_valid = false;
     cudaEvent_t pro = nullptr;  // end of a call's prologue (tiling) on its stream
+    cudaEvent_t piece[2] = {};  // staged copy-out pieces landed (d2h_out)
     int64_t budget = 0;         // group-workspace budget in bytes (0: automatic)
     // Small fp32 device calls repeated with identical arguments replay a captured graph
     // of the whole call (tiling .. fold): one launch instead of ~30.  The first call with
@@ -752,21 +753,51 @@ int h2d(void *dst, const void *src, size_t bytes, PinBuf &stage, cudaStream_t st
     return BF_OK;
 }
 
-// Device -> host of `bytes` into host memory that may be pageable (synchronises st).
-int d2h_sync(void *dst, const void *src, size_t bytes, PinBuf &stage, cudaStream_t st) {
+// The host call's results (acc, then evals) back into memory that may be pageable, then
+// synchronise st.  Pageable targets: all DMAs into pinned staging are enqueued first (acc
+// in two halves, each followed by an event), and the host threads copy each piece out as
+// soon as it has landed while the next ones are still in flight.
+int d2h_out(DeviceCtx *c, void *acc_dst, const void *acc_src, size_t acc_bytes,
+            void *ev_dst, const void *ev_src, size_t ev_bytes, cudaStream_t st) {
     cudaPointerAttributes at;
-    if (bytes == 0) return check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    if (cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost) {
-        BF_TRY_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
-        BF_TRY_CUDA(cudaStreamSynchronize(st));
-        return BF_OK;
-    }
+    const bool pa = cudaPointerGetAttributes(&at, acc_dst) == cudaSuccess &&
+                    at.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    void *p;
-    BF_TRY(stage.get(bytes, &p));
-    BF_TRY_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyDeviceToHost, st));
+    const bool pe = cudaPointerGetAttributes(&at, ev_dst) == cudaSuccess &&
+                    at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    for (auto &e : c->piece)
+        if (!e) BF_TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    char *sa = nullptr, *se = nullptr;
+    const size_t h0 = acc_bytes / 2 / 16 * 16, h1 = acc_bytes - h0;
+    if (pa) {
+        if (acc_bytes) BF_TRY_CUDA(cudaMemcpyAsync(acc_dst, acc_src, acc_bytes, cudaMemcpyDeviceToHost, st));
+    } else if (acc_bytes) {
+        void *p;
+        BF_TRY(c->hpin[H_ACC].get(acc_bytes, &p));
+        sa = (char *)p;
+        BF_TRY_CUDA(cudaMemcpyAsync(sa, acc_src, h0, cudaMemcpyDeviceToHost, st));
+        BF_TRY_CUDA(cudaEventRecord(c->piece[0], st));
+        BF_TRY_CUDA(cudaMemcpyAsync(sa + h0, (const char *)acc_src + h0, h1,
+                                    cudaMemcpyDeviceToHost, st));
+        BF_TRY_CUDA(cudaEventRecord(c->piece[1], st));
+    }
+    if (pe) {
+        if (ev_bytes) BF_TRY_CUDA(cudaMemcpyAsync(ev_dst, ev_src, ev_bytes, cudaMemcpyDeviceToHost, st));
+    } else if (ev_bytes) {
+        void *p;
+        BF_TRY(c->hpin[H_EV].get(ev_bytes, &p));
+        se = (char *)p;
+        BF_TRY_CUDA(cudaMemcpyAsync(se, ev_src, ev_bytes, cudaMemcpyDeviceToHost, st));
+    }
+    if (sa) {
+        BF_TRY_CUDA(cudaEventSynchronize(c->piece[0]));
+        parallel_copy(acc_dst, sa, h0);
+        BF_TRY_CUDA(cudaEventSynchronize(c->piece[1]));
+        parallel_copy((char *)acc_dst + h0, sa + h0, h1);
+    }
     BF_TRY_CUDA(cudaStreamSynchronize(st));
-    parallel_copy(dst, p, bytes);
+    if (se) parallel_copy(ev_dst, se, ev_bytes);
     return BF_OK;
 }
 
@@ -1475,8 +1506,8 @@ int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const dou
     if (!uploaded) BF_TRY(upload_fields());  // (no group ran: acc/evals come back unchanged)
     const auto t_c = now();
     if (dbg) cudaEventRecord(ev_dbg[1], st);
-    BF_TRY(d2h_sync(acc + 2 * obs_lo * nf, d_acc, 16 * (size_t)(no * nf), ctx->hpin[H_ACC], st));
-    BF_TRY(d2h_sync(evals + obs_lo, d_ev, 8 * (size_t)no, ctx->hpin[H_EV], st));
+    BF_TRY(d2h_out(ctx, acc + 2 * obs_lo * nf, d_acc, 16 * (size_t)(no * nf), evals + obs_lo,
+                   d_ev, 8 * (size_t)no, st));
     if (dbg) {
         const auto t_d = now();
         float gpu_ms = 0.f;
