@@ -1163,8 +1163,13 @@ int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t
     // second call: capture the whole call (the slot streams join the capture through the
     // call's fork/join events; waits on events of earlier calls are dropped -- the graph
     // launch itself is ordered after them on st)
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+        cudaGetLastError();  // a stream that cannot be captured: stay eager for this key
+        g.seen = false;
+        g.key.clear();
+        return run_fp32(c, a, omegas, nf, false, flags, st);
+    }
     for (Slot &sl : c->slot) sl.freed_valid = false;
-    BF_TRY_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
     const uint64_t n0 = g_launches.load();
     g_capturing = true;
     const int rc = run_fp32(c, a, omegas, nf, false, flags, st);
