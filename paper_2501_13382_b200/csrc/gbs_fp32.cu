@@ -61,6 +61,9 @@ namespace {
 #ifndef BF_ABL
 #define BF_ABL 0
 #endif
+#ifndef BF_JP_ALL
+#define BF_JP_ALL 1
+#endif
 #ifndef BF_HIST
 #define BF_HIST 0
 #endif
@@ -1112,10 +1115,22 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float ea = MF ? ana.z : fmaf(K.kh[0], ana.z, ana.x);
                     const float sb_ = MF ? anb.y : fmaf(K.kh[0], anb.y, anb.x);
                     ties += __popc(jp);
+#if BF_JP_ALL
+                    // the four decisions first and unconditionally: independent fp64 chains
+                    // the scheduler can interleave (a receiver not in jp is computed from
+                    // whatever its position slot holds and ignored)
+                    bool wbj[R];
+#pragma unroll
+                    for (int j = 0; j < R; ++j) wbj[j] = junction_pick(J, P64(j));
+#endif
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         if (!((jp >> j) & 1u)) continue;
+#if BF_JP_ALL
+                        const bool wb = wbj[j];
+#else
                         const bool wb = junction_pick(J, P64(j));
+#endif
                         const int rw = wb ? rb : ra;  // the winner's row (loads, not selects)
                         const float4 g1 = S.geo1[rw];
                         const float4 g2 = S.geo2[rw];
