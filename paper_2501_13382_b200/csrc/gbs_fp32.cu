@@ -61,6 +61,9 @@ namespace {
 #ifndef BF_ABL
 #define BF_ABL 0
 #endif
+#ifndef BF_MULTI_BF
+#define BF_MULTI_BF 1  // several candidates: branch-free per-receiver block
+#endif
 #ifndef BF_JP_ALL
 #define BF_JP_ALL 1
 #endif
@@ -1058,6 +1061,59 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 // two adjacent candidates: ties at the junction go to the wedge decision
                 const bool pair = surv == (3u << ka);
                 const float jtol = pair ? PROJ_ERR * Db : 0.f;  // Db >= either row's D
+#if BF_MULTI_BF
+                // every receiver's nearest point from its fp32 winner, unconditionally (the
+                // four blocks interleave); near ties and behind receivers only flagged here
+                unsigned exm = 0;
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const int k = kb[j];
+                    const float gap = second[j] - best[j];
+                    // fp32 error of the two distances: loose test first,
+                    // then 2^-18 d D + 2^-21 d^2 + 2^-39 D^2 with d^2 <= second
+                    bool exact = gap <= fmaf(TIE_REL, second[j], tie_abs) &&
+                                 gap <= fmaf(TIE_DD * Db, sqrt_approx(second[j]) * 1.0001f,
+                                             fmaf(TIE_D2, second[j], TIE_DSQ * Db * Db));
+                    const float4 g1 = S.geo1[r0 + k];
+                    const float4 g2 = S.geo2[r0 + k];
+                    const float2 ax = S.aux[r0 + k];
+                    const float4 an = S.anc[r0 + k];
+                    const float dl = fmaf(rx[j], g1.x, fmaf(ry[j], g1.y, rz[j] * g1.z));
+                    const float proj = dl + g1.w;
+                    exact = exact || (k == 0 && fabsf(proj) <= PROJ_ERR * Db);
+                    const bool behind = k == 0 && proj < 0.f;  // behind the source
+                    q2j[j] = fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j]))));
+                    const float c2 = clamp2(dl, an);
+                    sj[j] = fmaf(0.5f, c2, ax.x);
+                    Aj[j] = ax.y;
+                    if constexpr (!MF) {
+                        bj[j][0] = fmaf(K.kh[0], c2, an.x);
+                    } else {
+                        bj[j][0] = c2;
+                        pref[j] = r0 + k;
+                    }
+                    exm |= (exact ? 1u : 0u) << j;
+                    lvm |= (!exact && !behind ? 1u : 0u) << j;
+                }
+                exm &= (1u << nvalid) - 1u;
+                for (unsigned m = exm; m; m &= m - 1) {  // near ties: junction or fp64 search
+                    const int j = __ffs(m) - 1;
+                    if (pair) {
+                        // beyond the end of ka and before the start of ka+1?
+                        const float4 a0 = S.geo0[r0 + ka], a1 = S.geo1[r0 + ka];
+                        const float4 b1 = S.geo1[r0 + ka + 1];
+                        const float x = pick4(rx, j), y = pick4(ry, j), z = pick4(rz, j);
+                        const float pa = fmaf(x, a1.x, fmaf(y, a1.y, z * a1.z)) + a1.w;
+                        const float pb = fmaf(x, b1.x, fmaf(y, b1.y, z * b1.z)) + b1.w;
+                        if (pa - a0.w >= jtol && pb <= -jtol) {
+                            jp |= 1u << j;
+                            continue;
+                        }
+                    }
+                    pend |= 1u << j;
+                }
+                }
+#else
 #pragma unroll
                 for (int j = 0; j < R; ++j) {
                     const int k = kb[j];
@@ -1105,6 +1161,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     lvm |= 1u << j;
                 }
                 }
+#endif
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
                     const Junction J = load_junction(w.p0, w.p1, row0 + ka);
