@@ -64,6 +64,9 @@ namespace {
 #ifndef BF_MULTI_BF
 #define BF_MULTI_BF 1  // several candidates: branch-free per-receiver block
 #endif
+#ifndef BF_STAGE2
+#define BF_STAGE2 1
+#endif
 #ifndef BF_JP_ALL
 #define BF_JP_ALL 1
 #endif
@@ -718,6 +721,42 @@ template <int NF, bool MF>
 __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &w, int nrows,
                                            double cx, double cy, double cz, float RW,
                                            const Fp32Consts &K, int lane) {
+#if BF_STAGE2
+    // two rows per lane at a time (rows r and r + 32): both rows' loads in flight together
+    // and their fp64 chains interleave
+    auto row_out = [&](int r, const double4 &p0, const double4 &p1, float p2, bool st) {
+        const double wcx = cx - p0.x, wcy = cy - p0.y, wcz = cz - p0.z;
+        const double pc = wcx * p1.x + wcy * p1.y + wcz * p1.z;
+        const double ucx = wcx - pc * p1.x, ucy = wcy - pc * p1.y, ucz = wcz - pc * p1.z;
+        if (st) S.geo0[r] = make_float4((float)wcx, (float)wcy, (float)wcz, (float)p0.w);
+        if (st) S.geo1[r] = make_float4((float)p1.x, (float)p1.y, (float)p1.z, (float)pc);
+        if (st) S.geo2[r] = make_float4((float)(2.0 * ucx), (float)(2.0 * ucy), (float)(2.0 * ucz),
+                                (float)(ucx * ucx + ucy * ucy + ucz * ucz));
+        // the centre's projection clamped to the segment; phase references (clamp2)
+        const double pcc = pc < 0.0 ? 0.0 : (pc > p0.w ? p0.w : pc);
+        const double sp = p1.w + pcc;
+        if (st) S.aux[r] = make_float2((float)sp, p2 * K.omega[0]);
+        if (st) S.anc[r] = make_float4(frac_rad(K.kappa64[0] * sp), (float)(-2.0 * pcc),
+                               (float)(2.0 * (p0.w - pcc)), (float)(2.0 * (pc - pcc)));
+        if constexpr (MF) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) if (st) S.ancf[f][r] = frac_rad(K.kappa64[f] * sp);
+        }
+    };
+#pragma unroll 1
+    for (int r = lane; r < nrows; r += 64) {
+        const bool two = r + 32 < nrows;
+        const int64_t ga = (int64_t)S.rowinfo[r];
+        const int64_t gb = two ? (int64_t)S.rowinfo[r + 32] : ga;
+        const double4 a0 = w.p0[ga], a1 = w.p1[ga];
+        const float a2 = w.amp[ga];
+        const double4 b0 = w.p0[gb], b1 = w.p1[gb];
+        const float b2 = w.amp[gb];
+        row_out(r, a0, a1, a2, true);
+        row_out(two ? r + 32 : r, b0, b1, b2, two);  // (computed either way: the chains interleave)
+    }
+}
+#else
     // software-pipelined: the next row's loads are in flight while this row converts
     auto grow = [&](int r) { return (int64_t)S.rowinfo[r]; };
     int r = lane;
@@ -762,6 +801,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
         p2 = p2n;
     }
 }
+#endif
 
 
 // One (patch, beam range) unit.
