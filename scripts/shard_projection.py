@@ -46,7 +46,7 @@ def main():
         ev = torch.zeros(obs.shape[0], dtype=torch.int64, device=dev)
         best, kern = float("inf"), float("inf")
         for i in range(args.reps + 1):
-            bench.flush_l2(flush)
+            flush.add_(1.0)  # 256 MiB write > 126 MB L2
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             acc.zero_()
             ev.zero_()
