@@ -1837,12 +1837,7 @@ int64_t gbs_fp32_range_beams(int64_t n_beams, int nf) {
     // BF_RANGES ranges for one frequency, fewer with several (the partial buffer holds
     // ranges x receivers x frequencies complex values)
     // (small calls get 32-beam ranges: more (patch, range) units to spread over the SMs)
-    int64_t ranges = BF_RANGES / nf > 8 ? BF_RANGES / nf : 8;
-    // one frequency, 16k .. 2M beams: 16 ranges -- a quarter of the partial buffer and of
-    // the fold (config 2 -4 %, config 3 unchanged); small calls keep 64 ranges for
-    // parallelism (more units), large ones for L2 locality (a range's rows stay resident:
-    // config 4 +3 % with 16)
-    if (nf == 1 && n_beams > 16384 && n_beams <= ((int64_t)1 << 21)) ranges = 16;
+    const int64_t ranges = BF_RANGES / nf > 8 ? BF_RANGES / nf : 8;
     int64_t rb = (n_beams + ranges - 1) / ranges;
     rb = (rb + 31) / 32 * 32;
     return rb < 32 ? 32 : rb;
