@@ -126,6 +126,12 @@ enum {
  * They do depend on the call's beam and observer sets (patch-local fp32
  * geometry): splitting a call changes fp32 results within the fp32 tolerance,
  * while fp64 mode is bit-identical under any split of beams or observers.
+ *
+ * Small fp32 calls (<= 2^28 beam-receiver pairs) repeated with identical
+ * arguments (pointers, sizes, scalars, frequencies, flags, stream) replay a CUDA
+ * graph of the whole call captured on the second one; the graph reads the
+ * buffers at replay time, the bits equal an eager call's, and it is dropped when
+ * a workspace is reallocated.
  */
 int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
                           const double *seg_e1, const double *seg_e2,
