@@ -659,7 +659,8 @@ def test_tracer_cluster_culling_equals_exhaustive(src):
     assert int(a.n_refls.max()) >= 2  # the rays do bounce between buildings
 
 
-def test_repeated_small_calls_replay_a_graph_bitexact():
+@pytest.mark.parametrize("case", ["city_street", "city_corner_f5"])
+def test_repeated_small_calls_replay_a_graph_bitexact(case):
     """Identical small device calls: the first runs eagerly, the second is captured into a
     CUDA graph, later ones replay it (engine.cu run_fp32_graph).  The sequence must equal,
     bit for bit, the same calls made with a changing memory budget (a different key every
@@ -668,7 +669,7 @@ def test_repeated_small_calls_replay_a_graph_bitexact():
     import torch
 
     from paper_2501_13382_b200 import _lib, kernels
-    b = load_case("city_street")
+    b = load_case(case)
     dev = torch.device("cuda", 0)
     t = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa
     args = [t(b["seg_origin"]), t(b["seg_dir"]), t(b["seg_e1"]), t(b["seg_e2"]),
@@ -678,7 +679,8 @@ def test_repeated_small_calls_replay_a_graph_bitexact():
     n_obs, nb = b["obs"].shape[0], b["n_segs"].shape[0]
 
     def sequence(budgets, big_after=None):
-        acc = torch.zeros((n_obs, 1), dtype=torch.complex128, device=dev)
+        nf = b["omegas"].shape[0]
+        acc = torch.zeros((n_obs, nf), dtype=torch.complex128, device=dev)
         ev = torch.zeros(n_obs, dtype=torch.int64, device=dev)
         out, evs = [], []
         for i, bud in enumerate(budgets):
@@ -690,7 +692,7 @@ def test_repeated_small_calls_replay_a_graph_bitexact():
                         tuple(st["patch_beams"].values())))
             if big_after == i:  # a larger call grows the workspaces (new generation)
                 big = torch.cat([args[10]] * 4)
-                a2 = torch.zeros((big.shape[0], 1), dtype=torch.complex128, device=dev)
+                a2 = torch.zeros((big.shape[0], nf), dtype=torch.complex128, device=dev)
                 e2 = torch.zeros(big.shape[0], dtype=torch.int64, device=dev)
                 kernels.gbs_accumulate(*args[:10], big, *args[11:], a2, e2, 0, big.shape[0],
                                        0, nb, precision="fp32")
