@@ -81,7 +81,7 @@ namespace {
 #endif
 static_assert(BF_RANGES <= 64, "unit sort keys hold the beam range in 6 bits");
 #ifndef BF_FLUSHN
-#define BF_FLUSHN 4  // several frequencies: chunks per fp64 flush of the partials (power of 2)
+#define BF_FLUSHN 16  // several frequencies: chunks per fp64 flush of the partials (power of 2)
 #endif
 constexpr int R = 4;                    // receivers per lane
 constexpr int PATCH = 32 * R;           // receivers per warp patch
@@ -111,7 +111,10 @@ template <bool MF>
 constexpr bool P64G = MF && !BF_MF_P64_SMEM;  // fp64 receiver positions from global memory
 constexpr int CB = 32;                  // max beams per staged chunk
 constexpr int ROWCAP = BF_ROWCAP;       // max segment rows per staged chunk (one frequency)
-constexpr int ROWCAP_MF = 64;           // ... several frequencies (power of two, see ROWS)
+#ifndef BF_ROWCAP_MF
+#define BF_ROWCAP_MF 64
+#endif
+constexpr int ROWCAP_MF = BF_ROWCAP_MF;  // ... several frequencies (a multiple of 32)
 template <bool MF>
 constexpr int ROWS = MF ? ROWCAP_MF : ROWCAP;
 constexpr int EVG = BF_EVG;             // receivers evaluated per branch of the tail
@@ -1262,7 +1265,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 for (int j = 0; j < R; ++j) {
                     s64[j] = 0.0;
                     if ((lvm >> j) & 1u) {
-                        const int64_t g = S.rowinfo[pref[j] & (ROWS<MF> - 1)];
+                        const int64_t g = S.rowinfo[pref[j]];
                         const double4 o = w.p0[g], d = w.p1[g];
                         const D3 P = P64(j);
                         const double wx = __dsub_rn(P.x, o.x), wy = __dsub_rn(P.y, o.y),
