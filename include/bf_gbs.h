@@ -114,7 +114,10 @@ enum {
 /*
  * Same operator on DEVICE buffers (all pointers are device pointers on
  * `device`).  Asynchronous on `stream` (cudaStream_t, NULL = the engine's own
- * stream, which the call synchronises before returning).  `omegas` is a HOST
+ * stream, which the call synchronises before returning; cudaStreamLegacy or
+ * cudaStreamPerThread = the work runs on the engine's stream fenced in and out
+ * of that stream by events, asynchronous and graph-capturable -- torch's
+ * default stream is passed this way).  `omegas` is a HOST
  * array.  Any nf: frequencies are summed in groups of 8 (acc columns are
  * independent).  fp32 mode needs max_seg <= 30 (BF_EINVAL otherwise, before any
  * work) and fewer than 2^27 beams per call.

@@ -153,9 +153,14 @@ int launch_fp32_patches(const GbsArgs &a, const Tiling &t, Fp32Work &w, cudaStre
 // the counts, the entries (pass 2).
 // wstats (4 x n_tiles, zeroed): per tile a9 candidate beams, their segments, tight
 // candidate beams, their segments.
-// Queue order: keys (longest-first bucket << 32 | range) and unit values, radix-sorted.
+// Queue order: keys (wide << 13 | longest-first bucket << 6 | range) and unit values,
+// radix-sorted.
 int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
                           const int64_t *counts, uint64_t *keys, int32_t *vals, cudaStream_t st);
+// one CTA: unit keys + counting sort + wide count, for n_patches * n_ranges <= SMALL_QUEUE_N
+constexpr int64_t SMALL_QUEUE_N = 32768;
+int launch_fp32_small_queue(const Fp32Work &w, const int64_t *counts, int32_t *order,
+                            cudaStream_t st);
 int launch_fp32_wl_compact(const Tiling &t, const Fp32Work &w, cudaStream_t st);
 // The summation of one group of beam ranges (wide-patch kernel on st.aux first, the
 // common kernel on st.st), without the fold.

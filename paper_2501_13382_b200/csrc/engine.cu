@@ -131,7 +131,7 @@ constexpr int NSLOT = 3;  // beam groups in flight
 struct Slot {
     cudaStream_t ss = nullptr, sw = nullptr;  // the group's stream, its wide-kernel stream
     cudaEvent_t fork = nullptr, join = nullptr, kdone = nullptr, freed = nullptr,
-                h2d = nullptr;
+                h2d = nullptr, qfork = nullptr, qjoin = nullptr;
     bool freed_valid = false, h2d_valid = false;
     Buf buf[S_COUNT];
     PinBuf pin[P_COUNT];
@@ -162,6 +162,12 @@ struct DeviceCtx {
     cudaEvent_t done = nullptr;
     bool done_valid = false;
     cudaEvent_t pro = nullptr;  // end of a call's prologue (tiling) on its stream
+    cudaEvent_t fin = nullptr, fout = nullptr;  // CallStream fences (legacy stream handles)
+    // statistics read-back (stats_copy) on a side stream, off the caller's critical path;
+    // the next call waits for it (StreamOrder) before zeroing the counters again
+    cudaStream_t side = nullptr;
+    cudaEvent_t kend = nullptr, sdone = nullptr;
+    bool sdone_valid = false;
     cudaEvent_t piece[2] = {};  // staged copy-out pieces landed (d2h_out)
     int64_t budget = 0;         // group-workspace budget in bytes (0: automatic)
     // Small fp32 device calls repeated with identical arguments replay a captured graph
@@ -175,6 +181,8 @@ struct DeviceCtx {
         uint64_t gen = 0;
         int sb = -1;        // statistics buffer the graph writes
         int launches = 0;   // library kernels in the graph
+        const void *d_stats = nullptr, *d_cand = nullptr;  // its counters (stats_copy)
+        int64_t n_tiles = 0;
     } gc;
     std::mutex mu;
     Buf buf[B_COUNT];
@@ -203,9 +211,42 @@ struct StreamOrder {
     cudaStream_t st;
     StreamOrder(DeviceCtx *c_, cudaStream_t st_) : c(c_), st(st_) {
         if (c->done_valid) cudaStreamWaitEvent(st, c->done, 0);
+        if (c->sdone_valid) cudaStreamWaitEvent(st, c->sdone, 0);
     }
     ~StreamOrder() {
         if (cudaEventRecord(c->done, st) == cudaSuccess) c->done_valid = true;
+    }
+};
+
+// The stream a summation call's work goes on.  NULL: the context's stream, and the call
+// returns after the work.  cudaStreamLegacy / cudaStreamPerThread (what torch's default
+// stream is passed as): work on those cannot be captured into a CUDA graph, so the call
+// runs on the context's stream between two event fences -- ordered after the caller's
+// earlier work and before its later work, without a host wait.  Any other handle: that
+// stream itself.
+struct CallStream {
+    DeviceCtx *c;
+    cudaStream_t user, st;
+    bool fenced;
+    CallStream(DeviceCtx *c_, void *stream) : c(c_), user((cudaStream_t)stream) {
+        fenced = user == cudaStreamLegacy || user == cudaStreamPerThread;
+        st = (user && !fenced) ? user : c->stream;
+    }
+    int enter() {
+        if (fenced) {
+            BF_TRY_CUDA(cudaEventRecord(c->fin, user));
+            BF_TRY_CUDA(cudaStreamWaitEvent(st, c->fin, 0));
+        }
+        return BF_OK;
+    }
+    int leave() {
+        if (fenced) {
+            BF_TRY_CUDA(cudaEventRecord(c->fout, st));
+            BF_TRY_CUDA(cudaStreamWaitEvent(user, c->fout, 0));
+        } else if (!user) {
+            BF_TRY_CUDA(cudaStreamSynchronize(st));
+        }
+        return BF_OK;
     }
 };
 
@@ -238,6 +279,11 @@ int get_ctx(int device, DeviceCtx **out) {
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->pro, fl));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fin, fl));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fout, fl));
+        BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->kend, fl));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->sdone, fl));
         for (Slot &s : c->slot) {
             BF_TRY_CUDA(cudaStreamCreateWithFlags(&s.ss, cudaStreamNonBlocking));
             BF_TRY_CUDA(cudaStreamCreateWithFlags(&s.sw, cudaStreamNonBlocking));
@@ -246,6 +292,8 @@ int get_ctx(int device, DeviceCtx **out) {
             BF_TRY_CUDA(cudaEventCreateWithFlags(&s.kdone, fl));
             BF_TRY_CUDA(cudaEventCreateWithFlags(&s.freed, fl));
             BF_TRY_CUDA(cudaEventCreateWithFlags(&s.h2d, fl));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.qfork, fl));
+            BF_TRY_CUDA(cudaEventCreateWithFlags(&s.qjoin, fl));
         }
         g_ctx[device] = c;
     }
@@ -359,51 +407,6 @@ int stats_next(StatsBuf **out) {
     g_ps.cur = i;
     *out = &b;
     return BF_OK;
-}
-
-// ------------------------------------------------------------ small sort ----
-
-// Stable key-value radix sort of n <= SMALL_SORT_N pairs in one CTA (the unit queue of a
-// small call: one launch instead of cub's multi-kernel device sort; the same order, both
-// sorts being stable).  Keys past n are padded with 2^end_bit - 1, above every real key.
-constexpr int SMALL_SORT_T = 512, SMALL_SORT_I = 16;
-constexpr int64_t SMALL_SORT_N = SMALL_SORT_T * SMALL_SORT_I;
-using SmallSort = cub::BlockRadixSort<uint64_t, SMALL_SORT_T, SMALL_SORT_I, int32_t>;
-
-__global__ void __launch_bounds__(SMALL_SORT_T)
-    small_sort_kernel(const uint64_t *keys, const int32_t *vals, int n, int end_bit,
-                      int32_t *out) {
-    extern __shared__ __align__(16) unsigned char smem_sort[];
-    auto &tmp = *reinterpret_cast<typename SmallSort::TempStorage *>(smem_sort);
-    uint64_t k[SMALL_SORT_I];
-    int32_t v[SMALL_SORT_I];
-    const uint64_t pad = (end_bit >= 64 ? ~0ull : ((1ull << end_bit) - 1ull));
-#pragma unroll
-    for (int i = 0; i < SMALL_SORT_I; ++i) {
-        const int idx = threadIdx.x * SMALL_SORT_I + i;  // blocked arrangement
-        k[i] = idx < n ? keys[idx] : pad;
-        v[i] = idx < n ? vals[idx] : 0;
-    }
-    SmallSort(tmp).Sort(k, v, 0, end_bit);
-#pragma unroll
-    for (int i = 0; i < SMALL_SORT_I; ++i) {
-        const int idx = threadIdx.x * SMALL_SORT_I + i;
-        if (idx < n) out[idx] = v[i];
-    }
-}
-
-int small_sort(const uint64_t *keys, const int32_t *vals, int n, int end_bit, int32_t *out,
-               cudaStream_t st) {
-    static bool attr = false;  // benign race: the same value
-    const int smem = (int)sizeof(typename SmallSort::TempStorage);
-    if (!attr) {
-        BF_TRY_CUDA(cudaFuncSetAttribute(small_sort_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
-    small_sort_kernel<<<1, SMALL_SORT_T, smem, st>>>(keys, vals, n, end_bit, out);
-    note_launch();
-    return check_cuda(cudaGetLastError(), "small_sort_kernel");
 }
 
 // ------------------------------------------------------------ tiling ----
@@ -913,6 +916,52 @@ int rows_from_resident(const bf_rows &R, int64_t b0, int64_t nb, Slot &s, Rows *
     return BF_OK;
 }
 
+// Zeroes two word arrays in one launch (the call's counters: one graph node instead of
+// two memset nodes).
+__global__ void zero2_kernel(unsigned long long *a, int64_t na, unsigned long long *b,
+                             int64_t nb) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < na) a[i] = 0ull;
+        else b[i - na] = 0ull;
+    }
+}
+
+thread_local struct {
+    const void *d_stats, *d_cand;
+    int64_t n_tiles;
+} g_stats_src;  // the counters of the call being captured (run_fp32_graph copies them back)
+
+// The call's statistics back into sb's pinned buffers on the context's side stream after
+// everything enqueued on st so far: the caller's stream does not wait for the copies.
+int stats_copy(DeviceCtx *c, StatsBuf *sb, const void *d_stats, const void *d_cand,
+               int64_t n_tiles, cudaStream_t st) {
+    if (!sb->h_stats) {
+        g_pool_gen.fetch_add(1);
+        BF_TRY_CUDA(cudaHostAlloc(&sb->h_stats, sizeof(GbsStats), cudaHostAllocPortable));
+    }
+    if (sb->cand_cap < (size_t)(4 * n_tiles)) {
+        g_pool_gen.fetch_add(1);
+        if (sb->h_cand) cudaFreeHost(sb->h_cand);
+        sb->h_cand = nullptr;
+        sb->cand_cap = 0;
+        BF_TRY_CUDA(cudaHostAlloc(&sb->h_cand, 4 * sizeof(unsigned long long) * n_tiles,
+                                  cudaHostAllocPortable));
+        sb->cand_cap = (size_t)(4 * n_tiles);
+    }
+    BF_TRY_CUDA(cudaEventRecord(c->kend, st));
+    BF_TRY_CUDA(cudaStreamWaitEvent(c->side, c->kend, 0));
+    BF_TRY_CUDA(cudaMemcpyAsync(sb->h_stats, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost,
+                                c->side));
+    BF_TRY_CUDA(cudaMemcpyAsync(sb->h_cand, d_cand, 4 * sizeof(unsigned long long) * n_tiles,
+                                cudaMemcpyDeviceToHost, c->side));
+    BF_TRY_CUDA(cudaEventRecord(sb->ready, c->side));
+    BF_TRY_CUDA(cudaEventRecord(c->sdone, c->side));
+    c->sdone_valid = true;
+    sb->inflight = true;
+    return BF_OK;
+}
+
 // The fp32 operator on LOCAL ranges: base.obs/acc/evals are device pointers (offset to
 // obs_lo, acc rows of base.acc_stride complex values); base.seg_*/n_segs/weights are the
 // padded bundle from beam_lo, on the device or (host_rows) in host memory.
@@ -943,8 +992,13 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
     unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
     BF_TRY(c->get(B_STATS, 1, &d_stats));
     BF_TRY(c->get(B_CAND, (size_t)(4 * t.n_tiles), &d_cand));
-    BF_TRY_CUDA(cudaMemsetAsync(d_stats, 0, sizeof(GbsStats), st));
-    BF_TRY_CUDA(cudaMemsetAsync(d_cand, 0, 4 * sizeof(unsigned long long) * t.n_tiles, st));
+    {
+        const int64_t na = sizeof(GbsStats) / 8, nb = 4 * t.n_tiles;
+        zero2_kernel<<<(unsigned)std::min<int64_t>((na + nb + 255) / 256, 1024), 256, 0, st>>>(
+            reinterpret_cast<unsigned long long *>(d_stats), na, d_cand, nb);
+        note_launch();
+        BF_TRY_CUDA(cudaGetLastError());
+    }
     BF_TRY_CUDA(cudaEventRecord(c->pro, st));
     for (Slot &s : c->slot) BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->pro, 0));
     BF_TRY(stats_events(c->dev));
@@ -1036,25 +1090,34 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
                                                           (int)(nu_wl + 1), s.ss));
                 note_launch();
             }
+            // ---- compacted work list (on the wide-kernel stream, concurrent with the queue
+            //      order below): sized by its bound (tiles x beams), no host sync
+            BF_TRY(s.get(S_WLITEMS, (size_t)(t.n_tiles * gg.n_beams + 1), &w.wl_items));
+            BF_TRY_CUDA(cudaEventRecord(s.qfork, s.ss));
+            BF_TRY_CUDA(cudaStreamWaitEvent(s.sw, s.qfork, 0));
+            BF_TRY(launch_fp32_wl_compact(tg, w, s.sw));
+            BF_TRY_CUDA(cudaEventRecord(s.qjoin, s.sw));
             // ---- unit queue order (wide patches last; longest-first buckets, range-major
             //      inside a bucket) from the counts and the patch radii
             BF_TRY(s.get(S_UCTR, 3, &w.unit_ctr));
             w.n_wide = w.unit_ctr + 2;
-            BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), s.ss));
             {
                 const int64_t nu = w.n_patches * w.n_ranges;
-                uint64_t *k0, *k1;
-                int32_t *v0, *v1;
-                BF_TRY(s.get(S_UKEYS, (size_t)nu, &k0));
-                BF_TRY(s.get(S_UKEYS2, (size_t)nu, &k1));
-                BF_TRY(s.get(S_UVALS, (size_t)nu, &v0));
+                int32_t *v1;
                 BF_TRY(s.get(S_UVALS2, (size_t)nu, &v1));
-                BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
-                const int end_bit = 14;  // wide << 13 | bucket (7 bits) << 6 | range (< 64)
-                if (nu <= SMALL_SORT_N) {  // one CTA, one launch (small calls)
-                    BF_TRY(small_sort(k0, v0, (int)nu, end_bit, v1, s.ss));
+                if (nu <= SMALL_QUEUE_N) {  // one CTA, one launch (small calls; it also
+                                            // sets the queue heads and the wide count)
+                    BF_TRY(launch_fp32_small_queue(w, cnt, v1, s.ss));
                     w.unit_order = v1;
                 } else {
+                    BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), s.ss));
+                    uint64_t *k0, *k1;
+                    int32_t *v0;
+                    BF_TRY(s.get(S_UKEYS, (size_t)nu, &k0));
+                    BF_TRY(s.get(S_UKEYS2, (size_t)nu, &k1));
+                    BF_TRY(s.get(S_UVALS, (size_t)nu, &v0));
+                    BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
+                    const int end_bit = 14;  // wide << 13 | bucket (7 bits) << 6 | range (< 64)
                     cub::DoubleBuffer<uint64_t> dk(k0, k1);
                     cub::DoubleBuffer<int32_t> dv(v0, v1);
                     size_t tb = 0;
@@ -1068,9 +1131,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
                     w.unit_order = dv.Current();
                 }
             }
-            // ---- compacted work list: sized by its bound (tiles x beams), no host sync
-            BF_TRY(s.get(S_WLITEMS, (size_t)(t.n_tiles * gg.n_beams + 1), &w.wl_items));
-            BF_TRY(launch_fp32_wl_compact(tg, w, s.ss));
+            BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, s.qjoin, 0));
             BF_TRY(s.get(S_PART, (size_t)(w.n_ranges * w.n_pad * ag.nf), &w.part));
             BF_TRY(s.get(S_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
             if (!timed) {
@@ -1091,31 +1152,18 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
         }
     }
     BF_TRY_CUDA(rec_ext(sb->t1, st));
-    // ---- statistics: copied back asynchronously, reduced on request (bf_last_stats)
-    if (!sb->h_stats) {
-        g_pool_gen.fetch_add(1);
-        BF_TRY_CUDA(cudaHostAlloc(&sb->h_stats, sizeof(GbsStats), cudaHostAllocPortable));
-    }
-    if (sb->cand_cap < (size_t)(4 * t.n_tiles)) {
-        g_pool_gen.fetch_add(1);
-        if (sb->h_cand) cudaFreeHost(sb->h_cand);
-        sb->h_cand = nullptr;
-        sb->cand_cap = 0;
-        BF_TRY_CUDA(cudaHostAlloc(&sb->h_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
-                                  cudaHostAllocPortable));
-        sb->cand_cap = (size_t)(4 * t.n_tiles);
-    }
-    BF_TRY_CUDA(cudaMemcpyAsync(sb->h_stats, d_stats, sizeof(GbsStats), cudaMemcpyDeviceToHost,
-                                st));
-    BF_TRY_CUDA(cudaMemcpyAsync(sb->h_cand, d_cand, 4 * sizeof(unsigned long long) * t.n_tiles,
-                                cudaMemcpyDeviceToHost, st));
-    BF_TRY_CUDA(rec_ext(sb->ready, st));
-    sb->inflight = true;
+    // ---- statistics: copied back asynchronously, reduced on request (bf_last_stats); a
+    //      call being captured leaves the copies to run_fp32_graph (after the graph)
     sb->n_tiles = t.n_tiles;
     sb->tile = t.tile;
     sb->n_obs = base.n_obs;
     g_ps.pending = true;
-    return BF_OK;
+    if (g_capturing) {
+        g_stats_src = {d_stats, d_cand, t.n_tiles};
+        sb->inflight = true;
+        return BF_OK;
+    }
+    return stats_copy(c, sb, d_stats, d_cand, t.n_tiles, st);
 }
 
 // Small device calls (see DeviceCtx::GraphCache): identical repeated calls replay a graph
@@ -1147,9 +1195,8 @@ int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t
         BF_TRY_CUDA(cudaGraphLaunch(g.exec, st));
         note_launch(g.launches);
         g_ps.cur = g.sb;
-        b.inflight = true;
         g_ps.pending = true;
-        return BF_OK;
+        return stats_copy(c, &b, g.d_stats, g.d_cand, g.n_tiles, st);
     }
     if (g.exec) {
         cudaGraphExecDestroy(g.exec);
@@ -1185,11 +1232,14 @@ int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t
     cudaGraphDestroy(graph);
     BF_TRY_CUDA(ie);
     g.launches = (int)(g_launches.load() - n0);
-    g.gen = g_pool_gen.load();
     g.sb = g_ps.cur;
+    g.d_stats = g_stats_src.d_stats;
+    g.d_cand = g_stats_src.d_cand;
+    g.n_tiles = g_stats_src.n_tiles;
     for (Slot &sl : c->slot) sl.freed_valid = false;  // their events were capture-internal
     BF_TRY_CUDA(cudaGraphLaunch(g.exec, st));
-    g_ps.buf[g.sb].inflight = true;
+    BF_TRY(stats_copy(c, &g_ps.buf[g.sb], g.d_stats, g.d_cand, g.n_tiles, st));
+    g.gen = g_pool_gen.load();  // (after stats_copy: its first pinned allocation bumps it)
     return BF_OK;
 }
 
@@ -1394,7 +1444,9 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
     BF_TRY(get_ctx(device, &ctx));
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(device));
-    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    CallStream cs(ctx, stream);
+    const cudaStream_t st = cs.st;
+    BF_TRY(cs.enter());
     StreamOrder order(ctx, st);
     GbsArgs a{};
     const int64_t r0 = beam_lo * max_seg;
@@ -1429,8 +1481,7 @@ int bf_gbs_accumulate_dev(const double *seg_origin, const double *seg_dir,
     } else {
         BF_TRY(run_fp32(ctx, a, omegas, nf, false, flags, st));
     }
-    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
-    return BF_OK;
+    return cs.leave();
 }
 
 int bf_gbs_accumulate(const double *seg_origin, const double *seg_dir, const double *seg_e1,
@@ -1650,7 +1701,9 @@ int bf_gbs_accumulate_rows_dev(const bf_rows *rows, const double *obs, int64_t n
     BF_TRY(get_ctx(rows->device, &ctx));
     std::lock_guard<std::mutex> lk(ctx->mu);
     BF_TRY_CUDA(cudaSetDevice(rows->device));
-    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    CallStream cs(ctx, stream);
+    const cudaStream_t st = cs.st;
+    BF_TRY(cs.enter());
     StreamOrder order(ctx, st);
     GbsArgs a{};
     a.obs = obs + 3 * obs_lo;
@@ -1666,8 +1719,7 @@ int bf_gbs_accumulate_rows_dev(const bf_rows *rows, const double *obs, int64_t n
     a.acc_stride = nf;
     a.evals = evals + obs_lo;
     BF_TRY(run_fp32(ctx, a, omegas, nf, false, flags, st, nullptr, rows, beam_lo));
-    if (!stream) BF_TRY_CUDA(cudaStreamSynchronize(st));
-    return BF_OK;
+    return cs.leave();
 }
 
 int bf_nearest_on_segments(const double *seg_origin, const double *seg_dir,

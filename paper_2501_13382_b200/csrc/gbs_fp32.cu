@@ -1618,25 +1618,56 @@ __global__ void patch_kernel(const double *obs, int64_t n, const int32_t *perm,
     }
 }
 
-// acc[oi] += sum over beam ranges q (ascending) of the units' partials; evals alike.
-__global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, int64_t stride,
-                            double *acc, int64_t *evals) {
-    const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (si >= tl.n) return;
-    const int64_t oi = tl.perm[si];
+// acc[oi] += sum over beam ranges q (ascending) of the units' partials; evals alike.  The
+// adds stay one sequential chain per receiver, acc + v_0 + v_1 + ... (so beam groups and
+// chunk plans that split the same ranges give the same bits), but a block of 32 receivers
+// stages the partials through shared memory with FOLD_G threads per receiver: FOLD_G times
+// the loads in flight of a thread per receiver (small calls are latency bound here).
+constexpr int FOLD_G = 8, FOLD_Q = 64;
+__global__ void __launch_bounds__(32 * FOLD_G)
+    fold_kernel(const Tiling tl, const Fp32Work w, int nf, int64_t stride, double *acc,
+                int64_t *evals) {
+    __shared__ double2 vals[FOLD_Q][32];
+    __shared__ int rev[FOLD_G][32];
+    const int x = threadIdx.x, g = threadIdx.y;
+    const int64_t si = (int64_t)blockIdx.x * 32 + x;
+    const bool ok = si < tl.n;
+    const int64_t oi = ok ? tl.perm[si] : 0;
     for (int f = 0; f < nf; ++f) {
-        double re = acc[2 * (oi * stride + f)], im = acc[2 * (oi * stride + f) + 1];
-        for (int64_t q = 0; q < w.n_ranges; ++q) {
-            const double2 v = w.part[(q * w.n_pad + si) * nf + f];
-            re += v.x;
-            im += v.y;
+        double re = 0.0, im = 0.0;
+        if (g == 0 && ok) {
+            re = acc[2 * (oi * stride + f)];
+            im = acc[2 * (oi * stride + f) + 1];
         }
-        acc[2 * (oi * stride + f)] = re;
-        acc[2 * (oi * stride + f) + 1] = im;
+        for (int64_t qb = 0; qb < w.n_ranges; qb += FOLD_Q) {
+            const int nq = (int)(w.n_ranges - qb < FOLD_Q ? w.n_ranges - qb : FOLD_Q);
+            if (ok)
+                for (int j = g; j < nq; j += FOLD_G)
+                    vals[j][x] = w.part[((qb + j) * w.n_pad + si) * nf + f];
+            __syncthreads();
+            if (g == 0 && ok)
+                for (int j = 0; j < nq; ++j) {
+                    re += vals[j][x].x;
+                    im += vals[j][x].y;
+                }
+            __syncthreads();
+        }
+        if (g == 0 && ok) {
+            acc[2 * (oi * stride + f)] = re;
+            acc[2 * (oi * stride + f) + 1] = im;
+        }
     }
-    int64_t ev = 0;
-    for (int64_t q = 0; q < w.n_ranges; ++q) ev += w.part_ev[q * w.n_pad + si];
-    evals[oi] += ev;
+    int ev = 0;  // integer: any order
+    if (ok)
+        for (int64_t q = g; q < w.n_ranges; q += FOLD_G) ev += w.part_ev[q * w.n_pad + si];
+    rev[g][x] = ev;
+    __syncthreads();
+    if (g == 0 && ok) {
+        int64_t e = 0;
+#pragma unroll
+        for (int j = 0; j < FOLD_G; ++j) e += rev[j][x];
+        evals[oi] += e;
+    }
 }
 
 // Sort keys of the unit queue: longest-first in half-octave buckets of the unit's
@@ -1648,21 +1679,104 @@ __global__ void fold_kernel(const Tiling tl, const Fp32Work w, int nf, int64_t s
 // ~eps RW^2, which with strong cancellation between beams (a receiver 50 dB below the
 // field maximum) reaches the 0.01 dB gate once kappa RW is tens of turns (sparse
 // receiver sets); the wide kernel recomputes s, q^2 and the phase in fp64.
-__global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_t *counts,
-                                 uint64_t *keys, int32_t *vals) {
-    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= w.n_patches * w.n_ranges) return;
-    const int64_t q = u / w.n_patches, p = u - q * w.n_patches;
+__device__ __forceinline__ unsigned unit_key(const Fp32Work &w, const int64_t *counts,
+                                             int64_t q, int64_t p, bool *wide) {
     const int64_t tile = p / (TILE / PATCH);
     const uint64_t c = (uint64_t)counts[tile * w.n_ranges + q] + 1;
     const int msb = 63 - __clzll((long long)c);
     const int bucket = 2 * msb + (msb > 0 ? (int)((c >> (msb - 1)) & 1) : 0);  // < 128
-    const bool wide = wide_patch(w, p);
+    *wide = wide_patch(w, p);
+    // 14 significant bits (wide, 7-bit bucket, range q < 64): the radix sort needs 2
+    // passes (8-bit digits) instead of 5 over 40 bits
+    return ((unsigned)*wide << 13) | ((unsigned)(127 - bucket) << 6) | (unsigned)q;
+}
+
+__global__ void unit_keys_kernel(const Tiling tl, const Fp32Work w, const int64_t *counts,
+                                 uint64_t *keys, int32_t *vals) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= w.n_patches * w.n_ranges) return;
+    bool wide;
+    const int64_t q = u / w.n_patches;
+    keys[u] = unit_key(w, counts, q, u - q * w.n_patches, &wide);
     if (wide) atomicAdd(w.n_wide, 1u);
-    // 14 significant bits (wide, 7-bit bucket, range q < 64): the radix sorts need 2 (cub,
-    // 8-bit digits) or 4 (one CTA, 4-bit digits) passes instead of 5 / 10 over 40 bits
-    keys[u] = ((uint64_t)wide << 13) | ((uint64_t)(127 - bucket) << 6) | (uint64_t)q;
     vals[u] = (int32_t)u;
+}
+
+// Small calls (<= SMALL_QUEUE_N units): the keys, a counting sort and the wide-unit count
+// in one CTA and one launch (instead of the keys kernel and a radix sort).  The sort key is
+// the unit key without its range bits (wide, bucket: 256 values); units enter it in
+// ascending u = q n_patches + p, so inside a bucket the order stays range-major up to the
+// interleaving of concurrent warps.  That order only decides which warp takes a unit
+// first, never a result (every unit writes its own partial slot, fold_kernel adds them in
+// range order).
+constexpr int SQ_T = 1024, SQ_BINS = 256;
+__global__ void __launch_bounds__(SQ_T)
+    small_queue_kernel(const Fp32Work w, const int64_t *counts, int32_t *order) {
+    extern __shared__ unsigned char sq_key[];  // per unit: wide << 7 | (127 - bucket)
+    __shared__ int hist[SQ_BINS];
+    __shared__ unsigned nwide;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nu = (int)(w.n_patches * w.n_ranges);
+    if (tid < SQ_BINS) hist[tid] = 0;
+    if (tid == 0) nwide = 0;
+    __syncthreads();
+    unsigned nw = 0;
+    // keys first (independent global loads, unrolled so several are in flight; 32-bit
+    // index math: nu <= SMALL_QUEUE_N), then the histogram with one shared-memory atomic
+    // per distinct key of a warp (the 32 units of a warp are mostly one bucket)
+    const int np = (int)w.n_patches;
+#pragma unroll 4
+    for (int u = tid; u < nu; u += SQ_T) {
+        bool wide;
+        const int q = u / np;
+        sq_key[u] = (unsigned char)(unit_key(w, counts, q, u - q * np, &wide) >> 6);
+        nw += wide;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int u0 = wid * 32; u0 < nu; u0 += SQ_T) {
+        const int u = u0 + lane;
+        const unsigned live = __ballot_sync(0xffffffffu, u < nu);
+        const unsigned k = u < nu ? sq_key[u] : 0xffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, k) & live;
+        if (u < nu && (peers & lt) == 0) atomicAdd(&hist[k], __popc(peers));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) nw += __shfl_xor_sync(0xffffffffu, nw, o);
+    if (lane == 0 && nw) atomicAdd(&nwide, nw);
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the 256 counters, rows of 32
+        int carry = 0;
+#pragma unroll
+        for (int r = 0; r < SQ_BINS / 32; ++r) {
+            const int v = hist[32 * r + lane];
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            hist[32 * r + lane] = carry + incl - v;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    for (int u0 = wid * 32; u0 < nu; u0 += SQ_T) {
+        const int u = u0 + lane;
+        const unsigned live = __ballot_sync(0xffffffffu, u < nu);
+        const unsigned k = u < nu ? sq_key[u] : 0xffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, k) & live;
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (u < nu && lane == leader) base = atomicAdd(&hist[k], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader < 0 ? 0 : leader);
+        if (u < nu) order[base + __popc(peers & lt)] = u;
+    }
+    if (tid == 0) {  // the two queue heads and the wide count (w.n_wide = w.unit_ctr + 2)
+        w.unit_ctr[0] = 0u;
+        w.unit_ctr[1] = 0u;
+        *w.n_wide = nwide;
+    }
 }
 
 // One warp per (tile, beam range): ascending candidate beams with their segment
@@ -1898,6 +2012,28 @@ int launch_fp32_unit_keys(const Tiling &t, const Fp32Work &w,
     return BF_OK;
 }
 
+int launch_fp32_small_queue(const Fp32Work &w, const int64_t *counts, int32_t *order,
+                            cudaStream_t st) {
+    const int64_t nu = w.n_patches * w.n_ranges;
+    if (nu <= 0) return BF_OK;
+    if (nu > SMALL_QUEUE_N) return fail(BF_EINVAL, "small queue of %lld units", (long long)nu);
+    const size_t smem = SMALL_QUEUE_N;  // one key byte per unit
+    constexpr int MAXDEV = 64;
+    static bool attr_set[MAXDEV] = {};
+    int dev = 0;
+    BF_TRY_CUDA(cudaGetDevice(&dev));
+    if (dev >= MAXDEV) return fail(BF_ENODEV, "device index %d >= %d", dev, MAXDEV);
+    if (!attr_set[dev]) {
+        BF_TRY_CUDA(cudaFuncSetAttribute(small_queue_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set[dev] = true;
+    }
+    small_queue_kernel<<<1, SQ_T, smem, st>>>(w, counts, order);
+    note_launch();
+    BF_TRY_CUDA(cudaGetLastError());
+    return BF_OK;
+}
+
 int launch_fp32_wl_compact(const Tiling &t, const Fp32Work &w, cudaStream_t st) {
     const int64_t nu = t.n_tiles * w.n_ranges;
     if (nu > 0) {
@@ -1927,8 +2063,8 @@ int launch_gbs_fp32(const GbsArgs &a, const Tiling &t, const Fp32Work &w, GbsSta
 
 int launch_fp32_fold(const GbsArgs &a, const Tiling &t, const Fp32Work &w, cudaStream_t st) {
     if (t.n <= 0 || w.n_ranges <= 0) return BF_OK;
-    fold_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, st>>>(t, w, a.nf, a.acc_stride, a.acc,
-                                                               a.evals);
+    fold_kernel<<<(unsigned)((t.n + 31) / 32), dim3(32, FOLD_G), 0, st>>>(
+        t, w, a.nf, a.acc_stride, a.acc, a.evals);
     note_launch();
     BF_TRY_CUDA(cudaGetLastError());
     return BF_OK;

@@ -40,13 +40,18 @@ def _vp(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (cuda_runtime_api.h)
+
+
 def _stream_ptr(stream, device=None):
     """The cudaStream_t of `stream`; None -> torch's current stream on `device`, so the
-    engine's work is ordered after the torch kernels that produced its inputs."""
+    engine's work is ordered after the torch kernels that produced its inputs.  torch's
+    default stream has handle 0, which the C ABI reads as "the engine's own stream,
+    synchronous"; it is passed as cudaStreamLegacy instead (the same stream, explicitly)."""
     if stream is None:
         torch = _torch()
         stream = torch.cuda.current_stream(device)
-    return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(stream.cuda_stream or CUDA_STREAM_LEGACY)
 
 
 @dataclass

@@ -138,7 +138,10 @@ def _gbs_dev(lib, seg_origin, seg_dir, seg_e1, seg_e2, seg_len, seg_s0, seg_refl
         raise ValueError(f"acc shape {tuple(acc.shape)} != {(n_obs, nf)}")
     if stream is None:
         stream = torch.cuda.current_stream(dev)  # ordered after the producers of the inputs
-    st = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    # torch's default stream (handle 0) goes as cudaStreamLegacy: asynchronous and ordered
+    # on it (a bare 0 would ask the C ABI for its own stream and a synchronous call)
+    st = ctypes.c_void_p((stream.cuda_stream or 0x1) if hasattr(stream, "cuda_stream")
+                         else int(stream))
     _lib.check(lib.bf_gbs_accumulate_dev(
         _ptr(seg_origin), _ptr(seg_dir), _ptr(seg_e1) if prec == 1 else None,
         _ptr(seg_e2) if prec == 1 else None, _ptr(seg_len), _ptr(seg_s0), _ptr(seg_refl),

@@ -41,7 +41,7 @@ def tile_order(obs_dev):
     st = torch.cuda.current_stream(obs_dev.device)
     _lib.check(_lib.load().bf_tile_order_dev(
         ctypes.c_void_p(obs_dev.data_ptr()), n, ctypes.c_void_p(perm.data_ptr()),
-        obs_dev.device.index or 0, ctypes.c_void_p(st.cuda_stream)))
+        obs_dev.device.index or 0, ctypes.c_void_p(st.cuda_stream or 0x1)))  # 0x1: legacy
     return perm.long()
 
 

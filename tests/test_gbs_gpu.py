@@ -207,6 +207,41 @@ def test_device_call_returns_before_the_kernels_end():
     assert host_s < 0.05
 
 
+def test_default_stream_call_is_ordered_and_async():
+    """On torch's default stream (handle 0, passed as cudaStreamLegacy) a call is fenced in
+    and out of that stream: it returns while earlier default-stream work still runs, sees
+    that work's results (acc filled by a torch kernel queued behind a sleep), and later
+    default-stream work sees its result; repeated calls (graph replay) keep the bits."""
+    import time
+
+    import torch
+
+    from paper_2501_13382_b200 import engine
+    b = load_case("city_street")
+    dev = torch.device("cuda", 0)
+    db = engine.DeviceBundle.from_host(_pb(b), dev, with_frame=False)
+    obs = torch.from_numpy(b["obs"][:4096].copy()).to(dev)
+    acc = torch.zeros((obs.shape[0], 1), dtype=torch.complex128, device=dev)
+    ev = torch.zeros(obs.shape[0], dtype=torch.int64, device=dev)
+    assert torch.cuda.current_stream(dev).cuda_stream == 0
+    acc.fill_(1.0)
+    torch.cuda.synchronize()
+    engine.accumulate(db, obs, b["omegas"], 10.0, True, acc, ev)
+    torch.cuda.synchronize()
+    ref = acc.cpu().numpy().copy()  # acc = 1 + the field, summed onto the 1
+    for _ in range(4):  # eager, capture, replays
+        torch.cuda._sleep(100_000_000)  # ~50 ms of default-stream work in front
+        acc.fill_(1.0)                  # ... then the field the call must continue
+        ev.zero_()
+        t0 = time.perf_counter()
+        engine.accumulate(db, obs, b["omegas"], 10.0, True, acc, ev)
+        host_s = time.perf_counter() - t0
+        out = acc.clone()               # default-stream work after the call
+        torch.cuda.synchronize()
+        assert host_s < 0.03
+        assert np.array_equal(out.cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_chunked_and_ranged_calls(precision):
     """Beam chunks continue acc in place; rows outside [obs_lo, obs_hi) untouched."""
