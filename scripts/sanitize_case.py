@@ -30,3 +30,27 @@ _lib.set_memory_budget(0, 1 << 20)
 acc = np.zeros((obs.shape[0], 1), np.complex128); ev = np.zeros(obs.shape[0], np.int64)
 kernels.gbs_accumulate(*gbs_args(b, obs), acc, ev, 0, obs.shape[0], 0, nb, precision="fp32")
 print("budget 1 MiB", float(np.abs(acc).sum()), int(ev.sum()), flush=True)
+_lib.set_memory_budget(0, 0)
+# device ABI on torch's default stream (fenced onto the engine stream), repeated identical
+# calls: eager, captured, replayed graph; statistics read back on the side stream
+import torch
+from paper_2501_13382_b200 import engine
+from paper_2501_13382_b200.beamtrace import PathBundle
+b = load_case("cfg1_open_plane")
+pb = PathBundle(seg_origin=b["seg_origin"], seg_dir=b["seg_dir"], seg_e1=b["seg_e1"],
+                seg_e2=b["seg_e2"], seg_len=b["seg_len"], seg_s0=b["seg_s0"],
+                seg_refl=b["seg_refl"], n_segs=b["n_segs"], n_refls=b["n_refls"],
+                max_seg=int(b["max_seg"]), weights=b["weights"], gamma1=b["gamma1"],
+                gamma2=b["gamma2"], c=float(b["c"]), beam_param_im=float(b["beam_param_im"]),
+                amplitude_phi=float(b["amplitude_phi"]))
+dev = torch.device("cuda", 0)
+db = engine.DeviceBundle.from_host(pb, dev, with_frame=False)
+od = torch.from_numpy(np.ascontiguousarray(b["obs"][:4096])).to(dev)
+acc = torch.zeros((od.shape[0], 1), dtype=torch.complex128, device=dev)
+ev = torch.zeros(od.shape[0], dtype=torch.int64, device=dev)
+for i in range(4):
+    acc.zero_()
+    ev.zero_()
+    engine.accumulate(db, od, b["omegas"], -float(b["beam_param_im"]), True, acc, ev)
+    st = _lib.last_stats()
+    print("device call", i, float(acc.abs().sum()), int(ev.sum()), st["n_tiles"], flush=True)
