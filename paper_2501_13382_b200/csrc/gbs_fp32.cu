@@ -126,7 +126,7 @@ constexpr float TIE_D2 = 4.76837158203125e-07f;     // 2^-21 (x d^2)
 constexpr float TIE_DSQ = 1.8189894035458565e-12f;  // 2^-39 (x D^2)
 
 #if BF_HIST
-__device__ unsigned long long g_hist[8];  // debug counters (BF_HIST builds only)
+__device__ unsigned long long g_hist[16];  // debug counters (BF_HIST builds only)
 #endif
 #ifndef BF_UNIT_TIMES
 #define BF_UNIT_TIMES 0  // debug: clock64 cycles of every unit to $BF_UNIT_TIMES_OUT
@@ -149,6 +149,15 @@ struct Fp32Consts {
     float kh[BF_MAXF];       // omega/(2 c): phase = an' + kh (c2 + (q^2/m2) s) radians
     float nhkbl2e[BF_MAXF];  // -kh*b*log2(e): exp(-g b) = ex2((q^2/m2)*nhkbl2e)
     double nhkbl2e64[BF_MAXF];
+    // the summation tail works with the arc length in units of b, s' = s/b, and
+    // g' = q^2/(s'^2 + 1) = b^2 q^2/m2 (section 5 of DESIGN.md): the same terms with b folded
+    float gcutq[BF_MAXF];    // gcut b^2: g' > gcutq iff ex_re < -36
+    float khq[BF_MAXF];      // kh/b: phase = an' + kh c2 + khq g' s'
+    float nhkq[BF_MAXF];     // nhkbl2e/b^2: exp(-g b) = ex2(g' nhkq)
+    double nhkq64[BF_MAXF];
+    float hinvb;             // 0.5/b: s' = (s0 + Pc')/b + c2 hinvb
+    float invb;              // 1/b
+    double invb64;           // 1/b
     float b, b2;             // width_b, width_b^2
     int ascending;           // omegas nondecreasing (gcut nonincreasing)
     double amp_scale;        // phi*sqrt(c)/(2 pi c)
@@ -250,7 +259,7 @@ struct WarpSmem {
     float4 geo0[ROWS<MF>];     // wc.xyz (c_P - o), len
     float4 geo1[ROWS<MF>];     // d.xyz, Pc (projection of c_P)
     float4 geo2[ROWS<MF>];     // 2 u_c.xyz, |u_c|^2  (u_c = wc - Pc d: c_P's offset from the line)
-    float2 aux[ROWS<MF>];      // s0 + Pc', A (amplitude factor x omega_0); Pc' = clamp(Pc, 0, len)
+    float2 aux[ROWS<MF>];      // (s0 + Pc')/b, A/b (A: amplitude factor x omega_0); Pc' = clamp(Pc, 0, len)
     float4 anc[ROWS<MF>];      // an' (exact phase at s0 + Pc', radians), lo2, hi2, d2 (clamp2)
     float ancf[MF ? NF : 1][MF ? ROWS<MF> : 1];  // several frequencies: an' per frequency
     unsigned rowinfo[ROWS<MF>];  // chunk row -> compact row (Rows) of the group
@@ -315,48 +324,48 @@ struct Recv64 {
 // this code (TINY = false kernels do not contain it).
 __device__ __forceinline__ void tiny_contribution(const Fp32Consts &K, int f, float s, float gq,
                                                   float inv, float A, float ph, double *acc64) {
+    // scaled inputs (s' = s/b, g', 1/(s'^2 + 1), A/b): amp b (s' sin + cos), amp b (s' cos - sin)
     const float sn = sin_approx(ph), cs = cos_approx(ph);
-    const double e = exp2((double)gq * K.nhkbl2e64[f]);
+    const double e = exp2((double)gq * K.nhkq64[f]);
     const double amp = (double)(A * inv) * e * (double)(f > 0 ? K.omrel[f] : 1.f);
-    const double as = amp * (double)s, ab = amp * (double)K.b;
-    acc64[0] += -as * (double)sn - ab * (double)cs;
-    acc64[1] += as * (double)cs - ab * (double)sn;
+    acc64[0] += -amp * ((double)s * (double)sn + (double)cs);
+    acc64[1] += amp * ((double)s * (double)cs - (double)sn);
 }
 
 // One frequency of a pair's contribution (the several-frequency tail): ph the phase,
-// gq = q^2/m2, ais = A s/m2 and aib = A b/m2 shared across frequencies; omrel[f] folded
+// gq = g', s = s', ainv = (A/b)/(s'^2 + 1) shared across frequencies; omrel[f] folded
 // into the exponent (lomrel[f] = log2(omega_f/omega_0)).
 __device__ __forceinline__ void eval_freq(const Fp32Consts &K, int f, float ph, float gq,
-                                          float ais, float aib, float &are, float &aim,
+                                          float s, float ainv, float &are, float &aim,
                                           bool live) {
     const float sn = sin_approx(ph), cs = cos_approx(ph);
-    const float e = ex2_approx(fmaf(gq, K.nhkbl2e[f], K.lomrel[f]));
-    const float as = e * ais, ab = e * aib;
-    if (live) {  // i * amp * (s + i b) * (cos + i sin)
-        are = fmaf(-as, sn, fmaf(-ab, cs, are));
-        aim = fmaf(as, cs, fmaf(-ab, sn, aim));
+    const float amp = ainv * ex2_approx(fmaf(gq, K.nhkq[f], K.lomrel[f]));
+    if (live) {  // i amp (s + i b)(cos + i sin) = amp b (-(s' sin + cos) + i (s' cos - sin))
+        are = fmaf(-amp, fmaf(s, sn, cs), are);
+        aim = fmaf(amp, fmaf(s, cs, -sn), aim);
     }
 }
 
-// One frequency, receivers 2h, 2h+1 as packed pairs: gq = q^2/m2, inv = 1/m2, b = an' +
-// kh c2 (the axial phase); a receiver that is not live adds zero (its amplitude factor is
-// selected to 0, so its inputs must be finite: every path leaves finite s, q^2, A, b).
+// One frequency, receivers 2h, 2h+1 as packed pairs: s = s' = s/b, gq = g' = q^2/(s'^2 + 1),
+// inv = 1/(s'^2 + 1), A = A/b, base = an' + kh c2 (the axial phase); with m2 = b^2 (s'^2 + 1)
+// the contribution i (A/m2) e (s + i b)(cos + i sin) is amp (-(s' sin + cos) + i (s' cos -
+// sin)), amp = (A/b) inv e: two products fewer than with s and b apart.  A receiver that is
+// not live adds zero (its amplitude factor is selected to 0, so its inputs must be finite:
+// every path leaves finite s, q^2, A, b).
 __device__ __forceinline__ void eval_pair2(const Fp32Consts &K, float2 s, float2 gq, float2 inv,
                                            float2 A, float2 base, float2 &pre, float2 &pim,
                                            bool l0, bool l1) {
     float2 ainv = mul2<PE>(A, inv);
     ainv.x = l0 ? ainv.x : 0.f;
     ainv.y = l1 ? ainv.y : 0.f;
-    const float2 gk = mul2<PE>(gq, bc2(K.kh[0]));
+    const float2 gk = mul2<PE>(gq, bc2(K.khq[0]));
     const float2 ph = fma2<PE>(gk, s, base);
     const float2 sn = make_float2(sin_approx(ph.x), sin_approx(ph.y));
     const float2 cs = make_float2(cos_approx(ph.x), cos_approx(ph.y));
-    const float2 ex = mul2<PE>(gq, bc2(K.nhkbl2e[0]));
+    const float2 ex = mul2<PE>(gq, bc2(K.nhkq[0]));
     const float2 amp = mul2<PE>(ainv, make_float2(ex2_approx(ex.x), ex2_approx(ex.y)));
-    const float2 as = mul2<PE>(amp, s), ab = mul2<PE>(amp, bc2(K.b));
-    // i * amp * (s + i b) * (cos + i sin)
-    pre = fma2<PE>(neg2(as), sn, fma2<PE>(neg2(ab), cs, pre));
-    pim = fma2<PE>(as, cs, fma2<PE>(neg2(ab), sn, pim));
+    pre = fma2<PE>(neg2(amp), fma2<PE>(s, sn, cs), pre);
+    pim = fma2<PE>(amp, fma2<PE>(s, cs, neg2(sn)), pim);
 }
 
 // Evaluation counts (kernels.py:399) of a lane's R = 4 receivers as byte fields: bit j of a
@@ -403,7 +412,7 @@ __device__ __forceinline__ float patch_dist(const WarpSmem<NF, MF> &S, const Fp3
     const float hn = uc > 1e-6f ? 0.5f * rcp_approx(uc) : 0.f;
     const float rn = uc > 1e-6f ? reach(B, g2.x * hn, g2.y * hn, g2.z * hn, 1.f) : B.w;
     const float rd = reach(B, g1.x, g1.y, g1.z, 1.f);
-    const float s0 = fmaf(0.5f, S.anc[r].y, S.aux[r].x);  // s0 = (s0 + Pc') - Pc'
+    const float s0 = fmaf(0.5f, S.anc[r].y, S.aux[r].x * K.b);  // s0 = (s0 + Pc') - Pc'
     const float s_hi = s0 + fminf(fmaxf(proj + rd * 1.00002f + 2e-3f, 0.f), g0.w);
     const float rk = sqrt_approx(K.rscale * fmaf(s_hi, s_hi, K.b2)) * 1.00002f + 1e-3f;
     *cut = uc * 0.99999f > (rk + rn) * 1.00002f + 2e-3f;
@@ -555,18 +564,19 @@ struct Junction {
     double ox, oy, oz;  // o_k
     double lx, ly, lz;  // len_k * d_k (t = len, kernels.py:337-339)
     double bx, by, bz;  // o_{k+1}
-    float sa, sb;       // s of either winner: s0_k + len_k, s0_{k+1}
+    float sa, sb;       // s' = s/b of either winner: s0_k + len_k, s0_{k+1}
 };
 
 __device__ __forceinline__ Junction load_junction(const double4 *__restrict__ p0,
-                                                  const double4 *__restrict__ p1, int64_t grow) {
+                                                  const double4 *__restrict__ p1, int64_t grow,
+                                                  double invb = 1.0) {
     const double4 a0 = p0[grow], a1 = p1[grow], b0 = p0[grow + 1], b1 = p1[grow + 1];
     Junction J;
     J.ox = a0.x, J.oy = a0.y, J.oz = a0.z;
     J.lx = __dmul_rn(a0.w, a1.x), J.ly = __dmul_rn(a0.w, a1.y), J.lz = __dmul_rn(a0.w, a1.z);
     J.bx = b0.x, J.by = b0.y, J.bz = b0.z;
-    J.sa = (float)(a1.w + a0.w);
-    J.sb = (float)b1.w;
+    J.sa = (float)((a1.w + a0.w) * invb);  // s' = s/b
+    J.sb = (float)(b1.w * invb);
     return J;
 }
 
@@ -699,7 +709,7 @@ __device__ __forceinline__ void exact_pending(const GbsArgs &a, const Fp32Consts
         const float q2 =
             fmaxf(fmaf(-dl, dl, fmaf(g2.x, x, fmaf(g2.y, y, fmaf(g2.z, z, g2.w + pick4(rr, j))))),
                   0.f);
-        const float s = (float)(w.p1[row0 + k].w + e.bt);  // kernels.py:344
+        const float s = (float)((w.p1[row0 + k].w + e.bt) * K.invb64);  // kernels.py:344, s' = s/b
         // phase reference follows the exact clamp
         const float4 an = S.anc[r0 + k];
         const float c2 = e.bt == 0.0 ? an.y : e.bt == e.len ? an.z : clamp2(dl, an);
@@ -738,7 +748,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
         // the centre's projection clamped to the segment; phase references (clamp2)
         const double pcc = pc < 0.0 ? 0.0 : (pc > p0.w ? p0.w : pc);
         const double sp = p1.w + pcc;
-        if (st) S.aux[r] = make_float2((float)sp, p2 * K.omega[0]);
+        if (st) S.aux[r] = make_float2((float)(sp * K.invb64), (float)((double)(p2 * K.omega[0]) * K.invb64));
         if (st) S.anc[r] = make_float4(frac_rad(K.kappa64[0] * sp), (float)(-2.0 * pcc),
                                (float)(2.0 * (p0.w - pcc)), (float)(2.0 * (pc - pcc)));
         if constexpr (MF) {
@@ -792,7 +802,7 @@ __device__ __forceinline__ void stage_rows(WarpSmem<NF, MF> &S, const Fp32Work &
         // the centre's projection clamped to the segment; phase references (clamp2)
         const double pcc = pc < 0.0 ? 0.0 : (pc > p0.w ? p0.w : pc);
         const double sp = p1.w + pcc;
-        S.aux[r] = make_float2((float)sp, p2 * K.omega[0]);
+        S.aux[r] = make_float2((float)(sp * K.invb64), (float)((double)(p2 * K.omega[0]) * K.invb64));
         S.anc[r] = make_float4(frac_rad(K.kappa64[0] * sp), (float)(-2.0 * pcc),
                                (float)(2.0 * (p0.w - pcc)), (float)(2.0 * (pc - pcc)));
         if constexpr (MF) {
@@ -1017,7 +1027,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                                            fma2<PG>(bc2(g2.x), X, fma2<PG>(bc2(g2.y), Y,
                                                 fma2<PG>(bc2(g2.z), Z, add2<PG>(bc2(g2.w), pair(rr, h))))));
                     const float2 c2 = make_float2(clamp2(dl.x, an), clamp2(dl.y, an));
-                    const float2 sv = fma2<PG>(bc2(0.5f), c2, bc2(ax.x));
+                    const float2 sv = fma2<PG>(bc2(K.hinvb), c2, bc2(ax.x));  // s' = s/b
                     float2 bf;
                     if constexpr (!MF) bf = fma2<PG>(bc2(K.kh[0]), c2, bc2(an.x));
 #pragma unroll
@@ -1064,6 +1074,46 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                 } else {
                 // ---- several candidate segments: fp32 distances, fp64 re-decision of ties
                 Db = __int_as_float(dsc.w);
+#if BF_HIST
+                {   // debug: lane-level pruning potential of this several-candidate item
+                    float rl = 0.f;
+#pragma unroll
+                    for (int j = 1; j < R; ++j) {
+                        const float ex_ = rx[j] - rx[0], ey_ = ry[j] - ry[0], ez_ = rz[j] - rz[0];
+                        if (j < nvalid) rl = fmaxf(rl, sqrtf(ex_ * ex_ + ey_ * ey_ + ez_ * ez_));
+                    }
+                    auto dist0 = [&](int k) {
+                        const float4 g0 = S.geo0[r0 + k], g1 = S.geo1[r0 + k];
+                        const float wx = rx[0] + g0.x, wy = ry[0] + g0.y, wz = rz[0] + g0.z;
+                        const float pr = wx * g1.x + wy * g1.y + wz * g1.z;
+                        const float t = fminf(fmaxf(pr, 0.f), g0.w);
+                        const float vx = wx - t * g1.x, vy = wy - t * g1.y, vz = wz - t * g1.z;
+                        return sqrtf(vx * vx + vy * vy + vz * vz);
+                    };
+                    float bd = INFINITY;
+                    for (unsigned m = surv; m; m &= m - 1) bd = fminf(bd, dist0(__ffs(m) - 1));
+                    unsigned keep = 0;
+                    for (unsigned m = surv; m; m &= m - 1) {
+                        const int k = __ffs(m) - 1;
+                        const float d = dist0(k);
+                        if (d - bd <= 2.f * rl * 1.0001f + 2e-3f + 1e-5f * d) keep |= 1u << k;
+                    }
+                    if (nvalid == 0) keep = 0;
+                    const unsigned wk = __reduce_or_sync(0xffffffffu, keep);
+                    const unsigned mx = __reduce_max_sync(0xffffffffu, (unsigned)__popc(keep));
+                    const unsigned l1 = __popc(__ballot_sync(0xffffffffu, __popc(keep) == 1));
+                    if (lane == 0) {
+                        const int n = __popc(surv);
+                        atomicAdd(&g_hist[6], (unsigned long long)n);
+                        atomicAdd(&g_hist[7], (unsigned long long)__popc(wk));
+                        atomicAdd(&g_hist[8], (unsigned long long)(__popc(wk) == 1));
+                        atomicAdd(&g_hist[9], 1ull);
+                        atomicAdd(&g_hist[10], (unsigned long long)l1);
+                        atomicAdd(&g_hist[11], (unsigned long long)mx);
+                        atomicAdd(&g_hist[n == 2 ? 12 : n == 3 ? 13 : n == 4 ? 14 : 15], 1ull);
+                    }
+                }
+#endif
                 const float tie_abs = TIE_ABS * Db * Db;
                 jp = 0;
                 lvm = 0;
@@ -1127,7 +1177,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const bool behind = k == 0 && proj < 0.f;  // behind the source
                     q2j[j] = fmaf(-dl, dl, fmaf(g2.x, rx[j], fmaf(g2.y, ry[j], fmaf(g2.z, rz[j], g2.w + rr[j]))));
                     const float c2 = clamp2(dl, an);
-                    sj[j] = fmaf(0.5f, c2, ax.x);
+                    sj[j] = fmaf(K.hinvb, c2, ax.x);
                     Aj[j] = ax.y;
                     if constexpr (!MF) {
                         bj[j][0] = fmaf(K.kh[0], c2, an.x);
@@ -1193,7 +1243,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                     const float2 ax = S.aux[r0 + k];
                     const float4 an = S.anc[r0 + k];
                     const float c2 = clamp2(dl, an);
-                    sj[j] = fmaf(0.5f, c2, ax.x);
+                    sj[j] = fmaf(K.hinvb, c2, ax.x);
                     Aj[j] = ax.y;
                     if constexpr (!MF) {
                         bj[j][0] = fmaf(K.kh[0], c2, an.x);
@@ -1207,7 +1257,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
 #endif
                 if (__any_sync(0xffffffffu, jp != 0)) {
                     const int ra = r0 + ka, rb = ra + 1;
-                    const Junction J = load_junction(w.p0, w.p1, row0 + ka);
+                    const Junction J = load_junction(w.p0, w.p1, row0 + ka, K.invb64);
                     const float Aa = S.aux[ra].y, Ab = S.aux[rb].y;
                     // phase references at the end of ka (c2 = hi2) and the start of ka+1
                     // (c2 = lo2)
@@ -1276,17 +1326,18 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         const double ux = wx - proj * d.x, uy = wy - proj * d.y,
                                      uz = wz - proj * d.z;
                         s64[j] = __dadd_rn(d.w, t);  // kernels.py:344
-                        sj[j] = (float)s64[j];
+                        sj[j] = (float)(s64[j] * K.invb64);
                         q2j[j] = (float)(ux * ux + uy * uy + uz * uz);
                     }
                 }
             }
-            // 1/m2 and g = q^2/m2 of every receiver (m2 = s^2 + b^2)
+            // 1/(s'^2 + 1) and g' = q^2/(s'^2 + 1) of every receiver (s' = s/b; m2 = s^2 + b^2 =
+            // b^2 (s'^2 + 1))
             float invj[R], gqj[R];
             unsigned tiny = 0;  // (TINY) receivers beyond the cutoff exponent: fp64
 #pragma unroll
             for (int h = 0; h < R; h += 2) {
-                const float2 m2p = fma2<PG>(pair(sj, h), pair(sj, h), bc2(K.b2));
+                const float2 m2p = fma2<PG>(pair(sj, h), pair(sj, h), bc2(1.f));  // m2/b^2
                 invj[h] = rcp_nr(m2p.x);
                 invj[h + 1] = rcp_nr(m2p.y);
                 const float2 gp = mul2<PG>(pair(q2j, h), pair(invj, h));
@@ -1297,7 +1348,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             {   // ex_re < -36 (kernels.py:384) as one mask (no cutoff: fp64 below)
                 unsigned cutm = 0;
 #pragma unroll
-                for (int j = 0; j < R; ++j) cutm |= (gqj[j] > K.gcut[0] ? 1u : 0u) << j;
+                for (int j = 0; j < R; ++j) cutm |= (gqj[j] > K.gcutq[0] ? 1u : 0u) << j;
                 if (TINY) tiny = cutm & lvm;
                 lvm &= ~cutm;
             }
@@ -1321,7 +1372,7 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                             const float bv = j == 0 ? bj[0][0] : j == 1 ? bj[1][0]
                                            : j == 2 ? bj[2][0] : bj[3][0];
                             tiny_contribution(K, 0, sv, gv, pick4(invj, j), pick4(Aj, j),
-                                              fmaf(gv * K.kh[0], sv, bv), S.acc[R * lane + j][0]);
+                                              fmaf(gv * K.khq[0], sv, bv), S.acc[R * lane + j][0]);
                         }
                 }
             }
@@ -1331,19 +1382,18 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
             // independent; WIDE: c2 = 0 and an'_f from the fp64 arc length), amplitude
             // A/m2 (s + i b) shared; the cutoff grows with omega, so each frequency is
             // evaluated only if some receiver of the warp is live for it
-            float X[R], ais[R], aib[R];
+            float X[R], ainv[R];
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-                X[j] = fmaf(gqj[j], sj[j], WIDE ? 0.f : bj[j][0]);
-                const float ainv = Aj[j] * invj[j];
-                ais[j] = ainv * sj[j];
-                aib[j] = ainv * K.b;
+                // X = c2 + g s = c2 + g' s'/b
+                X[j] = fmaf(gqj[j] * K.invb, sj[j], WIDE ? 0.f : bj[j][0]);
+                ainv[j] = Aj[j] * invj[j];
             }
             // per frequency: partial sums in shared memory (no per-frequency registers)
 #pragma unroll FUNROLL
             for (int f = 0; f < NF; ++f) {
                 // fp32 / (TINY) fp64 receivers of frequency f: ex_re < -36 (kernels.py:384)
-                const float gc = K.gcut[f];
+                const float gc = K.gcutq[f];
                 unsigned cutm = 0;
 #pragma unroll
                 for (int j = 0; j < R; ++j) cutm |= (gqj[j] > gc ? 1u : 0u) << j;
@@ -1376,8 +1426,8 @@ __device__ __forceinline__ void run_unit(const GbsArgs &a, const Tiling &tl, con
                         float4 v = S.facc[f][h >> 1][lane];
                         ph[h] = fmaf(K.kh[f], X[h], an[h]);
                         ph[h + 1] = fmaf(K.kh[f], X[h + 1], an[h + 1]);
-                        eval_freq(K, f, ph[h], gqj[h], ais[h], aib[h], v.x, v.y, (lf >> h) & 1u);
-                        eval_freq(K, f, ph[h + 1], gqj[h + 1], ais[h + 1], aib[h + 1], v.z, v.w,
+                        eval_freq(K, f, ph[h], gqj[h], sj[h], ainv[h], v.x, v.y, (lf >> h) & 1u);
+                        eval_freq(K, f, ph[h + 1], gqj[h + 1], sj[h + 1], ainv[h + 1], v.z, v.w,
                                   (lf >> (h + 1)) & 1u);
                         S.facc[f][h >> 1][lane] = v;
                     }
@@ -1858,7 +1908,7 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
               GbsStats *stats, const StreamPair &sp) {
 #if BF_HIST
     {
-        unsigned long long z[8] = {};
+        unsigned long long z[16] = {};
         cudaMemcpyToSymbolAsync(g_hist, z, sizeof(z), 0, cudaMemcpyHostToDevice, sp.st);
     }
 #endif
@@ -1903,11 +1953,12 @@ int launch_nf(const GbsArgs &a, const Tiling &t, const Fp32Work &w, const Fp32Co
 #endif
 #if BF_HIST
     {
-        unsigned long long h[8];
+        unsigned long long h[16];
         cudaMemcpyFromSymbolAsync(h, g_hist, sizeof(h), 0, cudaMemcpyDeviceToHost, sp.st);
         cudaStreamSynchronize(sp.st);
         fprintf(stderr, "bf hist: items all-cut %llu culled %llu\n", h[4], h[5]);
         fprintf(stderr, "bf hist: pend(<=2 surv) %llu pend(>=3 surv) %llu exact rounds %llu junction %llu\n", h[0], h[1], h[2], h[3]);
+        fprintf(stderr, "bf hist: multi items %llu sum n %llu sum n_lane_union %llu union==1 %llu lanes single %llu sum max lane n %llu; n=2 %llu n=3 %llu n=4 %llu n>=5 %llu\n", h[9], h[6], h[7], h[8], h[10], h[11], h[12], h[13], h[14], h[15]);
     }
 #endif
     return BF_OK;
@@ -1933,6 +1984,16 @@ Fp32Consts make_consts(const GbsArgs &a) {
     for (int f = 1; f < a.nf; ++f)
         if (!(K.gcut[f] <= K.gcut[f - 1])) K.ascending = 0;
     K.b = (float)a.width_b;
+    K.invb64 = 1.0 / a.width_b;
+    K.hinvb = (float)(0.5 / a.width_b);
+    K.invb = (float)(1.0 / a.width_b);
+    for (int f = 0; f < BF_MAXF; ++f) {
+        const double b2 = a.width_b * a.width_b;
+        K.gcutq[f] = K.gcut[f] == INFINITY ? INFINITY : (float)((double)K.gcut[f] * b2);
+        K.khq[f] = (float)((double)K.kh[f] / a.width_b);
+        K.nhkq64[f] = K.nhkbl2e64[f] / b2;
+        K.nhkq[f] = (float)K.nhkq64[f];
+    }
     K.b2 = (float)(a.width_b * a.width_b);
     K.b2_64 = a.width_b * a.width_b;
     K.amp_scale = a.phi_amp * sqrt(a.c) / (two_pi * a.c);
