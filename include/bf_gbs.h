@@ -79,6 +79,11 @@ uint64_t bf_launch_count(void);
  * Changes the grouping only, never the results. */
 int bf_set_memory_budget(int device, int64_t bytes);
 
+/* Process-wide: record the fp32 summation's GPU time for bf_last_stats' kernel_ms
+ * (two events around the kernels of every later call; ~10 us of graph-node latency on a
+ * small call).  0 (default) = not recorded, kernel_ms reads 0.  Never changes results. */
+int bf_set_kernel_timing(int on);
+
 /*
  * Drop-in for kernels.gbs_accumulate (kernels.py:352-355) on HOST buffers
  * (pageable or pinned).  Argument order follows the reference; array sizes
@@ -270,7 +275,8 @@ int bf_plan_chunks(int64_t total_rays, int64_t memory_budget, int64_t per_ray_by
 /* Statistics of the last fp32 bf_gbs_accumulate* call on this thread:
  * candidate (beam, receiver) pairs of the tile work list, total pairs, fp64
  * tie re-decisions, receiver tiles, non-behind pairs (P_nb), the CUDA-event
- * duration of the summation (first summation kernel start to last kernel end),
+ * duration of the summation (first summation kernel start to last kernel end; 0
+ * unless bf_set_kernel_timing(1) was in effect for the call),
  * and the sum of n_segs over candidate pairs (the scan term of the FLOP model).
  * Any pointer may be NULL.  The counters are copied back asynchronously by the
  * call; this function waits for that copy (the only place the engine waits on

@@ -27,6 +27,7 @@ EXPORTS = (
     "bf_tile_size", "bf_tile_order_dev", "bf_probe_peaks", "bf_last_path_stats", "bf_worklist",
     "bf_last_pair_stats", "bf_write_field_csv", "bf_set_memory_budget", "bf_rows_create",
     "bf_rows_destroy", "bf_rows_info", "bf_rows_append_dev", "bf_gbs_accumulate_rows_dev",
+    "bf_set_kernel_timing",
 )
 FLAG_OBS_PRESORTED = 1
 TRACE_EXHAUSTIVE = 1
@@ -62,6 +63,7 @@ def _declare(lib):
     lib.bf_trace_range_dev.argtypes = ([VP, VP, VP, VP, I64, VP, F64, VP, VP, VP, VP, F64, I64,
                                         I64] + [VP] * 9 + [I64, I64, I64, INT, INT, VP])
     lib.bf_set_memory_budget.argtypes = [INT, I64]
+    lib.bf_set_kernel_timing.argtypes = [INT]
     lib.bf_rows_create.argtypes = [INT, ctypes.POINTER(VP)]
     lib.bf_rows_destroy.argtypes = [VP]
     lib.bf_rows_info.argtypes = [VP, I64P, I64P]
@@ -118,6 +120,12 @@ def set_memory_budget(device: int, nbytes: int) -> None:
 
     Changes how a call is grouped, never its results (bf_set_memory_budget)."""
     check(load().bf_set_memory_budget(int(device), int(nbytes)))
+
+
+def set_kernel_timing(on: bool) -> None:
+    """Record kernel_ms (last_stats) for later fp32 calls; off by default (it costs
+    ~10 us of graph-node latency per small call)."""
+    check(load().bf_set_kernel_timing(1 if on else 0))
 
 
 def launch_count() -> int:

@@ -313,6 +313,7 @@ struct StatsBuf {
     unsigned long long *h_cand = nullptr;
     size_t cand_cap = 0;
     int64_t n_tiles = 0, tile = 0, n_obs = 0;
+    bool timed = false;  // t0/t1 recorded by the call (bf_set_kernel_timing)
 };
 struct PendingStats {
     int dev = -1;
@@ -327,6 +328,9 @@ thread_local PendingStats g_ps;
 // While a call is being captured into a graph (GraphCache) the statistics events are
 // recorded as external event nodes, so every replay records them for real.
 thread_local bool g_capturing = false;
+// Kernel timing of fp32 calls (bf_last_stats kernel_ms): two event records around the
+// summation, ~10 us per call of graph-node latency on small calls, so off by default.
+std::atomic<int> g_kernel_timing{0};
 cudaError_t rec_ext(cudaEvent_t e, cudaStream_t s) {
     return g_capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
                        : cudaEventRecord(e, s);
@@ -363,7 +367,7 @@ void materialize_stats() {
     }
     GbsStats h = *b.h_stats;
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, b.t0, b.t1) != cudaSuccess) {
+    if (b.timed && cudaEventElapsedTime(&ms, b.t0, b.t1) != cudaSuccess) {
         cudaGetLastError();
         ms = 0.f;
     }
@@ -1004,6 +1008,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
     BF_TRY(stats_events(c->dev));
     StatsBuf *sb;
     BF_TRY(stats_next(&sb));
+    sb->timed = g_kernel_timing.load() != 0;
     bool timed = false;
     int64_t gi = 0;
     // ---- frequency groups of <= BF_MAXF (acc columns are independent)
@@ -1135,7 +1140,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             BF_TRY(s.get(S_PART, (size_t)(w.n_ranges * w.n_pad * ag.nf), &w.part));
             BF_TRY(s.get(S_PARTEV, (size_t)(w.n_ranges * w.n_pad), &w.part_ev));
             if (!timed) {
-                BF_TRY_CUDA(rec_ext(sb->t0, s.ss));
+                if (sb->timed) BF_TRY_CUDA(rec_ext(sb->t0, s.ss));
                 timed = true;
             }
             BF_TRY(launch_gbs_fp32(gg, tg, w, d_stats, StreamPair{s.ss, s.sw, s.fork, s.join}));
@@ -1151,7 +1156,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             s.freed_valid = true;
         }
     }
-    BF_TRY_CUDA(rec_ext(sb->t1, st));
+    if (sb->timed) BF_TRY_CUDA(rec_ext(sb->t1, st));
     // ---- statistics: copied back asynchronously, reduced on request (bf_last_stats); a
     //      call being captured leaves the copies to run_fp32_graph (after the graph)
     sb->n_tiles = t.n_tiles;
@@ -1182,7 +1187,8 @@ int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t
         (double)device, P(st), P(a.seg_origin), P(a.seg_dir), P(a.seg_len), P(a.seg_s0),
         P(a.seg_refl), P(a.n_segs), P(a.weights), P(a.obs), P(a.acc), P(a.evals),
         (double)a.n_beams, (double)a.max_seg, (double)a.n_obs, (double)nf, (double)a.acc_stride,
-        a.c, a.width_b, a.phi_amp, (double)a.use_cutoff, (double)flags, (double)c->budget};
+        a.c, a.width_b, a.phi_amp, (double)a.use_cutoff, (double)flags, (double)c->budget,
+        (double)g_kernel_timing.load()};
     for (int64_t f = 0; f < nf; ++f) key.push_back(omegas[f]);
     DeviceCtx::GraphCache &g = c->gc;
     const bool same = g.seen && g.key == key;
@@ -1192,6 +1198,7 @@ int run_fp32_graph(DeviceCtx *c, const GbsArgs &a, const double *omegas, int64_t
         BF_TRY(stats_events(c->dev));
         if (g.gen != g_pool_gen.load()) return run_fp32(c, a, omegas, nf, false, flags, st);
         StatsBuf &b = g_ps.buf[g.sb];  // (a replay overwrites the previous one's statistics)
+        b.timed = g_kernel_timing.load() != 0;  // as captured (part of the key)
         BF_TRY_CUDA(cudaGraphLaunch(g.exec, st));
         note_launch(g.launches);
         g_ps.cur = g.sb;
@@ -1379,6 +1386,11 @@ int bf_device_count(void) {
 }
 
 uint64_t bf_launch_count(void) { return g_launches.load(); }
+
+int bf_set_kernel_timing(int on) {
+    g_kernel_timing.store(on != 0);
+    return BF_OK;
+}
 
 int bf_set_memory_budget(int device, int64_t bytes) {
     if (bytes < 0) return fail(BF_EINVAL, "negative memory budget");

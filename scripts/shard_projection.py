@@ -29,6 +29,7 @@ def main():
 
     import bench
     from paper_2501_13382_b200 import _lib, engine, shard
+    _lib.set_kernel_timing(True)  # kernel_ms below
     dev = torch.device("cuda", 0)
     cfg = bench.CONFIGS[args.config]
     sc, src, launch, tcfg, c, obs_np = bench.make_inputs(cfg)

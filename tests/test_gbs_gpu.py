@@ -746,3 +746,43 @@ def test_repeated_small_calls_replay_a_graph_bitexact(case):
     got2, _ = sequence([1 << 30] * 5, big_after=2)             # graph invalidated midway
     for r, g in zip(ref, got2):
         assert np.array_equal(r, g)
+
+
+@pytest.mark.gpu
+def test_kernel_timing_switch_changes_no_bits():
+    """bf_set_kernel_timing: kernel_ms is 0 while off (the default: no event nodes in a small
+    call) and positive while on; the results, statistics and graph replays are identical
+    either way (the switch is part of the graph key)."""
+    import torch
+
+    from paper_2501_13382_b200 import _lib, kernels
+    b = load_case("city_street")
+    dev = torch.device("cuda", 0)
+    t = lambda a, dt=torch.float64: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa
+    args = [t(b["seg_origin"]), t(b["seg_dir"]), t(b["seg_e1"]), t(b["seg_e2"]),
+            t(b["seg_len"]), t(b["seg_s0"]), t(b["seg_refl"]), t(b["n_segs"], torch.int32),
+            b["max_seg"], t(b["weights"]), t(b["obs"]), b["omegas"], float(b["c"]),
+            -float(b["beam_param_im"]), 1.0, True]
+    n_obs, nb, nf = b["obs"].shape[0], b["n_segs"].shape[0], b["omegas"].shape[0]
+    runs = {}
+    try:
+        for on in (False, True, False, True):
+            _lib.set_kernel_timing(on)
+            res = []
+            for _ in range(4):  # eager, capture, replays
+                acc = torch.zeros((n_obs, nf), dtype=torch.complex128, device=dev)
+                ev = torch.zeros(n_obs, dtype=torch.int64, device=dev)
+                kernels.gbs_accumulate(*args, acc, ev, 0, n_obs, 0, nb, precision="fp32")
+                st = _lib.last_stats()
+                res.append((acc.cpu().numpy(), ev.cpu().numpy(), st["tie_pairs"],
+                            st["nonbehind_pairs"]))
+                assert (st["kernel_ms"] > 0) == on
+            runs.setdefault(on, []).append(res)
+    finally:
+        _lib.set_kernel_timing(False)
+    ref = runs[False][0][0]
+    for on in (False, True):
+        for res in runs[on]:
+            for r in res:
+                assert np.array_equal(r[0], ref[0]) and np.array_equal(r[1], ref[1])
+                assert r[2:] == ref[2:]
