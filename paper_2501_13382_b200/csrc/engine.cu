@@ -862,6 +862,53 @@ int rows_from_host(const GbsArgs &h, int64_t b0, int64_t nb, Slot &s, Rows *out,
     return BF_OK;
 }
 
+// Single-CTA scans for small arrays (small calls): one launch instead of a count kernel
+// plus cub's init and scan kernels.  Thread t sums a contiguous run of the input, a block
+// scan offsets the runs; integer sums, so the result equals cub's.
+constexpr int SCAN1_T = 1024;
+constexpr int64_t SCAN1_MAX = (int64_t)SCAN1_T * 64;
+
+// start[0] = 0, start[b + 1] = sum over k <= b of n_segs[k] clamped to [0, max_seg]
+// (= rows_count_kernel + an inclusive scan of n_beams + 1 entries)
+__global__ void __launch_bounds__(SCAN1_T)
+    rows_scan1_kernel(const int32_t *n_segs, int64_t n_beams, int64_t max_seg, int64_t *start) {
+    using BS = cub::BlockScan<int64_t, SCAN1_T>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t per = (n_beams + SCAN1_T - 1) / SCAN1_T;
+    const int64_t b0 = threadIdx.x * per, b1 = min(n_beams, b0 + per);
+    auto cnt = [&](int64_t b) {
+        const int64_t n = n_segs[b];
+        return n < 0 ? (int64_t)0 : (n > max_seg ? max_seg : n);
+    };
+    int64_t loc = 0;
+    for (int64_t b = b0; b < b1; ++b) loc += cnt(b);
+    int64_t pre;
+    BS(tmp).ExclusiveSum(loc, pre);
+    if (threadIdx.x == 0) start[0] = 0;
+    for (int64_t b = b0; b < b1; ++b) {
+        pre += cnt(b);
+        start[b + 1] = pre;
+    }
+}
+
+// out[i] = sum over k < i of in[k] for i < n (= cub::DeviceScan::ExclusiveSum)
+__global__ void __launch_bounds__(SCAN1_T)
+    exscan1_kernel(const int64_t *in, int64_t *out, int64_t n) {
+    using BS = cub::BlockScan<int64_t, SCAN1_T>;
+    __shared__ typename BS::TempStorage tmp;
+    const int64_t per = (n + SCAN1_T - 1) / SCAN1_T;
+    const int64_t i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+    int64_t loc = 0;
+    for (int64_t i = i0; i < i1; ++i) loc += in[i];
+    int64_t pre;
+    BS(tmp).ExclusiveSum(loc, pre);
+    for (int64_t i = i0; i < i1; ++i) {
+        const int64_t v = in[i];
+        out[i] = pre;
+        pre += v;
+    }
+}
+
 // Compact rows of device beams [b0, b0 + nb) of the padded bundle in g (local indices),
 // packed on s.ss.  The row count stays on the device; rows_bound = nb * max_seg.
 int rows_from_device(const GbsArgs &g, Slot &s, Rows *out) {
@@ -873,13 +920,19 @@ int rows_from_device(const GbsArgs &g, Slot &s, Rows *out) {
     BF_TRY(s.get(S_P0, (size_t)std::max<int64_t>(nb * S, 1), &dp0));
     BF_TRY(s.get(S_P1, (size_t)std::max<int64_t>(nb * S, 1), &dp1));
     BF_TRY(s.get(S_AMP, (size_t)std::max<int64_t>(nb * S, 1), &da));
-    BF_TRY(launch_rows_count(g.n_segs, nb, S, 0, ds, s.ss));
-    size_t tb = 0;
-    BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, ds, ds, (int)(nb + 1), s.ss));
-    void *tmp;
-    BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
-    BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, ds, ds, (int)(nb + 1), s.ss));
-    note_launch();
+    if (nb + 1 <= SCAN1_MAX) {
+        rows_scan1_kernel<<<1, SCAN1_T, 0, s.ss>>>(g.n_segs, nb, S, ds);
+        note_launch();
+        BF_TRY_CUDA(cudaGetLastError());
+    } else {
+        BF_TRY(launch_rows_count(g.n_segs, nb, S, 0, ds, s.ss));
+        size_t tb = 0;
+        BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, ds, ds, (int)(nb + 1), s.ss));
+        void *tmp;
+        BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
+        BF_TRY_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, ds, ds, (int)(nb + 1), s.ss));
+        note_launch();
+    }
     BF_TRY(launch_rows_pack(g, ds, dp0, dp1, da, s.ss));
     *out = Rows{ds, dp0, dp1, da, nb, S};
     return BF_OK;
@@ -1085,7 +1138,11 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             tg.wl_bits = bits;
             tg.wl_tight = tbits;
             tg.wl_words = n_words;
-            {
+            if (nu_wl + 1 <= SCAN1_MAX) {
+                exscan1_kernel<<<1, SCAN1_T, 0, s.ss>>>(cnt, w.wl_off, nu_wl + 1);
+                note_launch();
+                BF_TRY_CUDA(cudaGetLastError());
+            } else {
                 size_t tb = 0;
                 BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, w.wl_off,
                                                           (int)(nu_wl + 1), s.ss));
