@@ -547,58 +547,82 @@ __global__ void order_key_kernel(const double *obs, int64_t n, const double *bbo
     vals[i] = (int32_t)i;
 }
 
+// One block per tile: centre and half extents of the tile's bounding box, patch-local fp32
+// offsets, and the tile radius.  The six extrema reduce together (warp shuffles, one
+// shared-memory round; min/max are exact, so any order gives the same bits).  perm_in ==
+// nullptr: receivers already in tile order, the identity permutation is written to perm_out.
 template <int T>
-__global__ void tile_kernel(const double *obs, int64_t n, const int32_t *perm, float4 *rloc,
-                            double4 *centre, double4 *tbox) {
-    using BR = cub::BlockReduce<double, T>;
-    __shared__ typename BR::TempStorage tmp;
+__global__ void __launch_bounds__(T)
+    tile_kernel(const double *obs, int64_t n, const int32_t *perm_in, int32_t *perm_out,
+                float4 *rloc, double4 *centre, double4 *tbox) {
+    constexpr int NW = T / 32;
+    __shared__ double s_red[6][NW];
     __shared__ double s_c[3], s_h[3];
     __shared__ float s_r;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t si = (int64_t)blockIdx.x * T + threadIdx.x;
     const bool valid = si < n;
     double p[3] = {0, 0, 0};
     if (valid) {
-        const int64_t oi = perm[si];
+        int64_t oi = si;
+        if (perm_in)
+            oi = perm_in[si];
+        else
+            perm_out[si] = (int32_t)si;
         for (int d = 0; d < 3; ++d) p[d] = obs[3 * oi + d];
     }
+    // v[d] -> min p_d, v[3 + d] -> min -p_d = -max p_d
+    double v[6];
     for (int d = 0; d < 3; ++d) {
-        const double mn = BR(tmp).Reduce(valid ? p[d] : INFINITY, cub::Min());
-        __syncthreads();
-        const double mx = BR(tmp).Reduce(valid ? p[d] : -INFINITY, cub::Max());
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            s_c[d] = 0.5 * (mn + mx);
-            s_h[d] = 0.5 * (mx - mn);
-        }
+        v[d] = valid ? p[d] : INFINITY;
+        v[3 + d] = valid ? -p[d] : INFINITY;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = fmin(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+    if (lane == 0)
+        for (int k = 0; k < 6; ++k) s_red[k][wid] = v[k];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) v[k] = lane < NW ? s_red[k][lane] : INFINITY;
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v[k] = fmin(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+        if (lane == 0)
+            for (int d = 0; d < 3; ++d) {
+                const double mn = v[d], mx = -v[3 + d];
+                s_c[d] = 0.5 * (mn + mx);
+                s_h[d] = 0.5 * (mx - mn);
+            }
     }
     __syncthreads();
-    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid) {
-        r.x = (float)(p[0] - s_c[0]);
-        r.y = (float)(p[1] - s_c[1]);
-        r.z = (float)(p[2] - s_c[2]);
-        rloc[si] = r;
-    }
     // the tile radius bounds |p - c| from above: fp64 offsets, rounded up to fp32 (the
     // work-list cut tests use it as a conservative bound)
     double rad = 0.0;
     if (valid) {
         const double dx = p[0] - s_c[0], dy = p[1] - s_c[1], dz = p[2] - s_c[2];
+        rloc[si] = make_float4((float)dx, (float)dy, (float)dz, 0.f);
         rad = sqrt(dx * dx + dy * dy + dz * dz) * (1.0 + 1e-15);
     }
-    const double rmax = BR(tmp).Reduce(rad, cub::Max());
-    if (threadIdx.x == 0) s_r = __double2float_ru(rmax);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rad = fmax(rad, __shfl_xor_sync(0xffffffffu, rad, o));
+    if (lane == 0) s_red[0][wid] = rad;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        centre[blockIdx.x] = make_double4(s_c[0], s_c[1], s_c[2], (double)s_r);
-        tbox[blockIdx.x] = make_double4(s_h[0], s_h[1], s_h[2], (double)s_r);
+    if (wid == 0) {
+        rad = lane < NW ? s_red[0][lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) rad = fmax(rad, __shfl_xor_sync(0xffffffffu, rad, o));
+        if (lane == 0) {
+            s_r = __double2float_ru(rad);
+            centre[blockIdx.x] = make_double4(s_c[0], s_c[1], s_c[2], (double)s_r);
+            tbox[blockIdx.x] = make_double4(s_h[0], s_h[1], s_h[2], (double)s_r);
+        }
     }
 }
 
-__global__ void iota_kernel(int32_t *v, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (int32_t)i;
-}
 
 // Hilbert order of n observers into *perm (a workspace buffer).
 int hilbert_order(DeviceCtx *c, const double *obs, int64_t n, cudaStream_t st,
@@ -642,22 +666,24 @@ int build_tiling(DeviceCtx *c, const double *obs, int64_t n, bool presorted, cud
     BF_TRY(c->get(B_RLOC, n, &rloc));
     BF_TRY(c->get(B_CENTRE, out->n_tiles, &cen));
     BF_TRY(c->get(B_TBOX, out->n_tiles, &box));
-    const int32_t *perm;
-    if (presorted) {
-        int32_t *id;
-        BF_TRY(c->get(B_VALS, n, &id));
-        iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(id, n);
-        note_launch();
-        perm = id;
+    const int32_t *perm, *perm_in = nullptr;
+    int32_t *perm_out = nullptr;
+    if (presorted) {  // identity order, written by tile_kernel
+        BF_TRY(c->get(B_VALS, n, &perm_out));
+        perm = perm_out;
     } else {
         BF_TRY(hilbert_order(c, obs, n, st, &perm));
+        perm_in = perm;
     }
     if (T == 512)
-        tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm, rloc, cen, box);
+        tile_kernel<512><<<(unsigned)out->n_tiles, 512, 0, st>>>(obs, n, perm_in, perm_out, rloc,
+                                                                 cen, box);
     else if (T == 256)
-        tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm, rloc, cen, box);
+        tile_kernel<256><<<(unsigned)out->n_tiles, 256, 0, st>>>(obs, n, perm_in, perm_out, rloc,
+                                                                 cen, box);
     else if (T == 1024)
-        tile_kernel<1024><<<(unsigned)out->n_tiles, 1024, 0, st>>>(obs, n, perm, rloc, cen, box);
+        tile_kernel<1024><<<(unsigned)out->n_tiles, 1024, 0, st>>>(obs, n, perm_in, perm_out,
+                                                                   rloc, cen, box);
     else
         return fail(BF_EINVAL, "unsupported tile size %d", T);
     note_launch();
