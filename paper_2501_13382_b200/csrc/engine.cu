@@ -1164,59 +1164,73 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             tg.wl_bits = bits;
             tg.wl_tight = tbits;
             tg.wl_words = n_words;
-            if (nu_wl + 1 <= SCAN1_MAX) {
+            BF_TRY(s.get(S_WLITEMS, (size_t)(t.n_tiles * gg.n_beams + 1), &w.wl_items));
+            BF_TRY(s.get(S_UCTR, 3, &w.unit_ctr));
+            w.n_wide = w.unit_ctr + 2;
+            const int64_t nu = w.n_patches * w.n_ranges;
+            int32_t *v1;
+            BF_TRY(s.get(S_UVALS2, (size_t)nu, &v1));
+            if (nu <= SMALL_QUEUE_N && nu_wl + 1 <= SCAN1_MAX) {
+                // small calls: the unit queue (one CTA; it needs only the counts) on the
+                // wide-kernel stream, concurrent with the offsets scan and the compaction
+                BF_TRY_CUDA(cudaEventRecord(s.qfork, s.ss));
+                BF_TRY_CUDA(cudaStreamWaitEvent(s.sw, s.qfork, 0));
+                BF_TRY(launch_fp32_small_queue(w, cnt, v1, s.sw));
+                BF_TRY_CUDA(cudaEventRecord(s.qjoin, s.sw));
+                w.unit_order = v1;
                 exscan1_kernel<<<1, SCAN1_T, 0, s.ss>>>(cnt, w.wl_off, nu_wl + 1);
                 note_launch();
                 BF_TRY_CUDA(cudaGetLastError());
+                BF_TRY(launch_fp32_wl_compact(tg, w, s.ss));
             } else {
-                size_t tb = 0;
-                BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, w.wl_off,
-                                                          (int)(nu_wl + 1), s.ss));
-                void *tmp;
-                BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
-                BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, w.wl_off,
-                                                          (int)(nu_wl + 1), s.ss));
-                note_launch();
-            }
-            // ---- compacted work list (on the wide-kernel stream, concurrent with the queue
-            //      order below): sized by its bound (tiles x beams), no host sync
-            BF_TRY(s.get(S_WLITEMS, (size_t)(t.n_tiles * gg.n_beams + 1), &w.wl_items));
-            BF_TRY_CUDA(cudaEventRecord(s.qfork, s.ss));
-            BF_TRY_CUDA(cudaStreamWaitEvent(s.sw, s.qfork, 0));
-            BF_TRY(launch_fp32_wl_compact(tg, w, s.sw));
-            BF_TRY_CUDA(cudaEventRecord(s.qjoin, s.sw));
-            // ---- unit queue order (wide patches last; longest-first buckets, range-major
-            //      inside a bucket) from the counts and the patch radii
-            BF_TRY(s.get(S_UCTR, 3, &w.unit_ctr));
-            w.n_wide = w.unit_ctr + 2;
-            {
-                const int64_t nu = w.n_patches * w.n_ranges;
-                int32_t *v1;
-                BF_TRY(s.get(S_UVALS2, (size_t)nu, &v1));
-                if (nu <= SMALL_QUEUE_N) {  // one CTA, one launch (small calls; it also
-                                            // sets the queue heads and the wide count)
-                    BF_TRY(launch_fp32_small_queue(w, cnt, v1, s.ss));
-                    w.unit_order = v1;
+                if (nu_wl + 1 <= SCAN1_MAX) {
+                    exscan1_kernel<<<1, SCAN1_T, 0, s.ss>>>(cnt, w.wl_off, nu_wl + 1);
+                    note_launch();
+                    BF_TRY_CUDA(cudaGetLastError());
                 } else {
-                    BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), s.ss));
-                    uint64_t *k0, *k1;
-                    int32_t *v0;
-                    BF_TRY(s.get(S_UKEYS, (size_t)nu, &k0));
-                    BF_TRY(s.get(S_UKEYS2, (size_t)nu, &k1));
-                    BF_TRY(s.get(S_UVALS, (size_t)nu, &v0));
-                    BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
-                    const int end_bit = 14;  // wide << 13 | bucket (7 bits) << 6 | range (< 64)
-                    cub::DoubleBuffer<uint64_t> dk(k0, k1);
-                    cub::DoubleBuffer<int32_t> dv(v0, v1);
                     size_t tb = 0;
-                    BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nu, 0,
-                                                                end_bit, s.ss));
+                    BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, w.wl_off,
+                                                              (int)(nu_wl + 1), s.ss));
                     void *tmp;
                     BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
-                    BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nu, 0,
-                                                                end_bit, s.ss));
+                    BF_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, w.wl_off,
+                                                              (int)(nu_wl + 1), s.ss));
                     note_launch();
-                    w.unit_order = dv.Current();
+                }
+                // ---- compacted work list (on the wide-kernel stream, concurrent with the queue
+                //      order below): sized by its bound (tiles x beams), no host sync
+                BF_TRY_CUDA(cudaEventRecord(s.qfork, s.ss));
+                BF_TRY_CUDA(cudaStreamWaitEvent(s.sw, s.qfork, 0));
+                BF_TRY(launch_fp32_wl_compact(tg, w, s.sw));
+                BF_TRY_CUDA(cudaEventRecord(s.qjoin, s.sw));
+                // ---- unit queue order (wide patches last; longest-first buckets, range-major
+                //      inside a bucket) from the counts and the patch radii
+                {
+                    if (nu <= SMALL_QUEUE_N) {  // one CTA, one launch (small calls; it also
+                                                // sets the queue heads and the wide count)
+                        BF_TRY(launch_fp32_small_queue(w, cnt, v1, s.ss));
+                        w.unit_order = v1;
+                    } else {
+                        BF_TRY_CUDA(cudaMemsetAsync(w.unit_ctr, 0, 3 * sizeof(unsigned), s.ss));
+                        uint64_t *k0, *k1;
+                        int32_t *v0;
+                        BF_TRY(s.get(S_UKEYS, (size_t)nu, &k0));
+                        BF_TRY(s.get(S_UKEYS2, (size_t)nu, &k1));
+                        BF_TRY(s.get(S_UVALS, (size_t)nu, &v0));
+                        BF_TRY(launch_fp32_unit_keys(tg, w, cnt, k0, v0, s.ss));
+                        const int end_bit = 14;  // wide << 13 | bucket (7 bits) << 6 | range (< 64)
+                        cub::DoubleBuffer<uint64_t> dk(k0, k1);
+                        cub::DoubleBuffer<int32_t> dv(v0, v1);
+                        size_t tb = 0;
+                        BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)nu, 0,
+                                                                    end_bit, s.ss));
+                        void *tmp;
+                        BF_TRY(s.buf[S_CUB].get(tb + 16, &tmp));
+                        BF_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, dk, dv, (int)nu, 0,
+                                                                    end_bit, s.ss));
+                        note_launch();
+                        w.unit_order = dv.Current();
+                    }
                 }
             }
             BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, s.qjoin, 0));
