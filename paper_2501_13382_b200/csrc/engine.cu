@@ -162,6 +162,7 @@ struct DeviceCtx {
     cudaEvent_t done = nullptr;
     bool done_valid = false;
     cudaEvent_t pro = nullptr;  // end of a call's prologue (tiling) on its stream
+    cudaEvent_t entry = nullptr;  // start of an fp32 call on its stream (beam-side work)
     cudaEvent_t fin = nullptr, fout = nullptr;  // CallStream fences (legacy stream handles)
     // statistics read-back (stats_copy) on a side stream, off the caller's critical path;
     // the next call waits for it (StreamOrder) before zeroing the counters again
@@ -279,6 +280,7 @@ int get_ctx(int device, DeviceCtx **out) {
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->pro, fl));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->entry, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fin, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fout, fl));
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -1059,6 +1061,11 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
              const bf_rows *resident = nullptr, int64_t beam_off = 0) {
     stats_begin(base.n_obs * base.n_beams);
     if (base.n_obs <= 0 || base.n_beams <= 0 || nf <= 0) return BF_OK;
+    // the beam side of each group (compact rows) depends only on the call's inputs: the
+    // slot streams start from the call's entry and overlap the receiver tiling below;
+    // each group's work list waits for the tiling (c->pro)
+    BF_TRY_CUDA(cudaEventRecord(c->entry, st));
+    for (Slot &s : c->slot) BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->entry, 0));
     // ---- prologue on the call's stream: receiver tiling, patches, zeroed counters
     Tiling t;
     BF_TRY(build_tiling(c, base.obs, base.n_obs, (flags & BF_FLAG_OBS_PRESORTED) != 0, st, &t));
@@ -1083,7 +1090,6 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
         BF_TRY_CUDA(cudaGetLastError());
     }
     BF_TRY_CUDA(cudaEventRecord(c->pro, st));
-    for (Slot &s : c->slot) BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->pro, 0));
     BF_TRY(stats_events(c->dev));
     StatsBuf *sb;
     BF_TRY(stats_next(&sb));
@@ -1157,6 +1163,7 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
             BF_TRY(s.get(S_WLCNT, (size_t)(nu_wl + 1), &cnt));
             BF_TRY(s.get(S_WLOFF, (size_t)(nu_wl + 1), &w.wl_off));
             BF_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (nu_wl + 1), s.ss));
+            BF_TRY_CUDA(cudaStreamWaitEvent(s.ss, c->pro, 0));  // the tiling and counters
             BF_TRY(launch_worklist(gg, rv, t.centre, t.tbox, t.n_tiles, wmin, bits, tbits, rb,
                                    w.n_ranges, reinterpret_cast<unsigned long long *>(cnt),
                                    d_cand, s.ss));
