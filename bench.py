@@ -286,7 +286,8 @@ def measure(D, name, precision, steps, warmup, peaks, cpu_budget, e2e_steps, cpu
     #      kernel timing (kernel_ms, the roofline's denominator) costs ~10 us of graph-node
     #      latency per call: recorded inside the timed steps only for calls of >= 2^28 pairs
     #      (>= ~1 ms), else in separate steps after the timed region
-    inline_timing = float(nb) * float(n_loc) >= 2.0 ** 28
+    # (the same decision on every rank: the extra steps below include the field gather)
+    inline_timing = float(nb) * float(n_total) / D.world >= 2.0 ** 28
     _lib.set_kernel_timing(inline_timing)
     D.barrier()
     torch.cuda.synchronize()
