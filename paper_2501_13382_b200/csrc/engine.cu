@@ -163,6 +163,7 @@ struct DeviceCtx {
     bool done_valid = false;
     cudaEvent_t pro = nullptr;  // end of a call's prologue (tiling) on its stream
     cudaEvent_t entry = nullptr;  // start of an fp32 call on its stream (beam-side work)
+    cudaEvent_t zdone = nullptr;  // an fp32 call's counters zeroed (beside the tiling)
     cudaEvent_t fin = nullptr, fout = nullptr;  // CallStream fences (legacy stream handles)
     // statistics read-back (stats_copy) on a side stream, off the caller's critical path;
     // the next call waits for it (StreamOrder) before zeroing the counters again
@@ -281,6 +282,7 @@ int get_ctx(int device, DeviceCtx **out) {
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->done, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->pro, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->entry, fl));
+        BF_TRY_CUDA(cudaEventCreateWithFlags(&c->zdone, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fin, fl));
         BF_TRY_CUDA(cudaEventCreateWithFlags(&c->fout, fl));
         BF_TRY_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -1082,12 +1084,15 @@ int run_fp32(DeviceCtx *c, const GbsArgs &base, const double *omegas, int64_t nf
     unsigned long long *d_cand;  // per tile: a9 beams, a9 segments, tight beams, tight segments
     BF_TRY(c->get(B_STATS, 1, &d_stats));
     BF_TRY(c->get(B_CAND, (size_t)(4 * t.n_tiles), &d_cand));
-    {
+    {   // zeroed on slot 0's stream (started at the call's entry), beside the tiling
         const int64_t na = sizeof(GbsStats) / 8, nb = 4 * t.n_tiles;
-        zero2_kernel<<<(unsigned)std::min<int64_t>((na + nb + 255) / 256, 1024), 256, 0, st>>>(
+        const cudaStream_t zs = c->slot[0].ss;
+        zero2_kernel<<<(unsigned)std::min<int64_t>((na + nb + 255) / 256, 1024), 256, 0, zs>>>(
             reinterpret_cast<unsigned long long *>(d_stats), na, d_cand, nb);
         note_launch();
         BF_TRY_CUDA(cudaGetLastError());
+        BF_TRY_CUDA(cudaEventRecord(c->zdone, zs));
+        BF_TRY_CUDA(cudaStreamWaitEvent(st, c->zdone, 0));
     }
     BF_TRY_CUDA(cudaEventRecord(c->pro, st));
     BF_TRY(stats_events(c->dev));
